@@ -1,0 +1,266 @@
+"""Flatten a list of actor models into the per-env tables the kernels consume.
+
+Host-side, built once per scene.  Index conventions follow the reference
+`Scene` layout (`pkg/src/batchsim/physics.py:216-355`):
+
+* bodies of one env are contiguous, actor after actor; global body row
+  ``e * B + actor_body_offset[a] + link`` (physics.py:229-230, 271-272);
+* DOFs likewise, ``e * D + actor_dof_offset[a] + dof`` (physics.py:282);
+* joint slots are ordered actor-major, then depth-first joint order
+  (physics.py:262-287); each pass solves all joints, then plane slots, then
+  pair slots (physics.py:761-775);
+* collision slots: sphere -> 1 plane slot, capsule -> 2 end spheres, box -> 8
+  corner points with radius 0 (physics.py:314-327); sphere-sphere pair slots
+  between different actors of the same env (physics.py:331-338);
+* a fixed-base root link has inv_mass 0 and zero inertia (physics.py:236-238);
+* a DOF is in POSITION mode iff its joint stiffness > 0 (physics.py:288-289).
+
+Every table is a plain numpy array; ``joint_table()`` packs the joint rows in
+the C struct layout ``bsim_joint_t`` declared in ``include/batchsim_b200.h``.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .model import ArticulationModel
+
+JOINT_KIND = {"fixed": 0, "revolute": 1, "prismatic": 2, "spherical": 3}
+MODE_FORCE, MODE_POSITION, MODE_VELOCITY = 0, 1, 2
+MODES = {"force": MODE_FORCE, "position": MODE_POSITION, "velocity": MODE_VELOCITY}
+
+# bsim_joint_t: 8 int32 then 24 float32 (128 bytes)
+JOINT_INTS = 8
+JOINT_FLOATS = 24
+# bsim_tendon_t / bsim_tendon_elem_t sizes (see header)
+TENDON_INTS = 8
+TENDON_FLOATS = 8
+TELEM_INTS = 4
+TELEM_FLOATS = 4
+
+
+@dataclass
+class JointRow:
+    kind: int
+    parent: int        # local body index within the env
+    child: int
+    dof: int           # local DOF offset within the env, -1 for fixed joints
+    actor: int
+    has_limits: bool
+    axis: np.ndarray
+    origin_pos: np.ndarray
+    origin_quat: np.ndarray
+    child_pos: np.ndarray
+    child_quat: np.ndarray
+    stiffness: float
+    damping: float
+    armature: float
+    friction: float
+    limit_lo: float
+    limit_hi: float
+
+
+class SceneLayout:
+    """Per-env tables for a list of actors replicated over all envs."""
+
+    def __init__(self, models, ground=True):
+        if isinstance(models, ArticulationModel):
+            models = [models]
+        self.models = list(models)
+        self.ground = bool(ground)
+        self.actors_per_env = len(self.models)
+        self.actor_body_offset, self.actor_dof_offset = [], []
+        b = d = 0
+        for m in self.models:
+            self.actor_body_offset.append(b)
+            self.actor_dof_offset.append(d)
+            b += m.num_bodies
+            d += m.num_dofs
+        self.bodies_per_env, self.dofs_per_env = b, d
+
+        # bodies
+        B = self.bodies_per_env
+        self.body_actor = np.zeros(B, np.int32)
+        self.inv_mass = np.zeros(B)
+        self.inertia = np.zeros((B, 3))
+        for a, m in enumerate(self.models):
+            for li, link in enumerate(m.links):
+                gi = self.actor_body_offset[a] + li
+                self.body_actor[gi] = a
+                if not (m.fixed_base and li == 0):
+                    self.inv_mass[gi] = 1.0 / link.mass
+                    self.inertia[gi] = link.inertia
+        pos = self.inertia > 0
+        self.inv_inertia = np.where(pos, 1.0 / np.where(pos, self.inertia, 1.0), 0.0)
+
+        # joints
+        self.joints: list[JointRow] = []
+        self.dof_mode = np.zeros(self.dofs_per_env, np.int8)
+        self.dof_joint = np.zeros(self.dofs_per_env, np.int32)
+        self.dof_lower = np.full(self.dofs_per_env, -np.inf)
+        self.dof_upper = np.full(self.dofs_per_env, np.inf)
+        for a, m in enumerate(self.models):
+            boff, doff = self.actor_body_offset[a], self.actor_dof_offset[a]
+            cursor = 0
+            for j in m.joints:
+                dof = -1
+                if j.dof_count:
+                    dof = doff + cursor
+                    for k in range(j.dof_count):
+                        self.dof_joint[dof + k] = len(self.joints)
+                        if j.limits:
+                            self.dof_lower[dof + k], self.dof_upper[dof + k] = j.limits
+                    cursor += j.dof_count
+                    if j.stiffness > 0:
+                        self.dof_mode[dof] = MODE_POSITION
+                lo, hi = j.limits if j.limits else (-np.inf, np.inf)
+                self.joints.append(JointRow(
+                    JOINT_KIND[j.kind], boff + m.link_index(j.parent), boff + m.link_index(j.child),
+                    dof, a, j.limits is not None, np.asarray(j.axis, float),
+                    np.asarray(j.origin_pos, float), np.asarray(j.origin_quat, float),
+                    np.asarray(j.child_pos, float), np.asarray(j.child_quat, float),
+                    j.stiffness, j.damping, j.armature, j.friction, lo, hi))
+        self.joints_per_env = len(self.joints)
+
+        # collision slots
+        shapes = []
+        for a, m in enumerate(self.models):
+            for li, link in enumerate(m.links):
+                if link.shape is not None and link.collision and link.shape.kind != "none":
+                    shapes.append((a, self.actor_body_offset[a] + li, link.shape))
+        plane = []
+        for _, body, sh in shapes:
+            off = np.asarray(sh.offset, float)
+            if sh.kind == "sphere":
+                plane.append((body, off, sh.params[0]))
+            elif sh.kind == "capsule":
+                r, hh = sh.params
+                plane += [(body, off + [0.0, 0.0, s * hh], r) for s in (-1.0, 1.0)]
+            elif sh.kind == "box":
+                hx, hy, hz = sh.params
+                plane += [(body, off + [sx * hx, sy * hy, sz * hz], 0.0)
+                          for sx in (-1, 1) for sy in (-1, 1) for sz in (-1, 1)]
+        if not self.ground:
+            plane = []
+        self.plane_body = np.array([p[0] for p in plane], np.int32)
+        self.plane_off = np.array([p[1] for p in plane], float).reshape(-1, 3)
+        self.plane_rad = np.array([p[2] for p in plane], float)
+        pairs = []
+        for i in range(len(shapes)):
+            for k in range(i + 1, len(shapes)):
+                (ai, bi, si), (ak, bk, sk) = shapes[i], shapes[k]
+                if ai != ak and si.kind == "sphere" and sk.kind == "sphere":
+                    pairs.append((bi, si, bk, sk))
+        self.pair_body = np.array([[p[0], p[2]] for p in pairs], np.int32).reshape(-1, 2)
+        self.pair_off = np.array([[p[1].offset, p[3].offset] for p in pairs], float).reshape(-1, 2, 3)
+        self.pair_rad = np.array([[p[1].params[0], p[3].params[0]] for p in pairs],
+                                 float).reshape(-1, 2)
+        self.planes_per_env = len(plane)
+        self.pairs_per_env = len(pairs)
+
+        # sensors
+        sens = []
+        for a, m in enumerate(self.models):
+            for name in (m.sensor_links or ()):
+                sens.append(self.actor_body_offset[a] + m.link_index(name))
+        self.sensor_body = np.array(sens, np.int32)
+        self.sensors_per_env = len(sens)
+
+        self._build_tendons()
+
+    # ------------------------------------------------------------ tendons
+    def _build_tendons(self):
+        """Fixed tendons (reference tendons.py:65-95, physics.py:598-653) and
+        spatial tendons (tendons.py:148-188) flattened into rows + elements."""
+        rows, elems = [], []
+        for a, m in enumerate(self.models):
+            boff, doff = self.actor_body_offset[a], self.actor_dof_offset[a]
+            dof_of = {}
+            c = 0
+            for j in m.joints:
+                if j.dof_count:
+                    dof_of[j.name] = c
+                    c += j.dof_count
+            for spec in m.tendons:
+                lo, hi = spec.limits if spec.limits else (0.0, 0.0)
+                first = len(elems)
+                if spec.kind == "fixed":
+                    root_joint = m.joints[m.joint_index(spec.joints[0].dof)]
+                    reaction = boff + m.link_index(root_joint.parent)
+                    for tj in spec.joints:
+                        ji = m.joint_index(tj.dof)
+                        joint_slot = self._joint_slot(a, ji)
+                        elems.append(((doff + dof_of[tj.dof], tj.parent, joint_slot, 0),
+                                      (tj.coefficient, 0.0, 0.0, 0.0)))
+                    kind = 0
+                else:
+                    for at in spec.attachments:
+                        elems.append(((boff + m.link_index(at.link), at.parent, 0, 0),
+                                      (at.offset[0], at.offset[1], at.offset[2], at.weight)))
+                    reaction = -1
+                    kind = 1
+                rows.append(((kind, first, len(elems) - first, int(spec.limits is not None),
+                              reaction, a, 0, 0),
+                             (spec.rest_length, spec.stiffness, spec.damping, lo, hi,
+                              spec.limit_stiffness, 0.0, 0.0)))
+        self.tendons_per_env = len(rows)
+        self.tendon_int = np.array([r[0] for r in rows], np.int32).reshape(-1, TENDON_INTS)
+        self.tendon_flt = np.array([r[1] for r in rows], np.float32).reshape(-1, TENDON_FLOATS)
+        self.telem_int = np.array([e[0] for e in elems], np.int32).reshape(-1, TELEM_INTS)
+        self.telem_flt = np.array([e[1] for e in elems], np.float32).reshape(-1, TELEM_FLOATS)
+        # spatial sub-tendon paths (root-to-leaf, declaration order), as element indices
+        self.spatial_paths = []
+        for t in range(self.tendons_per_env):
+            kind, first, count = self.tendon_int[t, :3]
+            if kind != 1:
+                self.spatial_paths.append([])
+                continue
+            parents = [int(self.telem_int[first + i, 1]) for i in range(count)]
+            kids = {i: [k for k in range(count) if parents[k] == i] for i in range(count)}
+            root = parents.index(-1)
+            paths = []
+
+            def walk(i, path):
+                path = path + [i]
+                if not kids[i]:
+                    paths.append(path)
+                for k in kids[i]:
+                    walk(k, path)
+            walk(root, [])
+            self.spatial_paths.append(paths)
+
+    def _joint_slot(self, actor, joint_index):
+        n = 0
+        for a in range(actor):
+            n += len(self.models[a].joints)
+        return n + joint_index
+
+    # ------------------------------------------------------------ packing
+    def joint_table(self):
+        """(J, 8) int32 and (J, 24) float32 views of bsim_joint_t rows."""
+        J = self.joints_per_env
+        ints = np.zeros((J, JOINT_INTS), np.int32)
+        flts = np.zeros((J, JOINT_FLOATS), np.float64)
+        for i, j in enumerate(self.joints):
+            ints[i, :6] = (j.kind, j.parent, j.child, j.dof, j.actor, int(j.has_limits))
+            flts[i, 0:3] = j.axis
+            flts[i, 3:6] = j.origin_pos
+            flts[i, 6:10] = j.origin_quat
+            flts[i, 10:13] = j.child_pos
+            flts[i, 13:17] = j.child_quat
+        return ints, flts
+
+    def joint_param_defaults(self):
+        """(6, J): stiffness, damping, armature, friction, limit_lo, limit_hi."""
+        return np.array([[j.stiffness for j in self.joints], [j.damping for j in self.joints],
+                         [j.armature for j in self.joints], [j.friction for j in self.joints],
+                         [j.limit_lo for j in self.joints], [j.limit_hi for j in self.joints]],
+                        float).reshape(6, self.joints_per_env)
+
+    def default_env_origins(self, num_envs, spacing=4.0):
+        """Square grid, cols = ceil(sqrt(E)) (physics.py:163-169)."""
+        cols = int(np.ceil(np.sqrt(num_envs)))
+        e = np.arange(num_envs)
+        return np.stack([spacing * (e % cols), spacing * (e // cols), np.zeros(num_envs)], -1)
