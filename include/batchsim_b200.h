@@ -1,0 +1,222 @@
+/*
+ * batchsim_b200.h -- C ABI of the B200 batched rigid-body step.
+ *
+ * The reference has no native ABI: its drop-in boundary is the duck-typed
+ * Python `Scene` protocol plus the `SimBuffers` facade
+ * (/root/reference/pkg/src/batchsim/physics.py:140-1091,
+ *  /root/reference/pkg/src/batchsim/buffers.py:47-225).  Every entry point
+ * below replaces one method of that boundary (cited per function) and takes
+ * only plain pointers and sizes.  All state pointers are DEVICE pointers to
+ * float32 arrays in the reference's shapes; `stream` is a cudaStream_t passed
+ * as void*.  Every call is asynchronous on `stream` and returns 0 or a
+ * negative BSIM_E* code; nothing is returned through device memory except
+ * where stated.
+ *
+ * Precision / frame contract (B200 design): the canonical body state
+ * `body_q` is float32 *env-local* (world position minus env origin); the
+ * tensor-API outputs `root_state` / `body_state` are world frame like the
+ * reference.  See DESIGN.md "Data layout in HBM".
+ */
+#ifndef BATCHSIM_B200_H
+#define BATCHSIM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BSIM_ABI_VERSION 1
+
+enum bsim_status {
+    BSIM_OK = 0,
+    BSIM_E_INVALID = -1,   /* bad sizes / null pointers                          */
+    BSIM_E_CUDA = -2,      /* a CUDA launch or API call failed (bsim_last_error) */
+    BSIM_E_TOO_LARGE = -3, /* model does not fit the kernel's shared memory     */
+};
+
+enum bsim_joint_kind { BSIM_FIXED = 0, BSIM_REVOLUTE = 1, BSIM_PRISMATIC = 2, BSIM_SPHERICAL = 3 };
+enum bsim_dof_mode { BSIM_MODE_FORCE = 0, BSIM_MODE_POSITION = 1, BSIM_MODE_VELOCITY = 2 };
+
+/* Every real-valued table and array exists in two precisions: float (the
+   fast path) and double (the exact-parity path, run on B200's FP64 units).
+   The *64 structs are field-for-field the same with double in place of
+   float; entry points with the _f64 suffix take them. */
+
+/* One joint slot (reference physics.py:262-287).  parent/child are body
+   indices local to the env; dof is the env-local first DOF or -1. */
+#define BSIM_JOINT_FIELDS(REAL)                                             \
+    int32_t kind, parent, child, dof, actor, has_limits, pad0, pad1;        \
+    REAL axis[3], origin_pos[3], origin_quat[4], child_pos[3], child_quat[4]; \
+    REAL pad[7];
+typedef struct bsim_joint_t { BSIM_JOINT_FIELDS(float) } bsim_joint_t;      /* 128 B */
+typedef struct bsim_joint64_t { BSIM_JOINT_FIELDS(double) } bsim_joint64_t; /* 224 B */
+
+/* One tendon (reference model.py:123-134, tendons.py).  kind 0 fixed, 1 spatial;
+   elements [first, first+count) of the element table. */
+#define BSIM_TENDON_FIELDS(REAL)                                                       \
+    int32_t kind, first, count, has_limits, reaction_body, actor, path_offset, pad;    \
+    REAL rest_length, stiffness, damping, limit_lo, limit_hi, limit_stiffness, pad2[2];
+typedef struct bsim_tendon_t { BSIM_TENDON_FIELDS(float) } bsim_tendon_t;
+typedef struct bsim_tendon64_t { BSIM_TENDON_FIELDS(double) } bsim_tendon64_t;
+
+/* fixed: index = env-local dof, joint = joint slot, v[0] = coefficient;
+   spatial: index = env-local body, v[0..2] = offset, v[3] = weight. */
+#define BSIM_TELEM_FIELDS(REAL) int32_t index, parent, joint, pad; REAL v[4];
+typedef struct bsim_tendon_elem_t { BSIM_TELEM_FIELDS(float) } bsim_tendon_elem_t;
+typedef struct bsim_tendon_elem64_t { BSIM_TELEM_FIELDS(double) } bsim_tendon_elem64_t;
+
+/* Solver scalars (reference SimParams, physics.py:54-73). */
+#define BSIM_PARAMS_FIELDS(REAL)                                                        \
+    REAL dt;                                                                            \
+    int32_t position_iterations, velocity_iterations;                                   \
+    REAL max_bias, restitution, bounce_threshold, rest_offset, friction_offset_threshold, \
+         solver_offset_slop, max_force, linear_damping, angular_damping,                \
+         max_linear_velocity, max_angular_velocity;
+typedef struct bsim_params_t { BSIM_PARAMS_FIELDS(float) } bsim_params_t;
+typedef struct bsim_params64_t { BSIM_PARAMS_FIELDS(double) } bsim_params64_t;
+
+/* Static per-env tables, replicated over envs (reference physics.py:216-355).
+   Table pointers are DEVICE pointers; joints / tendons / tendon_elems point at
+   the float or double struct variant matching the entry point's precision. */
+typedef struct bsim_layout_t {
+    int32_t num_envs, actors_per_env, bodies_per_env, dofs_per_env, joints_per_env,
+            planes_per_env, pairs_per_env, sensors_per_env, tendons_per_env, env_offset;
+    const void *joints;                    /* [J]    */
+    const int32_t *plane_body;             /* [P]    */
+    const int32_t *pair_body;              /* [Q][2] */
+    const int32_t *sensor_body;            /* [S]    */
+    const int32_t *actor_body_offset;      /* [A+1]  */
+    const int32_t *actor_dof_offset;       /* [A+1]  */
+    const void *tendons;                   /* [T]    */
+    const void *tendon_elems;
+    const int32_t *spatial_paths;          /* per tendon at path_offset: npaths, {len, idx...}* */
+} bsim_layout_t;
+
+/* All per-env state, parameters, controls and tensor-API outputs
+   (reference parallel.py:24-42 `_SHARED` working set).  DEVICE pointers. */
+#define BSIM_STATE_FIELDS(REAL)                                                      \
+    REAL *body_q;            /* [E*B][13] env-local pos3 quat4 linvel3 angvel3     */ \
+    REAL *friction_anchor;   /* [P][E][3] env-local, NaN = none                    */ \
+    uint8_t *nonfinite;      /* [E] sticky poison flags                            */ \
+    const REAL *env_origins; /* [E][3]                                             */ \
+    REAL *inv_mass;          /* [E*B]      (domain randomization writes these)     */ \
+    REAL *inertia_local;     /* [E*B][3]                                           */ \
+    REAL *inv_inertia_local; /* [E*B][3]                                           */ \
+    REAL *gravity;           /* [E][3]                                             */ \
+    REAL *mu_static, *mu_dynamic;              /* [E]                               */ \
+    REAL *joint_stiffness, *joint_damping, *joint_armature, *joint_friction,          \
+         *joint_limit_lo, *joint_limit_hi;     /* [J][E]                            */ \
+    REAL *plane_off;         /* [P][E][3]                                          */ \
+    REAL *plane_rad;         /* [P][E]                                             */ \
+    REAL *pair_off;          /* [Q][E][2][3]                                       */ \
+    REAL *pair_rad;          /* [Q][E][2]                                          */ \
+    REAL *ctrl_dof_force, *ctrl_dof_pos_target, *ctrl_dof_vel_target; /* [E*D]      */ \
+    REAL *ctrl_body_force, *ctrl_body_torque;                         /* [E*B][3]   */ \
+    int8_t *dof_mode;                                                  /* [E*D]      */ \
+    REAL *root_state;        /* [E*A][13] world frame                              */ \
+    REAL *body_state;        /* [E*B][13] world frame                              */ \
+    REAL *dof_state;         /* [E*D][2]                                           */ \
+    REAL *net_contact;       /* [E*B][3]                                           */ \
+    REAL *dof_force;         /* [E*D]                                              */ \
+    REAL *sensor_forces;     /* [E*S][6]                                           */
+typedef struct bsim_state_t { BSIM_STATE_FIELDS(float) } bsim_state_t;
+typedef struct bsim_state64_t { BSIM_STATE_FIELDS(double) } bsim_state64_t;
+
+/* Optional fused action mapping applied before the first substep:
+   target = scale * clip(actions, -1, 1) written to ctrl_dof_pos_target
+   (mode 1) or ctrl_dof_force (mode 0) -- reference envs.py:180, 421-424.
+   Arrays have the entry point's precision. */
+typedef struct bsim_actions_t {
+    const void *actions;      /* [E][D] device, or NULL */
+    void *actions_clipped;    /* [E][D] device copy of the clipped actions, or NULL */
+    double scale;
+    int32_t mode, pad;
+} bsim_actions_t;
+
+int bsim_abi_version(void);
+const char *bsim_last_error(void);
+/* Bytes of dynamic shared memory one env needs in the step kernel, and the
+   envs per CTA the launcher picks; returns BSIM_E_TOO_LARGE if it cannot fit. */
+int bsim_step_smem_per_env(const bsim_layout_t *layout, int32_t fp64, int32_t *bytes_per_env,
+                           int32_t *envs_per_cta);
+
+/* Scene.step() x n_substeps (physics.py:538-592; envs.py:186-187 decimation),
+   fused in one launch.  actions may be NULL. */
+int bsim_step(const bsim_layout_t *layout, const bsim_params_t *params, const bsim_state_t *state,
+              int32_t n_substeps, const bsim_actions_t *actions, void *stream);
+
+/* Scene.forward_kinematics(env_mask, actors) (physics.py:366-425) followed by
+   the body/root repack of the touched rows (buffers.py:109-123).
+   env_mask: [E] uint8 device or NULL (= all); actor_mask: bit a = actor a. */
+int bsim_forward_kinematics(const bsim_layout_t *layout, const bsim_state_t *state,
+                            const uint8_t *env_mask, uint32_t actor_mask, void *stream);
+
+/* Scene.refresh_buffers() without a solver context (physics.py:1037-1046):
+   dof readout + body/root packing for every env. */
+int bsim_refresh_buffers(const bsim_layout_t *layout, const bsim_state_t *state, void *stream);
+
+/* SimBuffers.set_root_state(values, indices) (buffers.py:127-152).
+   values: [E*A][13] world frame device array (only rows at `actor_idx` are
+   read); actor_idx: [n] int64 device, unique.  Validation (finite values,
+   |quat| >= 0.5, index range) is the caller's (the Python facade raises the
+   reference's BufferApiError family first).  The kernels renormalise quats,
+   write the root bodies, then run FK over (touched envs) x (touched actors)
+   and repack those rows, exactly the reference's cross product.
+   env_mask_scratch: [E] uint8 device; actor_mask_scratch: [1] uint32 device. */
+int bsim_set_root_state_indexed(const bsim_layout_t *layout, const bsim_state_t *state,
+                                const float *values, const int64_t *actor_idx, int32_t n,
+                                uint8_t *env_mask_scratch, uint32_t *actor_mask_scratch,
+                                void *stream);
+
+/* SimBuffers.set_dof_state(values, indices) (buffers.py:154-178); values
+   [E*D][2].  Same scratch contract as above. */
+int bsim_set_dof_state_indexed(const bsim_layout_t *layout, const bsim_state_t *state,
+                               const float *values, const int64_t *actor_idx, int32_t n,
+                               uint8_t *env_mask_scratch, uint32_t *actor_mask_scratch,
+                               void *stream);
+
+/* Scene._contact_geometry() (physics.py:463-498) for every (slot, env),
+   planes then pairs, env-minor: active [(P+Q)*E] uint8, depth, point [..][3],
+   normal [..][3] (world frame points).  Together with a prefix sum this
+   yields the collide() list order (physics.py:500-517). */
+int bsim_contact_geometry(const bsim_layout_t *layout, const bsim_params_t *params,
+                          const bsim_state_t *state, uint8_t *active, float *depth,
+                          float *point, float *normal, void *stream);
+
+/* Compacted contact list in collide() order (slot-major, env-ascending,
+   planes then pairs): warp-aggregated compaction.  Writes count[0] and up to
+   `capacity` entries of body_a (-1 ground), body_b, depth, point, normal.
+   scratch: [ceil((P+Q)*E/256)] int32 device. */
+int bsim_collide(const bsim_layout_t *layout, const bsim_params_t *params,
+                 const bsim_state_t *state, int32_t capacity, int32_t *count,
+                 int32_t *body_a, int32_t *body_b, float *depth, float *point, float *normal,
+                 int32_t *scratch, void *stream);
+
+/* float64 variants (same semantics, double tables / params / state). */
+int bsim_step_f64(const bsim_layout_t *layout, const bsim_params64_t *params,
+                  const bsim_state64_t *state, int32_t n_substeps, const bsim_actions_t *actions,
+                  void *stream);
+int bsim_forward_kinematics_f64(const bsim_layout_t *layout, const bsim_state64_t *state,
+                                const uint8_t *env_mask, uint32_t actor_mask, void *stream);
+int bsim_refresh_buffers_f64(const bsim_layout_t *layout, const bsim_state64_t *state, void *stream);
+int bsim_set_root_state_indexed_f64(const bsim_layout_t *layout, const bsim_state64_t *state,
+                                    const double *values, const int64_t *actor_idx, int32_t n,
+                                    uint8_t *env_mask_scratch, uint32_t *actor_mask_scratch,
+                                    void *stream);
+int bsim_set_dof_state_indexed_f64(const bsim_layout_t *layout, const bsim_state64_t *state,
+                                   const double *values, const int64_t *actor_idx, int32_t n,
+                                   uint8_t *env_mask_scratch, uint32_t *actor_mask_scratch,
+                                   void *stream);
+int bsim_contact_geometry_f64(const bsim_layout_t *layout, const bsim_params64_t *params,
+                              const bsim_state64_t *state, uint8_t *active, double *depth,
+                              double *point, double *normal, void *stream);
+int bsim_collide_f64(const bsim_layout_t *layout, const bsim_params64_t *params,
+                     const bsim_state64_t *state, int32_t capacity, int32_t *count,
+                     int32_t *body_a, int32_t *body_b, double *depth, double *point,
+                     double *normal, int32_t *scratch, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,634 @@
+// bsim_step.cu -- sm_100a kernels for the batched TGS step, forward kinematics,
+// indexed state setters, contact queries, and their C-ABI entry points
+// (declared in include/batchsim_b200.h).
+//
+// Step kernel mapping: one CTA = one warp = 32
+// environments, one thread per environment.  The CTA's per-env workspace is
+// dynamic shared memory laid out item-major with stride 33 (odd => the
+// per-thread column accesses and the cooperative row-contiguous global
+// loads/stores are both bank-conflict free).  Body state is moved
+// HBM <-> shared memory with fully coalesced loads/stores of the CTA's
+// contiguous [32 envs x B bodies x 13] slab; all substeps of a control step
+// run on the resident workspace, so HBM sees the state once per control step.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "bsim_step.cuh"
+
+using namespace bsim;
+
+namespace {
+
+// CTA shape of the step kernel: NE environments, NTH threads.
+constexpr int NE32 = 16, NTH32 = 128;   // float path
+constexpr int NE64 = 8, NTH64 = 64;     // double path (2x the workspace per env)
+
+std::string g_err;
+
+int set_err(const char *what, cudaError_t e) {
+    g_err = std::string(what) + ": " + cudaGetErrorString(e);
+    return BSIM_E_CUDA;
+}
+
+int check_launch(const char *what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_err(what, e);
+    return BSIM_OK;
+}
+
+template <class R> struct Shape;
+template <> struct Shape<float> {
+    static constexpr int NE = NE32, NTH = NTH32;
+};
+template <> struct Shape<double> {
+    static constexpr int NE = NE64, NTH = NTH64;
+};
+
+template <class R> size_t step_smem_bytes(const Dims &d) {
+    return (size_t)d.J * sizeof(typename Abi<R>::Joint) + (size_t)d.items * (Shape<R>::NE + 1) * sizeof(R);
+}
+
+// ------------------------------------------------------------------ step
+template <class R>
+__global__ void __launch_bounds__(Shape<R>::NTH) step_kernel(Ctx<R> c, int n_substeps, bsim_actions_t act) {
+    constexpr int NE = Shape<R>::NE, NTH = Shape<R>::NTH, STR = NE + 1;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const Dims &d = c.d;
+    using Joint = typename Abi<R>::Joint;
+    Joint *sj = reinterpret_cast<Joint *>(smem_raw);
+    R *ws = reinterpret_cast<R *>(smem_raw + (size_t)d.J * sizeof(Joint));
+    const int tid = threadIdx.x;
+    const int e0 = blockIdx.x * NE;
+    const int ne = min(NE, d.E - e0);
+    const int per_env = 13 * d.B;
+
+    // joint table -> shared (uniform broadcast reads afterwards)
+    {
+        const int words = d.J * (int)(sizeof(Joint) / 4);
+        const int *src = reinterpret_cast<const int *>(c.joints);
+        int *dst = reinterpret_cast<int *>(sj);
+        for (int i = tid; i < words; i += NTH) dst[i] = src[i];
+    }
+    // coalesced load of the CTA's contiguous [ne x B x 13] body slab
+    {
+        const R *src = c.s.body_q + (size_t)e0 * per_env;
+        for (int i = tid; i < ne * per_env; i += NTH) {
+            int el = i / per_env, item = i - el * per_env;
+            int b = item / 13, k = item - b * 13;
+            ws[(d.o_body + b * BODY_ITEMS + k) * STR + el] = src[i];
+        }
+    }
+    __syncthreads();
+    c.joints = sj;
+    const Grp<R> g{ws, STR, e0, ne, tid, NTH};
+    stage_group(c, g);
+    if (act.actions) {  // fused action mapping (envs.py:180, 421-424)
+        BS_ITEMS(g, d.D, el, k) {
+            size_t o = (size_t)(e0 + el) * d.D + k;
+            R a = clampr(reinterpret_cast<const R *>(act.actions)[o], R(-1), R(1));
+            if (act.actions_clipped) reinterpret_cast<R *>(act.actions_clipped)[o] = a;
+            R v = R(act.scale) * a;
+            if (act.mode == BSIM_MODE_POSITION) {
+                c.s.ctrl_dof_pos_target[o] = v;
+                g.env(el).at(idf(d, k, DPT)) = v;
+            } else {
+                c.s.ctrl_dof_force[o] = v;
+                g.env(el).at(idf(d, k, DF)) = v;
+            }
+        }
+    }
+    __syncthreads();
+    for (int s = 0; s < n_substeps; ++s) {
+        group_step(c, g, s == n_substeps - 1);
+        if (d.T && s != n_substeps - 1) {  // fixed tendons read dof_state next substep
+            readout_group(c, g);
+            __syncthreads();
+        }
+    }
+    readout_group(c, g);
+    BS_ITEMS(g, d.P, el, i) {
+        for (int k = 0; k < 3; ++k)
+            c.s.friction_anchor[3 * ((size_t)i * d.E + e0 + el) + k] = g.env(el).at(d.o_anchor + 3 * i + k);
+    }
+    __syncthreads();
+    // coalesced stores: canonical env-local state, world-frame body_state / root_state
+    {
+        R *dq = c.s.body_q + (size_t)e0 * per_env;
+        R *db = c.s.body_state + (size_t)e0 * per_env;
+        for (int i = tid; i < ne * per_env; i += NTH) {
+            int el = i / per_env, item = i - el * per_env;
+            int b = item / 13, k = item - b * 13;
+            R x = ws[(d.o_body + b * BODY_ITEMS + k) * STR + el];
+            dq[i] = x;
+            db[i] = k < 3 ? x + c.s.env_origins[3 * (size_t)(e0 + el) + k] : x;
+        }
+        const int per_root = d.A * 13;
+        R *dr = c.s.root_state + (size_t)e0 * per_root;
+        for (int i = tid; i < ne * per_root; i += NTH) {
+            int el = i / per_root, item = i - el * per_root;
+            int a = item / 13, k = item - a * 13;
+            int b = c.L.actor_body_offset[a];
+            R x = ws[(d.o_body + b * BODY_ITEMS + k) * STR + el];
+            dr[i] = k < 3 ? x + c.s.env_origins[3 * (size_t)(e0 + el) + k] : x;
+        }
+    }
+}
+
+// --------------------------------------------------------- kinematics
+// Scene.forward_kinematics (physics.py:366-425) for one env directly on
+// global memory (reset path; not the hot loop).  Positions env-local.
+template <class R> __device__ void fk_env(const Ctx<R> &c, int e, uint32_t amask) {
+    const Dims &d = c.d;
+    R *bq = c.s.body_q + (size_t)e * d.B * 13;
+    const R *dof = c.s.dof_state + 2 * (size_t)e * d.D;
+    for (int j = 0; j < d.J; ++j) {
+        const auto &jt = c.joints[j];
+        if (!((amask >> jt.actor) & 1u)) continue;
+        R *P = bq + 13 * jt.parent, *Cc = bq + 13 * jt.child;
+        Q4<R> qp = Q4<R>{P[3], P[4], P[5], P[6]};
+        V3<R> pp = V3<R>{P[0], P[1], P[2]};
+        Q4<R> jq = qmul(qp, jq4(jt.origin_quat));
+        V3<R> jrel = qrot(qp, jv3(jt.origin_pos));   // joint origin relative to the parent body
+        Q4<R> mq = Q4<R>{0, 0, 0, 1};
+        V3<R> mp = zero3<R>(), qda = zero3<R>(), qdl = zero3<R>();
+        if (jt.kind == BSIM_REVOLUTE) {
+            R q = dof[2 * jt.dof], qd = dof[2 * jt.dof + 1];
+            R sh = r_sin(R(0.5) * q), ch = r_cos(R(0.5) * q);
+            mq = Q4<R>{jt.axis[0] * sh, jt.axis[1] * sh, jt.axis[2] * sh, ch};
+            qda = qrot(jq, jv3(jt.axis)) * qd;
+        } else if (jt.kind == BSIM_PRISMATIC) {
+            R q = dof[2 * jt.dof], qd = dof[2 * jt.dof + 1];
+            mp = jv3(jt.axis) * q;
+            qdl = qrot(jq, jv3(jt.axis)) * qd;
+        } else if (jt.kind == BSIM_SPHERICAL) {
+            V3<R> q3 = v3(dof[2 * jt.dof], dof[2 * jt.dof + 2], dof[2 * jt.dof + 4]);
+            V3<R> qd3 = v3(dof[2 * jt.dof + 1], dof[2 * jt.dof + 3], dof[2 * jt.dof + 5]);
+            mq = qexp(q3);
+            qda = qrot(jq, qd3);
+        }
+        Q4<R> qcf = qmul(jq, mq);
+        V3<R> arel = jrel + qrot(jq, mp);                   // anchor relative to the parent body
+        Q4<R> qc = qnormalize(qmul(qcf, qconj(jq4(jt.child_quat))));
+        V3<R> crel = arel - qrot(qc, jv3(jt.child_pos));    // child body relative to the parent body
+        V3<R> pc = pp + crel;
+        V3<R> wp = V3<R>{P[10], P[11], P[12]}, vp = V3<R>{P[7], P[8], P[9]};
+        V3<R> wc = wp + qda;
+        V3<R> vc = vp + cross(wp, arel) + qdl + cross(wc, crel - arel);
+        Cc[0] = pc.x; Cc[1] = pc.y; Cc[2] = pc.z;
+        Cc[3] = qc.x; Cc[4] = qc.y; Cc[5] = qc.z; Cc[6] = qc.w;
+        Cc[7] = vc.x; Cc[8] = vc.y; Cc[9] = vc.z;
+        Cc[10] = wc.x; Cc[11] = wc.y; Cc[12] = wc.z;
+    }
+}
+
+// repack body_state/root_state rows of the masked actors (buffers.py:109-123)
+template <class R> __device__ void repack_env(const Ctx<R> &c, int e, uint32_t amask) {
+    const Dims &d = c.d;
+    const R *o = c.s.env_origins + 3 * (size_t)e;
+    for (int a = 0; a < d.A; ++a) {
+        if (!((amask >> a) & 1u)) continue;
+        int b0 = c.L.actor_body_offset[a], b1 = c.L.actor_body_offset[a + 1];
+        for (int b = b0; b < b1; ++b) {
+            const R *src = c.s.body_q + 13 * ((size_t)e * d.B + b);
+            R *dst = c.s.body_state + 13 * ((size_t)e * d.B + b);
+            for (int k = 0; k < 13; ++k) dst[k] = k < 3 ? src[k] + o[k] : src[k];
+        }
+        const R *rb = c.s.body_state + 13 * ((size_t)e * d.B + b0);
+        R *rr = c.s.root_state + 13 * ((size_t)e * d.A + a);
+        for (int k = 0; k < 13; ++k) rr[k] = rb[k];
+    }
+}
+
+// dof readout for one env straight from global memory (physics.py:427-459)
+template <class R> __device__ void readout_env(const Ctx<R> &c, int e) {
+    const Dims &d = c.d;
+    const R *bq = c.s.body_q + (size_t)e * d.B * 13;
+    for (int j = 0; j < d.J; ++j) {
+        const auto &jt = c.joints[j];
+        if (jt.dof < 0) continue;
+        const R *P = bq + 13 * jt.parent, *Cc = bq + 13 * jt.child;
+        Q4<R> qp = Q4<R>{P[3], P[4], P[5], P[6]}, qc = Q4<R>{Cc[3], Cc[4], Cc[5], Cc[6]};
+        Q4<R> jqp = qmul(qp, jq4(jt.origin_quat)), jqc = qmul(qc, jq4(jt.child_quat));
+        V3<R> wp = V3<R>{P[10], P[11], P[12]}, wc = V3<R>{Cc[10], Cc[11], Cc[12]};
+        R *o = c.s.dof_state + 2 * ((size_t)e * d.D + jt.dof);
+        if (jt.kind == BSIM_REVOLUTE) {
+            Q4<R> qr = qmul(qconj(jqp), jqc);
+            V3<R> ax = jv3(jt.axis);
+            o[0] = wrap_pi(R(2) * r_atan2(dot(qvec(qr), ax), qr.w));
+            o[1] = dot(qrot(jqp, ax), wc - wp);
+        } else if (jt.kind == BSIM_PRISMATIC) {
+            V3<R> rp = qrot(qp, jv3(jt.origin_pos)), rc = qrot(qc, jv3(jt.child_pos));
+            V3<R> sep = (V3<R>{Cc[0], Cc[1], Cc[2]} - V3<R>{P[0], P[1], P[2]}) + (rc - rp);
+            V3<R> aw = qrot(jqp, jv3(jt.axis));
+            o[0] = dot(aw, sep);
+            V3<R> vap = V3<R>{P[7], P[8], P[9]} + cross(wp, rp), vac = V3<R>{Cc[7], Cc[8], Cc[9]} + cross(wc, rc);
+            o[1] = dot(aw, vac - vap);
+        } else if (jt.kind == BSIM_SPHERICAL) {
+            Q4<R> qr = qmul(qconj(jqp), jqc);
+            V3<R> rv = qlog(qr), wr = qrot(qconj(jqp), wc - wp);
+            o[0] = rv.x; o[1] = wr.x; o[2] = rv.y; o[3] = wr.y; o[4] = rv.z; o[5] = wr.z;
+        }
+    }
+}
+
+template <class R>
+__global__ void fk_kernel(Ctx<R> c, const uint8_t *env_mask, const uint32_t *amask_dev, uint32_t amask) {
+    int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= c.d.E) return;
+    if (env_mask && !env_mask[e]) return;
+    uint32_t m = amask_dev ? *amask_dev : amask;
+    fk_env(c, e, m);
+    repack_env(c, e, m);
+}
+
+template <class R> __global__ void refresh_kernel(Ctx<R> c) {
+    int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= c.d.E) return;
+    readout_env(c, e);
+    repack_env(c, e, 0xffffffffu);
+}
+
+// set_root_state: write the root bodies of the listed actors (env-local), renormalise quats
+template <class R>
+__global__ void set_root_kernel(Ctx<R> c, const R *values, const int64_t *idx, int n, uint8_t *env_mask,
+                                uint32_t *amask) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int64_t a_glob = idx[i];
+    int e = (int)(a_glob / c.d.A), a = (int)(a_glob % c.d.A);
+    const R *v = values + 13 * a_glob;
+    R nq = r_sqrt(v[3] * v[3] + v[4] * v[4] + v[5] * v[5] + v[6] * v[6]);
+    R *dst = c.s.body_q + 13 * ((size_t)e * c.d.B + c.L.actor_body_offset[a]);
+    const R *o = c.s.env_origins + 3 * (size_t)e;
+    for (int k = 0; k < 3; ++k) dst[k] = v[k] - o[k];
+    for (int k = 3; k < 7; ++k) dst[k] = v[k] / nq;
+    for (int k = 7; k < 13; ++k) dst[k] = v[k];
+    env_mask[e] = 1;
+    atomicOr(amask, 1u << a);
+}
+
+template <class R>
+__global__ void set_dof_kernel(Ctx<R> c, const R *values, const int64_t *idx, int n, uint8_t *env_mask,
+                               uint32_t *amask) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int64_t a_glob = idx[i];
+    int e = (int)(a_glob / c.d.A), a = (int)(a_glob % c.d.A);
+    int d0 = c.L.actor_dof_offset[a], d1 = c.L.actor_dof_offset[a + 1];
+    if (d1 == d0) return;
+    for (int k = d0; k < d1; ++k) {
+        size_t r = (size_t)e * c.d.D + k;
+        c.s.dof_state[2 * r] = values[2 * r];
+        c.s.dof_state[2 * r + 1] = values[2 * r + 1];
+    }
+    env_mask[e] = 1;
+    atomicOr(amask, 1u << a);
+}
+
+// contact candidate per (slot, env) (physics.py:463-498); world-frame point
+template <class R>
+__device__ void slot_geometry(const Ctx<R> &c, int i, int e, bool &active, R &depth, V3<R> &point, V3<R> &n) {
+    const Dims &d = c.d;
+    const size_t E = (size_t)d.E;
+    const R *bq = c.s.body_q + (size_t)e * d.B * 13;
+    V3<R> org = jv3(c.s.env_origins + 3 * (size_t)e);
+    if (i < d.P) {
+        int b = c.L.plane_body[i];
+        const R *B_ = bq + 13 * b;
+        const R *off = c.s.plane_off + 3 * ((size_t)i * E + e);
+        R rad = c.s.plane_rad[(size_t)i * E + e];
+        V3<R> arm = qrot(Q4<R>{B_[3], B_[4], B_[5], B_[6]}, jv3(off));
+        V3<R> pos = V3<R>{B_[0], B_[1], B_[2]};
+        R gap = (pos.z + arm.z) - rad;
+        depth = c.p.rest_offset - gap;
+        point = pos + v3(arm.x, arm.y, arm.z - rad) + org;
+        n = v3(R(0), R(0), R(1));
+    } else {
+        int q = i - d.P;
+        const R *A_ = bq + 13 * c.L.pair_body[2 * q], *B_ = bq + 13 * c.L.pair_body[2 * q + 1];
+        const R *off = c.s.pair_off + 6 * ((size_t)q * E + e);
+        const R *rr = c.s.pair_rad + 2 * ((size_t)q * E + e);
+        V3<R> arma = qrot(Q4<R>{A_[3], A_[4], A_[5], A_[6]}, jv3(off));
+        V3<R> armb = qrot(Q4<R>{B_[3], B_[4], B_[5], B_[6]}, jv3(off + 3));
+        V3<R> pa = V3<R>{A_[0], A_[1], A_[2]};
+        V3<R> dd = (V3<R>{B_[0], B_[1], B_[2]} - pa) + (armb - arma);
+        R dist = norm(dd);
+        R dn = dist > R(1e-12) ? dist : R(1);
+        n = v3(dd.x / dn, dd.y / dn, dd.z / dn);
+        R gap = dist - (rr[0] + rr[1]);
+        depth = c.p.rest_offset - gap;
+        point = pa + arma + n * (rr[0] + R(0.5) * gap) + org;
+    }
+    active = depth > -c.p.solver_offset_slop;
+}
+
+template <class R>
+__global__ void contact_geometry_kernel(Ctx<R> c, uint8_t *active, R *depth, R *point, R *normal) {
+    size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    size_t total = (size_t)(c.d.P + c.d.Q) * c.d.E;
+    if (t >= total) return;
+    int i = (int)(t / c.d.E), e = (int)(t % c.d.E);
+    bool a;
+    R dp;
+    V3<R> pt, n;
+    slot_geometry(c, i, e, a, dp, pt, n);
+    active[t] = a;
+    depth[t] = dp;
+    point[3 * t] = pt.x; point[3 * t + 1] = pt.y; point[3 * t + 2] = pt.z;
+    normal[3 * t] = n.x; normal[3 * t + 1] = n.y; normal[3 * t + 2] = n.z;
+}
+
+// collide(): warp-aggregated compaction in (slot, env) order (physics.py:500-517).
+constexpr int CT = 256;
+template <class R> __global__ void collide_count_kernel(Ctx<R> c, int32_t *block_counts) {
+    size_t t = (size_t)blockIdx.x * CT + threadIdx.x;
+    size_t total = (size_t)(c.d.P + c.d.Q) * c.d.E;
+    bool a = false;
+    if (t < total) {
+        R dp;
+        V3<R> pt, n;
+        slot_geometry(c, (int)(t / c.d.E), (int)(t % c.d.E), a, dp, pt, n);
+    }
+    unsigned m = __ballot_sync(0xffffffffu, a);
+    __shared__ int wc[CT / 32];
+    if ((threadIdx.x & 31) == 0) wc[threadIdx.x >> 5] = __popc(m);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int s = 0;
+        for (int k = 0; k < CT / 32; ++k) s += wc[k];
+        block_counts[blockIdx.x] = s;
+    }
+}
+
+// single-CTA exclusive scan of the per-CTA counts; total -> *total
+__global__ void scan_kernel(int32_t *counts, int n, int32_t *total) {
+    __shared__ int32_t carry;
+    __shared__ int ws_[32];
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int base = 0; base < n; base += blockDim.x) {
+        int i = base + threadIdx.x;
+        int v = i < n ? counts[i] : 0;
+        int x = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) ws_[wid] = x;
+        __syncthreads();
+        if (wid == 0) {
+            int s = lane < (int)(blockDim.x >> 5) ? ws_[lane] : 0;
+            for (int o = 1; o < 32; o <<= 1) {
+                int y = __shfl_up_sync(0xffffffffu, s, o);
+                if (lane >= o) s += y;
+            }
+            ws_[lane] = s;
+        }
+        __syncthreads();
+        int excl = x - v + (wid ? ws_[wid - 1] : 0) + carry;
+        if (i < n) counts[i] = excl;
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) carry = excl + v;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *total = carry;
+}
+
+template <class R>
+__global__ void collide_write_kernel(Ctx<R> c, const int32_t *block_offsets, int32_t capacity, int32_t *body_a,
+                                     int32_t *body_b, R *depth, R *point, R *normal) {
+    size_t t = (size_t)blockIdx.x * CT + threadIdx.x;
+    size_t total = (size_t)(c.d.P + c.d.Q) * c.d.E;
+    bool a = false;
+    R dp = R(0);
+    V3<R> pt = zero3<R>(), n = zero3<R>();
+    int i = 0, e = 0;
+    if (t < total) {
+        i = (int)(t / c.d.E);
+        e = (int)(t % c.d.E);
+        slot_geometry(c, i, e, a, dp, pt, n);
+    }
+    unsigned m = __ballot_sync(0xffffffffu, a);
+    __shared__ int wc[CT / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) wc[wid] = __popc(m);
+    __syncthreads();
+    int woff = 0;
+    for (int k = 0; k < wid; ++k) woff += wc[k];
+    if (a) {
+        int slot = block_offsets[blockIdx.x] + woff + __popc(m & ((1u << lane) - 1u));
+        if (slot < capacity) {
+            const Dims &d = c.d;
+            if (i < d.P) {
+                body_a[slot] = -1;
+                body_b[slot] = e * d.B + c.L.plane_body[i];
+            } else {
+                body_a[slot] = e * d.B + c.L.pair_body[2 * (i - d.P)];
+                body_b[slot] = e * d.B + c.L.pair_body[2 * (i - d.P) + 1];
+            }
+            depth[slot] = dp;
+            point[3 * slot] = pt.x; point[3 * slot + 1] = pt.y; point[3 * slot + 2] = pt.z;
+            normal[3 * slot] = n.x; normal[3 * slot + 1] = n.y; normal[3 * slot + 2] = n.z;
+        }
+    }
+}
+
+template <class R>
+Ctx<R> make_ctx(const bsim_layout_t *L, const typename Abi<R>::Params *p, const typename Abi<R>::State *s) {
+    Ctx<R> c;
+    c.L = *L;
+    if (p) c.p = *p; else std::memset(&c.p, 0, sizeof c.p);
+    c.s = *s;
+    c.d = make_dims(*L);
+    c.joints = reinterpret_cast<const typename Abi<R>::Joint *>(L->joints);
+    return c;
+}
+
+bool bad_layout(const bsim_layout_t *L) {
+    return !L || L->num_envs < 0 || L->bodies_per_env < 0 || L->actors_per_env < 1 ||
+           L->actors_per_env > 32 || (L->joints_per_env && !L->joints);
+}
+
+// ------------------------------------------------------------ launchers
+template <class R>
+int launch_step(const bsim_layout_t *layout, const typename Abi<R>::Params *params,
+                const typename Abi<R>::State *state, int32_t n_substeps, const bsim_actions_t *actions,
+                void *stream) {
+    if (bad_layout(layout) || !params || !state || n_substeps < 1) {
+        g_err = "bsim_step: invalid arguments";
+        return BSIM_E_INVALID;
+    }
+    Ctx<R> c = make_ctx<R>(layout, params, state);
+    if (c.d.E == 0) return BSIM_OK;
+    size_t smem = step_smem_bytes<R>(c.d);
+    if (smem > 227 * 1024) {
+        g_err = "bsim_step: model too large for the step kernel's shared-memory workspace";
+        return BSIM_E_TOO_LARGE;
+    }
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
+        cudaError_t e = cudaFuncSetAttribute(step_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return set_err("cudaFuncSetAttribute(step_kernel)", e);
+        configured = smem;
+    }
+    bsim_actions_t act;
+    if (actions) act = *actions; else std::memset(&act, 0, sizeof act);
+    int grid = (c.d.E + Shape<R>::NE - 1) / Shape<R>::NE;
+    step_kernel<R><<<grid, Shape<R>::NTH, smem, (cudaStream_t)stream>>>(c, n_substeps, act);
+    return check_launch("step_kernel");
+}
+
+template <class R>
+int launch_fk(const bsim_layout_t *layout, const typename Abi<R>::State *state, const uint8_t *env_mask,
+              uint32_t actor_mask, void *stream) {
+    if (bad_layout(layout) || !state) return BSIM_E_INVALID;
+    Ctx<R> c = make_ctx<R>(layout, nullptr, state);
+    if (c.d.E == 0) return BSIM_OK;
+    fk_kernel<R><<<(c.d.E + 127) / 128, 128, 0, (cudaStream_t)stream>>>(c, env_mask, nullptr, actor_mask);
+    return check_launch("fk_kernel");
+}
+
+template <class R> int launch_refresh(const bsim_layout_t *layout, const typename Abi<R>::State *state, void *stream) {
+    if (bad_layout(layout) || !state) return BSIM_E_INVALID;
+    Ctx<R> c = make_ctx<R>(layout, nullptr, state);
+    if (c.d.E == 0) return BSIM_OK;
+    refresh_kernel<R><<<(c.d.E + 127) / 128, 128, 0, (cudaStream_t)stream>>>(c);
+    return check_launch("refresh_kernel");
+}
+
+template <class R>
+int launch_set(bool root, const bsim_layout_t *layout, const typename Abi<R>::State *state, const R *values,
+               const int64_t *idx, int32_t n, uint8_t *env_mask, uint32_t *amask, void *stream) {
+    if (bad_layout(layout) || !state || !values || !idx || n < 0 || !env_mask || !amask) return BSIM_E_INVALID;
+    Ctx<R> c = make_ctx<R>(layout, nullptr, state);
+    if (n == 0 || c.d.E == 0) return BSIM_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e1 = cudaMemsetAsync(env_mask, 0, (size_t)c.d.E, st);
+    if (e1 != cudaSuccess) return set_err("memset env_mask", e1);
+    cudaError_t e2 = cudaMemsetAsync(amask, 0, sizeof(uint32_t), st);
+    if (e2 != cudaSuccess) return set_err("memset actor mask", e2);
+    if (root)
+        set_root_kernel<R><<<(n + 127) / 128, 128, 0, st>>>(c, values, idx, n, env_mask, amask);
+    else
+        set_dof_kernel<R><<<(n + 127) / 128, 128, 0, st>>>(c, values, idx, n, env_mask, amask);
+    int r = check_launch(root ? "set_root_kernel" : "set_dof_kernel");
+    if (r) return r;
+    // FK over (touched envs) x (touched actors), then repack (buffers.py:151-152, 177-178)
+    fk_kernel<R><<<(c.d.E + 127) / 128, 128, 0, st>>>(c, env_mask, amask, 0u);
+    return check_launch("fk_kernel");
+}
+
+template <class R>
+int launch_contact_geometry(const bsim_layout_t *layout, const typename Abi<R>::Params *params,
+                            const typename Abi<R>::State *state, uint8_t *active, R *depth, R *point, R *normal,
+                            void *stream) {
+    if (bad_layout(layout) || !params || !state) return BSIM_E_INVALID;
+    Ctx<R> c = make_ctx<R>(layout, params, state);
+    size_t total = (size_t)(c.d.P + c.d.Q) * c.d.E;
+    if (!total) return BSIM_OK;
+    contact_geometry_kernel<R><<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        c, active, depth, point, normal);
+    return check_launch("contact_geometry_kernel");
+}
+
+template <class R>
+int launch_collide(const bsim_layout_t *layout, const typename Abi<R>::Params *params,
+                   const typename Abi<R>::State *state, int32_t capacity, int32_t *count, int32_t *body_a,
+                   int32_t *body_b, R *depth, R *point, R *normal, int32_t *scratch, void *stream) {
+    if (bad_layout(layout) || !params || !state || !count || !scratch) return BSIM_E_INVALID;
+    Ctx<R> c = make_ctx<R>(layout, params, state);
+    size_t total = (size_t)(c.d.P + c.d.Q) * c.d.E;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (!total) {
+        cudaError_t e = cudaMemsetAsync(count, 0, sizeof(int32_t), st);
+        return e == cudaSuccess ? BSIM_OK : set_err("memset count", e);
+    }
+    int nb = (int)((total + CT - 1) / CT);
+    collide_count_kernel<R><<<nb, CT, 0, st>>>(c, scratch);
+    int r = check_launch("collide_count_kernel");
+    if (r) return r;
+    scan_kernel<<<1, 1024, 0, st>>>(scratch, nb, count);
+    if ((r = check_launch("scan_kernel"))) return r;
+    collide_write_kernel<R><<<nb, CT, 0, st>>>(c, scratch, capacity, body_a, body_b, depth, point, normal);
+    return check_launch("collide_write_kernel");
+}
+
+}  // namespace
+
+extern "C" {
+
+int bsim_abi_version(void) { return BSIM_ABI_VERSION; }
+const char *bsim_last_error(void) { return g_err.c_str(); }
+
+int bsim_step_smem_per_env(const bsim_layout_t *layout, int32_t fp64, int32_t *bytes_per_env,
+                           int32_t *envs_per_cta) {
+    if (bad_layout(layout)) return BSIM_E_INVALID;
+    Dims d = make_dims(*layout);
+    size_t total = fp64 ? step_smem_bytes<double>(d) : step_smem_bytes<float>(d);
+    if (bytes_per_env) *bytes_per_env = (int32_t)(d.items * (fp64 ? 8 : 4));
+    if (envs_per_cta) *envs_per_cta = fp64 ? NE64 : NE32;
+    return total > 227 * 1024 ? BSIM_E_TOO_LARGE : BSIM_OK;
+}
+
+int bsim_step(const bsim_layout_t *l, const bsim_params_t *p, const bsim_state_t *s, int32_t n,
+              const bsim_actions_t *a, void *st) {
+    return launch_step<float>(l, p, s, n, a, st);
+}
+int bsim_step_f64(const bsim_layout_t *l, const bsim_params64_t *p, const bsim_state64_t *s, int32_t n,
+                  const bsim_actions_t *a, void *st) {
+    return launch_step<double>(l, p, s, n, a, st);
+}
+int bsim_forward_kinematics(const bsim_layout_t *l, const bsim_state_t *s, const uint8_t *m, uint32_t am,
+                            void *st) {
+    return launch_fk<float>(l, s, m, am, st);
+}
+int bsim_forward_kinematics_f64(const bsim_layout_t *l, const bsim_state64_t *s, const uint8_t *m, uint32_t am,
+                                void *st) {
+    return launch_fk<double>(l, s, m, am, st);
+}
+int bsim_refresh_buffers(const bsim_layout_t *l, const bsim_state_t *s, void *st) {
+    return launch_refresh<float>(l, s, st);
+}
+int bsim_refresh_buffers_f64(const bsim_layout_t *l, const bsim_state64_t *s, void *st) {
+    return launch_refresh<double>(l, s, st);
+}
+int bsim_set_root_state_indexed(const bsim_layout_t *l, const bsim_state_t *s, const float *v, const int64_t *i,
+                                int32_t n, uint8_t *em, uint32_t *am, void *st) {
+    return launch_set<float>(true, l, s, v, i, n, em, am, st);
+}
+int bsim_set_root_state_indexed_f64(const bsim_layout_t *l, const bsim_state64_t *s, const double *v,
+                                    const int64_t *i, int32_t n, uint8_t *em, uint32_t *am, void *st) {
+    return launch_set<double>(true, l, s, v, i, n, em, am, st);
+}
+int bsim_set_dof_state_indexed(const bsim_layout_t *l, const bsim_state_t *s, const float *v, const int64_t *i,
+                               int32_t n, uint8_t *em, uint32_t *am, void *st) {
+    return launch_set<float>(false, l, s, v, i, n, em, am, st);
+}
+int bsim_set_dof_state_indexed_f64(const bsim_layout_t *l, const bsim_state64_t *s, const double *v,
+                                   const int64_t *i, int32_t n, uint8_t *em, uint32_t *am, void *st) {
+    return launch_set<double>(false, l, s, v, i, n, em, am, st);
+}
+int bsim_contact_geometry(const bsim_layout_t *l, const bsim_params_t *p, const bsim_state_t *s, uint8_t *a,
+                          float *d, float *pt, float *n, void *st) {
+    return launch_contact_geometry<float>(l, p, s, a, d, pt, n, st);
+}
+int bsim_contact_geometry_f64(const bsim_layout_t *l, const bsim_params64_t *p, const bsim_state64_t *s,
+                              uint8_t *a, double *d, double *pt, double *n, void *st) {
+    return launch_contact_geometry<double>(l, p, s, a, d, pt, n, st);
+}
+int bsim_collide(const bsim_layout_t *l, const bsim_params_t *p, const bsim_state_t *s, int32_t cap, int32_t *cnt,
+                 int32_t *ba, int32_t *bb, float *d, float *pt, float *n, int32_t *scr, void *st) {
+    return launch_collide<float>(l, p, s, cap, cnt, ba, bb, d, pt, n, scr, st);
+}
+int bsim_collide_f64(const bsim_layout_t *l, const bsim_params64_t *p, const bsim_state64_t *s, int32_t cap,
+                     int32_t *cnt, int32_t *ba, int32_t *bb, double *d, double *pt, double *n, int32_t *scr,
+                     void *st) {
+    return launch_collide<double>(l, p, s, cap, cnt, ba, bb, d, pt, n, scr, st);
+}
+
+}  // extern "C"

@@ -1,0 +1,1028 @@
+// bsim_step.cuh -- the batched Temporal-Gauss-Seidel step for a group of
+// environments (host+device), templated on the scalar type R (float fast
+// path / double exact-parity path).
+//
+// B200 mapping: one CTA owns NE environments and
+// NT = NE * TPE threads.  Every TGS pass is split in two:
+//
+//   phase A (lane-parallel over (env, body|joint|contact) items): effective
+//     poses, world inverse inertias, joint anchors/errors/axes and every
+//     row's velocity-independent constants (K^-1, impulse-response matrices,
+//     effective masses);
+//   phase B (one thread per env): the Gauss-Seidel sweep itself, which now
+//     only reads/writes body velocities and applies precomputed constants --
+//     the part of the algorithm that is inherently sequential within an env
+//     (environments are disjoint islands, reference physics.py:5-9).
+//
+// All per-env working state lives in shared memory, item-major / env-minor
+// with an odd stride (conflict-free per-thread columns and conflict-free
+// cooperative row loads).  The arithmetic follows the reference Scene.step
+// (/root/reference/pkg/src/batchsim/physics.py:538-592) row for row; each
+// function cites the lines it restates.  Positions are env-local.
+#pragma once
+
+#include "bsim_math.cuh"
+#include "../../include/batchsim_b200.h"
+
+#if defined(__CUDA_ARCH__)
+#define BS_SYNC() __syncthreads()
+#else
+#define BS_SYNC() ((void)0)
+#endif
+
+namespace bsim {
+
+// float / double variants of the C structs
+template <class R> struct Abi;
+template <> struct Abi<float> {
+    using Joint = bsim_joint_t;
+    using Tendon = bsim_tendon_t;
+    using TElem = bsim_tendon_elem_t;
+    using Params = bsim_params_t;
+    using State = bsim_state_t;
+};
+template <> struct Abi<double> {
+    using Joint = bsim_joint64_t;
+    using Tendon = bsim_tendon64_t;
+    using TElem = bsim_tendon_elem64_t;
+    using Params = bsim_params64_t;
+    using State = bsim_state64_t;
+};
+
+// ---------------------------------------------------------------- items
+// per body: pose, velocity, TGS deltas, world inverse inertia (sym), inverse
+// mass, effective pose scratch
+enum { BP = 0, BQ = 3, BV = 7, BW = 10, BDP = 13, BDA = 16, BI = 19, BM = 25, BPE = 26, BQE = 29,
+       BODY_ITEMS = 33 };
+// per joint: geometry, staged params, and the row constants of phase A
+enum {
+    JRP = 0, JRC = 3, JPE = 6, JRE = 9, JAX = 12, JQ0 = 15,          // geometry (freeze/refresh)
+    JSTIFF = 16, JDAMP = 17, JARM = 18, JFRIC = 19, JLO = 20, JHI = 21, // per-env parameters
+    JKI = 22,   // point-3: K^-1 ; prismatic-perp: T^T K^-1 T            (sym, 6)
+    JMC = 28,   // Ic [rc]x  (impulse at the child anchor -> d omega_c)  (3x3, 9)
+    JMP = 37,   // Ip [rp]x                                              (3x3, 9)
+    JHC = 46,   // Ic T^T K^-1 T  (angular rows)                         (3x3, 9)
+    JHP = 55,   // Ip T^T K^-1 T                                         (3x3, 9)
+    JX1 = 64, JX2 = 67,   // axis-row jacobians on omega_c / omega_p
+    JY1 = 70, JY2 = 73,   // axis-row responses on omega_c / omega_p per unit impulse
+    JMEFF = 76, JOINT_ITEMS = 77
+};
+// per plane contact slot
+enum { CR = 0, CD0 = 3, CREST = 4, CLN = 5, CLT = 6, CTE = 8, CACT = 10, CPT = 11, CXN = 14, CX1 = 17,
+       CX2 = 20, CIXN = 23, CIX1 = 26, CIX2 = 29, CMN = 32, CM1 = 33, CM2 = 34, PLANE_ITEMS = 35 };
+// per sphere-sphere pair slot
+enum { QR = 0, QRA = 3, QN = 6, QT1 = 9, QT2 = 12, QD0 = 15, QREST = 16, QLN = 17, QLT = 18, QACT = 20,
+       QPT = 21, QXN = 24, QX1 = 27, QX2 = 30, QYN = 33, QY1 = 36, QY2 = 39, QIXN = 42, QIX1 = 45,
+       QIX2 = 48, QIYN = 51, QIY1 = 54, QIY2 = 57, QMN = 60, QM1 = 61, QM2 = 62, PAIR_ITEMS = 63 };
+// per dof: impulse accumulator, start-of-step readout, staged controls
+enum { DIMP = 0, DQ0 = 1, DPT = 2, DVT = 3, DF = 4, DMODE = 5, DOF_ITEMS = 6 };
+// per env
+enum { EMUS = 0, EMUD = 1, EGX = 2, EGY = 3, EGZ = 4, EBAD = 5, ENV_ITEMS = 6 };
+
+struct Dims {
+    int E, A, B, D, J, P, Q, S, T;
+    int o_body, o_joint, o_plane, o_pair, o_anchor, o_dof, o_env, items;
+};
+
+BS_HD Dims make_dims(const bsim_layout_t &L) {
+    Dims d;
+    d.E = L.num_envs; d.A = L.actors_per_env; d.B = L.bodies_per_env; d.D = L.dofs_per_env;
+    d.J = L.joints_per_env; d.P = L.planes_per_env; d.Q = L.pairs_per_env;
+    d.S = L.sensors_per_env; d.T = L.tendons_per_env;
+    d.o_body = 0;
+    d.o_joint = d.o_body + BODY_ITEMS * d.B;
+    d.o_plane = d.o_joint + JOINT_ITEMS * d.J;
+    d.o_pair = d.o_plane + PLANE_ITEMS * d.P;
+    d.o_anchor = d.o_pair + PAIR_ITEMS * d.Q;
+    d.o_dof = d.o_anchor + 3 * d.P;
+    d.o_env = d.o_dof + DOF_ITEMS * d.D;
+    d.items = d.o_env + ENV_ITEMS;
+    return d;
+}
+
+// One env's column of the shared workspace.
+template <class R> struct Ws {
+    R *base;
+    int stride;
+    BS_HD R &at(int i) const { return base[i * stride]; }
+    BS_HD V3<R> l3(int i) const { return V3<R>{at(i), at(i + 1), at(i + 2)}; }
+    BS_HD void s3(int i, V3<R> v) const { at(i) = v.x; at(i + 1) = v.y; at(i + 2) = v.z; }
+    BS_HD Q4<R> l4(int i) const { return Q4<R>{at(i), at(i + 1), at(i + 2), at(i + 3)}; }
+    BS_HD void s4(int i, Q4<R> q) const { at(i) = q.x; at(i + 1) = q.y; at(i + 2) = q.z; at(i + 3) = q.w; }
+    BS_HD S3<R> lS(int i) const { return S3<R>{at(i), at(i + 1), at(i + 2), at(i + 3), at(i + 4), at(i + 5)}; }
+    BS_HD void sS(int i, const S3<R> &m) const {
+        at(i) = m.xx; at(i + 1) = m.xy; at(i + 2) = m.xz; at(i + 3) = m.yy; at(i + 4) = m.yz; at(i + 5) = m.zz;
+    }
+    BS_HD M3<R> lM(int i) const {
+        return M3<R>{at(i), at(i + 1), at(i + 2), at(i + 3), at(i + 4), at(i + 5), at(i + 6), at(i + 7), at(i + 8)};
+    }
+    BS_HD void sM(int i, const M3<R> &m) const {
+        at(i) = m.a00; at(i + 1) = m.a01; at(i + 2) = m.a02; at(i + 3) = m.a10; at(i + 4) = m.a11;
+        at(i + 5) = m.a12; at(i + 6) = m.a20; at(i + 7) = m.a21; at(i + 8) = m.a22;
+    }
+};
+
+template <class R> struct Ctx {
+    using Joint = typename Abi<R>::Joint;
+    using Tendon = typename Abi<R>::Tendon;
+    using TElem = typename Abi<R>::TElem;
+    bsim_layout_t L;
+    typename Abi<R>::Params p;
+    typename Abi<R>::State s;
+    Dims d;
+    const Joint *joints;   // shared-memory copy (device) or the host table
+    BS_HD const Tendon &tendon(int i) const { return reinterpret_cast<const Tendon *>(L.tendons)[i]; }
+    BS_HD const TElem *elems() const { return reinterpret_cast<const TElem *>(L.tendon_elems); }
+};
+
+BS_HD int ib(const Dims &d, int b, int item) { return d.o_body + b * BODY_ITEMS + item; }
+BS_HD int ij(const Dims &d, int j, int item) { return d.o_joint + j * JOINT_ITEMS + item; }
+BS_HD int ipl(const Dims &d, int i, int item) { return d.o_plane + i * PLANE_ITEMS + item; }
+BS_HD int ipr(const Dims &d, int i, int item) { return d.o_pair + i * PAIR_ITEMS + item; }
+BS_HD int idf(const Dims &d, int k, int item) { return d.o_dof + k * DOF_ITEMS + item; }
+
+template <class R> BS_HD V3<R> jv3(const R *a) { return V3<R>{a[0], a[1], a[2]}; }
+template <class R> BS_HD Q4<R> jq4(const R *a) { return Q4<R>{a[0], a[1], a[2], a[3]}; }
+
+// CTA-level view: thread `tid` of `nth`, envs [e0, e0 + ne) in the workspace.
+template <class R> struct Grp {
+    R *ws;
+    int stride, e0, ne, tid, nth;
+    BS_HD Ws<R> env(int el) const { return Ws<R>{ws + el, stride}; }
+};
+
+// ====================================================== phase A pieces
+// Per-env parameters / controls the rows reuse every pass (read once / step).
+template <class R> BS_HD void stage_env(const Ctx<R> &c, const Ws<R> &w, int e) {
+    const Dims &d = c.d;
+    const auto &s = c.s;
+    w.at(d.o_env + EMUS) = s.mu_static[e];
+    w.at(d.o_env + EMUD) = s.mu_dynamic[e];
+    w.at(d.o_env + EGX) = s.gravity[3 * (size_t)e];
+    w.at(d.o_env + EGY) = s.gravity[3 * (size_t)e + 1];
+    w.at(d.o_env + EGZ) = s.gravity[3 * (size_t)e + 2];
+    w.at(d.o_env + EBAD) = R(0);
+}
+template <class R> BS_HD void stage_joint(const Ctx<R> &c, const Ws<R> &w, int e, int j) {
+    const Dims &d = c.d;
+    size_t o = (size_t)j * d.E + e;
+    w.at(ij(d, j, JSTIFF)) = c.s.joint_stiffness[o];
+    w.at(ij(d, j, JDAMP)) = c.s.joint_damping[o];
+    w.at(ij(d, j, JARM)) = c.s.joint_armature[o];
+    w.at(ij(d, j, JFRIC)) = c.s.joint_friction[o];
+    w.at(ij(d, j, JLO)) = c.s.joint_limit_lo[o];
+    w.at(ij(d, j, JHI)) = c.s.joint_limit_hi[o];
+}
+template <class R> BS_HD void stage_dof(const Ctx<R> &c, const Ws<R> &w, int e, int k) {
+    const Dims &d = c.d;
+    size_t o = (size_t)e * d.D + k;
+    w.at(idf(d, k, DPT)) = c.s.ctrl_dof_pos_target[o];
+    w.at(idf(d, k, DVT)) = c.s.ctrl_dof_vel_target[o];
+    w.at(idf(d, k, DF)) = c.s.ctrl_dof_force[o];
+    w.at(idf(d, k, DMODE)) = (R)c.s.dof_mode[o];
+}
+
+// world inverse inertia of body b from the pose at `qitem` (physics.py:594-596)
+template <class R> BS_HD void body_inertia(const Ctx<R> &c, const Ws<R> &w, int e, int b, int qitem) {
+    V3<R> d = jv3(c.s.inv_inertia_local + 3 * ((size_t)e * c.d.B + b));
+    w.sS(ib(c.d, b, BI), world_inertia(w.l4(ib(c.d, b, qitem)), d));
+}
+
+// external forces on body b (physics.py:545-552) -- gravity, clipped body
+// force and torque (the torque needs the start-of-step world inertia)
+template <class R> BS_HD void body_external(const Ctx<R> &c, const Ws<R> &w, int e, int b) {
+    const Dims &d = c.d;
+    const R dt = c.p.dt, mf = c.p.max_force;
+    R im = w.at(ib(d, b, BM));
+    const R *f = c.s.ctrl_body_force + 3 * ((size_t)e * d.B + b);
+    const R *tq = c.s.ctrl_body_torque + 3 * ((size_t)e * d.B + b);
+    V3<R> v = w.l3(ib(d, b, BV));
+    if (im > R(0)) v = v + v3(w.at(d.o_env + EGX), w.at(d.o_env + EGY), w.at(d.o_env + EGZ)) * dt;
+    v = v + v3(clampr(f[0], -mf, mf) * dt * im, clampr(f[1], -mf, mf) * dt * im, clampr(f[2], -mf, mf) * dt * im);
+    w.s3(ib(d, b, BV), v);
+    V3<R> t = v3(clampr(tq[0], -mf, mf), clampr(tq[1], -mf, mf), clampr(tq[2], -mf, mf));
+    w.s3(ib(d, b, BW), w.l3(ib(d, b, BW)) + smul(w.lS(ib(d, b, BI)), t) * dt);
+}
+
+// Reduced coordinates of joint j from the pose/velocity in the workspace
+// (physics.py:427-459).  Writes q[k], qd[k] for its 1 or 3 DOFs.
+template <class R> BS_HD int joint_dofs(const Ctx<R> &c, const Ws<R> &w, int j, R *q, R *qd) {
+    const auto &jt = c.joints[j];
+    const Dims &d = c.d;
+    int p = jt.parent, ch = jt.child;
+    Q4<R> qp = w.l4(ib(d, p, BQ)), qc = w.l4(ib(d, ch, BQ));
+    Q4<R> jqp = qmul(qp, jq4(jt.origin_quat)), jqc = qmul(qc, jq4(jt.child_quat));
+    V3<R> wp = w.l3(ib(d, p, BW)), wc = w.l3(ib(d, ch, BW));
+    if (jt.kind == BSIM_REVOLUTE) {
+        Q4<R> qr = qmul(qconj(jqp), jqc);
+        V3<R> ax = jv3(jt.axis);
+        q[0] = wrap_pi(R(2) * r_atan2(dot(qvec(qr), ax), qr.w));
+        qd[0] = dot(qrot(jqp, ax), wc - wp);
+        return 1;
+    }
+    if (jt.kind == BSIM_PRISMATIC) {
+        V3<R> rp = qrot(qp, jv3(jt.origin_pos)), rc = qrot(qc, jv3(jt.child_pos));
+        V3<R> sep = (w.l3(ib(d, ch, BP)) - w.l3(ib(d, p, BP))) + (rc - rp);
+        V3<R> aw = qrot(jqp, jv3(jt.axis));
+        q[0] = dot(aw, sep);
+        V3<R> vap = w.l3(ib(d, p, BV)) + cross(wp, rp), vac = w.l3(ib(d, ch, BV)) + cross(wc, rc);
+        qd[0] = dot(aw, vac - vap);
+        return 1;
+    }
+    if (jt.kind == BSIM_SPHERICAL) {
+        Q4<R> qr = qmul(qconj(jqp), jqc);
+        V3<R> rv = qlog(qr);
+        V3<R> wr = qrot(qconj(jqp), wc - wp);
+        q[0] = rv.x; q[1] = rv.y; q[2] = rv.z;
+        qd[0] = wr.x; qd[1] = wr.y; qd[2] = wr.z;
+        return 3;
+    }
+    return 0;
+}
+
+// Anchor arms, errors and axis of joint j from the pose at (pitem, qitem)
+// (freeze physics.py:660-680, refresh 733-756).
+template <class R>
+BS_HD void joint_geometry(const Ctx<R> &c, const Ws<R> &w, int j, int pitem, int qitem, bool refresh_q0) {
+    const Dims &d = c.d;
+    const auto &jt = c.joints[j];
+    int p = jt.parent, ch = jt.child;
+    Q4<R> qp = w.l4(ib(d, p, qitem)), qc = w.l4(ib(d, ch, qitem));
+    Q4<R> jqp = qmul(qp, jq4(jt.origin_quat)), jqc = qmul(qc, jq4(jt.child_quat));
+    V3<R> rp = qrot(qp, jv3(jt.origin_pos)), rc = qrot(qc, jv3(jt.child_pos));
+    // ac - ap with the body-origin difference taken first (env-local)
+    V3<R> perr = (w.l3(ib(d, ch, pitem)) - w.l3(ib(d, p, pitem))) + (rc - rp);
+    Q4<R> qe = qmul(jqc, qconj(jqp));
+    R sg = signr(qe.w);
+    V3<R> aw = qrot(jqp, jv3(jt.axis));
+    w.s3(ij(d, j, JRP), rp);
+    w.s3(ij(d, j, JRC), rc);
+    w.s3(ij(d, j, JPE), perr);
+    w.s3(ij(d, j, JRE), qvec(qe) * (R(2) * sg));
+    w.s3(ij(d, j, JAX), aw);
+    if (refresh_q0 && jt.dof >= 0) {
+        if (jt.kind == BSIM_REVOLUTE) {
+            Q4<R> qr = qmul(qconj(jqp), jqc);
+            w.at(ij(d, j, JQ0)) = wrap_pi(R(2) * r_atan2(dot(qvec(qr), jv3(jt.axis)), qr.w));
+        } else if (jt.kind == BSIM_PRISMATIC) {
+            w.at(ij(d, j, JQ0)) = dot(aw, perr);
+        }
+    }
+}
+
+// Velocity-independent constants of every row of joint j (needs the current
+// world inverse inertias): the algebra of physics.py:777-928 with everything
+// that does not involve a velocity hoisted out of the serial sweep.
+template <class R> BS_HD void joint_constants(const Ctx<R> &c, const Ws<R> &w, int j) {
+    const Dims &d = c.d;
+    const auto &jt = c.joints[j];
+    int p = jt.parent, ch = jt.child;
+    R mp = w.at(ib(d, p, BM)), mc = w.at(ib(d, ch, BM));
+    S3<R> Ip = w.lS(ib(d, p, BI)), Ic = w.lS(ib(d, ch, BI));
+    V3<R> rp = w.l3(ij(d, j, JRP)), rc = w.l3(ij(d, j, JRC)), a = w.l3(ij(d, j, JAX));
+    const int kind = jt.kind;
+    // linear block: point-3 (revolute/spherical/fixed, 872-890) or the
+    // prismatic perpendicular pair (908-928)
+    if (kind != BSIM_PRISMATIC) {
+        R m = mp + mc;
+        S3<R> K{m, R(0), R(0), m, R(0), m};
+        add_rIr(K, rp, Ip);
+        add_rIr(K, rc, Ic);
+        w.sS(ij(d, j, JKI), sinv(K));
+    } else {
+        V3<R> t1, t2;
+        tangents(a, t1, t2);
+        R m = mp + mc;
+        V3<R> p1 = cross(rp, t1), p2 = cross(rp, t2), c1 = cross(rc, t1), c2 = cross(rc, t2);
+        V3<R> Ip1 = smul(Ip, p1), Ip2 = smul(Ip, p2), Ic1 = smul(Ic, c1), Ic2 = smul(Ic, c2);
+        R k00 = dot(t1, t1) * m + dot(p1, Ip1) + dot(c1, Ic1);
+        R k01 = dot(t1, t2) * m + dot(p1, Ip2) + dot(c1, Ic2);
+        R k11 = dot(t2, t2) * m + dot(p2, Ip2) + dot(c2, Ic2);
+        w.sS(ij(d, j, JKI), proj2(t1, t2, k00, k01, k11));
+    }
+    w.sM(ij(d, j, JMC), mskew(Ic, rc));
+    w.sM(ij(d, j, JMP), mskew(Ip, rp));
+    // angular block (892-906): G = T^T (T Isum T^T)^-1 T
+    if (kind != BSIM_SPHERICAL) {
+        V3<R> t1, t2;
+        tangents(a, t1, t2);
+        S3<R> Isum = sadd(Ip, Ic);
+        S3<R> G;
+        if (kind == BSIM_REVOLUTE) {
+            V3<R> i1 = smul(Isum, t1), i2 = smul(Isum, t2);
+            G = proj2(t1, t2, dot(t1, i1), dot(t1, i2), dot(t2, i2));
+        } else {
+            G = proj3(t1, t2, a, Isum);
+        }
+        w.sM(ij(d, j, JHC), smm(Ic, G));
+        w.sM(ij(d, j, JHP), smm(Ip, G));
+    }
+    // axis rows: drive (812-848) and limit (850-870), meff (777-788)
+    if (jt.dof >= 0 && kind != BSIM_SPHERICAL) {
+        R k;
+        V3<R> x1, x2;
+        if (kind == BSIM_REVOLUTE) {
+            x1 = a;
+            x2 = a;
+            k = dot(a, smul(sadd(Ip, Ic), a));
+        } else {
+            x1 = cross(rc, a);
+            x2 = cross(rp, a);
+            k = mp + mc + dot(x2, smul(Ip, x2)) + dot(x1, smul(Ic, x1));
+        }
+        w.s3(ij(d, j, JX1), x1);
+        w.s3(ij(d, j, JX2), x2);
+        w.s3(ij(d, j, JY1), smul(Ic, x1));
+        w.s3(ij(d, j, JY2), smul(Ip, x2));
+        w.at(ij(d, j, JMEFF)) = R(1) / r_max(k, R(1e-12));
+    }
+}
+
+// Plane contact slot i at freeze (physics.py:467-479, 683-697).
+template <class R> BS_HD void plane_freeze(const Ctx<R> &c, const Ws<R> &w, int e, int i) {
+    const Dims &d = c.d;
+    const auto &p = c.p;
+    int b = c.L.plane_body[i];
+    const R *off = c.s.plane_off + 3 * ((size_t)i * d.E + e);
+    R rad = c.s.plane_rad[(size_t)i * d.E + e];
+    V3<R> arm = qrot(w.l4(ib(d, b, BQ)), jv3(off));
+    V3<R> pos = w.l3(ib(d, b, BP));
+    R gap = (pos.z + arm.z) - rad;
+    R depth = p.rest_offset - gap;
+    V3<R> r = v3(arm.x, arm.y, arm.z - rad);
+    V3<R> point = pos + r;
+    R ax = w.at(d.o_anchor + 3 * i), ay = w.at(d.o_anchor + 3 * i + 1);
+    bool has = !(ax != ax);
+    w.at(ipl(d, i, CTE)) = has ? point.x - ax : R(0);
+    w.at(ipl(d, i, CTE + 1)) = has ? point.y - ay : R(0);
+    V3<R> v = w.l3(ib(d, b, BV)) + cross(w.l3(ib(d, b, BW)), r);
+    R vn = v.z;
+    w.s3(ipl(d, i, CR), r);
+    w.s3(ipl(d, i, CPT), point);
+    w.at(ipl(d, i, CD0)) = depth;
+    w.at(ipl(d, i, CREST)) = vn < -p.bounce_threshold ? -p.restitution * vn : R(0);
+    w.at(ipl(d, i, CACT)) = depth > -p.solver_offset_slop ? R(1) : R(0);
+    w.at(ipl(d, i, CLN)) = R(0);
+    w.at(ipl(d, i, CLT)) = R(0);
+    w.at(ipl(d, i, CLT + 1)) = R(0);
+    // plane normal z: tangents (0,-1,0) and (1,0,0) (physics.py:131-137)
+    w.s3(ipl(d, i, CXN), cross(r, v3(R(0), R(0), R(1))));
+    w.s3(ipl(d, i, CX1), cross(r, v3(R(0), R(-1), R(0))));
+    w.s3(ipl(d, i, CX2), cross(r, v3(R(1), R(0), R(0))));
+}
+
+// Sphere-sphere pair slot i at freeze (physics.py:481-497, 698-712).
+template <class R> BS_HD void pair_freeze(const Ctx<R> &c, const Ws<R> &w, int e, int i) {
+    const Dims &d = c.d;
+    const auto &p = c.p;
+    int pa = c.L.pair_body[2 * i], pb = c.L.pair_body[2 * i + 1];
+    const R *off = c.s.pair_off + 6 * ((size_t)i * d.E + e);
+    const R *rr = c.s.pair_rad + 2 * ((size_t)i * d.E + e);
+    V3<R> arma = qrot(w.l4(ib(d, pa, BQ)), jv3(off));
+    V3<R> armb = qrot(w.l4(ib(d, pb, BQ)), jv3(off + 3));
+    V3<R> pa0 = w.l3(ib(d, pa, BP));
+    V3<R> dd = (w.l3(ib(d, pb, BP)) - pa0) + (armb - arma);
+    R dist = norm(dd);
+    R dn = dist > R(1e-12) ? dist : R(1);
+    V3<R> n = v3(dd.x / dn, dd.y / dn, dd.z / dn);
+    R gap = dist - (rr[0] + rr[1]);
+    R depth = p.rest_offset - gap;
+    V3<R> ra = arma + n * (rr[0] + R(0.5) * gap);
+    V3<R> r = (pa0 - w.l3(ib(d, pb, BP))) + ra;
+    V3<R> va = w.l3(ib(d, pa, BV)) + cross(w.l3(ib(d, pa, BW)), ra);
+    V3<R> vb = w.l3(ib(d, pb, BV)) + cross(w.l3(ib(d, pb, BW)), r);
+    R vn = dot(n, vb - va);
+    V3<R> t1, t2;
+    tangents(n, t1, t2);
+    w.s3(ipr(d, i, QR), r);
+    w.s3(ipr(d, i, QRA), ra);
+    w.s3(ipr(d, i, QN), n);
+    w.s3(ipr(d, i, QT1), t1);
+    w.s3(ipr(d, i, QT2), t2);
+    w.s3(ipr(d, i, QPT), pa0 + ra);
+    w.at(ipr(d, i, QD0)) = depth;
+    w.at(ipr(d, i, QREST)) = vn < -p.bounce_threshold ? -p.restitution * vn : R(0);
+    w.at(ipr(d, i, QACT)) = depth > -p.solver_offset_slop ? R(1) : R(0);
+    w.at(ipr(d, i, QLN)) = R(0);
+    w.at(ipr(d, i, QLT)) = R(0);
+    w.at(ipr(d, i, QLT + 1)) = R(0);
+    w.s3(ipr(d, i, QXN), cross(r, n));
+    w.s3(ipr(d, i, QX1), cross(r, t1));
+    w.s3(ipr(d, i, QX2), cross(r, t2));
+    w.s3(ipr(d, i, QYN), cross(ra, n));
+    w.s3(ipr(d, i, QY1), cross(ra, t1));
+    w.s3(ipr(d, i, QY2), cross(ra, t2));
+}
+
+// contact row constants from the current inertia (physics.py:993-1006)
+template <class R> BS_HD void plane_constants(const Ctx<R> &c, const Ws<R> &w, int i) {
+    const Dims &d = c.d;
+    int b = c.L.plane_body[i];
+    R im = w.at(ib(d, b, BM));
+    S3<R> I = w.lS(ib(d, b, BI));
+    V3<R> xn = w.l3(ipl(d, i, CXN)), x1 = w.l3(ipl(d, i, CX1)), x2 = w.l3(ipl(d, i, CX2));
+    V3<R> in = smul(I, xn), i1 = smul(I, x1), i2 = smul(I, x2);
+    w.s3(ipl(d, i, CIXN), in);
+    w.s3(ipl(d, i, CIX1), i1);
+    w.s3(ipl(d, i, CIX2), i2);
+    w.at(ipl(d, i, CMN)) = R(1) / r_max(im + dot(xn, in), R(1e-12));
+    w.at(ipl(d, i, CM1)) = R(1) / r_max(im + dot(x1, i1), R(1e-12));
+    w.at(ipl(d, i, CM2)) = R(1) / r_max(im + dot(x2, i2), R(1e-12));
+}
+template <class R> BS_HD void pair_constants(const Ctx<R> &c, const Ws<R> &w, int i) {
+    const Dims &d = c.d;
+    int pa = c.L.pair_body[2 * i], pb = c.L.pair_body[2 * i + 1];
+    R ma = w.at(ib(d, pa, BM)), mb = w.at(ib(d, pb, BM));
+    S3<R> Ia = w.lS(ib(d, pa, BI)), Ib = w.lS(ib(d, pb, BI));
+    V3<R> xs[3] = {w.l3(ipr(d, i, QXN)), w.l3(ipr(d, i, QX1)), w.l3(ipr(d, i, QX2))};
+    V3<R> ys[3] = {w.l3(ipr(d, i, QYN)), w.l3(ipr(d, i, QY1)), w.l3(ipr(d, i, QY2))};
+    const int IX[3] = {QIXN, QIX1, QIX2}, IY[3] = {QIYN, QIY1, QIY2}, MM[3] = {QMN, QM1, QM2};
+    for (int k = 0; k < 3; ++k) {
+        V3<R> ix = smul(Ib, xs[k]), iy = smul(Ia, ys[k]);
+        w.s3(ipr(d, i, IX[k]), ix);
+        w.s3(ipr(d, i, IY[k]), iy);
+        w.at(ipr(d, i, MM[k])) = R(1) / r_max(ma + mb + dot(ys[k], iy) + dot(xs[k], ix), R(1e-12));
+    }
+}
+
+// ====================================================== phase B: the sweep
+// PD drive / direct actuation / joint friction (physics.py:812-848)
+template <class R> BS_HD void row_drive(const Ctx<R> &c, const Ws<R> &w, int j, R h) {
+    const auto &jt = c.joints[j];
+    const Dims &d = c.d;
+    const bool lin = jt.kind == BSIM_PRISMATIC;
+    const int p = jt.parent, ch = jt.child;
+    V3<R> wc = w.l3(ib(d, ch, BW)), wp = w.l3(ib(d, p, BW));
+    R qd = dot(w.l3(ij(d, j, JX1)), wc) - dot(w.l3(ij(d, j, JX2)), wp);
+    V3<R> a = w.l3(ij(d, j, JAX));
+    V3<R> vc, vp;
+    if (lin) {
+        vc = w.l3(ib(d, ch, BV));
+        vp = w.l3(ib(d, p, BV));
+        qd = qd + dot(a, vc - vp);
+    }
+    const R meff = w.at(ij(d, j, JMEFF));
+    const int mode = (int)w.at(idf(d, jt.dof, DMODE));
+    const R ia = meff + w.at(ij(d, j, JARM));
+    const R mf = c.p.max_force;
+    R tau = clampr(w.at(idf(d, jt.dof, DF)), -mf, mf);
+    R lam = mode == BSIM_MODE_FORCE ? tau * h * meff / ia : R(0);
+    R kk = mode == BSIM_MODE_POSITION ? w.at(ij(d, j, JSTIFF)) : R(0);
+    R cc = mode == BSIM_MODE_FORCE ? R(0) : w.at(ij(d, j, JDAMP));
+    R err = w.at(idf(d, jt.dof, DPT)) - w.at(ij(d, j, JQ0));
+    R dv = w.at(idf(d, jt.dof, DVT)) - qd;
+    R lpd = h * (kk * (err - h * qd) + cc * dv) / (R(1) + h * (h * kk + cc) / ia);
+    lam = lam + clampr(lpd, -mf * h, mf * h);
+    R fr = w.at(ij(d, j, JFRIC));
+    if (fr > R(0)) lam = lam + clampr(-qd * meff, -fr * h, fr * h);
+    w.s3(ib(d, ch, BW), wc + w.l3(ij(d, j, JY1)) * lam);
+    w.s3(ib(d, p, BW), wp - w.l3(ij(d, j, JY2)) * lam);
+    if (lin) {
+        w.s3(ib(d, ch, BV), vc + a * (lam * w.at(ib(d, ch, BM))));
+        w.s3(ib(d, p, BV), vp - a * (lam * w.at(ib(d, p, BM))));
+    }
+    w.at(idf(d, jt.dof, DIMP)) += lam;
+}
+
+// one-sided limit (physics.py:850-870)
+template <class R> BS_HD void row_limit(const Ctx<R> &c, const Ws<R> &w, int j, R h, bool biased) {
+    const auto &jt = c.joints[j];
+    const Dims &d = c.d;
+    R lo = w.at(ij(d, j, JLO)), hi = w.at(ij(d, j, JHI));
+    R q = biased ? w.at(ij(d, j, JQ0)) : w.at(idf(d, jt.dof, DQ0));
+    if (!(q < lo) && !(q > hi)) return;
+    const bool lin = jt.kind == BSIM_PRISMATIC;
+    const int p = jt.parent, ch = jt.child;
+    V3<R> wc = w.l3(ib(d, ch, BW)), wp = w.l3(ib(d, p, BW));
+    R qd = dot(w.l3(ij(d, j, JX1)), wc) - dot(w.l3(ij(d, j, JX2)), wp);
+    V3<R> a = w.l3(ij(d, j, JAX));
+    V3<R> vc, vp;
+    if (lin) {
+        vc = w.l3(ib(d, ch, BV));
+        vp = w.l3(ib(d, p, BV));
+        qd = qd + dot(a, vc - vp);
+    }
+    R meff = w.at(ij(d, j, JMEFF));
+    R lam = R(0);
+    if (q < lo) lam = r_max(meff * ((biased ? r_max(lo - q, R(0)) / h : R(0)) - qd), R(0));
+    if (q > hi) lam = -r_max(meff * ((biased ? r_max(q - hi, R(0)) / h : R(0)) + qd), R(0));
+    w.s3(ib(d, ch, BW), wc + w.l3(ij(d, j, JY1)) * lam);
+    w.s3(ib(d, p, BW), wp - w.l3(ij(d, j, JY2)) * lam);
+    if (lin) {
+        w.s3(ib(d, ch, BV), vc + a * (lam * w.at(ib(d, ch, BM))));
+        w.s3(ib(d, p, BV), vp - a * (lam * w.at(ib(d, p, BM))));
+    }
+    w.at(idf(d, jt.dof, DIMP)) += lam;
+}
+
+// point-3 (872-890) or prismatic perpendicular pair (908-928): P = G d
+template <class R> BS_HD void row_linear(const Ctx<R> &c, const Ws<R> &w, int j, R h, bool biased) {
+    const auto &jt = c.joints[j];
+    const Dims &d = c.d;
+    const int p = jt.parent, ch = jt.child;
+    V3<R> vc = w.l3(ib(d, ch, BV)), wc = w.l3(ib(d, ch, BW));
+    V3<R> vp = w.l3(ib(d, p, BV)), wp = w.l3(ib(d, p, BW));
+    V3<R> rel = (vc + cross(wc, w.l3(ij(d, j, JRC)))) - (vp + cross(wp, w.l3(ij(d, j, JRP))));
+    V3<R> tgt = zero3<R>();
+    if (biased) {
+        V3<R> pe = w.l3(ij(d, j, JPE));
+        tgt = v3(-pe.x / h, -pe.y / h, -pe.z / h);
+    }
+    V3<R> P = smul(w.lS(ij(d, j, JKI)), tgt - rel);
+    w.s3(ib(d, ch, BV), vc + P * w.at(ib(d, ch, BM)));
+    w.s3(ib(d, ch, BW), wc + mmul(w.lM(ij(d, j, JMC)), P));
+    w.s3(ib(d, p, BV), vp - P * w.at(ib(d, p, BM)));
+    w.s3(ib(d, p, BW), wp - mmul(w.lM(ij(d, j, JMP)), P));
+}
+
+// angular rows (892-906): omega_c += Hc d, omega_p -= Hp d
+template <class R> BS_HD void row_angular(const Ctx<R> &c, const Ws<R> &w, int j, R h, bool biased) {
+    const auto &jt = c.joints[j];
+    const Dims &d = c.d;
+    const int p = jt.parent, ch = jt.child;
+    V3<R> wc = w.l3(ib(d, ch, BW)), wp = w.l3(ib(d, p, BW));
+    V3<R> tgt = zero3<R>();
+    if (biased) {
+        V3<R> re = w.l3(ij(d, j, JRE));
+        tgt = v3(-re.x / h, -re.y / h, -re.z / h);
+    }
+    V3<R> dv = tgt - (wc - wp);
+    w.s3(ib(d, ch, BW), wc + mmul(w.lM(ij(d, j, JHC)), dv));
+    w.s3(ib(d, p, BW), wp - mmul(w.lM(ij(d, j, JHP)), dv));
+}
+
+// plane contact row (930-983) with the plane's fixed normal/tangents
+template <class R> BS_HD void row_plane(const Ctx<R> &c, const Ws<R> &w, int i, bool biased) {
+    const Dims &d = c.d;
+    if (w.at(ipl(d, i, CACT)) == R(0)) return;
+    const R dt = c.p.dt;
+    const int b = c.L.plane_body[i];
+    const R im = w.at(ib(d, b, BM));
+    V3<R> v = w.l3(ib(d, b, BV)), om = w.l3(ib(d, b, BW));
+    R vn = v.z + dot(w.l3(ipl(d, i, CXN)), om);
+    R depth = w.at(ipl(d, i, CD0));
+    if (biased) depth = depth + w.at(ib(d, b, BDP) + 2) * R(-1);
+    R bias = biased ? c.p.max_bias * r_max(depth, R(0)) / dt : R(0);
+    R target = r_max(w.at(ipl(d, i, CREST)), bias);
+    R lam_n = w.at(ipl(d, i, CLN));
+    R dl = w.at(ipl(d, i, CMN)) * (target - vn);
+    R nl = r_max(lam_n + dl, R(0));
+    dl = nl - lam_n;
+    lam_n = lam_n + dl;
+    w.at(ipl(d, i, CLN)) = lam_n;
+    v.z = v.z + dl * im;
+    om = om + w.l3(ipl(d, i, CIXN)) * dl;
+    // friction with t1 = (0,-1,0), t2 = (1,0,0)
+    R vt1 = -v.y + dot(w.l3(ipl(d, i, CX1)), om);
+    R vt2 = v.x + dot(w.l3(ipl(d, i, CX2)), om);
+    R mu = r_sqrt(vt1 * vt1 + vt2 * vt2) > R(1e-3) ? w.at(d.o_env + EMUD) : w.at(d.o_env + EMUS);
+    if (biased) {
+        R tex = w.at(ipl(d, i, CTE)) + w.at(ib(d, b, BDP));
+        R tey = w.at(ipl(d, i, CTE + 1)) + w.at(ib(d, b, BDP) + 1);
+        vt1 = vt1 + (-tey) / dt;
+        vt2 = vt2 + tex / dt;
+    }
+    R lt0 = w.at(ipl(d, i, CLT)), lt1 = w.at(ipl(d, i, CLT + 1));
+    R c0 = lt0 + (-w.at(ipl(d, i, CM1)) * vt1), c1 = lt1 + (-w.at(ipl(d, i, CM2)) * vt2);
+    R lim = mu * lam_n;
+    R nrm = r_sqrt(c0 * c0 + c1 * c1);
+    R sc = nrm > lim ? lim / r_max(nrm, R(1e-12)) : R(1);
+    c0 = c0 * sc;
+    c1 = c1 * sc;
+    R d0 = c0 - lt0, d1 = c1 - lt1;
+    w.at(ipl(d, i, CLT)) = lt0 + d0;
+    w.at(ipl(d, i, CLT + 1)) = lt1 + d1;
+    v.x = v.x + d1 * im;
+    v.y = v.y + (-d0) * im;
+    om = om + w.l3(ipl(d, i, CIX1)) * d0 + w.l3(ipl(d, i, CIX2)) * d1;
+    w.s3(ib(d, b, BV), v);
+    w.s3(ib(d, b, BW), om);
+}
+
+// sphere-sphere pair row (930-983, pair branches)
+template <class R> BS_HD void row_pair(const Ctx<R> &c, const Ws<R> &w, int i, bool biased) {
+    const Dims &d = c.d;
+    if (w.at(ipr(d, i, QACT)) == R(0)) return;
+    const R dt = c.p.dt;
+    const int pa = c.L.pair_body[2 * i], pb = c.L.pair_body[2 * i + 1];
+    const R ma = w.at(ib(d, pa, BM)), mb = w.at(ib(d, pb, BM));
+    V3<R> n = w.l3(ipr(d, i, QN)), t1 = w.l3(ipr(d, i, QT1)), t2 = w.l3(ipr(d, i, QT2));
+    V3<R> va = w.l3(ib(d, pa, BV)), wa = w.l3(ib(d, pa, BW));
+    V3<R> vb = w.l3(ib(d, pb, BV)), wb = w.l3(ib(d, pb, BW));
+    V3<R> xn = w.l3(ipr(d, i, QXN)), yn = w.l3(ipr(d, i, QYN));
+    R vn = dot(n, vb - va) + dot(xn, wb) - dot(yn, wa);
+    R depth = w.at(ipr(d, i, QD0));
+    if (biased) depth = depth + dot(n, w.l3(ib(d, pb, BDP)) - w.l3(ib(d, pa, BDP))) * R(-1);
+    R bias = biased ? c.p.max_bias * r_max(depth, R(0)) / dt : R(0);
+    R target = r_max(w.at(ipr(d, i, QREST)), bias);
+    R lam_n = w.at(ipr(d, i, QLN));
+    R dl = w.at(ipr(d, i, QMN)) * (target - vn);
+    R nl = r_max(lam_n + dl, R(0));
+    dl = nl - lam_n;
+    lam_n = lam_n + dl;
+    w.at(ipr(d, i, QLN)) = lam_n;
+    vb = vb + n * (dl * mb);
+    wb = wb + w.l3(ipr(d, i, QIXN)) * dl;
+    va = va - n * (dl * ma);
+    wa = wa - w.l3(ipr(d, i, QIYN)) * dl;
+    V3<R> x1 = w.l3(ipr(d, i, QX1)), x2 = w.l3(ipr(d, i, QX2));
+    V3<R> y1 = w.l3(ipr(d, i, QY1)), y2 = w.l3(ipr(d, i, QY2));
+    V3<R> dv = vb - va;
+    R vt1 = dot(t1, dv) + dot(x1, wb) - dot(y1, wa);
+    R vt2 = dot(t2, dv) + dot(x2, wb) - dot(y2, wa);
+    R mu = r_sqrt(vt1 * vt1 + vt2 * vt2) > R(1e-3) ? w.at(d.o_env + EMUD) : w.at(d.o_env + EMUS);
+    R lt0 = w.at(ipr(d, i, QLT)), lt1 = w.at(ipr(d, i, QLT + 1));
+    R c0 = lt0 + (-w.at(ipr(d, i, QM1)) * vt1), c1 = lt1 + (-w.at(ipr(d, i, QM2)) * vt2);
+    R lim = mu * lam_n;
+    R nrm = r_sqrt(c0 * c0 + c1 * c1);
+    R sc = nrm > lim ? lim / r_max(nrm, R(1e-12)) : R(1);
+    c0 = c0 * sc;
+    c1 = c1 * sc;
+    R d0 = c0 - lt0, d1 = c1 - lt1;
+    w.at(ipr(d, i, QLT)) = lt0 + d0;
+    w.at(ipr(d, i, QLT + 1)) = lt1 + d1;
+    V3<R> Q = t1 * d0 + t2 * d1;
+    vb = vb + Q * mb;
+    wb = wb + w.l3(ipr(d, i, QIX1)) * d0 + w.l3(ipr(d, i, QIX2)) * d1;
+    va = va - Q * ma;
+    wa = wa - (w.l3(ipr(d, i, QIY1)) * d0 + w.l3(ipr(d, i, QIY2)) * d1);
+    w.s3(ib(d, pa, BV), va);
+    w.s3(ib(d, pa, BW), wa);
+    w.s3(ib(d, pb, BV), vb);
+    w.s3(ib(d, pb, BW), wb);
+}
+
+// one Gauss-Seidel pass for one env (physics.py:760-775)
+template <class R> BS_HD void sweep(const Ctx<R> &c, const Ws<R> &w, R h, bool biased) {
+    const Dims &d = c.d;
+    for (int j = 0; j < d.J; ++j) {
+        const auto &jt = c.joints[j];
+        const int kind = jt.kind;
+        const bool axis = jt.dof >= 0 && kind != BSIM_SPHERICAL;
+        if (biased && axis) row_drive(c, w, j, h);
+        if (kind != BSIM_PRISMATIC) row_linear(c, w, j, h, biased);
+        if (kind != BSIM_SPHERICAL) row_angular(c, w, j, h, biased);
+        if (kind == BSIM_PRISMATIC) row_linear(c, w, j, h, biased);
+        if (axis && jt.has_limits) row_limit(c, w, j, h, biased);
+    }
+    for (int i = 0; i < d.P; ++i) row_plane(c, w, i, biased);
+    for (int i = 0; i < d.Q; ++i) row_pair(c, w, i, biased);
+}
+
+// ------------------------------------------------------------ tendons
+template <class T, class R> BS_HD R tendon_spring(const T &t, R L, R Ld) {  // tendons.py:52-62
+    R f = -t.stiffness * (L - t.rest_length) - t.damping * Ld;
+    if (t.has_limits) {
+        R below = r_max(t.limit_lo - L, R(0)), above = r_max(L - t.limit_hi, R(0));
+        f = f + t.limit_stiffness * below - t.limit_stiffness * above;
+        if (below > R(0) || above > R(0)) f = f - t.damping * Ld;
+    }
+    return f;
+}
+
+template <class R> BS_HD void add_w(const Dims &d, const Ws<R> &w, int b, V3<R> dw) {
+    w.s3(ib(d, b, BW), w.l3(ib(d, b, BW)) + dw);
+}
+template <class R> BS_HD void add_v(const Dims &d, const Ws<R> &w, int b, V3<R> dv) {
+    w.s3(ib(d, b, BV), w.l3(ib(d, b, BV)) + dv);
+}
+
+// physics.py:598-653; fixed tendons read the dof_state buffer of the previous
+// readout (physics.py:605-606), spatial tendons the current body state.
+template <class R> BS_HD void apply_tendons(const Ctx<R> &c, const Ws<R> &w, int e) {
+    const Dims &d = c.d;
+    const R dt = c.p.dt;
+    for (int ti = 0; ti < d.T; ++ti) {
+        const auto &t = c.tendon(ti);
+        const auto *el = c.elems() + t.first;
+        if (t.kind == 0) {
+            const int MAXE = 16;
+            R len[MAXE], rate[MAXE];
+            int n = t.count < MAXE ? t.count : MAXE;
+            for (int i = 0; i < n; ++i) {
+                const R *dq = c.s.dof_state + 2 * ((size_t)e * d.D + el[i].index);
+                R pl = el[i].parent >= 0 ? len[el[i].parent] : R(0);
+                R pr = el[i].parent >= 0 ? rate[el[i].parent] : R(0);
+                len[i] = pl + el[i].v[0] * dq[0];
+                rate[i] = pr + el[i].v[0] * dq[1];
+            }
+            int last = -1;   // ascending dof order (physics.py:614-620)
+            for (int pass = 0; pass < n; ++pass) {
+                int dof = 0x7fffffff;
+                for (int i = 0; i < n; ++i)
+                    if (el[i].index > last && el[i].index < dof) dof = el[i].index;
+                if (dof == 0x7fffffff) break;
+                last = dof;
+                R qf = R(0);
+                int jslot = -1;
+                for (int i = 0; i < n; ++i)
+                    if (el[i].index == dof) {
+                        qf = qf + el[i].v[0] * tendon_spring(t, len[i], rate[i]);
+                        jslot = el[i].joint;
+                    }
+                if (qf == R(0)) continue;
+                const auto &jt = c.joints[jslot];
+                int ci = jt.child, ri = t.reaction_body;
+                V3<R> aw = qrot(qmul(w.l4(ib(d, jt.parent, BQ)), jq4(jt.origin_quat)), jv3(jt.axis));
+                V3<R> P = aw * qf * dt;
+                if (jt.kind == BSIM_REVOLUTE) {
+                    add_w(d, w, ci, smul(w.lS(ib(d, ci, BI)), P));
+                    add_w(d, w, ri, -smul(w.lS(ib(d, ri, BI)), P));
+                } else {
+                    add_v(d, w, ci, P * w.at(ib(d, ci, BM)));
+                    add_v(d, w, ri, -(P * w.at(ib(d, ri, BM))));
+                }
+            }
+        } else {
+            const int MAXA = 16;
+            V3<R> pts[MAXA], vel[MAXA];
+            int n = t.count < MAXA ? t.count : MAXA;
+            for (int i = 0; i < n; ++i) {
+                int b = el[i].index;
+                V3<R> r = qrot(w.l4(ib(d, b, BQ)), v3(el[i].v[0], el[i].v[1], el[i].v[2]));
+                pts[i] = w.l3(ib(d, b, BP)) + r;
+                V3<R> rr = pts[i] - w.l3(ib(d, b, BP));
+                vel[i] = w.l3(ib(d, b, BV)) + cross(w.l3(ib(d, b, BW)), rr);
+            }
+            const int32_t *pth = c.L.spatial_paths + t.path_offset;
+            int npaths = pth[0];
+            const int MAXENT = 32;   // all entries from the pre-application state
+            V3<R> ef[MAXENT];
+            int ei[MAXENT];
+            int nent = 0;
+            const int32_t *cur = pth + 1;
+            for (int pi = 0; pi < npaths && nent + 2 <= MAXENT; ++pi) {
+                int len = cur[0];
+                const int32_t *ix = cur + 1;
+                R L = R(0), Ld = R(0);
+                for (int k = 1; k < len; ++k) {
+                    V3<R> dd = pts[ix[k]] - pts[ix[k - 1]];
+                    R dist = norm(dd);
+                    R sf = dist > R(1e-12) ? dist : R(1);
+                    L = L + el[ix[k]].v[3] * dist;
+                    Ld = Ld + el[ix[k]].v[3] * dot(vel[ix[k]] - vel[ix[k - 1]], v3(dd.x / sf, dd.y / sf, dd.z / sf));
+                }
+                R f = tendon_spring(t, L, Ld);
+                int leaf = ix[len - 1], root = ix[0];
+                V3<R> dl = pts[ix[len - 2]] - pts[leaf], dr = pts[ix[1]] - pts[root];
+                R nl = norm(dl), nr = norm(dr);
+                nl = nl > R(1e-12) ? nl : R(1);
+                nr = nr > R(1e-12) ? nr : R(1);
+                ef[nent] = v3(dl.x / nl, dl.y / nl, dl.z / nl) * -f;
+                ei[nent++] = leaf;
+                ef[nent] = v3(dr.x / nr, dr.y / nr, dr.z / nr) * -f;
+                ei[nent++] = root;
+                cur += 1 + len;
+            }
+            for (int k = 0; k < nent; ++k) {
+                int b = el[ei[k]].index;
+                V3<R> r = pts[ei[k]] - w.l3(ib(d, b, BP));
+                add_v(d, w, b, ef[k] * dt * w.at(ib(d, b, BM)));
+                add_w(d, w, b, smul(w.lS(ib(d, b, BI)), cross(r, ef[k])) * dt);
+            }
+        }
+    }
+}
+
+// ====================================================== the group step
+// Loops over (env, item) pairs distributed over the CTA's threads; on the
+// host (tid 0 of 1) they degenerate to plain sequential loops.
+#define BS_ITEMS(g, count, el, k)                                                   \
+    for (int it_ = (g).tid, n_ = (g).ne * (count); it_ < n_; it_ += (g).nth)       \
+        for (int el = it_ % (g).ne, k = it_ / (g).ne, once_ = 1; once_; once_ = 0)
+#define BS_ENVS(g, el) for (int el = (g).tid; el < (g).ne; el += (g).nth)
+
+// refresh (physics.py:718-756): optional effective pose, inertias, joint
+// geometry and all row constants
+template <class R> BS_HD void refresh_group(const Ctx<R> &c, const Grp<R> &g, bool with_deltas) {
+    const Dims &d = c.d;
+    int pitem = BP, qitem = BQ;
+    if (with_deltas) {
+        pitem = BPE;
+        qitem = BQE;
+    }
+    BS_ITEMS(g, d.B, el, b) {
+        Ws<R> w = g.env(el);
+        if (with_deltas) {
+            w.s3(ib(d, b, BPE), w.l3(ib(d, b, BP)) + w.l3(ib(d, b, BDP)));
+            w.s4(ib(d, b, BQE), qnormalize(qmul(qexp(w.l3(ib(d, b, BDA))), w.l4(ib(d, b, BQ)))));
+        }
+        body_inertia(c, w, g.e0 + el, b, qitem);
+    }
+    BS_SYNC();
+    BS_ITEMS(g, d.J, el, j) {
+        Ws<R> w = g.env(el);
+        joint_geometry(c, w, j, pitem, qitem, true);
+        joint_constants(c, w, j);
+    }
+    BS_ITEMS(g, d.P, el, i) { plane_constants(c, g.env(el), i); }
+    BS_ITEMS(g, d.Q, el, i) { pair_constants(c, g.env(el), i); }
+    BS_SYNC();
+}
+
+// Scene.step() for the CTA's envs on the resident workspace
+// (physics.py:538-592).  `write_outputs`: contact-derived outputs of this
+// step go to global memory (the last substep of a fused launch).
+template <class R> BS_HD void group_step(const Ctx<R> &c, const Grp<R> &g, bool write_outputs) {
+    const Dims &d = c.d;
+    const auto &p = c.p;
+    const R dt = p.dt;
+    const int N = p.position_iterations;
+    const R h = dt / (R)N;
+
+    // external forces, start-of-step inertia (545-555)
+    BS_ITEMS(g, d.B, el, b) {
+        Ws<R> w = g.env(el);
+        body_inertia(c, w, g.e0 + el, b, BQ);
+        body_external(c, w, g.e0 + el, b);
+        w.s3(ib(d, b, BDP), zero3<R>());   // TGS delta buffers (564-566)
+        w.s3(ib(d, b, BDA), zero3<R>());
+    }
+    BS_SYNC();
+    if (d.T) {
+        BS_ENVS(g, el) { apply_tendons(c, g.env(el), g.e0 + el); }
+        BS_SYNC();
+    }
+    const R ld = r_max(R(0), R(1) - p.linear_damping * dt), ad = r_max(R(0), R(1) - p.angular_damping * dt);
+    if (ld != R(1) || ad != R(1)) {
+        BS_ITEMS(g, d.B, el, b) {
+            Ws<R> w = g.env(el);
+            w.s3(ib(d, b, BV), w.l3(ib(d, b, BV)) * ld);
+            w.s3(ib(d, b, BW), w.l3(ib(d, b, BW)) * ad);
+        }
+        BS_SYNC();
+    }
+    // read_dof_states (557) + freeze (657-716)
+    BS_ITEMS(g, d.J, el, j) {
+        Ws<R> w = g.env(el);
+        R q[3], qd[3];
+        int n = joint_dofs(c, w, j, q, qd);
+        for (int k = 0; k < n; ++k) {
+            w.at(idf(d, c.joints[j].dof + k, DQ0)) = q[k];
+            w.at(idf(d, c.joints[j].dof + k, DIMP)) = R(0);
+        }
+        if (n == 1) w.at(ij(d, j, JQ0)) = q[0];
+        joint_geometry(c, w, j, BP, BQ, false);
+        joint_constants(c, w, j);
+    }
+    BS_ITEMS(g, d.P, el, i) {
+        Ws<R> w = g.env(el);
+        plane_freeze(c, w, g.e0 + el, i);
+        plane_constants(c, w, i);
+    }
+    BS_ITEMS(g, d.Q, el, i) {
+        Ws<R> w = g.env(el);
+        pair_freeze(c, w, g.e0 + el, i);
+        pair_constants(c, w, i);
+    }
+    BS_SYNC();
+
+    // TGS position iterations (567-572)
+    for (int k = 0; k < N; ++k) {
+        if (k) refresh_group(c, g, true);
+        BS_ENVS(g, el) { sweep(c, g.env(el), h, true); }
+        BS_SYNC();
+        BS_ITEMS(g, d.B, el, b) {
+            Ws<R> w = g.env(el);
+            w.s3(ib(d, b, BDP), w.l3(ib(d, b, BDP)) + w.l3(ib(d, b, BV)) * h);
+            w.s3(ib(d, b, BDA), w.l3(ib(d, b, BDA)) + w.l3(ib(d, b, BW)) * h);
+        }
+        BS_SYNC();
+    }
+    // integrate (574-575), refresh from the new poses, velocity passes (579-581)
+    BS_ITEMS(g, d.B, el, b) {
+        Ws<R> w = g.env(el);
+        w.s3(ib(d, b, BP), w.l3(ib(d, b, BP)) + w.l3(ib(d, b, BDP)));
+        w.s4(ib(d, b, BQ), qnormalize(qmul(qexp(w.l3(ib(d, b, BDA))), w.l4(ib(d, b, BQ)))));
+    }
+    BS_SYNC();
+    refresh_group(c, g, false);
+    for (int k = 0; k < p.velocity_iterations; ++k) {
+        BS_ENVS(g, el) { sweep(c, g.env(el), h, false); }
+        BS_SYNC();
+    }
+    // velocity clamps (584-587)
+    BS_ITEMS(g, d.B, el, b) {
+        Ws<R> w = g.env(el);
+        V3<R> lv = w.l3(ib(d, b, BV)), av = w.l3(ib(d, b, BW));
+        R sl = r_min(R(1), p.max_linear_velocity / r_max(norm(lv), R(1e-12)));
+        R sa = r_min(R(1), p.max_angular_velocity / r_max(norm(av), R(1e-12)));
+        w.s3(ib(d, b, BV), lv * sl);
+        w.s3(ib(d, b, BW), av * sa);
+    }
+    // friction anchors (1021-1033)
+    BS_ITEMS(g, d.P, el, i) {
+        Ws<R> w = g.env(el);
+        const R nanv = r_nan(R(0));
+        bool near_ = w.at(ipl(d, i, CD0)) > -p.friction_offset_threshold;
+        int a = d.o_anchor + 3 * i;
+        bool has = !(w.at(a) != w.at(a));
+        if (near_ && !has) w.s3(a, w.l3(ipl(d, i, CPT)));
+        if (!near_) w.s3(a, v3(nanv, nanv, nanv));
+    }
+    BS_SYNC();
+
+    // refresh_buffers(ctx) (1037-1071): contact wrench per body (BDP/BDA reused)
+    if (write_outputs) {
+        BS_ITEMS(g, d.B, el, b) {
+            Ws<R> w = g.env(el);
+            V3<R> F = zero3<R>(), Tq = zero3<R>();
+            for (int i = 0; i < d.P; ++i) {
+                if (c.L.plane_body[i] != b) continue;
+                V3<R> P = v3(R(0), R(0), R(1)) * w.at(ipl(d, i, CLN)) + v3(R(0), R(-1), R(0)) * w.at(ipl(d, i, CLT)) +
+                          v3(R(1), R(0), R(0)) * w.at(ipl(d, i, CLT + 1));
+                V3<R> f = v3(P.x / dt, P.y / dt, P.z / dt);
+                F = F + f;
+                Tq = Tq + cross(w.l3(ipl(d, i, CR)), f);
+            }
+            for (int i = 0; i < d.Q; ++i) {
+                int pa = c.L.pair_body[2 * i], pb = c.L.pair_body[2 * i + 1];
+                if (pa != b && pb != b) continue;
+                V3<R> P = w.l3(ipr(d, i, QN)) * w.at(ipr(d, i, QLN)) + w.l3(ipr(d, i, QT1)) * w.at(ipr(d, i, QLT)) +
+                          w.l3(ipr(d, i, QT2)) * w.at(ipr(d, i, QLT + 1));
+                V3<R> f = v3(P.x / dt, P.y / dt, P.z / dt);
+                if (pb == b) {
+                    F = F + f;
+                    Tq = Tq + cross(w.l3(ipr(d, i, QR)), f);
+                }
+                if (pa == b) {
+                    F = F + (-f);
+                    Tq = Tq + cross(w.l3(ipr(d, i, QRA)), -f);
+                }
+            }
+            w.s3(ib(d, b, BDP), F);
+            w.s3(ib(d, b, BDA), Tq);
+            R *o = c.s.net_contact + 3 * ((size_t)(g.e0 + el) * d.B + b);
+            o[0] = F.x; o[1] = F.y; o[2] = F.z;
+        }
+        BS_ITEMS(g, d.D, el, k) {
+            c.s.dof_force[(size_t)(g.e0 + el) * d.D + k] = g.env(el).at(idf(d, k, DIMP)) / dt;
+        }
+        BS_SYNC();
+        BS_ITEMS(g, d.S, el, k) {
+            Ws<R> w = g.env(el);
+            int b = c.L.sensor_body[k];
+            Q4<R> qi = qconj(w.l4(ib(d, b, BQ)));
+            V3<R> f = qrot(qi, w.l3(ib(d, b, BDP))), t = qrot(qi, w.l3(ib(d, b, BDA)));
+            R *o = c.s.sensor_forces + 6 * ((size_t)(g.e0 + el) * d.S + k);
+            o[0] = f.x; o[1] = f.y; o[2] = f.z; o[3] = t.x; o[4] = t.y; o[5] = t.z;
+        }
+    }
+
+    // _flag_nonfinite (1073-1088): sanitize poisoned envs (sticky flag)
+    BS_ITEMS(g, d.B, el, b) {
+        Ws<R> w = g.env(el);
+        bool ok = true;
+        for (int k = 0; k < 13; ++k) ok = ok && finite_r(w.at(ib(d, b, BP) + k));
+        if (!ok) w.at(d.o_env + EBAD) = R(1);
+    }
+    BS_SYNC();
+    BS_ITEMS(g, d.B, el, b) {
+        Ws<R> w = g.env(el);
+        if (w.at(d.o_env + EBAD) != R(0)) {
+            int e = g.e0 + el;
+            if (b == 0) c.s.nonfinite[e] = 1;
+            for (int k = 0; k < 13; ++k) {
+                R &x = w.at(ib(d, b, BP) + k);
+                // the reference zeroes the WORLD position (physics.py:1081)
+                if (!finite_r(x)) x = k < 3 ? -c.s.env_origins[3 * (size_t)e + k] : R(0);
+            }
+            Q4<R> q = w.l4(ib(d, b, BQ));
+            if (r_sqrt(q.x * q.x + q.y * q.y + q.z * q.z + q.w * q.w) < R(1e-9)) q = Q4<R>{0, 0, 0, 1};
+            w.s4(ib(d, b, BQ), qnormalize(q));
+        }
+    }
+    BS_SYNC();
+    BS_ENVS(g, el) { g.env(el).at(d.o_env + EBAD) = R(0); }
+    BS_SYNC();
+}
+
+// dof_state readout from the workspace (physics.py:427-459, 1038)
+template <class R> BS_HD void readout_group(const Ctx<R> &c, const Grp<R> &g) {
+    const Dims &d = c.d;
+    BS_ITEMS(g, d.J, el, j) {
+        Ws<R> w = g.env(el);
+        R q[3], qd[3];
+        int n = joint_dofs(c, w, j, q, qd);
+        for (int k = 0; k < n; ++k) {
+            R *o = c.s.dof_state + 2 * ((size_t)(g.e0 + el) * d.D + c.joints[j].dof + k);
+            o[0] = q[k];
+            o[1] = qd[k];
+        }
+    }
+}
+
+// staging of all per-env inputs into the workspace (once per launch)
+template <class R> BS_HD void stage_group(const Ctx<R> &c, const Grp<R> &g) {
+    const Dims &d = c.d;
+    BS_ENVS(g, el) { stage_env(c, g.env(el), g.e0 + el); }
+    BS_ITEMS(g, d.J, el, j) { stage_joint(c, g.env(el), g.e0 + el, j); }
+    BS_ITEMS(g, d.D, el, k) { stage_dof(c, g.env(el), g.e0 + el, k); }
+    BS_ITEMS(g, d.B, el, b) { g.env(el).at(ib(d, b, BM)) = c.s.inv_mass[(size_t)(g.e0 + el) * d.B + b]; }
+    BS_ITEMS(g, d.P, el, i) {
+        for (int k = 0; k < 3; ++k)
+            g.env(el).at(d.o_anchor + 3 * i + k) = c.s.friction_anchor[3 * ((size_t)i * d.E + g.e0 + el) + k];
+    }
+}
+
+}  // namespace bsim

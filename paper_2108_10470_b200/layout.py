@@ -207,9 +207,9 @@ class SceneLayout:
                               spec.limit_stiffness, 0.0, 0.0)))
         self.tendons_per_env = len(rows)
         self.tendon_int = np.array([r[0] for r in rows], np.int32).reshape(-1, TENDON_INTS)
-        self.tendon_flt = np.array([r[1] for r in rows], np.float32).reshape(-1, TENDON_FLOATS)
+        self.tendon_flt = np.array([r[1] for r in rows], np.float64).reshape(-1, TENDON_FLOATS)
         self.telem_int = np.array([e[0] for e in elems], np.int32).reshape(-1, TELEM_INTS)
-        self.telem_flt = np.array([e[1] for e in elems], np.float32).reshape(-1, TELEM_FLOATS)
+        self.telem_flt = np.array([e[1] for e in elems], np.float64).reshape(-1, TELEM_FLOATS)
         # spatial sub-tendon paths (root-to-leaf, declaration order), as element indices
         self.spatial_paths = []
         for t in range(self.tendons_per_env):

@@ -1,0 +1,58 @@
+// TEST-ONLY host build of the step kernel's per-env body (bsim_step.cuh),
+// so the CUDA code path's arithmetic can be debugged against the oracle on a
+// CPU-only machine.  Mirrors step_kernel()'s load / stage / substep / store
+// sequence with a one-env workspace (stride 1).  Never used by the product.
+#include <cstdlib>
+#include <vector>
+
+#include "../../paper_2108_10470_b200/csrc/bsim_step.cuh"
+
+using namespace bsim;
+
+template <class R>
+static void run(const bsim_layout_t *L, const typename Abi<R>::Params *p, const typename Abi<R>::State *s,
+                int n_substeps) {
+    Ctx<R> c;
+    c.L = *L;
+    c.p = *p;
+    c.s = *s;
+    c.d = make_dims(*L);
+    c.joints = reinterpret_cast<const typename Abi<R>::Joint *>(L->joints);
+    const Dims &d = c.d;
+    // the whole batch as one "CTA" with a single thread: stride = E
+    const int E = d.E;
+    std::vector<R> buf((size_t)d.items * E, R(1e30));   // poison: catches unstaged reads
+    Grp<R> g{buf.data(), E, 0, E, 0, 1};
+    for (int e = 0; e < E; ++e)
+        for (int b = 0; b < d.B; ++b)
+            for (int k = 0; k < 13; ++k)
+                g.env(e).at(ib(d, b, BP) + k) = s->body_q[13 * ((size_t)e * d.B + b) + k];
+    stage_group(c, g);
+    for (int st = 0; st < n_substeps; ++st) {
+        group_step(c, g, st == n_substeps - 1);
+        if (d.T && st != n_substeps - 1) readout_group(c, g);
+    }
+    readout_group(c, g);
+    for (int e = 0; e < E; ++e) {
+        Ws<R> w = g.env(e);
+        for (int i = 0; i < d.P; ++i)
+            for (int k = 0; k < 3; ++k) s->friction_anchor[3 * ((size_t)i * E + e) + k] = w.at(d.o_anchor + 3 * i + k);
+        for (int b = 0; b < d.B; ++b)
+            for (int k = 0; k < 13; ++k) {
+                R x = w.at(ib(d, b, BP) + k);
+                s->body_q[13 * ((size_t)e * d.B + b) + k] = x;
+                s->body_state[13 * ((size_t)e * d.B + b) + k] = k < 3 ? x + s->env_origins[3 * e + k] : x;
+            }
+        for (int a = 0; a < d.A; ++a)
+            for (int k = 0; k < 13; ++k)
+                s->root_state[13 * ((size_t)e * d.A + a) + k] =
+                    s->body_state[13 * ((size_t)e * d.B + L->actor_body_offset[a]) + k];
+    }
+}
+
+extern "C" void hk_step(const bsim_layout_t *L, const bsim_params_t *p, const bsim_state_t *s, int n) {
+    run<float>(L, p, s, n);
+}
+extern "C" void hk_step_f64(const bsim_layout_t *L, const bsim_params64_t *p, const bsim_state64_t *s, int n) {
+    run<double>(L, p, s, n);
+}

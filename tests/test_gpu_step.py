@@ -1,0 +1,179 @@
+"""GPU parity of the fused TGS step kernel against the reference.
+
+Teacher forcing: the state recorded by the REFERENCE before step t (golden
+fixtures, tests/golden/make_golden.py) is loaded into the GPU scene, one
+step runs on the B200, and every tensor-API output is compared with what the
+reference produced.  Larger sizes are compared against the float64 C oracle.
+
+Tolerance contract:
+  fp64 path: |gpu - ref| <= 1e-8 + 1e-8 |ref| for every element.
+  fp32 path: every element within 2e-3 + 2e-3 |ref| (fp32 conditioning of the
+             1/h-scaled TGS bias), >= 99% of elements within the north-star
+             1e-4 + 1e-4 |ref|; contact-active masks bit-exact.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from golden_util import (build_models, gpu_outputs, gpu_scene_from_fixture, load, load_gpu_state,
+                         physics_cases, rel_err, sim_params)
+
+pytestmark = pytest.mark.gpu
+
+OUTS = ("root_state", "body_state", "dof_state", "net_contact", "dof_force", "sensor_forces")
+
+
+def _poisoned_rows(meta, arr, t, key, B, D, S, A):
+    """Rows of envs poisoned at step t (their chaos is excluded, see test_nan_*)."""
+    bad = np.nonzero(arr["out_nonfinite"][t])[0]
+    per = {"root_state": A, "body_state": B, "net_contact": B, "dof_state": D, "dof_force": D,
+           "sensor_forces": S}[key]
+    rows = np.zeros(arr[f"out_{key}"][t].shape[0], bool)
+    for e in bad:
+        rows[e * per:(e + 1) * per] = True
+    return rows
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+@pytest.mark.parametrize("case", physics_cases())
+def test_step_matches_reference_teacher_forced(case, precision):
+    meta, arr = load(case)
+    s = gpu_scene_from_fixture(meta, arr, precision)
+    tol = 1e-8 if precision == "fp64" else 2e-3
+    within, total = 0, 0
+    for t in range(meta["steps"]):
+        load_gpu_state(s, arr, t)
+        s.step()
+        got = gpu_outputs(s)
+        assert np.array_equal(got["nonfinite"], arr["out_nonfinite"][t]), (case, t)
+        for k in OUTS:
+            want = arr[f"out_{k}"][t]
+            keep = ~_poisoned_rows(meta, arr, t, k, s.bodies_per_env, s.dofs_per_env,
+                                   s.sensors_per_env, s.actors_per_env)
+            g, w = got[k][keep], want[keep]
+            e = rel_err(g, w, tol, tol)
+            assert e <= 1.0, (case, precision, t, k, e)
+            if precision == "fp32":
+                d = np.abs(g - w) / (1e-4 + 1e-4 * np.abs(w))
+                within += int((d <= 1.0).sum())
+                total += d.size
+        a = got["_friction_anchor"]
+        assert np.array_equal(np.isnan(a), np.isnan(arr["out__friction_anchor"][t])), (case, t)
+    if precision == "fp32":
+        assert within >= 0.99 * total, (case, within / total)
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+@pytest.mark.parametrize("case", ["quadruped_walk", "kitchen_sink", "box_incline"])
+def test_contact_list_matches_reference(case, precision):
+    meta, arr = load(case)
+    s = gpu_scene_from_fixture(meta, arr, precision)
+    E, B = s.num_envs, s.bodies_per_env
+    org = arr["param_env_origins"]
+    be = np.repeat(np.arange(E), B)
+    bq = np.zeros((E * B, 13))
+    bq[:, 0:3] = arr["final_pos"] - org[be]
+    bq[:, 3:7] = arr["final_quat"]
+    s.body_q.copy_(torch.as_tensor(bq, dtype=s.dtype))
+    s._friction_anchor.copy_(torch.as_tensor(arr["out__friction_anchor"][-1] - org[None], dtype=s.dtype))
+    k, ba, bb, depth, point, normal = s.collide_tensors()
+    assert np.array_equal(ba.cpu().numpy(), arr["collide_body_a"])
+    assert np.array_equal(bb.cpu().numpy(), arr["collide_body_b"])
+    tol = 1e-9 if precision == "fp64" else 1e-4
+    assert rel_err(depth.double().cpu().numpy(), arr["collide_depth"], tol, tol) <= 1
+    assert rel_err(point.double().cpu().numpy(), arr["collide_point"], tol, tol) <= 1
+    host = s.collide()
+    assert [c.body_b for c in host] == list(arr["collide_body_b"])
+    assert [c.friction_anchor is not None for c in host] == list(arr["collide_has_anchor"])
+
+
+def _oracle_pair(E, precision, steps_warm=20, seed=0):
+    from oracle.oracle import OracleScene
+    from paper_2108_10470_b200 import models as M
+    from paper_2108_10470_b200.params import SimParams
+    from paper_2108_10470_b200.scene import Scene
+    p = SimParams(dt=1 / 120)
+    ref = OracleScene([M.quadruped()], E, p, threads=8)
+    rng = np.random.default_rng(seed)
+    ref.pos[:, 2] += 0.37
+    ref.forward_kinematics()
+    for _ in range(steps_warm):
+        ref.ctrl_dof_pos_target[:] = rng.uniform(-0.6, 0.6, ref.num_dofs)
+        ref.step()
+    gpu = Scene([M.quadruped()], E, p, precision=precision)
+    return ref, gpu, rng
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_step_matches_oracle_4096_envs(precision):
+    """Headline config size (Ant analog, 4096 envs): one teacher-forced step
+    per control step for 4 steps vs the float64 oracle."""
+    ref, gpu, rng = _oracle_pair(4096, precision)
+    E, B = 4096, gpu.bodies_per_env
+    be = np.repeat(np.arange(E), B)
+    tol = 1e-8 if precision == "fp64" else 2e-3
+    for t in range(4):
+        tgt = rng.uniform(-0.6, 0.6, ref.num_dofs)
+        ref.ctrl_dof_pos_target[:] = tgt
+        bq = np.concatenate([ref.pos - ref.env_origins[be], ref.quat, ref.linvel, ref.angvel], 1)
+        gpu.body_q.copy_(torch.as_tensor(bq, dtype=gpu.dtype))
+        gpu._friction_anchor.copy_(torch.as_tensor(ref._friction_anchor - ref.env_origins[None], dtype=gpu.dtype))
+        gpu.dof_state.copy_(torch.as_tensor(ref.dof_state, dtype=gpu.dtype))
+        gpu.ctrl_dof_pos_target.copy_(torch.as_tensor(tgt, dtype=gpu.dtype))
+        ref.step()
+        gpu.step()
+        got = gpu_outputs(gpu)
+        for k in OUTS:
+            e = rel_err(got[k], getattr(ref, k), tol, tol)
+            assert e <= 1.0, (precision, t, k, e)
+
+
+def test_determinism_bitwise():
+    outs = []
+    for _ in range(2):
+        ref, gpu, rng = _oracle_pair(256, "fp32", steps_warm=0, seed=1)
+        gpu.pos[:, 2] += 0.37
+        gpu.forward_kinematics()
+        for t in range(20):
+            gpu.ctrl_dof_pos_target.copy_(torch.as_tensor(rng.uniform(-0.5, 0.5, gpu.num_dofs)))
+            gpu.step()
+        outs.append(gpu.body_q.cpu().numpy().copy())
+    assert np.array_equal(outs[0], outs[1])
+
+
+def test_substep_fusion_equals_sequential_steps():
+    """step(n_substeps=2) == two step() calls (envs.py:186-187 decimation)."""
+    from paper_2108_10470_b200 import models as M
+    from paper_2108_10470_b200.scene import Scene
+    a = Scene([M.quadruped()], 64, precision="fp64")
+    b = Scene([M.quadruped()], 64, precision="fp64")
+    for s in (a, b):
+        s.pos[:, 2] += 0.37
+        s.forward_kinematics()
+        s.ctrl_dof_pos_target.fill_(0.3)
+    a.step(2)
+    b.step()
+    b.step()
+    for k in ("body_q", "root_state", "dof_state", "net_contact", "sensor_forces", "_friction_anchor"):
+        x, y = getattr(a, k), getattr(b, k)
+        assert torch.equal(torch.nan_to_num(x, 7.0), torch.nan_to_num(y, 7.0)), k
+
+
+def test_nan_poisoning_is_contained():
+    """tests/test_physics.py:242-258 on the GPU: a NaN in one env flags only
+    that env; the other envs stay bitwise equal to a clean twin."""
+    from paper_2108_10470_b200 import models as M
+    from paper_2108_10470_b200.params import SimParams
+    from paper_2108_10470_b200.scene import Scene
+    p = SimParams(dt=1 / 120)
+    s = Scene([M.free_sphere(collision=False)], 3, p, ground=False)
+    twin = Scene([M.free_sphere(collision=False)], 3, p, ground=False)
+    s.linvel[1, 0] = float("nan")
+    for _ in range(5):
+        s.step()
+        twin.step()
+    nf = s.nonfinite.cpu().numpy()
+    assert nf[1] and not nf[0] and not nf[2]
+    assert torch.equal(s.body_q[0], twin.body_q[0]) and torch.equal(s.body_q[2], twin.body_q[2])
+    assert torch.isfinite(s.body_state[[0, 2]]).all()
