@@ -82,6 +82,8 @@ typedef struct bsim_params64_t { BSIM_PARAMS_FIELDS(double) } bsim_params64_t;
 typedef struct bsim_layout_t {
     int32_t num_envs, actors_per_env, bodies_per_env, dofs_per_env, joints_per_env,
             planes_per_env, pairs_per_env, sensors_per_env, tendons_per_env, env_offset;
+    int32_t topology_id;   /* 0 = generic; k > 0 = the AOT-specialised topology k
+                              (paper_2108_10470_b200/csrc/bsim_topologies.cuh) */
     const void *joints;                    /* [J]    */
     const int32_t *plane_body;             /* [P]    */
     const int32_t *pair_body;              /* [Q][2] */

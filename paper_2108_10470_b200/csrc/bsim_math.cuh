@@ -17,6 +17,8 @@
 #endif
 
 #define BS_HD __host__ __device__ __forceinline__
+// large per-item phase functions: one copy in the binary (instruction-cache footprint)
+#define BS_NI __host__ __device__ __noinline__
 
 namespace bsim {
 

@@ -17,6 +17,7 @@
 #include <string>
 
 #include "bsim_step.cuh"
+#include "bsim_topologies.cuh"
 
 using namespace bsim;
 
@@ -48,30 +49,21 @@ template <> struct Shape<double> {
 };
 
 template <class R> size_t step_smem_bytes(const Dims &d) {
-    return (size_t)d.J * sizeof(typename Abi<R>::Joint) + (size_t)d.items * (Shape<R>::NE + 1) * sizeof(R);
+    return (size_t)d.items * (Shape<R>::NE + 1) * sizeof(R);
 }
 
 // ------------------------------------------------------------------ step
-template <class R>
-__global__ void __launch_bounds__(Shape<R>::NTH) step_kernel(Ctx<R> c, int n_substeps, bsim_actions_t act) {
+template <class R, class T>
+__global__ void __launch_bounds__(Shape<R>::NTH) step_kernel(const Ctx<R> c, int n_substeps, bsim_actions_t act) {
     constexpr int NE = Shape<R>::NE, NTH = Shape<R>::NTH, STR = NE + 1;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const Dims &d = c.d;
-    using Joint = typename Abi<R>::Joint;
-    Joint *sj = reinterpret_cast<Joint *>(smem_raw);
-    R *ws = reinterpret_cast<R *>(smem_raw + (size_t)d.J * sizeof(Joint));
+    R *ws = reinterpret_cast<R *>(smem_raw);
     const int tid = threadIdx.x;
     const int e0 = blockIdx.x * NE;
     const int ne = min(NE, d.E - e0);
     const int per_env = 13 * d.B;
 
-    // joint table -> shared (uniform broadcast reads afterwards)
-    {
-        const int words = d.J * (int)(sizeof(Joint) / 4);
-        const int *src = reinterpret_cast<const int *>(c.joints);
-        int *dst = reinterpret_cast<int *>(sj);
-        for (int i = tid; i < words; i += NTH) dst[i] = src[i];
-    }
     // coalesced load of the CTA's contiguous [ne x B x 13] body slab
     {
         const R *src = c.s.body_q + (size_t)e0 * per_env;
@@ -82,7 +74,6 @@ __global__ void __launch_bounds__(Shape<R>::NTH) step_kernel(Ctx<R> c, int n_sub
         }
     }
     __syncthreads();
-    c.joints = sj;
     const Grp<R> g{ws, STR, e0, ne, tid, NTH};
     stage_group(c, g);
     if (act.actions) {  // fused action mapping (envs.py:180, 421-424)
@@ -102,7 +93,7 @@ __global__ void __launch_bounds__(Shape<R>::NTH) step_kernel(Ctx<R> c, int n_sub
     }
     __syncthreads();
     for (int s = 0; s < n_substeps; ++s) {
-        group_step(c, g, s == n_substeps - 1);
+        group_step<R, T>(c, g, s == n_substeps - 1);
         if (d.T && s != n_substeps - 1) {  // fixed tendons read dof_state next substep
             readout_group(c, g);
             __syncthreads();
@@ -454,6 +445,20 @@ bool bad_layout(const bsim_layout_t *L) {
 }
 
 // ------------------------------------------------------------ launchers
+template <class R, class T>
+int launch_step_t(const Ctx<R> &c, size_t smem, int grid, int n_substeps, const bsim_actions_t &act,
+                  cudaStream_t st) {
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
+        cudaError_t e = cudaFuncSetAttribute(step_kernel<R, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return set_err("cudaFuncSetAttribute(step_kernel)", e);
+        configured = smem;
+    }
+    step_kernel<R, T><<<grid, Shape<R>::NTH, smem, st>>>(c, n_substeps, act);
+    return check_launch("step_kernel");
+}
+
 template <class R>
 int launch_step(const bsim_layout_t *layout, const typename Abi<R>::Params *params,
                 const typename Abi<R>::State *state, int32_t n_substeps, const bsim_actions_t *actions,
@@ -469,18 +474,19 @@ int launch_step(const bsim_layout_t *layout, const typename Abi<R>::Params *para
         g_err = "bsim_step: model too large for the step kernel's shared-memory workspace";
         return BSIM_E_TOO_LARGE;
     }
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
-        cudaError_t e = cudaFuncSetAttribute(step_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e != cudaSuccess) return set_err("cudaFuncSetAttribute(step_kernel)", e);
-        configured = smem;
-    }
     bsim_actions_t act;
     if (actions) act = *actions; else std::memset(&act, 0, sizeof act);
     int grid = (c.d.E + Shape<R>::NE - 1) / Shape<R>::NE;
-    step_kernel<R><<<grid, Shape<R>::NTH, smem, (cudaStream_t)stream>>>(c, n_substeps, act);
-    return check_launch("step_kernel");
+    cudaStream_t st = (cudaStream_t)stream;
+    switch (layout->topology_id) {
+#define BSIM_LAUNCH_TOPO(ID, TYPE)                                      \
+    case ID:                                                            \
+        return launch_step_t<R, TYPE>(c, smem, grid, n_substeps, act, st);
+        BSIM_TOPOLOGIES(BSIM_LAUNCH_TOPO)
+#undef BSIM_LAUNCH_TOPO
+    default:
+        return launch_step_t<R, TopoGeneric>(c, smem, grid, n_substeps, act, st);
+    }
 }
 
 template <class R>

@@ -52,7 +52,7 @@ template <> struct Abi<double> {
 // ---------------------------------------------------------------- items
 // per body: pose, velocity, TGS deltas, world inverse inertia (sym), inverse
 // mass, effective pose scratch
-enum { BP = 0, BQ = 3, BV = 7, BW = 10, BDP = 13, BDA = 16, BI = 19, BM = 25, BPE = 26, BQE = 29,
+enum { BP = 0, BQ = 3, BV_ = 7, BW = 10, BDP = 13, BDA = 16, BI = 19, BM = 25, BPE = 26, BQE = 29,
        BODY_ITEMS = 33 };
 // per joint: geometry, staged params, and the row constants of phase A
 enum {
@@ -65,15 +65,25 @@ enum {
     JHP = 55,   // Ip T^T K^-1 T                                         (3x3, 9)
     JX1 = 64, JX2 = 67,   // axis-row jacobians on omega_c / omega_p
     JY1 = 70, JY2 = 73,   // axis-row responses on omega_c / omega_p per unit impulse
-    JMEFF = 76, JOINT_ITEMS = 77
+    JMEFF = 76,
+    // per-pass constants of the drive / limit rows (phase A, so the sweep divides nothing)
+    JDA = 77, JDB = 78,   // PD impulse = DA - DB * qd  (812-848, implicit discretisation)
+    JLF = 79,             // direct-actuation impulse (FORCE mode)
+    JMFH = 80,            // max_force * h clamp
+    JFRH = 81,            // joint friction bound fr * h (0 = off)
+    JLV = 82,             // limit state this pass: 0 none, 1 below lo, 2 above hi
+    JLB = 83,             // limit bias velocity this pass
+    JOINT_ITEMS = 84
 };
 // per plane contact slot
 enum { CR = 0, CD0 = 3, CREST = 4, CLN = 5, CLT = 6, CTE = 8, CACT = 10, CPT = 11, CXN = 14, CX1 = 17,
-       CX2 = 20, CIXN = 23, CIX1 = 26, CIX2 = 29, CMN = 32, CM1 = 33, CM2 = 34, PLANE_ITEMS = 35 };
+       CX2 = 20, CIXN = 23, CIX1 = 26, CIX2 = 29, CMN = 32, CM1 = 33, CM2 = 34,
+       CTGT = 35, CST1 = 36, CST2 = 37,   // per pass: normal target velocity, stiction terms
+       PLANE_ITEMS = 38 };
 // per sphere-sphere pair slot
 enum { QR = 0, QRA = 3, QN = 6, QT1 = 9, QT2 = 12, QD0 = 15, QREST = 16, QLN = 17, QLT = 18, QACT = 20,
        QPT = 21, QXN = 24, QX1 = 27, QX2 = 30, QYN = 33, QY1 = 36, QY2 = 39, QIXN = 42, QIX1 = 45,
-       QIX2 = 48, QIYN = 51, QIY1 = 54, QIY2 = 57, QMN = 60, QM1 = 61, QM2 = 62, PAIR_ITEMS = 63 };
+       QIX2 = 48, QIYN = 51, QIY1 = 54, QIY2 = 57, QMN = 60, QM1 = 61, QM2 = 62, QTGT = 63, PAIR_ITEMS = 64 };
 // per dof: impulse accumulator, start-of-step readout, staged controls
 enum { DIMP = 0, DQ0 = 1, DPT = 2, DVT = 3, DF = 4, DMODE = 5, DOF_ITEMS = 6 };
 // per env
@@ -196,10 +206,10 @@ template <class R> BS_HD void body_external(const Ctx<R> &c, const Ws<R> &w, int
     R im = w.at(ib(d, b, BM));
     const R *f = c.s.ctrl_body_force + 3 * ((size_t)e * d.B + b);
     const R *tq = c.s.ctrl_body_torque + 3 * ((size_t)e * d.B + b);
-    V3<R> v = w.l3(ib(d, b, BV));
+    V3<R> v = w.l3(ib(d, b, BV_));
     if (im > R(0)) v = v + v3(w.at(d.o_env + EGX), w.at(d.o_env + EGY), w.at(d.o_env + EGZ)) * dt;
     v = v + v3(clampr(f[0], -mf, mf) * dt * im, clampr(f[1], -mf, mf) * dt * im, clampr(f[2], -mf, mf) * dt * im);
-    w.s3(ib(d, b, BV), v);
+    w.s3(ib(d, b, BV_), v);
     V3<R> t = v3(clampr(tq[0], -mf, mf), clampr(tq[1], -mf, mf), clampr(tq[2], -mf, mf));
     w.s3(ib(d, b, BW), w.l3(ib(d, b, BW)) + smul(w.lS(ib(d, b, BI)), t) * dt);
 }
@@ -225,7 +235,7 @@ template <class R> BS_HD int joint_dofs(const Ctx<R> &c, const Ws<R> &w, int j, 
         V3<R> sep = (w.l3(ib(d, ch, BP)) - w.l3(ib(d, p, BP))) + (rc - rp);
         V3<R> aw = qrot(jqp, jv3(jt.axis));
         q[0] = dot(aw, sep);
-        V3<R> vap = w.l3(ib(d, p, BV)) + cross(wp, rp), vac = w.l3(ib(d, ch, BV)) + cross(wc, rc);
+        V3<R> vap = w.l3(ib(d, p, BV_)) + cross(wp, rp), vac = w.l3(ib(d, ch, BV_)) + cross(wc, rc);
         qd[0] = dot(aw, vac - vap);
         return 1;
     }
@@ -355,7 +365,7 @@ template <class R> BS_HD void plane_freeze(const Ctx<R> &c, const Ws<R> &w, int 
     bool has = !(ax != ax);
     w.at(ipl(d, i, CTE)) = has ? point.x - ax : R(0);
     w.at(ipl(d, i, CTE + 1)) = has ? point.y - ay : R(0);
-    V3<R> v = w.l3(ib(d, b, BV)) + cross(w.l3(ib(d, b, BW)), r);
+    V3<R> v = w.l3(ib(d, b, BV_)) + cross(w.l3(ib(d, b, BW)), r);
     R vn = v.z;
     w.s3(ipl(d, i, CR), r);
     w.s3(ipl(d, i, CPT), point);
@@ -389,8 +399,8 @@ template <class R> BS_HD void pair_freeze(const Ctx<R> &c, const Ws<R> &w, int e
     R depth = p.rest_offset - gap;
     V3<R> ra = arma + n * (rr[0] + R(0.5) * gap);
     V3<R> r = (pa0 - w.l3(ib(d, pb, BP))) + ra;
-    V3<R> va = w.l3(ib(d, pa, BV)) + cross(w.l3(ib(d, pa, BW)), ra);
-    V3<R> vb = w.l3(ib(d, pb, BV)) + cross(w.l3(ib(d, pb, BW)), r);
+    V3<R> va = w.l3(ib(d, pa, BV_)) + cross(w.l3(ib(d, pa, BW)), ra);
+    V3<R> vb = w.l3(ib(d, pb, BV_)) + cross(w.l3(ib(d, pb, BW)), r);
     R vn = dot(n, vb - va);
     V3<R> t1, t2;
     tangents(n, t1, t2);
@@ -445,228 +455,339 @@ template <class R> BS_HD void pair_constants(const Ctx<R> &c, const Ws<R> &w, in
     }
 }
 
-// ====================================================== phase B: the sweep
-// PD drive / direct actuation / joint friction (physics.py:812-848)
-template <class R> BS_HD void row_drive(const Ctx<R> &c, const Ws<R> &w, int j, R h) {
-    const auto &jt = c.joints[j];
+// Per-pass constants (phase A): everything in a row that is fixed for the
+// duration of one Gauss-Seidel pass -- targets (-perr/h, -rerr/h), the PD
+// drive's affine impulse law, limit activation and bias, the contact normal
+// target and stiction terms (dpos only changes between passes).
+template <class R> BS_HD void joint_pass_constants(const Ctx<R> &c, const Ws<R> &w, int j, R h, bool biased) {
     const Dims &d = c.d;
-    const bool lin = jt.kind == BSIM_PRISMATIC;
-    const int p = jt.parent, ch = jt.child;
-    V3<R> wc = w.l3(ib(d, ch, BW)), wp = w.l3(ib(d, p, BW));
-    R qd = dot(w.l3(ij(d, j, JX1)), wc) - dot(w.l3(ij(d, j, JX2)), wp);
-    V3<R> a = w.l3(ij(d, j, JAX));
-    V3<R> vc, vp;
-    if (lin) {
-        vc = w.l3(ib(d, ch, BV));
-        vp = w.l3(ib(d, p, BV));
-        qd = qd + dot(a, vc - vp);
-    }
+    const auto &jt = c.joints[j];
+    V3<R> pe = w.l3(ij(d, j, JPE)), re = w.l3(ij(d, j, JRE));
+    // JPE / JRE now hold the row targets (physics.py:881, 898)
+    w.s3(ij(d, j, JPE), biased ? v3(-pe.x / h, -pe.y / h, -pe.z / h) : zero3<R>());
+    w.s3(ij(d, j, JRE), biased ? v3(-re.x / h, -re.y / h, -re.z / h) : zero3<R>());
+    if (jt.dof < 0 || jt.kind == BSIM_SPHERICAL) return;
     const R meff = w.at(ij(d, j, JMEFF));
-    const int mode = (int)w.at(idf(d, jt.dof, DMODE));
-    const R ia = meff + w.at(ij(d, j, JARM));
-    const R mf = c.p.max_force;
-    R tau = clampr(w.at(idf(d, jt.dof, DF)), -mf, mf);
-    R lam = mode == BSIM_MODE_FORCE ? tau * h * meff / ia : R(0);
-    R kk = mode == BSIM_MODE_POSITION ? w.at(ij(d, j, JSTIFF)) : R(0);
-    R cc = mode == BSIM_MODE_FORCE ? R(0) : w.at(ij(d, j, JDAMP));
-    R err = w.at(idf(d, jt.dof, DPT)) - w.at(ij(d, j, JQ0));
-    R dv = w.at(idf(d, jt.dof, DVT)) - qd;
-    R lpd = h * (kk * (err - h * qd) + cc * dv) / (R(1) + h * (h * kk + cc) / ia);
-    lam = lam + clampr(lpd, -mf * h, mf * h);
-    R fr = w.at(ij(d, j, JFRIC));
-    if (fr > R(0)) lam = lam + clampr(-qd * meff, -fr * h, fr * h);
-    w.s3(ib(d, ch, BW), wc + w.l3(ij(d, j, JY1)) * lam);
-    w.s3(ib(d, p, BW), wp - w.l3(ij(d, j, JY2)) * lam);
-    if (lin) {
-        w.s3(ib(d, ch, BV), vc + a * (lam * w.at(ib(d, ch, BM))));
-        w.s3(ib(d, p, BV), vp - a * (lam * w.at(ib(d, p, BM))));
+    if (biased) {  // drive (812-848): lam = LF + clip(DA - DB qd, +-mf h) [+ friction]
+        const int mode = (int)w.at(idf(d, jt.dof, DMODE));
+        const R ia = meff + w.at(ij(d, j, JARM));
+        const R mf = c.p.max_force;
+        R tau = clampr(w.at(idf(d, jt.dof, DF)), -mf, mf);
+        R kk = mode == BSIM_MODE_POSITION ? w.at(ij(d, j, JSTIFF)) : R(0);
+        R cc = mode == BSIM_MODE_FORCE ? R(0) : w.at(ij(d, j, JDAMP));
+        R den = R(1) + h * (h * kk + cc) / ia;
+        R err = w.at(idf(d, jt.dof, DPT)) - w.at(ij(d, j, JQ0));
+        w.at(ij(d, j, JDA)) = h * (kk * err + cc * w.at(idf(d, jt.dof, DVT))) / den;
+        w.at(ij(d, j, JDB)) = h * (kk * h + cc) / den;
+        w.at(ij(d, j, JLF)) = mode == BSIM_MODE_FORCE ? tau * h * meff / ia : R(0);
+        w.at(ij(d, j, JMFH)) = mf * h;
+        R fr = w.at(ij(d, j, JFRIC));
+        w.at(ij(d, j, JFRH)) = fr > R(0) ? fr * h : R(0);
     }
-    w.at(idf(d, jt.dof, DIMP)) += lam;
+    if (jt.has_limits) {  // limit (850-870): q0 in biased passes, start-of-step q otherwise
+        R lo = w.at(ij(d, j, JLO)), hi = w.at(ij(d, j, JHI));
+        R q = biased ? w.at(ij(d, j, JQ0)) : w.at(idf(d, jt.dof, DQ0));
+        R state = R(0), bias = R(0);
+        if (q < lo) {
+            state = R(1);
+            bias = biased ? r_max(lo - q, R(0)) / h : R(0);
+        }
+        if (q > hi) {
+            state = R(2);
+            bias = biased ? r_max(q - hi, R(0)) / h : R(0);
+        }
+        w.at(ij(d, j, JLV)) = state;
+        w.at(ij(d, j, JLB)) = bias;
+    }
+}
+template <class R> BS_HD void plane_pass_constants(const Ctx<R> &c, const Ws<R> &w, int i, bool biased) {
+    const Dims &d = c.d;
+    const int b = c.L.plane_body[i];
+    const R dt = c.p.dt;
+    R depth = w.at(ipl(d, i, CD0));
+    R bias = R(0), st1 = R(0), st2 = R(0);
+    if (biased) {
+        V3<R> dp = w.l3(ib(d, b, BDP));
+        depth = depth + dp.z * R(-1);                       // 942
+        bias = c.p.max_bias * r_max(depth, R(0)) / dt;      // 953
+        R tex = w.at(ipl(d, i, CTE)) + dp.x, tey = w.at(ipl(d, i, CTE + 1)) + dp.y;
+        st1 = (-tey) / dt;                                  // 971-973, t1 = (0,-1,0)
+        st2 = tex / dt;                                     //           t2 = (1,0,0)
+    }
+    w.at(ipl(d, i, CTGT)) = r_max(w.at(ipl(d, i, CREST)), bias);
+    w.at(ipl(d, i, CST1)) = st1;
+    w.at(ipl(d, i, CST2)) = st2;
+}
+template <class R> BS_HD void pair_pass_constants(const Ctx<R> &c, const Ws<R> &w, int i, bool biased) {
+    const Dims &d = c.d;
+    R depth = w.at(ipr(d, i, QD0));
+    R bias = R(0);
+    if (biased) {
+        int pa = c.L.pair_body[2 * i], pb = c.L.pair_body[2 * i + 1];
+        depth = depth + dot(w.l3(ipr(d, i, QN)), w.l3(ib(d, pb, BDP)) - w.l3(ib(d, pa, BDP))) * R(-1);  // 949
+        bias = c.p.max_bias * r_max(depth, R(0)) / c.p.dt;
+    }
+    w.at(ipr(d, i, QTGT)) = r_max(w.at(ipr(d, i, QREST)), bias);
+}
+
+// ====================================================== phase B: the sweep
+// Rows act on body velocities held in registers (BV); the generic sweep
+// loads/stores them around each row, the topology-specialised sweep keeps
+// every body of the env in registers for the whole pass.
+template <class R> struct BV {
+    V3<R> v, w;
+    R m;   // inverse mass
+};
+template <class R> BS_HD BV<R> load_bv(const Dims &d, const Ws<R> &w, int b) {
+    return BV<R>{w.l3(ib(d, b, BV_)), w.l3(ib(d, b, BW)), w.at(ib(d, b, BM))};
+}
+template <class R> BS_HD void store_bv(const Dims &d, const Ws<R> &w, int b, const BV<R> &x) {
+    w.s3(ib(d, b, BV_), x.v);
+    w.s3(ib(d, b, BW), x.w);
+}
+
+// rate along a 1-DOF joint axis (physics.py:804-810) from the hoisted jacobians
+template <class R>
+BS_HD R axis_rate(const Dims &d, const Ws<R> &w, int j, bool lin, const BV<R> &C, const BV<R> &P) {
+    R qd = dot(w.l3(ij(d, j, JX1)), C.w) - dot(w.l3(ij(d, j, JX2)), P.w);
+    if (lin) qd = qd + dot(w.l3(ij(d, j, JAX)), C.v - P.v);
+    return qd;
+}
+template <class R>
+BS_HD void axis_apply(const Dims &d, const Ws<R> &w, int j, bool lin, R lam, BV<R> &C, BV<R> &P) {
+    C.w = C.w + w.l3(ij(d, j, JY1)) * lam;
+    P.w = P.w - w.l3(ij(d, j, JY2)) * lam;
+    if (lin) {
+        V3<R> a = w.l3(ij(d, j, JAX));
+        C.v = C.v + a * (lam * C.m);
+        P.v = P.v - a * (lam * P.m);
+    }
+}
+
+// PD drive / direct actuation / joint friction (physics.py:812-848)
+template <class R>
+BS_HD void row_drive(const Ctx<R> &c, const Ws<R> &w, int j, int dof, bool lin, BV<R> &C, BV<R> &P) {
+    const Dims &d = c.d;
+    R qd = axis_rate(d, w, j, lin, C, P);
+    const R mfh = w.at(ij(d, j, JMFH));
+    R lam = w.at(ij(d, j, JLF)) + clampr(w.at(ij(d, j, JDA)) - w.at(ij(d, j, JDB)) * qd, -mfh, mfh);
+    R frh = w.at(ij(d, j, JFRH));
+    if (frh > R(0)) lam = lam + clampr(-qd * w.at(ij(d, j, JMEFF)), -frh, frh);
+    axis_apply(d, w, j, lin, lam, C, P);
+    w.at(idf(d, dof, DIMP)) += lam;
 }
 
 // one-sided limit (physics.py:850-870)
-template <class R> BS_HD void row_limit(const Ctx<R> &c, const Ws<R> &w, int j, R h, bool biased) {
-    const auto &jt = c.joints[j];
+template <class R>
+BS_HD void row_limit(const Ctx<R> &c, const Ws<R> &w, int j, int dof, bool lin, BV<R> &C, BV<R> &P) {
     const Dims &d = c.d;
-    R lo = w.at(ij(d, j, JLO)), hi = w.at(ij(d, j, JHI));
-    R q = biased ? w.at(ij(d, j, JQ0)) : w.at(idf(d, jt.dof, DQ0));
-    if (!(q < lo) && !(q > hi)) return;
-    const bool lin = jt.kind == BSIM_PRISMATIC;
-    const int p = jt.parent, ch = jt.child;
-    V3<R> wc = w.l3(ib(d, ch, BW)), wp = w.l3(ib(d, p, BW));
-    R qd = dot(w.l3(ij(d, j, JX1)), wc) - dot(w.l3(ij(d, j, JX2)), wp);
-    V3<R> a = w.l3(ij(d, j, JAX));
-    V3<R> vc, vp;
-    if (lin) {
-        vc = w.l3(ib(d, ch, BV));
-        vp = w.l3(ib(d, p, BV));
-        qd = qd + dot(a, vc - vp);
-    }
-    R meff = w.at(ij(d, j, JMEFF));
-    R lam = R(0);
-    if (q < lo) lam = r_max(meff * ((biased ? r_max(lo - q, R(0)) / h : R(0)) - qd), R(0));
-    if (q > hi) lam = -r_max(meff * ((biased ? r_max(q - hi, R(0)) / h : R(0)) + qd), R(0));
-    w.s3(ib(d, ch, BW), wc + w.l3(ij(d, j, JY1)) * lam);
-    w.s3(ib(d, p, BW), wp - w.l3(ij(d, j, JY2)) * lam);
-    if (lin) {
-        w.s3(ib(d, ch, BV), vc + a * (lam * w.at(ib(d, ch, BM))));
-        w.s3(ib(d, p, BV), vp - a * (lam * w.at(ib(d, p, BM))));
-    }
-    w.at(idf(d, jt.dof, DIMP)) += lam;
+    R state = w.at(ij(d, j, JLV));
+    if (state == R(0)) return;
+    R qd = axis_rate(d, w, j, lin, C, P);
+    R meff = w.at(ij(d, j, JMEFF)), bias = w.at(ij(d, j, JLB));
+    R lam = state == R(1) ? r_max(meff * (bias - qd), R(0)) : -r_max(meff * (bias + qd), R(0));
+    axis_apply(d, w, j, lin, lam, C, P);
+    w.at(idf(d, dof, DIMP)) += lam;
 }
 
-// point-3 (872-890) or prismatic perpendicular pair (908-928): P = G d
-template <class R> BS_HD void row_linear(const Ctx<R> &c, const Ws<R> &w, int j, R h, bool biased) {
-    const auto &jt = c.joints[j];
-    const Dims &d = c.d;
-    const int p = jt.parent, ch = jt.child;
-    V3<R> vc = w.l3(ib(d, ch, BV)), wc = w.l3(ib(d, ch, BW));
-    V3<R> vp = w.l3(ib(d, p, BV)), wp = w.l3(ib(d, p, BW));
-    V3<R> rel = (vc + cross(wc, w.l3(ij(d, j, JRC)))) - (vp + cross(wp, w.l3(ij(d, j, JRP))));
-    V3<R> tgt = zero3<R>();
-    if (biased) {
-        V3<R> pe = w.l3(ij(d, j, JPE));
-        tgt = v3(-pe.x / h, -pe.y / h, -pe.z / h);
-    }
-    V3<R> P = smul(w.lS(ij(d, j, JKI)), tgt - rel);
-    w.s3(ib(d, ch, BV), vc + P * w.at(ib(d, ch, BM)));
-    w.s3(ib(d, ch, BW), wc + mmul(w.lM(ij(d, j, JMC)), P));
-    w.s3(ib(d, p, BV), vp - P * w.at(ib(d, p, BM)));
-    w.s3(ib(d, p, BW), wp - mmul(w.lM(ij(d, j, JMP)), P));
+// point-3 (872-890) or prismatic perpendicular pair (908-928): P = G (tgt - rel)
+template <class R> BS_HD void row_linear(const Dims &d, const Ws<R> &w, int j, BV<R> &C, BV<R> &P) {
+    V3<R> rel = (C.v + cross(C.w, w.l3(ij(d, j, JRC)))) - (P.v + cross(P.w, w.l3(ij(d, j, JRP))));
+    V3<R> imp = smul(w.lS(ij(d, j, JKI)), w.l3(ij(d, j, JPE)) - rel);
+    C.v = C.v + imp * C.m;
+    C.w = C.w + mmul(w.lM(ij(d, j, JMC)), imp);
+    P.v = P.v - imp * P.m;
+    P.w = P.w - mmul(w.lM(ij(d, j, JMP)), imp);
 }
 
 // angular rows (892-906): omega_c += Hc d, omega_p -= Hp d
-template <class R> BS_HD void row_angular(const Ctx<R> &c, const Ws<R> &w, int j, R h, bool biased) {
-    const auto &jt = c.joints[j];
-    const Dims &d = c.d;
-    const int p = jt.parent, ch = jt.child;
-    V3<R> wc = w.l3(ib(d, ch, BW)), wp = w.l3(ib(d, p, BW));
-    V3<R> tgt = zero3<R>();
-    if (biased) {
-        V3<R> re = w.l3(ij(d, j, JRE));
-        tgt = v3(-re.x / h, -re.y / h, -re.z / h);
-    }
-    V3<R> dv = tgt - (wc - wp);
-    w.s3(ib(d, ch, BW), wc + mmul(w.lM(ij(d, j, JHC)), dv));
-    w.s3(ib(d, p, BW), wp - mmul(w.lM(ij(d, j, JHP)), dv));
+template <class R> BS_HD void row_angular(const Dims &d, const Ws<R> &w, int j, BV<R> &C, BV<R> &P) {
+    V3<R> dv = w.l3(ij(d, j, JRE)) - (C.w - P.w);
+    C.w = C.w + mmul(w.lM(ij(d, j, JHC)), dv);
+    P.w = P.w - mmul(w.lM(ij(d, j, JHP)), dv);
 }
 
-// plane contact row (930-983) with the plane's fixed normal/tangents
-template <class R> BS_HD void row_plane(const Ctx<R> &c, const Ws<R> &w, int i, bool biased) {
+// all rows of joint j in reference order (physics.py:761-773)
+template <class R>
+BS_HD void joint_rows(const Ctx<R> &c, const Ws<R> &w, int j, int kind, int dof, bool limits, bool biased,
+                      BV<R> &C, BV<R> &P) {
+    const Dims &d = c.d;
+    const bool axis = dof >= 0 && kind != BSIM_SPHERICAL;
+    const bool lin = kind == BSIM_PRISMATIC;
+    if (biased && axis) row_drive(c, w, j, dof, lin, C, P);
+    if (kind != BSIM_PRISMATIC) row_linear(d, w, j, C, P);
+    if (kind != BSIM_SPHERICAL) row_angular(d, w, j, C, P);
+    if (kind == BSIM_PRISMATIC) row_linear(d, w, j, C, P);
+    if (axis && limits) row_limit(c, w, j, dof, lin, C, P);
+}
+
+// plane contact row (930-983) with the plane's fixed normal / tangents
+template <class R> BS_HD void row_plane(const Ctx<R> &c, const Ws<R> &w, int i, BV<R> &X) {
     const Dims &d = c.d;
     if (w.at(ipl(d, i, CACT)) == R(0)) return;
-    const R dt = c.p.dt;
-    const int b = c.L.plane_body[i];
-    const R im = w.at(ib(d, b, BM));
-    V3<R> v = w.l3(ib(d, b, BV)), om = w.l3(ib(d, b, BW));
-    R vn = v.z + dot(w.l3(ipl(d, i, CXN)), om);
-    R depth = w.at(ipl(d, i, CD0));
-    if (biased) depth = depth + w.at(ib(d, b, BDP) + 2) * R(-1);
-    R bias = biased ? c.p.max_bias * r_max(depth, R(0)) / dt : R(0);
-    R target = r_max(w.at(ipl(d, i, CREST)), bias);
+    R vn = X.v.z + dot(w.l3(ipl(d, i, CXN)), X.w);
     R lam_n = w.at(ipl(d, i, CLN));
-    R dl = w.at(ipl(d, i, CMN)) * (target - vn);
+    R dl = w.at(ipl(d, i, CMN)) * (w.at(ipl(d, i, CTGT)) - vn);
     R nl = r_max(lam_n + dl, R(0));
     dl = nl - lam_n;
     lam_n = lam_n + dl;
     w.at(ipl(d, i, CLN)) = lam_n;
-    v.z = v.z + dl * im;
-    om = om + w.l3(ipl(d, i, CIXN)) * dl;
+    X.v.z = X.v.z + dl * X.m;
+    X.w = X.w + w.l3(ipl(d, i, CIXN)) * dl;
     // friction with t1 = (0,-1,0), t2 = (1,0,0)
-    R vt1 = -v.y + dot(w.l3(ipl(d, i, CX1)), om);
-    R vt2 = v.x + dot(w.l3(ipl(d, i, CX2)), om);
+    R vt1 = -X.v.y + dot(w.l3(ipl(d, i, CX1)), X.w);
+    R vt2 = X.v.x + dot(w.l3(ipl(d, i, CX2)), X.w);
     R mu = r_sqrt(vt1 * vt1 + vt2 * vt2) > R(1e-3) ? w.at(d.o_env + EMUD) : w.at(d.o_env + EMUS);
-    if (biased) {
-        R tex = w.at(ipl(d, i, CTE)) + w.at(ib(d, b, BDP));
-        R tey = w.at(ipl(d, i, CTE + 1)) + w.at(ib(d, b, BDP) + 1);
-        vt1 = vt1 + (-tey) / dt;
-        vt2 = vt2 + tex / dt;
-    }
+    vt1 = vt1 + w.at(ipl(d, i, CST1));
+    vt2 = vt2 + w.at(ipl(d, i, CST2));
     R lt0 = w.at(ipl(d, i, CLT)), lt1 = w.at(ipl(d, i, CLT + 1));
     R c0 = lt0 + (-w.at(ipl(d, i, CM1)) * vt1), c1 = lt1 + (-w.at(ipl(d, i, CM2)) * vt2);
     R lim = mu * lam_n;
-    R nrm = r_sqrt(c0 * c0 + c1 * c1);
-    R sc = nrm > lim ? lim / r_max(nrm, R(1e-12)) : R(1);
-    c0 = c0 * sc;
-    c1 = c1 * sc;
+    R nrm2 = c0 * c0 + c1 * c1;
+    if (nrm2 > lim * lim) {  // circular cone clamp
+        R nrm = r_sqrt(nrm2);
+        if (nrm > lim) {
+            R sc = lim / r_max(nrm, R(1e-12));
+            c0 = c0 * sc;
+            c1 = c1 * sc;
+        }
+    }
     R d0 = c0 - lt0, d1 = c1 - lt1;
     w.at(ipl(d, i, CLT)) = lt0 + d0;
     w.at(ipl(d, i, CLT + 1)) = lt1 + d1;
-    v.x = v.x + d1 * im;
-    v.y = v.y + (-d0) * im;
-    om = om + w.l3(ipl(d, i, CIX1)) * d0 + w.l3(ipl(d, i, CIX2)) * d1;
-    w.s3(ib(d, b, BV), v);
-    w.s3(ib(d, b, BW), om);
+    X.v.x = X.v.x + d1 * X.m;
+    X.v.y = X.v.y + (-d0) * X.m;
+    X.w = X.w + w.l3(ipl(d, i, CIX1)) * d0 + w.l3(ipl(d, i, CIX2)) * d1;
 }
 
-// sphere-sphere pair row (930-983, pair branches)
-template <class R> BS_HD void row_pair(const Ctx<R> &c, const Ws<R> &w, int i, bool biased) {
+// sphere-sphere pair row (930-983, pair branches); A = body a, X = body b
+template <class R> BS_HD void row_pair(const Ctx<R> &c, const Ws<R> &w, int i, BV<R> &A, BV<R> &X) {
     const Dims &d = c.d;
     if (w.at(ipr(d, i, QACT)) == R(0)) return;
-    const R dt = c.p.dt;
-    const int pa = c.L.pair_body[2 * i], pb = c.L.pair_body[2 * i + 1];
-    const R ma = w.at(ib(d, pa, BM)), mb = w.at(ib(d, pb, BM));
     V3<R> n = w.l3(ipr(d, i, QN)), t1 = w.l3(ipr(d, i, QT1)), t2 = w.l3(ipr(d, i, QT2));
-    V3<R> va = w.l3(ib(d, pa, BV)), wa = w.l3(ib(d, pa, BW));
-    V3<R> vb = w.l3(ib(d, pb, BV)), wb = w.l3(ib(d, pb, BW));
     V3<R> xn = w.l3(ipr(d, i, QXN)), yn = w.l3(ipr(d, i, QYN));
-    R vn = dot(n, vb - va) + dot(xn, wb) - dot(yn, wa);
-    R depth = w.at(ipr(d, i, QD0));
-    if (biased) depth = depth + dot(n, w.l3(ib(d, pb, BDP)) - w.l3(ib(d, pa, BDP))) * R(-1);
-    R bias = biased ? c.p.max_bias * r_max(depth, R(0)) / dt : R(0);
-    R target = r_max(w.at(ipr(d, i, QREST)), bias);
+    R vn = dot(n, X.v - A.v) + dot(xn, X.w) - dot(yn, A.w);
     R lam_n = w.at(ipr(d, i, QLN));
-    R dl = w.at(ipr(d, i, QMN)) * (target - vn);
+    R dl = w.at(ipr(d, i, QMN)) * (w.at(ipr(d, i, QTGT)) - vn);
     R nl = r_max(lam_n + dl, R(0));
     dl = nl - lam_n;
     lam_n = lam_n + dl;
     w.at(ipr(d, i, QLN)) = lam_n;
-    vb = vb + n * (dl * mb);
-    wb = wb + w.l3(ipr(d, i, QIXN)) * dl;
-    va = va - n * (dl * ma);
-    wa = wa - w.l3(ipr(d, i, QIYN)) * dl;
-    V3<R> x1 = w.l3(ipr(d, i, QX1)), x2 = w.l3(ipr(d, i, QX2));
-    V3<R> y1 = w.l3(ipr(d, i, QY1)), y2 = w.l3(ipr(d, i, QY2));
-    V3<R> dv = vb - va;
-    R vt1 = dot(t1, dv) + dot(x1, wb) - dot(y1, wa);
-    R vt2 = dot(t2, dv) + dot(x2, wb) - dot(y2, wa);
+    X.v = X.v + n * (dl * X.m);
+    X.w = X.w + w.l3(ipr(d, i, QIXN)) * dl;
+    A.v = A.v - n * (dl * A.m);
+    A.w = A.w - w.l3(ipr(d, i, QIYN)) * dl;
+    V3<R> dv = X.v - A.v;
+    R vt1 = dot(t1, dv) + dot(w.l3(ipr(d, i, QX1)), X.w) - dot(w.l3(ipr(d, i, QY1)), A.w);
+    R vt2 = dot(t2, dv) + dot(w.l3(ipr(d, i, QX2)), X.w) - dot(w.l3(ipr(d, i, QY2)), A.w);
     R mu = r_sqrt(vt1 * vt1 + vt2 * vt2) > R(1e-3) ? w.at(d.o_env + EMUD) : w.at(d.o_env + EMUS);
     R lt0 = w.at(ipr(d, i, QLT)), lt1 = w.at(ipr(d, i, QLT + 1));
     R c0 = lt0 + (-w.at(ipr(d, i, QM1)) * vt1), c1 = lt1 + (-w.at(ipr(d, i, QM2)) * vt2);
     R lim = mu * lam_n;
-    R nrm = r_sqrt(c0 * c0 + c1 * c1);
-    R sc = nrm > lim ? lim / r_max(nrm, R(1e-12)) : R(1);
-    c0 = c0 * sc;
-    c1 = c1 * sc;
+    R nrm2 = c0 * c0 + c1 * c1;
+    if (nrm2 > lim * lim) {
+        R nrm = r_sqrt(nrm2);
+        if (nrm > lim) {
+            R sc = lim / r_max(nrm, R(1e-12));
+            c0 = c0 * sc;
+            c1 = c1 * sc;
+        }
+    }
     R d0 = c0 - lt0, d1 = c1 - lt1;
     w.at(ipr(d, i, QLT)) = lt0 + d0;
     w.at(ipr(d, i, QLT + 1)) = lt1 + d1;
     V3<R> Q = t1 * d0 + t2 * d1;
-    vb = vb + Q * mb;
-    wb = wb + w.l3(ipr(d, i, QIX1)) * d0 + w.l3(ipr(d, i, QIX2)) * d1;
-    va = va - Q * ma;
-    wa = wa - (w.l3(ipr(d, i, QIY1)) * d0 + w.l3(ipr(d, i, QIY2)) * d1);
-    w.s3(ib(d, pa, BV), va);
-    w.s3(ib(d, pa, BW), wa);
-    w.s3(ib(d, pb, BV), vb);
-    w.s3(ib(d, pb, BW), wb);
+    X.v = X.v + Q * X.m;
+    X.w = X.w + w.l3(ipr(d, i, QIX1)) * d0 + w.l3(ipr(d, i, QIX2)) * d1;
+    A.v = A.v - Q * A.m;
+    A.w = A.w - (w.l3(ipr(d, i, QIY1)) * d0 + w.l3(ipr(d, i, QIY2)) * d1);
 }
 
-// one Gauss-Seidel pass for one env (physics.py:760-775)
+// after a biased pass: dpos += v h, dang += w h (physics.py:571-572)
+template <class R> BS_HD void accumulate_deltas(const Dims &d, const Ws<R> &w, int b, const BV<R> &x, R h) {
+    w.s3(ib(d, b, BDP), w.l3(ib(d, b, BDP)) + x.v * h);
+    w.s3(ib(d, b, BDA), w.l3(ib(d, b, BDA)) + x.w * h);
+}
+
+// one Gauss-Seidel pass for one env, any topology (physics.py:760-775)
 template <class R> BS_HD void sweep(const Ctx<R> &c, const Ws<R> &w, R h, bool biased) {
     const Dims &d = c.d;
     for (int j = 0; j < d.J; ++j) {
         const auto &jt = c.joints[j];
-        const int kind = jt.kind;
-        const bool axis = jt.dof >= 0 && kind != BSIM_SPHERICAL;
-        if (biased && axis) row_drive(c, w, j, h);
-        if (kind != BSIM_PRISMATIC) row_linear(c, w, j, h, biased);
-        if (kind != BSIM_SPHERICAL) row_angular(c, w, j, h, biased);
-        if (kind == BSIM_PRISMATIC) row_linear(c, w, j, h, biased);
-        if (axis && jt.has_limits) row_limit(c, w, j, h, biased);
+        BV<R> C = load_bv(d, w, jt.child), P = load_bv(d, w, jt.parent);
+        joint_rows(c, w, j, jt.kind, jt.dof, jt.has_limits != 0, biased, C, P);
+        store_bv(d, w, jt.child, C);
+        store_bv(d, w, jt.parent, P);
     }
-    for (int i = 0; i < d.P; ++i) row_plane(c, w, i, biased);
-    for (int i = 0; i < d.Q; ++i) row_pair(c, w, i, biased);
+    for (int i = 0; i < d.P; ++i) {
+        int b = c.L.plane_body[i];
+        BV<R> X = load_bv(d, w, b);
+        row_plane(c, w, i, X);
+        store_bv(d, w, b, X);
+    }
+    for (int i = 0; i < d.Q; ++i) {
+        int pa = c.L.pair_body[2 * i], pb = c.L.pair_body[2 * i + 1];
+        BV<R> A = load_bv(d, w, pa), X = load_bv(d, w, pb);
+        row_pair(c, w, i, A, X);
+        store_bv(d, w, pa, A);
+        store_bv(d, w, pb, X);
+    }
+    if (biased)
+        for (int b = 0; b < d.B; ++b) accumulate_deltas(d, w, b, load_bv(d, w, b), h);
+}
+
+// The same pass with the topology known at compile time (T = a generated
+// bsim_topologies.cuh entry): every body velocity of the env stays in
+// registers for the whole pass and rows on disjoint bodies can overlap.
+template <class R, class T, int j>
+BS_HD void static_joints(const Ctx<R> &c, const Ws<R> &w, R h, bool biased, BV<R> *bv) {
+    if constexpr (j < T::J) {
+        constexpr int kind = T::kind[j], dof = T::dof[j], ch = T::child[j], pa = T::parent[j];
+        constexpr bool lim = T::limits[j] != 0;
+        joint_rows(c, w, j, kind, dof, lim, biased, bv[ch], bv[pa]);
+        static_joints<R, T, j + 1>(c, w, h, biased, bv);
+    }
+}
+template <class R, class T, int i>
+BS_HD void static_planes(const Ctx<R> &c, const Ws<R> &w, bool biased, BV<R> *bv) {
+    if constexpr (i < T::P) {
+        constexpr int b = T::plane_body[i];
+        row_plane(c, w, i, bv[b]);
+        static_planes<R, T, i + 1>(c, w, biased, bv);
+    }
+}
+template <class R, class T, int i>
+BS_HD void static_pairs(const Ctx<R> &c, const Ws<R> &w, bool biased, BV<R> *bv) {
+    if constexpr (i < T::Q) {
+        constexpr int pa = T::pair_a[i], pb = T::pair_b[i];
+        row_pair(c, w, i, bv[pa], bv[pb]);
+        static_pairs<R, T, i + 1>(c, w, biased, bv);
+    }
+}
+template <class R, class T> BS_HD void sweep_static(const Ctx<R> &c, const Ws<R> &w, R h, bool biased) {
+    const Dims &d = c.d;
+    BV<R> bv[T::B];
+#pragma unroll
+    for (int b = 0; b < T::B; ++b) bv[b] = load_bv(d, w, b);
+    static_joints<R, T, 0>(c, w, h, biased, bv);
+    static_planes<R, T, 0>(c, w, biased, bv);
+    static_pairs<R, T, 0>(c, w, biased, bv);
+#pragma unroll
+    for (int b = 0; b < T::B; ++b) {
+        store_bv(d, w, b, bv[b]);
+        if (biased) accumulate_deltas(d, w, b, bv[b], h);
+    }
+}
+
+// no compile-time topology: use the generic sweep
+struct TopoGeneric {
+    static constexpr bool is_static = false;
+};
+template <class R, class T> BS_HD void sweep_any(const Ctx<R> &c, const Ws<R> &w, R h, bool biased) {
+    if constexpr (T::is_static)
+        sweep_static<R, T>(c, w, h, biased);
+    else
+        sweep(c, w, h, biased);
 }
 
 // ------------------------------------------------------------ tendons
@@ -684,7 +805,7 @@ template <class R> BS_HD void add_w(const Dims &d, const Ws<R> &w, int b, V3<R> 
     w.s3(ib(d, b, BW), w.l3(ib(d, b, BW)) + dw);
 }
 template <class R> BS_HD void add_v(const Dims &d, const Ws<R> &w, int b, V3<R> dv) {
-    w.s3(ib(d, b, BV), w.l3(ib(d, b, BV)) + dv);
+    w.s3(ib(d, b, BV_), w.l3(ib(d, b, BV_)) + dv);
 }
 
 // physics.py:598-653; fixed tendons read the dof_state buffer of the previous
@@ -742,7 +863,7 @@ template <class R> BS_HD void apply_tendons(const Ctx<R> &c, const Ws<R> &w, int
                 V3<R> r = qrot(w.l4(ib(d, b, BQ)), v3(el[i].v[0], el[i].v[1], el[i].v[2]));
                 pts[i] = w.l3(ib(d, b, BP)) + r;
                 V3<R> rr = pts[i] - w.l3(ib(d, b, BP));
-                vel[i] = w.l3(ib(d, b, BV)) + cross(w.l3(ib(d, b, BW)), rr);
+                vel[i] = w.l3(ib(d, b, BV_)) + cross(w.l3(ib(d, b, BW)), rr);
             }
             const int32_t *pth = c.L.spatial_paths + t.path_offset;
             int npaths = pth[0];
@@ -792,50 +913,26 @@ template <class R> BS_HD void apply_tendons(const Ctx<R> &c, const Ws<R> &w, int
         for (int el = it_ % (g).ne, k = it_ / (g).ne, once_ = 1; once_; once_ = 0)
 #define BS_ENVS(g, el) for (int el = (g).tid; el < (g).ne; el += (g).nth)
 
-// refresh (physics.py:718-756): optional effective pose, inertias, joint
-// geometry and all row constants
-template <class R> BS_HD void refresh_group(const Ctx<R> &c, const Grp<R> &g, bool with_deltas) {
-    const Dims &d = c.d;
-    int pitem = BP, qitem = BQ;
-    if (with_deltas) {
-        pitem = BPE;
-        qitem = BQE;
-    }
-    BS_ITEMS(g, d.B, el, b) {
-        Ws<R> w = g.env(el);
-        if (with_deltas) {
-            w.s3(ib(d, b, BPE), w.l3(ib(d, b, BP)) + w.l3(ib(d, b, BDP)));
-            w.s4(ib(d, b, BQE), qnormalize(qmul(qexp(w.l3(ib(d, b, BDA))), w.l4(ib(d, b, BQ)))));
-        }
-        body_inertia(c, w, g.e0 + el, b, qitem);
-    }
-    BS_SYNC();
-    BS_ITEMS(g, d.J, el, j) {
-        Ws<R> w = g.env(el);
-        joint_geometry(c, w, j, pitem, qitem, true);
-        joint_constants(c, w, j);
-    }
-    BS_ITEMS(g, d.P, el, i) { plane_constants(c, g.env(el), i); }
-    BS_ITEMS(g, d.Q, el, i) { pair_constants(c, g.env(el), i); }
-    BS_SYNC();
-}
-
 // Scene.step() for the CTA's envs on the resident workspace
 // (physics.py:538-592).  `write_outputs`: contact-derived outputs of this
 // step go to global memory (the last substep of a fused launch).
-template <class R> BS_HD void group_step(const Ctx<R> &c, const Grp<R> &g, bool write_outputs) {
+//
+// The N biased passes and the final velocity stage share one phase-A body
+// (freeze at k = 0, refresh-with-deltas at 0 < k < N, integrate + refresh at
+// k = N), so every piece of the step appears once in the binary.
+template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> &g, bool write_outputs) {
     const Dims &d = c.d;
     const auto &p = c.p;
     const R dt = p.dt;
     const int N = p.position_iterations;
     const R h = dt / (R)N;
 
-    // external forces, start-of-step inertia (545-555)
+    // external forces, start-of-step inertia (545-555), zeroed TGS deltas (564-566)
     BS_ITEMS(g, d.B, el, b) {
         Ws<R> w = g.env(el);
         body_inertia(c, w, g.e0 + el, b, BQ);
         body_external(c, w, g.e0 + el, b);
-        w.s3(ib(d, b, BDP), zero3<R>());   // TGS delta buffers (564-566)
+        w.s3(ib(d, b, BDP), zero3<R>());
         w.s3(ib(d, b, BDA), zero3<R>());
     }
     BS_SYNC();
@@ -847,67 +944,76 @@ template <class R> BS_HD void group_step(const Ctx<R> &c, const Grp<R> &g, bool 
     if (ld != R(1) || ad != R(1)) {
         BS_ITEMS(g, d.B, el, b) {
             Ws<R> w = g.env(el);
-            w.s3(ib(d, b, BV), w.l3(ib(d, b, BV)) * ld);
+            w.s3(ib(d, b, BV_), w.l3(ib(d, b, BV_)) * ld);
             w.s3(ib(d, b, BW), w.l3(ib(d, b, BW)) * ad);
         }
         BS_SYNC();
     }
-    // read_dof_states (557) + freeze (657-716)
-    BS_ITEMS(g, d.J, el, j) {
-        Ws<R> w = g.env(el);
-        R q[3], qd[3];
-        int n = joint_dofs(c, w, j, q, qd);
-        for (int k = 0; k < n; ++k) {
-            w.at(idf(d, c.joints[j].dof + k, DQ0)) = q[k];
-            w.at(idf(d, c.joints[j].dof + k, DIMP)) = R(0);
-        }
-        if (n == 1) w.at(ij(d, j, JQ0)) = q[0];
-        joint_geometry(c, w, j, BP, BQ, false);
-        joint_constants(c, w, j);
-    }
-    BS_ITEMS(g, d.P, el, i) {
-        Ws<R> w = g.env(el);
-        plane_freeze(c, w, g.e0 + el, i);
-        plane_constants(c, w, i);
-    }
-    BS_ITEMS(g, d.Q, el, i) {
-        Ws<R> w = g.env(el);
-        pair_freeze(c, w, g.e0 + el, i);
-        pair_constants(c, w, i);
-    }
-    BS_SYNC();
 
-    // TGS position iterations (567-572)
-    for (int k = 0; k < N; ++k) {
-        if (k) refresh_group(c, g, true);
-        BS_ENVS(g, el) { sweep(c, g.env(el), h, true); }
-        BS_SYNC();
+    for (int k = 0; k <= N; ++k) {
+        const bool biased = k < N, freeze = k == 0, deltas = k > 0 && k < N;
+        if (k == N) {  // integrate (574-575)
+            BS_ITEMS(g, d.B, el, b) {
+                Ws<R> w = g.env(el);
+                w.s3(ib(d, b, BP), w.l3(ib(d, b, BP)) + w.l3(ib(d, b, BDP)));
+                w.s4(ib(d, b, BQ), qnormalize(qmul(qexp(w.l3(ib(d, b, BDA))), w.l4(ib(d, b, BQ)))));
+            }
+            BS_SYNC();
+        }
+        // phase A: poses -> inertias -> joint/contact geometry and row constants
+        // (freeze 657-716, refresh 718-756)
+        const int pitem = deltas ? BPE : BP, qitem = deltas ? BQE : BQ;
         BS_ITEMS(g, d.B, el, b) {
             Ws<R> w = g.env(el);
-            w.s3(ib(d, b, BDP), w.l3(ib(d, b, BDP)) + w.l3(ib(d, b, BV)) * h);
-            w.s3(ib(d, b, BDA), w.l3(ib(d, b, BDA)) + w.l3(ib(d, b, BW)) * h);
+            if (deltas) {
+                w.s3(ib(d, b, BPE), w.l3(ib(d, b, BP)) + w.l3(ib(d, b, BDP)));
+                w.s4(ib(d, b, BQE), qnormalize(qmul(qexp(w.l3(ib(d, b, BDA))), w.l4(ib(d, b, BQ)))));
+            }
+            if (!freeze) body_inertia(c, w, g.e0 + el, b, qitem);
         }
         BS_SYNC();
-    }
-    // integrate (574-575), refresh from the new poses, velocity passes (579-581)
-    BS_ITEMS(g, d.B, el, b) {
-        Ws<R> w = g.env(el);
-        w.s3(ib(d, b, BP), w.l3(ib(d, b, BP)) + w.l3(ib(d, b, BDP)));
-        w.s4(ib(d, b, BQ), qnormalize(qmul(qexp(w.l3(ib(d, b, BDA))), w.l4(ib(d, b, BQ)))));
-    }
-    BS_SYNC();
-    refresh_group(c, g, false);
-    for (int k = 0; k < p.velocity_iterations; ++k) {
-        BS_ENVS(g, el) { sweep(c, g.env(el), h, false); }
+        BS_ITEMS(g, d.J, el, j) {
+            Ws<R> w = g.env(el);
+            if (freeze) {  // read_dof_states (557): q0 and the unbiased limit rows' q
+                R q[3], qd[3];
+                int n = joint_dofs(c, w, j, q, qd);
+                for (int kk = 0; kk < n; ++kk) {
+                    w.at(idf(d, c.joints[j].dof + kk, DQ0)) = q[kk];
+                    w.at(idf(d, c.joints[j].dof + kk, DIMP)) = R(0);
+                }
+                if (n == 1) w.at(ij(d, j, JQ0)) = q[0];
+            }
+            joint_geometry(c, w, j, pitem, qitem, !freeze);
+            joint_constants(c, w, j);
+            joint_pass_constants(c, w, j, h, biased);
+        }
+        BS_ITEMS(g, d.P, el, i) {
+            Ws<R> w = g.env(el);
+            if (freeze) plane_freeze(c, w, g.e0 + el, i);
+            plane_constants(c, w, i);
+            plane_pass_constants(c, w, i, biased);
+        }
+        BS_ITEMS(g, d.Q, el, i) {
+            Ws<R> w = g.env(el);
+            if (freeze) pair_freeze(c, w, g.e0 + el, i);
+            pair_constants(c, w, i);
+            pair_pass_constants(c, w, i, biased);
+        }
         BS_SYNC();
+        // phase B: one biased pass (567-572) or the velocity passes (580-581)
+        const int reps = biased ? 1 : p.velocity_iterations;
+        for (int r = 0; r < reps; ++r) {
+            BS_ENVS(g, el) { sweep_any<R, T>(c, g.env(el), h, biased); }
+            BS_SYNC();
+        }
     }
     // velocity clamps (584-587)
     BS_ITEMS(g, d.B, el, b) {
         Ws<R> w = g.env(el);
-        V3<R> lv = w.l3(ib(d, b, BV)), av = w.l3(ib(d, b, BW));
+        V3<R> lv = w.l3(ib(d, b, BV_)), av = w.l3(ib(d, b, BW));
         R sl = r_min(R(1), p.max_linear_velocity / r_max(norm(lv), R(1e-12)));
         R sa = r_min(R(1), p.max_angular_velocity / r_max(norm(av), R(1e-12)));
-        w.s3(ib(d, b, BV), lv * sl);
+        w.s3(ib(d, b, BV_), lv * sl);
         w.s3(ib(d, b, BW), av * sa);
     }
     // friction anchors (1021-1033)

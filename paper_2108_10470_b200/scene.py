@@ -54,7 +54,7 @@ class Scene:
 
     def __init__(self, models, num_envs, params: SimParams | None = None, spacing=4.0,
                  ground=True, env_origins=None, device=None, precision="fp32",
-                 env_offset=0, total_envs=None, stream=None):
+                 env_offset=0, total_envs=None, stream=None, specialize=True):
         if not torch.cuda.is_available():
             raise N.NativeError("paper_2108_10470_b200.Scene needs a CUDA device (no CPU fallback)")
         if isinstance(models, ArticulationModel):
@@ -76,6 +76,9 @@ class Scene:
         self.total_envs = int(total_envs) if total_envs is not None else self.env_offset + E
 
         L = self.layout = SceneLayout(self.models, ground)
+        # AOT-specialised step kernel for known topologies (codegen.py), else generic
+        from .codegen import topology_id
+        self.topology_id = topology_id(L) if specialize else 0
         self.actors_per_env, self.bodies_per_env = L.actors_per_env, L.bodies_per_env
         self.dofs_per_env, self.sensors_per_env = L.dofs_per_env, L.sensors_per_env
         self.num_bodies, self.num_dofs = E * L.bodies_per_env, E * L.dofs_per_env
@@ -121,7 +124,8 @@ class Scene:
     def _structs(self):
         if self._struct_cache is None:
             ptrs = {k: v.data_ptr() for k, v in self._tab.items()}
-            lay = tables.layout_struct(self.layout, self.num_envs, ptrs, self.env_offset)
+            lay = tables.layout_struct(self.layout, self.num_envs, ptrs, self.env_offset,
+                                       self.topology_id)
             sp = {}
             for name in _STATE_TENSORS:
                 t = self.__dict__["_friction_anchor" if name == "friction_anchor" else name]

@@ -116,8 +116,10 @@ def init_state_arrays(L: SceneLayout, E: int, params: SimParams, env_origins: np
     return a
 
 
-def layout_struct(L: SceneLayout, E: int, ptrs: dict, env_offset: int = 0) -> N.Layout:
+def layout_struct(L: SceneLayout, E: int, ptrs: dict, env_offset: int = 0,
+                  topology_id: int = 0) -> N.Layout:
     s = N.Layout()
+    s.topology_id = topology_id
     (s.num_envs, s.actors_per_env, s.bodies_per_env, s.dofs_per_env, s.joints_per_env,
      s.planes_per_env, s.pairs_per_env, s.sensors_per_env, s.tendons_per_env, s.env_offset) = (
         E, L.actors_per_env, L.bodies_per_env, L.dofs_per_env, L.joints_per_env,

@@ -16,7 +16,8 @@ ROOT = os.path.dirname(os.path.dirname(HERE))
 
 def build():
     srcs = [os.path.join(HERE, "host_step.cu")] + [
-        os.path.join(ROOT, "paper_2108_10470_b200", "csrc", f) for f in ("bsim_step.cuh", "bsim_math.cuh")]
+        os.path.join(ROOT, "paper_2108_10470_b200", "csrc", f)
+        for f in ("bsim_step.cuh", "bsim_math.cuh", "bsim_topologies.cuh")]
     if os.path.exists(SO) and os.path.getmtime(SO) >= max(os.path.getmtime(s) for s in srcs):
         return SO
     os.makedirs(os.path.dirname(SO), exist_ok=True)
@@ -26,7 +27,9 @@ def build():
 
 
 class HostKernel:
-    def __init__(self, layout, num_envs, params, env_origins, fp64=False):
+    def __init__(self, layout, num_envs, params, env_origins, fp64=False, specialize=True):
+        from paper_2108_10470_b200.codegen import topology_id
+        self.topo = topology_id(layout) if specialize else 0
         self.L = layout
         self.E = num_envs
         self.params = params
@@ -38,7 +41,8 @@ class HostKernel:
         self.lib.hk_step_f64.argtypes = [C.POINTER(N.Layout), C.POINTER(N.Params64), C.POINTER(N.State), C.c_int]
 
     def step(self, n=1):
-        lay = tables.layout_struct(self.L, self.E, {k: v.ctypes.data for k, v in self.tab.items()})
+        lay = tables.layout_struct(self.L, self.E, {k: v.ctypes.data for k, v in self.tab.items()},
+                                   topology_id=self.topo)
         st = tables.state_struct({k: v.ctypes.data for k, v in self.arr.items()})
         par = tables.params_struct(self.params, self.fp64)
         fn = self.lib.hk_step_f64 if self.fp64 else self.lib.hk_step

@@ -6,11 +6,12 @@
 #include <vector>
 
 #include "../../paper_2108_10470_b200/csrc/bsim_step.cuh"
+#include "../../paper_2108_10470_b200/csrc/bsim_topologies.cuh"
 
 using namespace bsim;
 
-template <class R>
-static void run(const bsim_layout_t *L, const typename Abi<R>::Params *p, const typename Abi<R>::State *s,
+template <class R, class T>
+static void run_t(const bsim_layout_t *L, const typename Abi<R>::Params *p, const typename Abi<R>::State *s,
                 int n_substeps) {
     Ctx<R> c;
     c.L = *L;
@@ -29,7 +30,7 @@ static void run(const bsim_layout_t *L, const typename Abi<R>::Params *p, const 
                 g.env(e).at(ib(d, b, BP) + k) = s->body_q[13 * ((size_t)e * d.B + b) + k];
     stage_group(c, g);
     for (int st = 0; st < n_substeps; ++st) {
-        group_step(c, g, st == n_substeps - 1);
+        group_step<R, T>(c, g, st == n_substeps - 1);
         if (d.T && st != n_substeps - 1) readout_group(c, g);
     }
     readout_group(c, g);
@@ -47,6 +48,19 @@ static void run(const bsim_layout_t *L, const typename Abi<R>::Params *p, const 
             for (int k = 0; k < 13; ++k)
                 s->root_state[13 * ((size_t)e * d.A + a) + k] =
                     s->body_state[13 * ((size_t)e * d.B + L->actor_body_offset[a]) + k];
+    }
+}
+
+template <class R>
+static void run(const bsim_layout_t *L, const typename Abi<R>::Params *p, const typename Abi<R>::State *s, int n) {
+    switch (L->topology_id) {
+#define HK_TOPO(ID, TYPE) \
+    case ID:              \
+        return run_t<R, TYPE>(L, p, s, n);
+        BSIM_TOPOLOGIES(HK_TOPO)
+#undef HK_TOPO
+    default:
+        return run_t<R, TopoGeneric>(L, p, s, n);
     }
 }
 

@@ -25,12 +25,13 @@ def _local(arr, t, E, B, key):
     return bq, arr[f"{key}_friction_anchor"][t] - org[None]
 
 
-def _host(case, fp64):
+def _host(case, fp64, specialize=True):
     from hostkernel.hk import HostKernel
     from paper_2108_10470_b200.layout import SceneLayout
     meta, arr = load(case)
     L = SceneLayout(build_models(meta), meta["ground"])
-    hk = HostKernel(L, meta["num_envs"], sim_params(meta), arr["param_env_origins"], fp64=fp64)
+    hk = HostKernel(L, meta["num_envs"], sim_params(meta), arr["param_env_origins"], fp64=fp64,
+                    specialize=specialize)
     for k in PARAMS:
         hk.arr[k][...] = arr[f"param_{k}"]
     return meta, arr, L, hk
@@ -45,9 +46,10 @@ def _load(hk, arr, t, E, B):
         hk.arr[k][...] = arr[f"in_{k}"][t]
 
 
+@pytest.mark.parametrize("specialize", [True, False])
 @pytest.mark.parametrize("case", physics_cases())
-def test_host_build_fp64_matches_reference(case):
-    meta, arr, L, hk = _host(case, True)
+def test_host_build_fp64_matches_reference(case, specialize):
+    meta, arr, L, hk = _host(case, True, specialize)
     E, B = meta["num_envs"], L.bodies_per_env
     for t in range(meta["steps"]):
         _load(hk, arr, t, E, B)
