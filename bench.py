@@ -1,0 +1,318 @@
+"""Throughput benchmark of the batched control step (physics + task layer).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--envs E] [--precision fp32|fp64]
+    python bench.py --impl reference ...          # the CPU reference arm
+
+One "step" = one control step of the Ant-analog locomotion task for every
+env: fused action mapping + 2 physics substeps (TGS, 8 position / 1 velocity
+iterations) + reward / done / observation / auto-reset (reference
+`EnvBatch.step`, envs.py:178-200).  Workload = BASELINE.json north-star
+configuration: Ant at 16384 envs per GPU, control dt 1/60, 2 substeps,
+uniform random actions.  Multi-GPU: one process per GPU (torchrun), each
+rank owns a contiguous global env range (weak scaling, no data-path
+collective); timing is the max over ranks.
+
+Timed-region rules: W untimed warm-up steps; K timed steps, each bracketed by
+CUDA events on the launching stream, an L2 flush (256 MiB write) between
+steps outside the events; barrier + synchronize on both sides.  `value` uses
+device-resident inputs; `e2e` repeats the run through the public EnvBatch API
+with the actions copied from pinned host memory and obs / reward / done
+copied back every step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "env-steps/sec (whole box) at 1/2/4/8 B200 vs host-CPU ref; % of HBM roofline"
+UNIT = "env-steps/s"
+WORKLOAD = "ant-quadruped locomotion, 16384 envs/GPU, control dt 1/60 (2 substeps), random actions"
+
+
+def dist_info():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return json.load(f), "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu):
+        self.gpu, self.samples, self.proc = gpu, [], None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons}
+
+
+def kernel_bytes(env):
+    """Compulsory HBM bytes of one fused step-kernel launch (reads + writes of
+    every array the launch touches, counted once), per env."""
+    s = env.scene
+    E = s.num_envs
+    read = ("body_q", "friction_anchor", "inv_mass", "inv_inertia_local", "gravity", "mu_static",
+            "mu_dynamic", "joint_stiffness", "joint_damping", "joint_armature", "joint_friction",
+            "joint_limit_lo", "joint_limit_hi", "plane_off", "plane_rad", "ctrl_dof_vel_target",
+            "ctrl_dof_force", "ctrl_body_force", "ctrl_body_torque", "dof_mode", "env_origins",
+            "nonfinite")
+    write = ("body_q", "friction_anchor", "body_state", "root_state", "dof_state", "net_contact",
+             "dof_force", "sensor_forces", "ctrl_dof_pos_target")
+    def nb(name):
+        t = s._friction_anchor if name == "friction_anchor" else getattr(s, name)
+        return t.numel() * t.element_size()
+    total = sum(nb(n) for n in read) + sum(nb(n) for n in write)
+    total += 2 * env.actions.numel() * env.actions.element_size()   # actions in, clipped out
+    return total / E
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_info()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl")
+    from paper_2108_10470_b200.envs import make_env
+
+    E = args.envs
+    env = make_env("quadruped", num_envs=E, seed=args.seed, precision=args.precision,
+                   env_offset=rank * E, total_envs=world * E)
+    dev = env.scene.device
+    stream = torch.cuda.current_stream()
+    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+    acts = [torch.rand((E, env.act_dim), generator=gen, device=dev, dtype=env.scene.dtype) * 2 - 1
+            for _ in range(8)]
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    # ---------------- device-resident inputs
+    for i in range(args.warmup):
+        env.step(acts[i % len(acts)])
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        for i in range(args.steps):
+            flush.zero_()                       # L2 flush between timed steps (outside the events)
+            ev[i][0].record(stream)
+            env.step(acts[i % len(acts)])
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = sum(a.elapsed_time(b) for a, b in ev)
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total = float(t.item())
+    value = world * E * args.steps / (ms_total / 1e3)
+
+    # ---------------- dominant kernel alone: the fused physics launch
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.zero_()
+        kev[i][0].record(stream)
+        env.scene.step(2, actions=acts[i % len(acts)], action_scale=env.action_scale,
+                       actions_clipped=env.actions)
+        kev[i][1].record(stream)
+    torch.cuda.synchronize()
+    k_ms = sum(a.elapsed_time(b) for a, b in kev) / args.steps
+    env.reset()
+
+    # ---------------- end to end through the public API with host buffers
+    h_act = [a.cpu().pin_memory() for a in acts]
+    h_obs = torch.empty(env.obs.shape, dtype=env.obs.dtype, pin_memory=True)
+    h_rew = torch.empty(env.reward.shape, dtype=env.reward.dtype, pin_memory=True)
+    h_done = torch.empty(env.done.shape, dtype=env.done.dtype, pin_memory=True)
+    for i in range(args.warmup):
+        out = env.step(h_act[i % len(h_act)].to(dev, non_blocking=True))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(args.steps):
+        a = h_act[i % len(h_act)].to(dev, non_blocking=True)
+        out = env.step(a)
+        h_obs.copy_(out.obs, non_blocking=True)
+        h_rew.copy_(out.reward, non_blocking=True)
+        h_done.copy_(out.done, non_blocking=True)
+        torch.cuda.current_stream().synchronize()   # the host consumes the step's results
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e = world * E * args.steps / (float(t.item()) / 1e3)
+    h2d = h_act[0].numel() * h_act[0].element_size()
+    d2h = (h_obs.numel() * h_obs.element_size() + h_rew.numel() * h_rew.element_size()
+           + h_done.numel() * h_done.element_size())
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    pk, src = peaks()
+    bytes_env = kernel_bytes(env)
+    achieved = bytes_env * E / (k_ms / 1e3) / 1e9
+    # FP32 issue bound: ~9.3e4 flop per env-sim-step, 2 substeps per launch
+    flops = 9.3e4 * 2 * E
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32" if args.precision == "fp32" else "f64",
+        "data": "synthetic (uniform random actions, bundled Ant-analog model, no checkpoints)",
+        "config": {"workload": WORKLOAD, "model": "quadruped (Ant analog, 9 bodies / 8 DOF)",
+                   "envs_per_gpu": E, "global_envs": world * E, "substeps": 2,
+                   "position_iterations": 8, "velocity_iterations": 1, "precision": args.precision,
+                   "parallelism": f"env-shard x{world}", "l2": "flushed between timed steps (256 MiB write)"},
+        "gpu_launches": 2 * args.steps,
+        "clocks": clocks.summary(),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                     "frac": achieved / pk["hbm_gbs"], "traffic": None, "peak_source": src,
+                     "kernel": "step_kernel (fused 2 substeps)", "kernel_ms": k_ms,
+                     "bytes_per_env": bytes_env,
+                     "fp32_tflops_est": flops / (k_ms / 1e3) / 1e12,
+                     "note": "compulsory bytes; the fused kernel is latency/FP32-issue bound, not HBM bound "
+                             "(DESIGN.md)"},
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args, bounded=True)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def cpu_baseline(args, bounded=True):
+    """The C oracle (float64 port of the reference step) on this host's cores,
+    on a bounded sample of the same workload."""
+    import numpy as np
+
+    from oracle.oracle import OracleScene, build
+    from paper_2108_10470_b200 import models as M
+    from paper_2108_10470_b200.params import SimParams
+    build()
+    threads = os.cpu_count() or 1
+    sample = min(args.envs, args.cpu_sample_envs)
+    s = OracleScene([M.quadruped()], sample, SimParams(dt=1 / 120), threads=threads)
+    s.pos[:, 2] += 0.37
+    s.forward_kinematics()
+    rng = np.random.default_rng(0)
+    s.ctrl_dof_pos_target[:] = 0.6 * rng.uniform(-1, 1, s.num_dofs)
+    s.step()
+    s.step()
+    n = 0
+    t0 = time.perf_counter()
+    while True:
+        s.ctrl_dof_pos_target[:] = 0.6 * rng.uniform(-1, 1, s.num_dofs)
+        s.step()
+        s.step()
+        n += 1
+        dt = time.perf_counter() - t0
+        if dt > args.cpu_seconds or n >= args.cpu_max_steps:
+            break
+    return {"value": sample * n / dt, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{sample} envs x {n} control steps (2 substeps each) of the same Ant workload, "
+                      f"C oracle float64 (oracle/bso.c, OpenMP {threads} threads), physics only "
+                      f"(the reference's obs/reward is <0.4% of its step time)"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_info()
+    if rank != 0:
+        return
+    base = cpu_baseline(args, bounded=True)
+    # per-step bounded samples: warm-up + K steps of the same sample
+    line = {"metric": METRIC, "value": base["value"], "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (uniform random actions)", "impl": "reference",
+            "config": {"workload": WORKLOAD, "envs_per_gpu": args.envs, "substeps": 2},
+            "cpu_baseline": base,
+            "e2e": {"value": base["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    line["ms_per_step"] = 1e3 * args.envs / base["value"]
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--envs", type=int, default=16384)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-envs", type=int, default=2048)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--cpu-max-steps", type=int, default=400)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

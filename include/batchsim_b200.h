@@ -195,6 +195,43 @@ int bsim_collide(const bsim_layout_t *layout, const bsim_params_t *params,
                  int32_t *body_a, int32_t *body_b, float *depth, float *point, float *normal,
                  int32_t *scratch, void *stream);
 
+/* ------------------------------------------------------------------------
+   Fused task layer (reference envs.py:145-200, 359-565; rewards.py:78-158):
+   after the physics launch, one thread per env computes reward / done /
+   timeout / poison handling, the observation, and -- for finished envs --
+   the reset (numpy-identical PCG64 draws keyed (seed, global env, count)),
+   forward kinematics of the new state and the post-reset observation.
+   ------------------------------------------------------------------------ */
+enum bsim_task_kind { BSIM_TASK_QUADRUPED = 1, BSIM_TASK_ANYMAL = 2 };
+
+typedef struct bsim_task_t {
+    int32_t kind, obs_dim, act_dim, episode_length;
+    uint32_t seed;
+    int32_t pad;
+    double control_dt, rest_height;
+    /* device buffers; real arrays have the entry point's precision */
+    void *obs;                  /* [E][obs_dim]                                  */
+    void *reward;               /* [E]                                           */
+    uint8_t *done, *timeout, *poisoned;   /* [E] info flags of the last step      */
+    int32_t *episode_steps, *reset_count; /* [E]                                  */
+    void *actions;              /* [E][act_dim] clipped actions (zeroed by reset) */
+    void *potentials;           /* [E] quadruped progress potential               */
+    void *commands;             /* [E][3] anymal velocity commands                */
+    const void *dof_lower, *dof_upper;    /* [D] static joint limits              */
+} bsim_task_t;
+
+/* EnvBatch.step() tail (envs.py:188-199): call after bsim_step(). */
+int bsim_task_step(const bsim_layout_t *layout, const bsim_state_t *state, const bsim_task_t *task,
+                   void *stream);
+/* EnvBatch.reset(idx) (envs.py:145-176): reset the masked envs (NULL = all)
+   and write the observation of every env. */
+int bsim_task_reset(const bsim_layout_t *layout, const bsim_state_t *state, const bsim_task_t *task,
+                    const uint8_t *env_mask, void *stream);
+int bsim_task_step_f64(const bsim_layout_t *layout, const bsim_state64_t *state, const bsim_task_t *task,
+                       void *stream);
+int bsim_task_reset_f64(const bsim_layout_t *layout, const bsim_state64_t *state, const bsim_task_t *task,
+                        const uint8_t *env_mask, void *stream);
+
 /* float64 variants (same semantics, double tables / params / state). */
 int bsim_step_f64(const bsim_layout_t *layout, const bsim_params64_t *params,
                   const bsim_state64_t *state, int32_t n_substeps, const bsim_actions_t *actions,

@@ -39,6 +39,8 @@ BS_HD float r_max(float a, float b) { return fmaxf(a, b); }
 BS_HD double r_max(double a, double b) { return fmax(a, b); }
 BS_HD float r_min(float a, float b) { return fminf(a, b); }
 BS_HD double r_min(double a, double b) { return fmin(a, b); }
+BS_HD float exp_r(float x) { return expf(x); }
+BS_HD double exp_r(double x) { return exp(x); }
 BS_HD float r_nan(float) { return nanf(""); }
 BS_HD double r_nan(double) { return nan(""); }
 

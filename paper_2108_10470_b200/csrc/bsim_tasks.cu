@@ -1,0 +1,91 @@
+// bsim_tasks.cu -- the fused task-layer kernels (one thread per env) and their
+// C-ABI entry points: EnvBatch.step's reward / done / obs / auto-reset tail
+// and EnvBatch.reset (reference envs.py:145-200, 359-565).
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <string>
+
+#include "bsim_tasks.cuh"
+
+using namespace bsim;
+
+namespace {
+
+std::string t_err;
+
+int t_set_err(const char *what, cudaError_t e) {
+    t_err = std::string(what) + ": " + cudaGetErrorString(e);
+    return BSIM_E_CUDA;
+}
+
+template <class R> __global__ void task_step_kernel(const Ctx<R> c, const bsim_task_t t) {
+    int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= c.d.E) return;
+    task_step_env(c, TaskView<R>{t}, e);
+}
+
+template <class R> __global__ void task_reset_kernel(const Ctx<R> c, const bsim_task_t t, const uint8_t *mask) {
+    int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= c.d.E) return;
+    TaskView<R> tv{t};
+    if (!mask || mask[e]) task_reset_env(c, tv, e);
+    task_obs(c, tv, e);
+}
+
+template <class R>
+Ctx<R> task_ctx(const bsim_layout_t *L, const typename Abi<R>::State *s) {
+    Ctx<R> c;
+    c.L = *L;
+    std::memset(&c.p, 0, sizeof c.p);
+    c.s = *s;
+    c.d = make_dims(*L);
+    c.joints = reinterpret_cast<const typename Abi<R>::Joint *>(L->joints);
+    return c;
+}
+
+bool bad(const bsim_layout_t *L, const void *s, const bsim_task_t *t) {
+    return !L || !s || !t || (t->kind != BSIM_TASK_QUADRUPED && t->kind != BSIM_TASK_ANYMAL) ||
+           t->act_dim != L->dofs_per_env || L->actors_per_env != 1;
+}
+
+template <class R>
+int launch_task(const bsim_layout_t *L, const typename Abi<R>::State *s, const bsim_task_t *t, bool reset,
+                const uint8_t *mask, void *stream) {
+    if (bad(L, s, t)) {
+        t_err = "bsim_task: invalid arguments";
+        return BSIM_E_INVALID;
+    }
+    Ctx<R> c = task_ctx<R>(L, s);
+    if (c.d.E == 0) return BSIM_OK;
+    const int TPB = 128;
+    int grid = (c.d.E + TPB - 1) / TPB;
+    if (reset)
+        task_reset_kernel<R><<<grid, TPB, 0, (cudaStream_t)stream>>>(c, *t, mask);
+    else
+        task_step_kernel<R><<<grid, TPB, 0, (cudaStream_t)stream>>>(c, *t);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? BSIM_OK : t_set_err(reset ? "task_reset_kernel" : "task_step_kernel", e);
+}
+
+}  // namespace
+
+extern "C" {
+
+int bsim_task_step(const bsim_layout_t *l, const bsim_state_t *s, const bsim_task_t *t, void *st) {
+    return launch_task<float>(l, s, t, false, nullptr, st);
+}
+int bsim_task_step_f64(const bsim_layout_t *l, const bsim_state64_t *s, const bsim_task_t *t, void *st) {
+    return launch_task<double>(l, s, t, false, nullptr, st);
+}
+int bsim_task_reset(const bsim_layout_t *l, const bsim_state_t *s, const bsim_task_t *t, const uint8_t *m,
+                    void *st) {
+    return launch_task<float>(l, s, t, true, m, st);
+}
+int bsim_task_reset_f64(const bsim_layout_t *l, const bsim_state64_t *s, const bsim_task_t *t, const uint8_t *m,
+                        void *st) {
+    return launch_task<double>(l, s, t, true, m, st);
+}
+const char *bsim_task_last_error(void) { return t_err.c_str(); }
+
+}  // extern "C"

@@ -1,0 +1,223 @@
+// bsim_tasks.cuh -- per-env task logic of the two locomotion tasks
+// (host+device): reward, termination, observation and reset, fused so one
+// thread per env finishes a whole EnvBatch.step() tail.
+//
+// QuadrupedEnv: reference envs.py:359-478, locomotion_reward rewards.py:78-112.
+// AnymalObsEnv: reference envs.py:484-565, anymal_reward (flat) rewards.py:129-158.
+#pragma once
+
+#include "bsim_kin.cuh"
+#include "bsim_rng.cuh"
+
+namespace bsim {
+
+template <class R> struct TaskView {
+    const bsim_task_t &t;
+    BS_HD R *obs(int e) const { return reinterpret_cast<R *>(t.obs) + (size_t)e * t.obs_dim; }
+    BS_HD R &reward(int e) const { return reinterpret_cast<R *>(t.reward)[e]; }
+    BS_HD R *act(int e) const { return reinterpret_cast<R *>(t.actions) + (size_t)e * t.act_dim; }
+    BS_HD R &potential(int e) const { return reinterpret_cast<R *>(t.potentials)[e]; }
+    BS_HD R *cmd(int e) const { return reinterpret_cast<R *>(t.commands) + 3 * (size_t)e; }
+    BS_HD R lo(int k) const { return reinterpret_cast<const R *>(t.dof_lower)[k]; }
+    BS_HD R hi(int k) const { return reinterpret_cast<const R *>(t.dof_upper)[k]; }
+};
+
+// env-local root pose / velocity of actor 0
+template <class R> struct Root {
+    V3<R> p, v, w;
+    Q4<R> q;
+};
+template <class R> BS_HD Root<R> root_of(const Ctx<R> &c, int e) {
+    const R *b = c.s.body_q + (size_t)e * c.d.B * 13;
+    return Root<R>{V3<R>{b[0], b[1], b[2]}, V3<R>{b[7], b[8], b[9]}, V3<R>{b[10], b[11], b[12]},
+                   Q4<R>{b[3], b[4], b[5], b[6]}};
+}
+template <class R> BS_HD V3<R> rot_inv(Q4<R> q, V3<R> v) { return qrot(qconj(q), v); }
+
+// ------------------------------------------------------------ quadruped
+constexpr double QUAD_TARGET_X = 1000.0;
+
+// heading / up projections shared by obs and reward (envs.py:426-439)
+template <class R> struct Frame {
+    V3<R> lin_b, ang_b;
+    R up_z, heading_proj;
+};
+template <class R> BS_HD Frame<R> quad_frame(const Root<R> &r) {
+    Frame<R> f;
+    f.lin_b = rot_inv(r.q, r.v);
+    f.ang_b = rot_inv(r.q, r.w);
+    f.up_z = qrot(r.q, v3(R(0), R(0), R(1))).z;
+    V3<R> heading = qrot(r.q, v3(R(1), R(0), R(0)));
+    R tx = R(QUAD_TARGET_X) - r.p.x, ty = R(0) - r.p.y;
+    R nrm = r_max(r_sqrt(tx * tx + ty * ty), R(1e-9));
+    f.heading_proj = heading.x * (tx / nrm) + heading.y * (ty / nrm);
+    return f;
+}
+
+// locomotion_reward (rewards.py:78-112); returns reward, writes the new potential
+template <class R>
+BS_HD R quad_reward(const Ctx<R> &c, const TaskView<R> &tv, int e, const Root<R> &r, const Frame<R> &f,
+                    bool &done) {
+    const R dt = R(tv.t.control_dt), term = R(0.26);
+    R dx = R(QUAD_TARGET_X) - r.p.x, dy = -r.p.y, dz = -r.p.z;
+    R dist = r_sqrt(dx * dx + dy * dy + dz * dz);
+    R potential = -dist / dt;
+    R rew = potential - tv.potential(e);
+    R height = r.p.z;
+    rew = rew + (height >= term ? R(0.5) : R(0));
+    rew = rew + (height <= term ? R(-1) : R(0));
+    rew = rew + (f.up_z > R(0.93) ? R(0.1) : R(0));
+    rew = rew + R(0.5) * (f.heading_proj >= R(0.8) ? R(1) : f.heading_proj / R(0.8));
+    const R *a = tv.act(e);
+    const R *dof = c.s.dof_state + 2 * (size_t)e * c.d.D;
+    R sa = R(0), se = R(0), near_ = R(0);
+    for (int k = 0; k < tv.t.act_dim; ++k) {
+        sa = sa + a[k] * a[k];
+        se = se + a[k] * R(1) * dof[2 * k + 1];
+        R lo = tv.lo(k), hi = tv.hi(k);
+        if (finite_r(lo) && finite_r(hi)) {
+            R frac = (dof[2 * k] - lo) / (hi - lo);
+            if (frac < R(0.01) || frac > R(0.99)) near_ = near_ + R(1);
+        }
+    }
+    rew = rew - R(0.005) * sa;
+    rew = rew + R(0.05) * se;
+    rew = rew - R(0.1) * near_;
+    tv.potential(e) = potential;
+    done = height <= term;
+    return rew;
+}
+
+// 60-dim observation (envs.py:441-461)
+template <class R> BS_HD void quad_obs(const Ctx<R> &c, const TaskView<R> &tv, int e) {
+    Root<R> r = root_of(c, e);
+    Frame<R> f = quad_frame(r);
+    R *o = tv.obs(e);
+    R x = r.q.x, y = r.q.y, z = r.q.z, w = r.q.w;
+    R yaw = r_atan2(R(2) * (w * z + x * y), R(1) - R(2) * (y * y + z * z));
+    R roll = r_atan2(R(2) * (w * x + y * z), R(1) - R(2) * (x * x + y * y));
+    R ang = r_atan2(-r.p.y, R(QUAD_TARGET_X) - r.p.x) - yaw;
+    ang = r_atan2(r_sin(ang), r_cos(ang));
+    o[0] = r.p.z;
+    o[1] = f.lin_b.x; o[2] = f.lin_b.y; o[3] = f.lin_b.z;
+    o[4] = f.ang_b.x; o[5] = f.ang_b.y; o[6] = f.ang_b.z;
+    o[7] = yaw; o[8] = roll; o[9] = ang; o[10] = f.up_z; o[11] = f.heading_proj;
+    const int A = tv.t.act_dim, S = c.d.S;
+    const R *dof = c.s.dof_state + 2 * (size_t)e * c.d.D;
+    for (int k = 0; k < A; ++k) {
+        o[12 + k] = R(2) * (dof[2 * k] - tv.lo(k)) / (tv.hi(k) - tv.lo(k)) - R(1);
+        o[12 + A + k] = dof[2 * k + 1] * R(0.05);
+    }
+    const R *sf = c.s.sensor_forces + 6 * (size_t)e * S;
+    for (int k = 0; k < 6 * S; ++k) o[12 + 2 * A + k] = sf[k] * R(0.01);
+    const R *a = tv.act(e);
+    for (int k = 0; k < A; ++k) o[12 + 2 * A + 6 * S + k] = a[k];
+}
+
+// ------------------------------------------------------------ anymal
+template <class R> BS_HD R anymal_reward(const Ctx<R> &c, const TaskView<R> &tv, int e, const Root<R> &r, bool &done) {
+    const R dt = R(tv.t.control_dt);
+    V3<R> lin_b = rot_inv(r.q, r.v), ang_b = rot_inv(r.q, r.w);
+    const R *cmd = tv.cmd(e);
+    R ex = cmd[0] - lin_b.x, ey = cmd[1] - lin_b.y, ez = cmd[2] - ang_b.z;
+    R err_xy = ex * ex + ey * ey, err_yaw = ez * ez;
+    R tq = R(0);
+    const R *df = c.s.dof_force + (size_t)e * c.d.D;
+    for (int k = 0; k < tv.t.act_dim; ++k) tq = tq + df[k] * df[k];
+    R rew = R(1) * dt * exp_r(-err_xy / R(0.25)) + R(0.5) * dt * exp_r(-err_yaw / R(0.25)) - R(0.00002) * dt * tq;
+    R up_z = qrot(r.q, v3(R(0), R(0), R(1))).z;
+    done = up_z < R(0.3) || r.p.z < R(0.18);
+    return rew;
+}
+
+// 48-dim observation (envs.py:538-550)
+template <class R> BS_HD void anymal_obs(const Ctx<R> &c, const TaskView<R> &tv, int e) {
+    Root<R> r = root_of(c, e);
+    R *o = tv.obs(e);
+    V3<R> lin_b = rot_inv(r.q, r.v), ang_b = rot_inv(r.q, r.w), gb = rot_inv(r.q, v3(R(0), R(0), R(-1)));
+    o[0] = lin_b.x; o[1] = lin_b.y; o[2] = lin_b.z;
+    o[3] = ang_b.x; o[4] = ang_b.y; o[5] = ang_b.z;
+    o[6] = gb.x; o[7] = gb.y; o[8] = gb.z;
+    const R *cmd = tv.cmd(e);
+    o[9] = cmd[0]; o[10] = cmd[1]; o[11] = cmd[2];
+    const int A = tv.t.act_dim;
+    const R *dof = c.s.dof_state + 2 * (size_t)e * c.d.D;
+    for (int k = 0; k < A; ++k) {
+        o[12 + k] = dof[2 * k];
+        o[12 + A + k] = dof[2 * k + 1] * R(0.05);
+    }
+    const R *a = tv.act(e);
+    for (int k = 0; k < A; ++k) o[12 + 2 * A + k] = a[k];
+}
+
+// ------------------------------------------------------------ reset
+// EnvBatch.reset for one env (envs.py:145-166) with the task's _reset_envs
+// (404-419 / 517-531) and _post_reset (385-397 / 506-515).
+template <class R> BS_HD void task_reset_env(const Ctx<R> &c, const TaskView<R> &tv, int e) {
+    const bsim_task_t &t = tv.t;
+    const Dims &d = c.d;
+    if (c.s.nonfinite[e]) c.s.nonfinite[e] = 0;   // clear_nonfinite (physics.py:1090)
+    const uint32_t genv = (uint32_t)(c.L.env_offset + e);
+    uint32_t key[4] = {t.seed, genv, (uint32_t)t.reset_count[e], 0xCu};
+    NpRng rng = np_rng(key, 3);
+    double qx = 0.0, qy = 0.0, qz = 0.0, qw = 1.0;
+    if (t.kind == BSIM_TASK_QUADRUPED) {
+        double yaw = np_uniform(rng, -0.1, 0.1);
+        qz = sin(yaw / 2.0);
+        qw = cos(yaw / 2.0);
+    }
+    double n = sqrt(qx * qx + qy * qy + qz * qz + qw * qw);  // set_root_state renormalises (buffers.py:145)
+    R *root = c.s.body_q + (size_t)e * d.B * 13;
+    root[0] = R(0); root[1] = R(0); root[2] = R(t.rest_height + 0.02);
+    root[3] = R(qx / n); root[4] = R(qy / n); root[5] = R(qz / n); root[6] = R(qw / n);
+    for (int k = 7; k < 13; ++k) root[k] = R(0);
+    R *dof = c.s.dof_state + 2 * (size_t)e * d.D;
+    for (int k = 0; k < t.act_dim; ++k) {
+        dof[2 * k] = R(np_uniform(rng, -0.1, 0.1));
+        dof[2 * k + 1] = R(0);
+    }
+    fk_env(c, e, 0xffffffffu);
+    repack_env(c, e, 0xffffffffu);
+    t.episode_steps[e] = 0;
+    t.reset_count[e] += 1;
+    R *a = tv.act(e);
+    for (int k = 0; k < t.act_dim; ++k) a[k] = R(0);
+    if (t.kind == BSIM_TASK_QUADRUPED) {
+        R z = R(t.rest_height + 0.02);
+        R dist = r_sqrt(R(QUAD_TARGET_X) * R(QUAD_TARGET_X) + z * z);
+        tv.potential(e) = -dist / R(t.control_dt);
+    } else {
+        key[2] = (uint32_t)t.reset_count[e];
+        NpRng cr = np_rng(key, 4);
+        R *cmd = tv.cmd(e);
+        for (int k = 0; k < 3; ++k) cmd[k] = R(np_uniform(cr, -1.0, 1.0));
+    }
+}
+
+template <class R> BS_HD void task_obs(const Ctx<R> &c, const TaskView<R> &tv, int e) {
+    if (tv.t.kind == BSIM_TASK_QUADRUPED) quad_obs(c, tv, e);
+    else anymal_obs(c, tv, e);
+}
+
+// EnvBatch.step tail after the decimated physics (envs.py:188-199)
+template <class R> BS_HD void task_step_env(const Ctx<R> &c, const TaskView<R> &tv, int e) {
+    const bsim_task_t &t = tv.t;
+    int steps = t.episode_steps[e] + 1;
+    t.episode_steps[e] = steps;
+    Root<R> r = root_of(c, e);
+    bool done;
+    R rew;
+    if (t.kind == BSIM_TASK_QUADRUPED) rew = quad_reward(c, tv, e, r, quad_frame(r), done);
+    else rew = anymal_reward(c, tv, e, r, done);
+    bool timeout = steps >= t.episode_length;
+    bool pois = c.s.nonfinite[e] != 0;
+    done = done || timeout || pois;
+    tv.reward(e) = pois ? R(0) : rew;
+    t.done[e] = done;
+    t.timeout[e] = timeout;
+    t.poisoned[e] = pois;
+    if (done) task_reset_env(c, tv, e);
+    task_obs(c, tv, e);   // reset rows get the post-reset observation (envs.py:195-198)
+}
+
+}  // namespace bsim

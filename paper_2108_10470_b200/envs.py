@@ -1,0 +1,255 @@
+"""Vectorised RL tasks on the GPU scene (reference `pkg/src/batchsim/envs.py`).
+
+Same classes, config, registry and step/reset contract as the reference
+`EnvBatch` (envs.py:73-205): actions are clipped to [-1, 1] and scaled into
+position targets, the physics runs `decimation` sim steps, then reward, done
+(termination | timeout | poisoned), observation and auto-reset are produced
+-- here by two launches per control step:
+
+1. ``bsim_step``: the fused action mapping + all decimation substeps;
+2. ``bsim_task_step``: one thread per env computes reward / done / obs and,
+   for finished envs, draws the reset state with numpy-identical PCG64
+   streams keyed (seed, global env id, reset count), runs forward kinematics
+   and writes the post-reset observation.
+
+Outputs are device tensors that alias persistent buffers (zero-copy; clone a
+result to keep it across steps).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field, replace
+from typing import NamedTuple
+
+import numpy as np
+import torch
+
+from . import _native as N
+from . import models as M
+from .buffers import SimBuffers
+from .layout import MODE_POSITION
+from .params import SimParams
+from .scene import Scene
+
+ALL = None
+TASK_QUADRUPED, TASK_ANYMAL = 1, 2
+
+
+@dataclass
+class EnvConfig:
+    """Reference EnvConfig (envs.py:38-63) plus the B200 knobs."""
+    num_envs: int = 16
+    seed: int = 0
+    sim_dt: float = 1.0 / 120.0
+    control_dt: float = 1.0 / 60.0
+    episode_length: int = 1000
+    workers: int = 1
+    randomize: bool = False
+    obs_noise: bool = False
+    obs_noise_uncorr: float = 0.002
+    obs_noise_corr: float = 0.001
+    extra: dict = field(default_factory=dict)
+    precision: str = "fp32"
+    device: str | None = None
+    env_offset: int = 0           # global id of env 0 (multi-GPU sharding)
+    total_envs: int | None = None
+
+    def validate(self):
+        if self.num_envs < 1:
+            raise ValueError("num_envs must be >= 1")
+        ratio = self.control_dt / self.sim_dt
+        if abs(ratio - round(ratio)) > 1e-9 or round(ratio) < 1:
+            raise ValueError("control_dt must be a positive integer multiple of sim_dt")
+        if not 0 <= self.seed < 2 ** 32:
+            raise ValueError("seed must fit in 32 bits")
+        return self
+
+    @property
+    def decimation(self):
+        return int(round(self.control_dt / self.sim_dt))
+
+
+class StepOutput(NamedTuple):
+    obs: torch.Tensor
+    reward: torch.Tensor
+    done: torch.Tensor
+    info: dict
+
+
+class Task(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("obs_dim", C.c_int32), ("act_dim", C.c_int32),
+                ("episode_length", C.c_int32), ("seed", C.c_uint32), ("pad", C.c_int32),
+                ("control_dt", C.c_double), ("rest_height", C.c_double)] + [
+        (n, C.c_void_p) for n in ("obs", "reward", "done", "timeout", "poisoned", "episode_steps",
+                                  "reset_count", "actions", "potentials", "commands", "dof_lower",
+                                  "dof_upper")]
+
+
+def dof_limits(model):
+    """Per-DOF (lower, upper); unlimited DOFs get +-inf (envs.py:28-35)."""
+    lo, hi = [], []
+    for j in model.joints:
+        for _ in range(j.dof_count):
+            lo.append(j.limits[0] if j.limits else -np.inf)
+            hi.append(j.limits[1] if j.limits else np.inf)
+    return np.asarray(lo, float), np.asarray(hi, float)
+
+
+class EnvBatch:
+    """Base: GPU scene construction, fused decimated stepping, auto-reset."""
+
+    name = "base"
+    obs_dim = 0
+    act_dim = 0
+    action_scale = 1.0
+    task_kind = 0
+    rest_height = 0.0
+
+    def __init__(self, config: EnvConfig):
+        self.config = cfg = config.validate()
+        if cfg.randomize or cfg.obs_noise:
+            from .randomize import check_supported
+            check_supported(cfg)
+        E = cfg.num_envs
+        self.model = self._model()
+        self.scene = self.sim = Scene([self.model], E, self._sim_params(), device=cfg.device,
+                                      precision=cfg.precision, env_offset=cfg.env_offset,
+                                      total_envs=cfg.total_envs)
+        self.buffers = SimBuffers(self.scene)
+        s = self.scene
+        dev, dt = s.device, s.dtype
+        self.obs = torch.zeros((E, self.obs_dim), dtype=dt, device=dev)
+        self.reward = torch.zeros(E, dtype=dt, device=dev)
+        self.done = torch.zeros(E, dtype=torch.bool, device=dev)
+        self.timeout = torch.zeros(E, dtype=torch.bool, device=dev)
+        self.poisoned = torch.zeros(E, dtype=torch.bool, device=dev)
+        self.episode_steps = torch.zeros(E, dtype=torch.int32, device=dev)
+        self.reset_count = torch.zeros(E, dtype=torch.int32, device=dev)
+        self.actions = torch.zeros((E, self.act_dim), dtype=dt, device=dev)
+        self.potentials = torch.zeros(E, dtype=dt, device=dev)
+        self.commands = torch.zeros((E, 3), dtype=dt, device=dev)
+        lo, hi = dof_limits(self.model)
+        self.dof_lower = torch.as_tensor(lo, dtype=dt, device=dev)
+        self.dof_upper = torch.as_tensor(hi, dtype=dt, device=dev)
+        self._mask = torch.zeros(E, dtype=torch.uint8, device=dev)
+        self._task = Task(self.task_kind, self.obs_dim, self.act_dim, cfg.episode_length, cfg.seed, 0,
+                          cfg.control_dt, self.rest_height,
+                          *(t.data_ptr() for t in (self.obs, self.reward, self.done, self.timeout,
+                                                   self.poisoned, self.episode_steps, self.reset_count,
+                                                   self.actions, self.potentials, self.commands,
+                                                   self.dof_lower, self.dof_upper)))
+        self.reset()
+
+    # ------------------------------------------------------------ hooks
+    def _model(self):
+        raise NotImplementedError
+
+    def _sim_params(self):
+        return SimParams(dt=self.config.sim_dt)
+
+    # ------------------------------------------------------------ helpers
+    def _call(self, name, *args):
+        lib = self.scene._lib
+        fn = getattr(lib, name + ("_f64" if self.scene.fp64 else ""))
+        lay, _, st = self.scene._structs()
+        rc = fn(C.byref(lay), C.byref(st), C.byref(self._task), *args)
+        if rc != 0:
+            raise N.NativeError(f"{name} failed ({rc}): {lib.bsim_task_last_error().decode()}")
+
+    def local_root(self):
+        """Root states with the env origins removed (envs.py:135-139)."""
+        root = self.scene.root_state.clone()
+        root[:, 0:3] -= self.scene.env_origins.repeat_interleave(self.scene.actors_per_env, 0)
+        return root
+
+    def dof_view(self):
+        return self.scene.dof_state.reshape(self.config.num_envs, -1, 2)
+
+    # ------------------------------------------------------------ API
+    def reset(self, env_indices=ALL):
+        """Reset all envs (None) or the given ones; returns the full obs."""
+        E = self.config.num_envs
+        mptr = None
+        if env_indices is not None:
+            idx = torch.as_tensor(np.atleast_1d(np.asarray(env_indices, dtype=np.int64))
+                                  if not isinstance(env_indices, torch.Tensor) else env_indices,
+                                  device=self.scene.device).reshape(-1).long()
+            if idx.numel() == 0:
+                return self.obs
+            if int(idx.min()) < 0 or int(idx.max()) >= E:
+                raise IndexError("env index out of range")
+            self._mask.zero_()
+            self._mask[idx] = 1
+            mptr = self._mask.data_ptr()
+        self._call("bsim_task_reset", mptr, self.scene._s)
+        return self.obs
+
+    def step(self, actions) -> StepOutput:
+        cfg = self.config
+        a = actions if isinstance(actions, torch.Tensor) else torch.as_tensor(np.asarray(actions, dtype=np.float64))
+        if tuple(a.shape) != (cfg.num_envs, self.act_dim):
+            raise ValueError(f"actions must have shape ({cfg.num_envs}, {self.act_dim})")
+        a = a.to(self.scene.device, self.scene.dtype)
+        if not a.is_contiguous():
+            a = a.contiguous()
+        self.scene.step(cfg.decimation, actions=a, action_scale=self.action_scale,
+                        action_mode=MODE_POSITION, actions_clipped=self.actions)
+        self._call("bsim_task_step", self.scene._s)
+        return StepOutput(self.obs, self.reward, self.done,
+                          {"timeout": self.timeout, "poisoned": self.poisoned})
+
+    def close(self):
+        self.scene.close()
+
+
+class QuadrupedEnv(EnvBatch):
+    """Ant analog: 8-DOF walker, 60-dim obs, locomotion reward (envs.py:359-478)."""
+
+    name = "quadruped"
+    obs_dim = 60
+    act_dim = 8
+    action_scale = 0.6
+    task_kind = TASK_QUADRUPED
+    rest_height = M.QUADRUPED_REST_HEIGHT
+    target_x = 1000.0
+
+    def __init__(self, config=None):
+        cfg = config or EnvConfig()
+        super().__init__(replace(cfg, sim_dt=1.0 / 120.0, control_dt=1.0 / 60.0))
+
+    def _model(self):
+        return M.quadruped()
+
+
+class AnymalObsEnv(EnvBatch):
+    """ANYmal analog: 12-DOF walker, 48-dim obs, velocity tracking (envs.py:484-565)."""
+
+    name = "quadruped-anymal-obs"
+    obs_dim = 48
+    act_dim = 12
+    action_scale = 0.5
+    task_kind = TASK_ANYMAL
+    rest_height = M.QUADRUPED12_REST_HEIGHT
+
+    def __init__(self, config=None):
+        cfg = config or EnvConfig()
+        super().__init__(replace(cfg, sim_dt=1.0 / 120.0, control_dt=1.0 / 60.0))
+
+    def _model(self):
+        return M.quadruped12()
+
+
+TASKS = {
+    "quadruped": QuadrupedEnv,
+    "quadruped-anymal-obs": AnymalObsEnv,
+}
+
+
+def make_env(name, config=None, **overrides):
+    if name not in TASKS:
+        raise KeyError(f"unknown task {name!r}; have {sorted(TASKS)}")
+    cfg = config or EnvConfig()
+    if overrides:
+        cfg = replace(cfg, **overrides)
+    return TASKS[name](cfg)

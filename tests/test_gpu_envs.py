@@ -1,0 +1,109 @@
+"""GPU task layer (fused reward / done / obs / auto-reset) vs the reference.
+
+Golden traces come from the reference EnvBatch itself
+(tests/golden/make_golden.py -> env_*.npz).  Each control step is teacher
+forced: the reference's pre-step state is loaded, one fused control step
+runs on the B200, and obs / reward / done / timeout and the reset rows are
+compared.  Reset draws use numpy-identical PCG64 streams, so reset states
+and done masks are exact.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from golden_util import load, rel_err
+
+pytestmark = pytest.mark.gpu
+
+CASES = [("quadruped", "env_quadruped"), ("quadruped-anymal-obs", "env_quadruped_anymal_obs")]
+
+
+def _make(task, meta, precision):
+    from paper_2108_10470_b200.envs import make_env
+    return make_env(task, num_envs=meta["num_envs"], seed=meta["seed"],
+                    episode_length=meta["episode_length"], precision=precision)
+
+
+def _load_pre(env, arr, t, extra_name):
+    s = env.scene
+    E, B = s.num_envs, s.bodies_per_env
+    org = arr["env_origins"]
+    be = np.repeat(np.arange(E), B)
+    bq = np.concatenate([arr["pos"][t] - org[be], arr["quat"][t], arr["linvel"][t], arr["angvel"][t]], 1)
+    s.body_q.copy_(torch.as_tensor(bq, dtype=s.dtype))
+    s._friction_anchor.copy_(torch.as_tensor(arr["_friction_anchor"][t] - org[None], dtype=s.dtype))
+    s.dof_state.copy_(torch.as_tensor(arr["dof_state"][t], dtype=s.dtype))
+    s.sensor_forces.copy_(torch.as_tensor(arr["sensor_forces"][t], dtype=s.dtype))
+    s.root_state.copy_(torch.as_tensor(arr["root_state"][t], dtype=s.dtype))
+    env.episode_steps.copy_(torch.as_tensor(arr["episode_steps"][t].astype(np.int32)))
+    env.reset_count.copy_(torch.as_tensor(arr["reset_count"][t].astype(np.int32)))
+    getattr(env, extra_name).copy_(torch.as_tensor(arr["extra_before"][t], dtype=s.dtype))
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+@pytest.mark.parametrize("task,fixture", CASES)
+def test_initial_reset_matches_reference(task, fixture, precision):
+    meta, arr = load(fixture)
+    env = _make(task, meta, precision)
+    # the fixture's obs0 is the reference's explicit env.reset() right after
+    # construction (its second reset: reset_count keys 1)
+    obs = env.reset()
+    tol = 1e-9 if precision == "fp64" else 1e-5
+    assert rel_err(obs.double().cpu().numpy(), arr["obs0"], tol, tol) <= 1
+    assert torch.all(env.reset_count == 2)
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+@pytest.mark.parametrize("task,fixture", CASES)
+def test_env_step_teacher_forced(task, fixture, precision):
+    meta, arr = load(fixture)
+    env = _make(task, meta, precision)
+    extra = "potentials" if task == "quadruped" else "commands"
+    # fp32: the physics step carries the documented fp32 tolerance, and the
+    # progress reward differentiates positions at 1/control_dt = 60 Hz
+    otol, rtol_ = (1e-7, 1e-7) if precision == "fp64" else (2e-3, 2e-2)
+    n_resets = 0
+    for t in range(meta["steps"]):
+        _load_pre(env, arr, t, extra)
+        out = env.step(torch.as_tensor(arr["actions"][t]))
+        done = out.done.cpu().numpy()
+        assert np.array_equal(done, arr["done"][t]), (t, done, arr["done"][t])
+        assert np.array_equal(out.info["timeout"].cpu().numpy(), arr["timeout"][t])
+        assert rel_err(out.obs.double().cpu().numpy(), arr["obs"][t], otol, otol) <= 1, (t, "obs")
+        assert rel_err(out.reward.double().cpu().numpy(), arr["reward"][t], rtol_, rtol_) <= 1, (t, "reward")
+        n_resets += int(done.sum())
+        if t + 1 < meta["steps"] and done.any():
+            # the reset rows equal the reference's next pre-step state
+            B = env.scene.bodies_per_env
+            rows = np.concatenate([np.arange(e * B, (e + 1) * B) for e in np.nonzero(done)[0]])
+            org = arr["env_origins"][rows // B]
+            got = env.scene.body_q.double().cpu().numpy()[rows]
+            assert rel_err(got[:, 0:3], arr["pos"][t + 1][rows] - org, 1e-6, 1e-6) <= 1
+            assert rel_err(got[:, 3:7], arr["quat"][t + 1][rows], 1e-6, 1e-6) <= 1
+            assert np.array_equal(env.reset_count.cpu().numpy(), arr["reset_count"][t + 1])
+            assert rel_err(getattr(env, extra).double().cpu().numpy(), arr["extra_before"][t + 1],
+                           1e-6, 1e-6) <= 1
+    assert n_resets > 0, "trace should exercise the auto-reset path"
+
+
+def test_step_validates_actions():
+    from paper_2108_10470_b200.envs import make_env
+    env = make_env("quadruped", num_envs=4)
+    with pytest.raises(ValueError):
+        env.step(torch.zeros(3, 8))
+    env.step(torch.full((4, 8), 100.0))
+    assert torch.all(env.actions == 1.0)
+
+
+def test_fused_env_step_equals_manual_substeps():
+    """envs.py:40-50 analogue: decimated fused step == clip/scale + 2 scene steps."""
+    from paper_2108_10470_b200.envs import make_env
+    a = make_env("quadruped", num_envs=8, seed=7, precision="fp64")
+    b = make_env("quadruped", num_envs=8, seed=7, precision="fp64")
+    act = torch.as_tensor(np.random.default_rng(42).uniform(-1.3, 1.3, (8, 8)))
+    a.step(act)
+    b.scene.ctrl_dof_pos_target.copy_((0.6 * act.clamp(-1, 1)).reshape(-1).to(b.scene.dtype).cuda())
+    b.scene.step()
+    b.scene.step()
+    assert torch.equal(a.scene.body_q, b.scene.body_q)
