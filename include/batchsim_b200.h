@@ -204,11 +204,31 @@ int bsim_collide(const bsim_layout_t *layout, const bsim_params_t *params,
    ------------------------------------------------------------------------ */
 enum bsim_task_kind { BSIM_TASK_QUADRUPED = 1, BSIM_TASK_ANYMAL = 2 };
 
+/* Domain randomisation (reference randomize.py:86-189).  Targets in the
+   reference's order: 0 dims, 1 masses, 2 friction, 3 damping, 4 gains,
+   5 joint_limits, 6 gravity.  dist: 0 uniform, 1 loguniform, 2 gaussian;
+   mode: 0 scaling, 1 additive.  Draws use numpy-identical PCG64 streams keyed
+   (seed, global env, epoch) and numpy's normal ziggurat. */
+typedef struct bsim_dr_t {
+    int32_t enabled;
+    uint32_t seed;
+    int32_t min_interval, pad;
+    int32_t use[7], dist[7], mode[7], pad2;
+    double a[7], b[7];
+    int32_t *epoch, *last_step;     /* [E] */
+    /* base snapshots (same shapes / precision as the state arrays) */
+    const void *inv_mass, *inertia_local, *inv_inertia_local, *gravity, *mu_static, *mu_dynamic,
+               *joint_stiffness, *joint_damping, *joint_limit_lo, *joint_limit_hi,
+               *plane_rad, *plane_off, *pair_rad, *pair_off;
+} bsim_dr_t;
+
 typedef struct bsim_task_t {
     int32_t kind, obs_dim, act_dim, episode_length;
     uint32_t seed;
-    int32_t pad;
+    int32_t obs_noise;          /* 1: correlated + uncorrelated observation noise on */
     double control_dt, rest_height;
+    double obs_noise_uncorr, obs_noise_corr;
+    int64_t step_count;         /* scene.step_count, for the DR interval (envs.py:155) */
     /* device buffers; real arrays have the entry point's precision */
     void *obs;                  /* [E][obs_dim]                                  */
     void *reward;               /* [E]                                           */
@@ -218,7 +238,16 @@ typedef struct bsim_task_t {
     void *potentials;           /* [E] quadruped progress potential               */
     void *commands;             /* [E][3] anymal velocity commands                */
     const void *dof_lower, *dof_upper;    /* [D] static joint limits              */
+    void *corr_noise;           /* [E][obs_dim] per-episode correlated noise      */
+    int32_t *noise_count;       /* [E] uncorrelated-noise stream counter          */
+    bsim_dr_t dr;
 } bsim_task_t;
+
+/* DomainRandomizer.randomize(env_indices, step) on its own (randomize.py:116-134). */
+int bsim_randomize(const bsim_layout_t *layout, const bsim_state_t *state, const bsim_dr_t *dr,
+                   const uint8_t *env_mask, int64_t step, void *stream);
+int bsim_randomize_f64(const bsim_layout_t *layout, const bsim_state64_t *state, const bsim_dr_t *dr,
+                       const uint8_t *env_mask, int64_t step, void *stream);
 
 /* EnvBatch.step() tail (envs.py:188-199): call after bsim_step(). */
 int bsim_task_step(const bsim_layout_t *layout, const bsim_state_t *state, const bsim_task_t *task,
@@ -231,6 +260,46 @@ int bsim_task_step_f64(const bsim_layout_t *layout, const bsim_state64_t *state,
                        void *stream);
 int bsim_task_reset_f64(const bsim_layout_t *layout, const bsim_state64_t *state, const bsim_task_t *task,
                         const uint8_t *env_mask, void *stream);
+
+/* ------------------------------------------------------------------------
+   Batched reward kernels (reference rewards.py:78-219), one thread per env.
+   Arrays are float (fp64 = 0) or double (fp64 = 1) device arrays. */
+typedef struct bsim_loco_params_t {
+    double heading_weight, alive_bonus, death_penalty, termination_height, upright_threshold,
+        upright_weight, action_cost_weight, effort_weight, dof_limit_weight, dt;
+} bsim_loco_params_t;
+typedef struct bsim_anymal_params_t {
+    double w_vel_xy, w_vel_yaw, w_vel_z, w_pitch_roll, w_joint_motion, w_torque, w_action_rate,
+        w_collision, w_air_time, dt;
+} bsim_anymal_params_t;
+typedef struct bsim_cube_params_t {
+    double dist_reward_scale, rot_reward_scale, rot_eps, action_penalty_scale, success_tolerance,
+        reach_goal_bonus, fall_dist, fall_penalty;
+} bsim_cube_params_t;
+typedef struct bsim_franka_params_t {
+    double w_stack, w_align, w_lift, w_reach, lift_height, align_tolerance, away_distance;
+} bsim_franka_params_t;
+
+/* locomotion_reward (rewards.py:78-112): writes reward[n] and the new potential[n] */
+int bsim_reward_locomotion(int n, int D, int fp64, const void *torso, const void *target, const void *up,
+                           const void *heading, const void *actions, const void *dof_pos,
+                           const void *dof_vel, const void *dof_lower, const void *dof_upper,
+                           const void *motor_strength, const void *prev_potential,
+                           const bsim_loco_params_t *params, void *reward, void *potential, void *stream);
+/* anymal_reward (rewards.py:129-158), rough = 1 for the nine-term variant */
+int bsim_reward_anymal(int n, int D, int A, int F, int fp64, const void *lin_vel, const void *ang_vel,
+                       const void *commands, const void *dof_vel, const void *dof_acc, const void *torques,
+                       const void *action_rate, const void *collisions, const void *feet_air_time,
+                       const bsim_anymal_params_t *params, int rough, void *reward, void *stream);
+/* cube_reorientation_reward (rewards.py:161-176) */
+int bsim_reward_cube(int n, int A, int fp64, const void *object_pos, const void *object_quat,
+                     const void *target_pos, const void *target_quat, const void *actions,
+                     const bsim_cube_params_t *params, void *reward, uint8_t *goal_reset,
+                     uint8_t *success, void *stream);
+/* franka_stack_reward (rewards.py:200-219) */
+int bsim_reward_franka(int n, int fp64, const void *cubeA_pos, const void *cubeB_pos,
+                       const void *gripper_pos, const void *lfinger_pos, const void *rfinger_pos,
+                       const bsim_franka_params_t *params, void *reward, void *stream);
 
 /* float64 variants (same semantics, double tables / params / state). */
 int bsim_step_f64(const bsim_layout_t *layout, const bsim_params64_t *params,

@@ -11,4 +11,14 @@ def declare(lib):
         f = getattr(lib, "bsim_task_reset" + suffix)
         f.argtypes, f.restype = [vp, vp, vp, vp, vp], C.c_int
     lib.bsim_task_last_error.argtypes, lib.bsim_task_last_error.restype = [], C.c_char_p
+    for suffix in ("", "_f64"):
+        f = getattr(lib, "bsim_randomize" + suffix)
+        f.argtypes, f.restype = [vp, vp, vp, vp, C.c_int64, vp], C.c_int
+    i = C.c_int
+    lib.bsim_reward_locomotion.argtypes = [i, i, i] + [vp] * 11 + [vp, vp, vp, vp]
+    lib.bsim_reward_anymal.argtypes = [i, i, i, i, i] + [vp] * 9 + [vp, i, vp, vp]
+    lib.bsim_reward_cube.argtypes = [i, i, i] + [vp] * 5 + [vp, vp, vp, vp, vp]
+    lib.bsim_reward_franka.argtypes = [i, i] + [vp] * 5 + [vp, vp, vp]
+    for n in ("bsim_reward_locomotion", "bsim_reward_anymal", "bsim_reward_cube", "bsim_reward_franka"):
+        getattr(lib, n).restype = C.c_int
     return lib

@@ -34,6 +34,13 @@ template <class R> __global__ void task_reset_kernel(const Ctx<R> c, const bsim_
 }
 
 template <class R>
+__global__ void randomize_kernel(const Ctx<R> c, const bsim_dr_t dr, const uint8_t *mask, int64_t step) {
+    int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= c.d.E || (mask && !mask[e])) return;
+    dr_randomize_env(c, dr, e, step);
+}
+
+template <class R>
 Ctx<R> task_ctx(const bsim_layout_t *L, const typename Abi<R>::State *s) {
     Ctx<R> c;
     c.L = *L;
@@ -68,9 +75,32 @@ int launch_task(const bsim_layout_t *L, const typename Abi<R>::State *s, const b
     return e == cudaSuccess ? BSIM_OK : t_set_err(reset ? "task_reset_kernel" : "task_step_kernel", e);
 }
 
+template <class R>
+int launch_randomize(const bsim_layout_t *L, const typename Abi<R>::State *s, const bsim_dr_t *dr,
+                     const uint8_t *mask, int64_t step, void *stream) {
+    if (!L || !s || !dr) {
+        t_err = "bsim_randomize: invalid arguments";
+        return BSIM_E_INVALID;
+    }
+    Ctx<R> c = task_ctx<R>(L, s);
+    if (c.d.E == 0) return BSIM_OK;
+    randomize_kernel<R><<<(c.d.E + 127) / 128, 128, 0, (cudaStream_t)stream>>>(c, *dr, mask, step);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? BSIM_OK : t_set_err("randomize_kernel", e);
+}
+
 }  // namespace
 
 extern "C" {
+
+int bsim_randomize(const bsim_layout_t *l, const bsim_state_t *s, const bsim_dr_t *dr, const uint8_t *m,
+                   int64_t step, void *st) {
+    return launch_randomize<float>(l, s, dr, m, step, st);
+}
+int bsim_randomize_f64(const bsim_layout_t *l, const bsim_state64_t *s, const bsim_dr_t *dr, const uint8_t *m,
+                       int64_t step, void *st) {
+    return launch_randomize<double>(l, s, dr, m, step, st);
+}
 
 int bsim_task_step(const bsim_layout_t *l, const bsim_state_t *s, const bsim_task_t *t, void *st) {
     return launch_task<float>(l, s, t, false, nullptr, st);

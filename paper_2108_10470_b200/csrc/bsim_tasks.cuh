@@ -6,6 +6,7 @@
 // AnymalObsEnv: reference envs.py:484-565, anymal_reward (flat) rewards.py:129-158.
 #pragma once
 
+#include "bsim_dr.cuh"
 #include "bsim_kin.cuh"
 #include "bsim_rng.cuh"
 
@@ -153,10 +154,11 @@ template <class R> BS_HD void anymal_obs(const Ctx<R> &c, const TaskView<R> &tv,
 // ------------------------------------------------------------ reset
 // EnvBatch.reset for one env (envs.py:145-166) with the task's _reset_envs
 // (404-419 / 517-531) and _post_reset (385-397 / 506-515).
-template <class R> BS_HD void task_reset_env(const Ctx<R> &c, const TaskView<R> &tv, int e) {
+template <class R> __device__ void task_reset_env(const Ctx<R> &c, const TaskView<R> &tv, int e) {
     const bsim_task_t &t = tv.t;
     const Dims &d = c.d;
     if (c.s.nonfinite[e]) c.s.nonfinite[e] = 0;   // clear_nonfinite (physics.py:1090)
+    dr_randomize_env(c, t.dr, e, t.step_count);   // randomizer.randomize (envs.py:154-155)
     const uint32_t genv = (uint32_t)(c.L.env_offset + e);
     uint32_t key[4] = {t.seed, genv, (uint32_t)t.reset_count[e], 0xCu};
     NpRng rng = np_rng(key, 3);
@@ -176,6 +178,11 @@ template <class R> BS_HD void task_reset_env(const Ctx<R> &c, const TaskView<R> 
         dof[2 * k] = R(np_uniform(rng, -0.1, 0.1));
         dof[2 * k + 1] = R(0);
     }
+    if (t.obs_noise) {  // per-episode correlated noise continues the reset stream (envs.py:161-164)
+        R *cn = reinterpret_cast<R *>(t.corr_noise) + (size_t)e * t.obs_dim;
+        for (int k = 0; k < t.obs_dim; ++k)
+            cn[k] = t.obs_noise_corr > 0.0 ? R(0.0 + t.obs_noise_corr * np_std_normal(rng)) : R(0);
+    }
     fk_env(c, e, 0xffffffffu);
     repack_env(c, e, 0xffffffffu);
     t.episode_steps[e] = 0;
@@ -194,13 +201,27 @@ template <class R> BS_HD void task_reset_env(const Ctx<R> &c, const TaskView<R> 
     }
 }
 
-template <class R> BS_HD void task_obs(const Ctx<R> &c, const TaskView<R> &tv, int e) {
-    if (tv.t.kind == BSIM_TASK_QUADRUPED) quad_obs(c, tv, e);
+template <class R> __device__ void task_obs(const Ctx<R> &c, const TaskView<R> &tv, int e) {
+    const bsim_task_t &t = tv.t;
+    if (t.kind == BSIM_TASK_QUADRUPED) quad_obs(c, tv, e);
     else anymal_obs(c, tv, e);
+    if (t.obs_noise) {  // perturb_observations (randomize.py:231-237)
+        R *o = tv.obs(e);
+        const R *cn = reinterpret_cast<const R *>(t.corr_noise) + (size_t)e * t.obs_dim;
+        if (t.obs_noise_uncorr > 0.0) {
+            // numpy draws this from one batch-wide stream; a per-env stream
+            // keyed (seed, 0xE7, env, count) keeps it parallel (same law)
+            uint32_t key[4] = {t.seed, 0xE7u, (uint32_t)(c.L.env_offset + e), (uint32_t)t.noise_count[e]};
+            NpRng r = np_rng(key, 4);
+            for (int k = 0; k < t.obs_dim; ++k) o[k] = o[k] + R(0.0 + t.obs_noise_uncorr * np_std_normal(r));
+            t.noise_count[e] += 1;
+        }
+        for (int k = 0; k < t.obs_dim; ++k) o[k] = o[k] + cn[k];
+    }
 }
 
 // EnvBatch.step tail after the decimated physics (envs.py:188-199)
-template <class R> BS_HD void task_step_env(const Ctx<R> &c, const TaskView<R> &tv, int e) {
+template <class R> __device__ void task_step_env(const Ctx<R> &c, const TaskView<R> &tv, int e) {
     const bsim_task_t &t = tv.t;
     int steps = t.episode_steps[e] + 1;
     t.episode_steps[e] = steps;

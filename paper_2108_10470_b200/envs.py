@@ -30,6 +30,7 @@ from . import models as M
 from .buffers import SimBuffers
 from .layout import MODE_POSITION
 from .params import SimParams
+from .randomize import DEFAULT_SCHEDULE, DR, DomainRandomizer
 from .scene import Scene
 
 ALL = None
@@ -78,12 +79,15 @@ class StepOutput(NamedTuple):
 
 
 class Task(C.Structure):
+    """bsim_task_t (include/batchsim_b200.h)."""
     _fields_ = [("kind", C.c_int32), ("obs_dim", C.c_int32), ("act_dim", C.c_int32),
-                ("episode_length", C.c_int32), ("seed", C.c_uint32), ("pad", C.c_int32),
-                ("control_dt", C.c_double), ("rest_height", C.c_double)] + [
+                ("episode_length", C.c_int32), ("seed", C.c_uint32), ("obs_noise", C.c_int32),
+                ("control_dt", C.c_double), ("rest_height", C.c_double),
+                ("obs_noise_uncorr", C.c_double), ("obs_noise_corr", C.c_double),
+                ("step_count", C.c_int64)] + [
         (n, C.c_void_p) for n in ("obs", "reward", "done", "timeout", "poisoned", "episode_steps",
                                   "reset_count", "actions", "potentials", "commands", "dof_lower",
-                                  "dof_upper")]
+                                  "dof_upper", "corr_noise", "noise_count")] + [("dr", DR)]
 
 
 def dof_limits(model):
@@ -108,9 +112,6 @@ class EnvBatch:
 
     def __init__(self, config: EnvConfig):
         self.config = cfg = config.validate()
-        if cfg.randomize or cfg.obs_noise:
-            from .randomize import check_supported
-            check_supported(cfg)
         E = cfg.num_envs
         self.model = self._model()
         self.scene = self.sim = Scene([self.model], E, self._sim_params(), device=cfg.device,
@@ -133,12 +134,20 @@ class EnvBatch:
         self.dof_lower = torch.as_tensor(lo, dtype=dt, device=dev)
         self.dof_upper = torch.as_tensor(hi, dtype=dt, device=dev)
         self._mask = torch.zeros(E, dtype=torch.uint8, device=dev)
-        self._task = Task(self.task_kind, self.obs_dim, self.act_dim, cfg.episode_length, cfg.seed, 0,
-                          cfg.control_dt, self.rest_height,
+        self.corr_noise = torch.zeros((E, self.obs_dim), dtype=dt, device=dev)
+        self.noise_count = torch.zeros(E, dtype=torch.int32, device=dev)
+        # domain randomisation (envs.py:94-96): snapshot after scene construction
+        self.randomizer = (DomainRandomizer(self.scene, DEFAULT_SCHEDULE, seed=cfg.seed)
+                           if cfg.randomize else None)
+        self._task = Task(self.task_kind, self.obs_dim, self.act_dim, cfg.episode_length, cfg.seed,
+                          int(cfg.obs_noise), cfg.control_dt, self.rest_height,
+                          float(cfg.obs_noise_uncorr), float(cfg.obs_noise_corr), 0,
                           *(t.data_ptr() for t in (self.obs, self.reward, self.done, self.timeout,
                                                    self.poisoned, self.episode_steps, self.reset_count,
                                                    self.actions, self.potentials, self.commands,
-                                                   self.dof_lower, self.dof_upper)))
+                                                   self.dof_lower, self.dof_upper, self.corr_noise,
+                                                   self.noise_count)),
+                          self.randomizer.struct if self.randomizer is not None else DR())
         self.reset()
 
     # ------------------------------------------------------------ hooks
@@ -150,6 +159,7 @@ class EnvBatch:
 
     # ------------------------------------------------------------ helpers
     def _call(self, name, *args):
+        self._task.step_count = int(self.scene.step_count)
         lib = self.scene._lib
         fn = getattr(lib, name + ("_f64" if self.scene.fp64 else ""))
         lay, _, st = self.scene._structs()

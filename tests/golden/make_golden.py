@@ -306,6 +306,7 @@ def main():
     env_cases()
     buffer_cases()
     reward_cases()
+    randomize_cases()
 
 
 # ------------------------------------------------------------- env layer
@@ -390,6 +391,46 @@ def buffer_cases():
               "root_values": root, "dof_values": dof, "idx_root": idx_r, "idx_dof": idx_d,
               "env_origins": s.env_origins}
     save("buffers_quadruped", {"kind": "buffers", "num_envs": 6}, arrays)
+
+
+def randomize_cases():
+    """DomainRandomizer (randomize.py:86-189) on an Ant-analog scene, and a
+    randomised + correlated-obs-noise env trace (uncorrelated noise off: the
+    reference draws it from one batch-wide sequential stream)."""
+    from batchsim.randomize import DEFAULT_SCHEDULE, DomainRandomizer
+    watched = ("inv_mass", "inertia_local", "inv_inertia_local", "gravity", "mu_static", "mu_dynamic",
+               "joint_stiffness", "joint_damping", "joint_limit_lo", "joint_limit_hi", "plane_rad",
+               "plane_off")
+    s = Scene([RM.quadruped()], 6, SimParams(dt=1 / 120))
+    dr = DomainRandomizer(s, DEFAULT_SCHEDULE, seed=11)
+    arrays = {}
+    dr.randomize(np.arange(6), step=0)
+    arrays.update({f"e0_{k}": getattr(s, k).copy() for k in watched})
+    dr.randomize(np.array([1, 3]), step=100)            # not due: unchanged
+    dr.randomize(np.array([0, 2, 5]), step=800)         # epoch 1 for three envs
+    arrays.update({f"e1_{k}": getattr(s, k).copy() for k in watched})
+    arrays["epoch"] = dr.epoch.copy()
+    save("randomize_quadruped", {"kind": "randomize", "num_envs": 6, "seed": 11}, arrays)
+
+    env = make_env("quadruped", num_envs=6, seed=4, episode_length=12, randomize=True, obs_noise=True,
+                   obs_noise_uncorr=0.0)
+    rng = np.random.default_rng(5)
+    rec = {k: [] for k in ("actions", "obs", "reward", "done", "gravity", "joint_stiffness", "corr")}
+    obs0 = env.reset()
+    for t in range(20):
+        a = rng.uniform(-1, 1, (6, env.act_dim))
+        out = env.step(a)
+        rec["actions"].append(a)
+        rec["obs"].append(out.obs.copy())
+        rec["reward"].append(out.reward.copy())
+        rec["done"].append(out.done.copy())
+        rec["gravity"].append(env.scene.gravity.copy())
+        rec["joint_stiffness"].append(env.scene.joint_stiffness.copy())
+        rec["corr"].append(env._corr_noise.copy())
+    arrays = {k: np.stack(v) for k, v in rec.items()}
+    arrays["obs0"] = obs0
+    save("env_quadruped_dr_noise", {"kind": "env", "task": "quadruped", "num_envs": 6, "steps": 20,
+                                    "seed": 4, "episode_length": 12}, arrays)
 
 
 def reward_cases():
