@@ -2,14 +2,16 @@
 // indexed state setters, contact queries, and their C-ABI entry points
 // (declared in include/batchsim_b200.h).
 //
-// Step kernel mapping: one CTA = one warp = 32
-// environments, one thread per environment.  The CTA's per-env workspace is
-// dynamic shared memory laid out item-major with stride 33 (odd => the
-// per-thread column accesses and the cooperative row-contiguous global
-// loads/stores are both bank-conflict free).  Body state is moved
-// HBM <-> shared memory with fully coalesced loads/stores of the CTA's
-// contiguous [32 envs x B bodies x 13] slab; all substeps of a control step
-// run on the resident workspace, so HBM sees the state once per control step.
+// Step kernel mapping: one CTA owns NE envs
+// (Shape<R> in bsim_step.cuh: 16 fp32 / 8 fp64) with 8 threads per env for
+// the lane-parallel phase A and one thread per env for the Gauss-Seidel
+// sweep.  The CTA's per-env workspace is dynamic shared memory laid out
+// item-major with the compile-time odd stride NE + 1 (per-thread column
+// accesses and the cooperative row-contiguous global loads/stores are both
+// bank-conflict free).  Body state is moved HBM <-> shared memory with fully
+// coalesced loads/stores of the CTA's contiguous [NE envs x B bodies x 13]
+// slab; all substeps of a control step run on the resident workspace, so HBM
+// sees the state once per control step.
 #include <cuda_runtime.h>
 
 #include <cstdio>
@@ -24,10 +26,6 @@ using namespace bsim;
 
 namespace {
 
-// CTA shape of the step kernel: NE environments, NTH threads.
-constexpr int NE32 = 16, NTH32 = 128;   // float path
-constexpr int NE64 = 8, NTH64 = 64;     // double path (2x the workspace per env)
-
 std::string g_err;
 
 int set_err(const char *what, cudaError_t e) {
@@ -41,22 +39,14 @@ int check_launch(const char *what) {
     return BSIM_OK;
 }
 
-template <class R> struct Shape;
-template <> struct Shape<float> {
-    static constexpr int NE = NE32, NTH = NTH32;
-};
-template <> struct Shape<double> {
-    static constexpr int NE = NE64, NTH = NTH64;
-};
-
 template <class R> size_t step_smem_bytes(const Dims &d) {
-    return (size_t)d.items * (Shape<R>::NE + 1) * sizeof(R);
+    return (size_t)d.items * Shape<R>::STR * sizeof(R);
 }
 
 // ------------------------------------------------------------------ step
 template <class R, class T>
 __global__ void __launch_bounds__(Shape<R>::NTH) step_kernel(const Ctx<R> c, int n_substeps, bsim_actions_t act) {
-    constexpr int NE = Shape<R>::NE, NTH = Shape<R>::NTH, STR = NE + 1;
+    constexpr int NE = Shape<R>::NE, NTH = Shape<R>::NTH, STR = Shape<R>::STR;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const Dims &d = c.d;
     R *ws = reinterpret_cast<R *>(smem_raw);
@@ -75,7 +65,7 @@ __global__ void __launch_bounds__(Shape<R>::NTH) step_kernel(const Ctx<R> c, int
         }
     }
     __syncthreads();
-    const Grp<R> g{ws, STR, e0, ne, tid, NTH};
+    const Grp<R> g{ws, e0, ne, tid, NTH};
     stage_group(c, g);
     if (act.actions) {  // fused action mapping (envs.py:180, 421-424)
         BS_ITEMS(g, d.D, el, k) {
@@ -83,13 +73,10 @@ __global__ void __launch_bounds__(Shape<R>::NTH) step_kernel(const Ctx<R> c, int
             R a = clampr(reinterpret_cast<const R *>(act.actions)[o], R(-1), R(1));
             if (act.actions_clipped) reinterpret_cast<R *>(act.actions_clipped)[o] = a;
             R v = R(act.scale) * a;
-            if (act.mode == BSIM_MODE_POSITION) {
+            if (act.mode == BSIM_MODE_POSITION)
                 c.s.ctrl_dof_pos_target[o] = v;
-                g.env(el).at(idf(d, k, DPT)) = v;
-            } else {
+            else
                 c.s.ctrl_dof_force[o] = v;
-                g.env(el).at(idf(d, k, DF)) = v;
-            }
         }
     }
     __syncthreads();
@@ -481,7 +468,7 @@ int bsim_step_smem_per_env(const bsim_layout_t *layout, int32_t fp64, int32_t *b
     Dims d = make_dims(*layout);
     size_t total = fp64 ? step_smem_bytes<double>(d) : step_smem_bytes<float>(d);
     if (bytes_per_env) *bytes_per_env = (int32_t)(d.items * (fp64 ? 8 : 4));
-    if (envs_per_cta) *envs_per_cta = fp64 ? NE64 : NE32;
+    if (envs_per_cta) *envs_per_cta = fp64 ? Shape<double>::NE : Shape<float>::NE;
     return total > 227 * 1024 ? BSIM_E_TOO_LARGE : BSIM_OK;
 }
 

@@ -3,22 +3,22 @@
 // path / double exact-parity path).
 //
 // B200 mapping: one CTA owns NE environments and
-// NT = NE * TPE threads.  Every TGS pass is split in two:
+// NTH = NE * 8 threads.  Every TGS pass is split in two:
 //
 //   phase A (lane-parallel over (env, body|joint|contact) items): effective
 //     poses, world inverse inertias, joint anchors/errors/axes and every
-//     row's velocity-independent constants (K^-1, impulse-response matrices,
-//     effective masses);
-//   phase B (one thread per env): the Gauss-Seidel sweep itself, which now
-//     only reads/writes body velocities and applies precomputed constants --
-//     the part of the algorithm that is inherently sequential within an env
+//     row's velocity-independent constants;
+//   phase B (one thread per env): the Gauss-Seidel sweep itself, which only
+//     reads/writes body velocities and applies precomputed constants -- the
+//     part of the algorithm that is inherently sequential within an env
 //     (environments are disjoint islands, reference physics.py:5-9).
 //
 // All per-env working state lives in shared memory, item-major / env-minor
-// with an odd stride (conflict-free per-thread columns and conflict-free
-// cooperative row loads).  The arithmetic follows the reference Scene.step
-// (/root/reference/pkg/src/batchsim/physics.py:538-592) row for row; each
-// function cites the lines it restates.  Positions are env-local.
+// with a compile-time odd stride NE + 1 (conflict-free per-thread columns and
+// conflict-free cooperative row loads; every field access is a register base
+// plus an immediate offset).  The arithmetic follows the reference
+// Scene.step (/root/reference/pkg/src/batchsim/physics.py:538-592) row for
+// row; each function cites the lines it restates.  Positions are env-local.
 #pragma once
 
 #include "bsim_math.cuh"
@@ -49,43 +49,48 @@ template <> struct Abi<double> {
     using State = bsim_state64_t;
 };
 
+// CTA shape of the step kernel: NE environments, NTH threads; the workspace
+// stride STR = NE + 1 is odd.
+template <class R> struct Shape;
+template <> struct Shape<float> {
+    static constexpr int NE = 16, NTH = 128, STR = NE + 1;
+};
+template <> struct Shape<double> {
+    static constexpr int NE = 8, NTH = 64, STR = NE + 1;
+};
+
 // ---------------------------------------------------------------- items
 // per body: pose, velocity, TGS deltas, world inverse inertia (sym), inverse
-// mass, effective pose scratch
-enum { BP = 0, BQ = 3, BV_ = 7, BW = 10, BDP = 13, BDA = 16, BI = 19, BM = 25, BPE = 26, BQE = 29,
-       BODY_ITEMS = 33 };
-// per joint: geometry, staged params, and the row constants of phase A
+// mass, effective orientation scratch
+enum { BP = 0, BQ = 3, BV_ = 7, BW = 10, BDP = 13, BDA = 16, BI = 19, BM = 25, BQE = 26, BODY_ITEMS = 30 };
+// per joint: geometry and the row constants of phase A
 enum {
-    JRP = 0, JRC = 3, JPE = 6, JRE = 9, JAX = 12, JQ0 = 15,          // geometry (freeze/refresh)
-    JSTIFF = 16, JDAMP = 17, JARM = 18, JFRIC = 19, JLO = 20, JHI = 21, // per-env parameters
-    JKI = 22,   // point-3: K^-1 ; prismatic-perp: T^T K^-1 T            (sym, 6)
-    JMC = 28,   // Ic [rc]x  (impulse at the child anchor -> d omega_c)  (3x3, 9)
-    JMP = 37,   // Ip [rp]x                                              (3x3, 9)
-    JHC = 46,   // Ic T^T K^-1 T  (angular rows)                         (3x3, 9)
-    JHP = 55,   // Ip T^T K^-1 T                                         (3x3, 9)
-    JX1 = 64, JX2 = 67,   // axis-row jacobians on omega_c / omega_p
-    JY1 = 70, JY2 = 73,   // axis-row responses on omega_c / omega_p per unit impulse
-    JMEFF = 76,
-    // per-pass constants of the drive / limit rows (phase A, so the sweep divides nothing)
-    JDA = 77, JDB = 78,   // PD impulse = DA - DB * qd  (812-848, implicit discretisation)
-    JLF = 79,             // direct-actuation impulse (FORCE mode)
-    JMFH = 80,            // max_force * h clamp
-    JFRH = 81,            // joint friction bound fr * h (0 = off)
-    JLV = 82,             // limit state this pass: 0 none, 1 below lo, 2 above hi
-    JLB = 83,             // limit bias velocity this pass
-    JOINT_ITEMS = 84
+    JRP = 0, JRC = 3,     // anchor arms (parent / child)
+    JPE = 6,              // perr0 after geometry; the linear target -perr0/h after pass constants
+    JRE = 9,              // rerr0 after geometry; the angular target -rerr0/h after pass constants
+    JAX = 12, JQ0 = 15,   // world joint axis, joint coordinate q0
+    JKI = 16,             // point-3: K^-1 ; prismatic-perp: T^T K^-1 T            (sym, 6)
+    JG = 22,              // angular rows: T^T (T Isum T^T)^-1 T                   (sym, 6)
+    JY1 = 28, JY2 = 31,   // axis rows: I_c x1 / I_p x2 per unit impulse
+    JMEFF = 34,
+    // per-pass constants of the drive / limit rows (so the sweep divides nothing)
+    JDA = 35, JDB = 36,   // PD impulse = DA - DB * qd  (812-848, implicit discretisation)
+    JLF = 37,             // direct-actuation impulse (FORCE mode)
+    JFRH = 38,            // joint friction bound fr * h (0 = off)
+    JLV = 39,             // limit state this pass: 0 none, 1 below lo, 2 above hi
+    JLB = 40,             // limit bias velocity this pass
+    JOINT_ITEMS = 41
 };
-// per plane contact slot
-enum { CR = 0, CD0 = 3, CREST = 4, CLN = 5, CLT = 6, CTE = 8, CACT = 10, CPT = 11, CXN = 14, CX1 = 17,
-       CX2 = 20, CIXN = 23, CIX1 = 26, CIX2 = 29, CMN = 32, CM1 = 33, CM2 = 34,
-       CTGT = 35, CST1 = 36, CST2 = 37,   // per pass: normal target velocity, stiction terms
-       PLANE_ITEMS = 38 };
+// per plane contact slot (normal z, tangents (0,-1,0) and (1,0,0): every
+// jacobian is a permutation of the arm r, so only r is stored)
+enum { CR = 0, CD0 = 3, CREST = 4, CLN = 5, CLT = 6, CTE = 8, CACT = 10, CIXN = 11, CIX1 = 14, CIX2 = 17,
+       CMN = 20, CM1 = 21, CM2 = 22, CTGT = 23, CST1 = 24, CST2 = 25, PLANE_ITEMS = 26 };
 // per sphere-sphere pair slot
 enum { QR = 0, QRA = 3, QN = 6, QT1 = 9, QT2 = 12, QD0 = 15, QREST = 16, QLN = 17, QLT = 18, QACT = 20,
        QPT = 21, QXN = 24, QX1 = 27, QX2 = 30, QYN = 33, QY1 = 36, QY2 = 39, QIXN = 42, QIX1 = 45,
        QIX2 = 48, QIYN = 51, QIY1 = 54, QIY2 = 57, QMN = 60, QM1 = 61, QM2 = 62, QTGT = 63, PAIR_ITEMS = 64 };
-// per dof: impulse accumulator, start-of-step readout, staged controls
-enum { DIMP = 0, DQ0 = 1, DPT = 2, DVT = 3, DF = 4, DMODE = 5, DOF_ITEMS = 6 };
+// per dof: impulse accumulator, start-of-step readout
+enum { DIMP = 0, DQ0 = 1, DOF_ITEMS = 2 };
 // per env
 enum { EMUS = 0, EMUD = 1, EGX = 2, EGY = 3, EGZ = 4, EBAD = 5, ENV_ITEMS = 6 };
 
@@ -110,11 +115,10 @@ BS_HD Dims make_dims(const bsim_layout_t &L) {
     return d;
 }
 
-// One env's column of the shared workspace.
+// One env's column of the shared workspace (compile-time stride).
 template <class R> struct Ws {
     R *base;
-    int stride;
-    BS_HD R &at(int i) const { return base[i * stride]; }
+    BS_HD R &at(int i) const { return base[i * Shape<R>::STR]; }
     BS_HD V3<R> l3(int i) const { return V3<R>{at(i), at(i + 1), at(i + 2)}; }
     BS_HD void s3(int i, V3<R> v) const { at(i) = v.x; at(i + 1) = v.y; at(i + 2) = v.z; }
     BS_HD Q4<R> l4(int i) const { return Q4<R>{at(i), at(i + 1), at(i + 2), at(i + 3)}; }
@@ -122,13 +126,6 @@ template <class R> struct Ws {
     BS_HD S3<R> lS(int i) const { return S3<R>{at(i), at(i + 1), at(i + 2), at(i + 3), at(i + 4), at(i + 5)}; }
     BS_HD void sS(int i, const S3<R> &m) const {
         at(i) = m.xx; at(i + 1) = m.xy; at(i + 2) = m.xz; at(i + 3) = m.yy; at(i + 4) = m.yz; at(i + 5) = m.zz;
-    }
-    BS_HD M3<R> lM(int i) const {
-        return M3<R>{at(i), at(i + 1), at(i + 2), at(i + 3), at(i + 4), at(i + 5), at(i + 6), at(i + 7), at(i + 8)};
-    }
-    BS_HD void sM(int i, const M3<R> &m) const {
-        at(i) = m.a00; at(i + 1) = m.a01; at(i + 2) = m.a02; at(i + 3) = m.a10; at(i + 4) = m.a11;
-        at(i + 5) = m.a12; at(i + 6) = m.a20; at(i + 7) = m.a21; at(i + 8) = m.a22;
     }
 };
 
@@ -140,7 +137,7 @@ template <class R> struct Ctx {
     typename Abi<R>::Params p;
     typename Abi<R>::State s;
     Dims d;
-    const Joint *joints;   // shared-memory copy (device) or the host table
+    const Joint *joints;
     BS_HD const Tendon &tendon(int i) const { return reinterpret_cast<const Tendon *>(L.tendons)[i]; }
     BS_HD const TElem *elems() const { return reinterpret_cast<const TElem *>(L.tendon_elems); }
 };
@@ -157,12 +154,11 @@ template <class R> BS_HD Q4<R> jq4(const R *a) { return Q4<R>{a[0], a[1], a[2], 
 // CTA-level view: thread `tid` of `nth`, envs [e0, e0 + ne) in the workspace.
 template <class R> struct Grp {
     R *ws;
-    int stride, e0, ne, tid, nth;
-    BS_HD Ws<R> env(int el) const { return Ws<R>{ws + el, stride}; }
+    int e0, ne, tid, nth;
+    BS_HD Ws<R> env(int el) const { return Ws<R>{ws + el}; }
 };
 
 // ====================================================== phase A pieces
-// Per-env parameters / controls the rows reuse every pass (read once / step).
 template <class R> BS_HD void stage_env(const Ctx<R> &c, const Ws<R> &w, int e) {
     const Dims &d = c.d;
     const auto &s = c.s;
@@ -173,33 +169,14 @@ template <class R> BS_HD void stage_env(const Ctx<R> &c, const Ws<R> &w, int e) 
     w.at(d.o_env + EGZ) = s.gravity[3 * (size_t)e + 2];
     w.at(d.o_env + EBAD) = R(0);
 }
-template <class R> BS_HD void stage_joint(const Ctx<R> &c, const Ws<R> &w, int e, int j) {
-    const Dims &d = c.d;
-    size_t o = (size_t)j * d.E + e;
-    w.at(ij(d, j, JSTIFF)) = c.s.joint_stiffness[o];
-    w.at(ij(d, j, JDAMP)) = c.s.joint_damping[o];
-    w.at(ij(d, j, JARM)) = c.s.joint_armature[o];
-    w.at(ij(d, j, JFRIC)) = c.s.joint_friction[o];
-    w.at(ij(d, j, JLO)) = c.s.joint_limit_lo[o];
-    w.at(ij(d, j, JHI)) = c.s.joint_limit_hi[o];
-}
-template <class R> BS_HD void stage_dof(const Ctx<R> &c, const Ws<R> &w, int e, int k) {
-    const Dims &d = c.d;
-    size_t o = (size_t)e * d.D + k;
-    w.at(idf(d, k, DPT)) = c.s.ctrl_dof_pos_target[o];
-    w.at(idf(d, k, DVT)) = c.s.ctrl_dof_vel_target[o];
-    w.at(idf(d, k, DF)) = c.s.ctrl_dof_force[o];
-    w.at(idf(d, k, DMODE)) = (R)c.s.dof_mode[o];
-}
 
-// world inverse inertia of body b from the pose at `qitem` (physics.py:594-596)
+// world inverse inertia of body b from orientation item qitem (physics.py:594-596)
 template <class R> BS_HD void body_inertia(const Ctx<R> &c, const Ws<R> &w, int e, int b, int qitem) {
     V3<R> d = jv3(c.s.inv_inertia_local + 3 * ((size_t)e * c.d.B + b));
     w.sS(ib(c.d, b, BI), world_inertia(w.l4(ib(c.d, b, qitem)), d));
 }
 
-// external forces on body b (physics.py:545-552) -- gravity, clipped body
-// force and torque (the torque needs the start-of-step world inertia)
+// external forces on body b (physics.py:545-552)
 template <class R> BS_HD void body_external(const Ctx<R> &c, const Ws<R> &w, int e, int b) {
     const Dims &d = c.d;
     const R dt = c.p.dt, mf = c.p.max_force;
@@ -250,18 +227,21 @@ template <class R> BS_HD int joint_dofs(const Ctx<R> &c, const Ws<R> &w, int j, 
     return 0;
 }
 
-// Anchor arms, errors and axis of joint j from the pose at (pitem, qitem)
-// (freeze physics.py:660-680, refresh 733-756).
+// Anchor arms, errors and axis of joint j (freeze physics.py:660-680,
+// refresh 733-756).  deltas: effective pose (pos + dpos, BQE).
 template <class R>
-BS_HD void joint_geometry(const Ctx<R> &c, const Ws<R> &w, int j, int pitem, int qitem, bool refresh_q0) {
+BS_HD void joint_geometry(const Ctx<R> &c, const Ws<R> &w, int j, bool deltas, bool refresh_q0) {
     const Dims &d = c.d;
     const auto &jt = c.joints[j];
     int p = jt.parent, ch = jt.child;
+    const int qitem = deltas ? BQE : BQ;
     Q4<R> qp = w.l4(ib(d, p, qitem)), qc = w.l4(ib(d, ch, qitem));
     Q4<R> jqp = qmul(qp, jq4(jt.origin_quat)), jqc = qmul(qc, jq4(jt.child_quat));
     V3<R> rp = qrot(qp, jv3(jt.origin_pos)), rc = qrot(qc, jv3(jt.child_pos));
     // ac - ap with the body-origin difference taken first (env-local)
-    V3<R> perr = (w.l3(ib(d, ch, pitem)) - w.l3(ib(d, p, pitem))) + (rc - rp);
+    V3<R> sep = w.l3(ib(d, ch, BP)) - w.l3(ib(d, p, BP));
+    if (deltas) sep = (w.l3(ib(d, ch, BP)) + w.l3(ib(d, ch, BDP))) - (w.l3(ib(d, p, BP)) + w.l3(ib(d, p, BDP)));
+    V3<R> perr = sep + (rc - rp);
     Q4<R> qe = qmul(jqc, qconj(jqp));
     R sg = signr(qe.w);
     V3<R> aw = qrot(jqp, jv3(jt.axis));
@@ -291,8 +271,9 @@ template <class R> BS_HD void joint_constants(const Ctx<R> &c, const Ws<R> &w, i
     S3<R> Ip = w.lS(ib(d, p, BI)), Ic = w.lS(ib(d, ch, BI));
     V3<R> rp = w.l3(ij(d, j, JRP)), rc = w.l3(ij(d, j, JRC)), a = w.l3(ij(d, j, JAX));
     const int kind = jt.kind;
-    // linear block: point-3 (revolute/spherical/fixed, 872-890) or the
-    // prismatic perpendicular pair (908-928)
+    V3<R> t1, t2;
+    tangents(a, t1, t2);
+    // linear block: point-3 K^-1 (872-890) or the prismatic perpendicular pair (908-928)
     if (kind != BSIM_PRISMATIC) {
         R m = mp + mc;
         S3<R> K{m, R(0), R(0), m, R(0), m};
@@ -300,8 +281,6 @@ template <class R> BS_HD void joint_constants(const Ctx<R> &c, const Ws<R> &w, i
         add_rIr(K, rc, Ic);
         w.sS(ij(d, j, JKI), sinv(K));
     } else {
-        V3<R> t1, t2;
-        tangents(a, t1, t2);
         R m = mp + mc;
         V3<R> p1 = cross(rp, t1), p2 = cross(rp, t2), c1 = cross(rc, t1), c2 = cross(rc, t2);
         V3<R> Ip1 = smul(Ip, p1), Ip2 = smul(Ip, p2), Ic1 = smul(Ic, c1), Ic2 = smul(Ic, c2);
@@ -310,22 +289,15 @@ template <class R> BS_HD void joint_constants(const Ctx<R> &c, const Ws<R> &w, i
         R k11 = dot(t2, t2) * m + dot(p2, Ip2) + dot(c2, Ic2);
         w.sS(ij(d, j, JKI), proj2(t1, t2, k00, k01, k11));
     }
-    w.sM(ij(d, j, JMC), mskew(Ic, rc));
-    w.sM(ij(d, j, JMP), mskew(Ip, rp));
     // angular block (892-906): G = T^T (T Isum T^T)^-1 T
     if (kind != BSIM_SPHERICAL) {
-        V3<R> t1, t2;
-        tangents(a, t1, t2);
         S3<R> Isum = sadd(Ip, Ic);
-        S3<R> G;
         if (kind == BSIM_REVOLUTE) {
             V3<R> i1 = smul(Isum, t1), i2 = smul(Isum, t2);
-            G = proj2(t1, t2, dot(t1, i1), dot(t1, i2), dot(t2, i2));
+            w.sS(ij(d, j, JG), proj2(t1, t2, dot(t1, i1), dot(t1, i2), dot(t2, i2)));
         } else {
-            G = proj3(t1, t2, a, Isum);
+            w.sS(ij(d, j, JG), proj3(t1, t2, a, Isum));
         }
-        w.sM(ij(d, j, JHC), smm(Ic, G));
-        w.sM(ij(d, j, JHP), smm(Ip, G));
     }
     // axis rows: drive (812-848) and limit (850-870), meff (777-788)
     if (jt.dof >= 0 && kind != BSIM_SPHERICAL) {
@@ -340,15 +312,65 @@ template <class R> BS_HD void joint_constants(const Ctx<R> &c, const Ws<R> &w, i
             x2 = cross(rp, a);
             k = mp + mc + dot(x2, smul(Ip, x2)) + dot(x1, smul(Ic, x1));
         }
-        w.s3(ij(d, j, JX1), x1);
-        w.s3(ij(d, j, JX2), x2);
         w.s3(ij(d, j, JY1), smul(Ic, x1));
         w.s3(ij(d, j, JY2), smul(Ip, x2));
         w.at(ij(d, j, JMEFF)) = R(1) / r_max(k, R(1e-12));
     }
 }
 
-// Plane contact slot i at freeze (physics.py:467-479, 683-697).
+// Per-pass constants of joint j: targets (-perr/h, -rerr/h), the PD drive's
+// affine impulse law, limit activation and bias.  Per-env gains / limits /
+// controls are read from HBM here (L1/L2 resident) instead of being staged.
+template <class R> BS_HD void joint_pass_constants(const Ctx<R> &c, const Ws<R> &w, int e, int j, R h, bool biased) {
+    const Dims &d = c.d;
+    const auto &jt = c.joints[j];
+    V3<R> pe = w.l3(ij(d, j, JPE)), re = w.l3(ij(d, j, JRE));
+    w.s3(ij(d, j, JPE), biased ? v3(-pe.x / h, -pe.y / h, -pe.z / h) : zero3<R>());   // 881
+    w.s3(ij(d, j, JRE), biased ? v3(-re.x / h, -re.y / h, -re.z / h) : zero3<R>());   // 898
+    if (jt.dof < 0 || jt.kind == BSIM_SPHERICAL) return;
+    const size_t pj = (size_t)j * d.E + e, pd = (size_t)e * d.D + jt.dof;
+    const R meff = w.at(ij(d, j, JMEFF));
+    if (biased) {  // drive (812-848): lam = LF + clip(DA - DB qd, +-mf h) [+ friction]
+        const int mode = (int)c.s.dof_mode[pd];
+        const R ia = meff + c.s.joint_armature[pj];
+        const R mf = c.p.max_force;
+        R tau = clampr(c.s.ctrl_dof_force[pd], -mf, mf);
+        R kk = mode == BSIM_MODE_POSITION ? c.s.joint_stiffness[pj] : R(0);
+        R cc = mode == BSIM_MODE_FORCE ? R(0) : c.s.joint_damping[pj];
+        R den = R(1) + h * (h * kk + cc) / ia;
+        R err = c.s.ctrl_dof_pos_target[pd] - w.at(ij(d, j, JQ0));
+        w.at(ij(d, j, JDA)) = h * (kk * err + cc * c.s.ctrl_dof_vel_target[pd]) / den;
+        w.at(ij(d, j, JDB)) = h * (kk * h + cc) / den;
+        w.at(ij(d, j, JLF)) = mode == BSIM_MODE_FORCE ? tau * h * meff / ia : R(0);
+        R fr = c.s.joint_friction[pj];
+        w.at(ij(d, j, JFRH)) = fr > R(0) ? fr * h : R(0);
+    }
+    if (jt.has_limits) {  // limit (850-870): q0 in biased passes, start-of-step q otherwise
+        R lo = c.s.joint_limit_lo[pj], hi = c.s.joint_limit_hi[pj];
+        R q = biased ? w.at(ij(d, j, JQ0)) : w.at(idf(d, jt.dof, DQ0));
+        R state = R(0), bias = R(0);
+        if (q < lo) {
+            state = R(1);
+            bias = biased ? r_max(lo - q, R(0)) / h : R(0);
+        }
+        if (q > hi) {
+            state = R(2);
+            bias = biased ? r_max(q - hi, R(0)) / h : R(0);
+        }
+        w.at(ij(d, j, JLV)) = state;
+        w.at(ij(d, j, JLB)) = bias;
+    }
+}
+
+// plane-contact jacobians: xn = r x z, x1 = r x (0,-1,0), x2 = r x (1,0,0)
+template <class R> BS_HD V3<R> plane_xn(V3<R> r) { return v3(r.y, -r.x, R(0)); }
+template <class R> BS_HD V3<R> plane_x1(V3<R> r) { return v3(r.z, R(0), -r.x); }
+template <class R> BS_HD V3<R> plane_x2(V3<R> r) { return v3(R(0), r.z, -r.y); }
+
+// Plane contact slot i at freeze (physics.py:467-479, 683-697).  The
+// friction anchor of this slot is consumed here (terr0) and immediately
+// replaced by its end-of-step value (physics.py:1021-1033 depends only on
+// frozen quantities).
 template <class R> BS_HD void plane_freeze(const Ctx<R> &c, const Ws<R> &w, int e, int i) {
     const Dims &d = c.d;
     const auto &p = c.p;
@@ -361,24 +383,26 @@ template <class R> BS_HD void plane_freeze(const Ctx<R> &c, const Ws<R> &w, int 
     R depth = p.rest_offset - gap;
     V3<R> r = v3(arm.x, arm.y, arm.z - rad);
     V3<R> point = pos + r;
-    R ax = w.at(d.o_anchor + 3 * i), ay = w.at(d.o_anchor + 3 * i + 1);
+    const int an = d.o_anchor + 3 * i;
+    R ax = w.at(an), ay = w.at(an + 1);
     bool has = !(ax != ax);
     w.at(ipl(d, i, CTE)) = has ? point.x - ax : R(0);
     w.at(ipl(d, i, CTE + 1)) = has ? point.y - ay : R(0);
+    bool near_ = depth > -p.friction_offset_threshold;
+    if (near_ && !has) w.s3(an, point);
+    if (!near_) {
+        const R nanv = r_nan(R(0));
+        w.s3(an, v3(nanv, nanv, nanv));
+    }
     V3<R> v = w.l3(ib(d, b, BV_)) + cross(w.l3(ib(d, b, BW)), r);
     R vn = v.z;
     w.s3(ipl(d, i, CR), r);
-    w.s3(ipl(d, i, CPT), point);
     w.at(ipl(d, i, CD0)) = depth;
     w.at(ipl(d, i, CREST)) = vn < -p.bounce_threshold ? -p.restitution * vn : R(0);
     w.at(ipl(d, i, CACT)) = depth > -p.solver_offset_slop ? R(1) : R(0);
     w.at(ipl(d, i, CLN)) = R(0);
     w.at(ipl(d, i, CLT)) = R(0);
     w.at(ipl(d, i, CLT + 1)) = R(0);
-    // plane normal z: tangents (0,-1,0) and (1,0,0) (physics.py:131-137)
-    w.s3(ipl(d, i, CXN), cross(r, v3(R(0), R(0), R(1))));
-    w.s3(ipl(d, i, CX1), cross(r, v3(R(0), R(-1), R(0))));
-    w.s3(ipl(d, i, CX2), cross(r, v3(R(1), R(0), R(0))));
 }
 
 // Sphere-sphere pair slot i at freeze (physics.py:481-497, 698-712).
@@ -430,7 +454,8 @@ template <class R> BS_HD void plane_constants(const Ctx<R> &c, const Ws<R> &w, i
     int b = c.L.plane_body[i];
     R im = w.at(ib(d, b, BM));
     S3<R> I = w.lS(ib(d, b, BI));
-    V3<R> xn = w.l3(ipl(d, i, CXN)), x1 = w.l3(ipl(d, i, CX1)), x2 = w.l3(ipl(d, i, CX2));
+    V3<R> r = w.l3(ipl(d, i, CR));
+    V3<R> xn = plane_xn(r), x1 = plane_x1(r), x2 = plane_x2(r);
     V3<R> in = smul(I, xn), i1 = smul(I, x1), i2 = smul(I, x2);
     w.s3(ipl(d, i, CIXN), in);
     w.s3(ipl(d, i, CIX1), i1);
@@ -455,51 +480,8 @@ template <class R> BS_HD void pair_constants(const Ctx<R> &c, const Ws<R> &w, in
     }
 }
 
-// Per-pass constants (phase A): everything in a row that is fixed for the
-// duration of one Gauss-Seidel pass -- targets (-perr/h, -rerr/h), the PD
-// drive's affine impulse law, limit activation and bias, the contact normal
-// target and stiction terms (dpos only changes between passes).
-template <class R> BS_HD void joint_pass_constants(const Ctx<R> &c, const Ws<R> &w, int j, R h, bool biased) {
-    const Dims &d = c.d;
-    const auto &jt = c.joints[j];
-    V3<R> pe = w.l3(ij(d, j, JPE)), re = w.l3(ij(d, j, JRE));
-    // JPE / JRE now hold the row targets (physics.py:881, 898)
-    w.s3(ij(d, j, JPE), biased ? v3(-pe.x / h, -pe.y / h, -pe.z / h) : zero3<R>());
-    w.s3(ij(d, j, JRE), biased ? v3(-re.x / h, -re.y / h, -re.z / h) : zero3<R>());
-    if (jt.dof < 0 || jt.kind == BSIM_SPHERICAL) return;
-    const R meff = w.at(ij(d, j, JMEFF));
-    if (biased) {  // drive (812-848): lam = LF + clip(DA - DB qd, +-mf h) [+ friction]
-        const int mode = (int)w.at(idf(d, jt.dof, DMODE));
-        const R ia = meff + w.at(ij(d, j, JARM));
-        const R mf = c.p.max_force;
-        R tau = clampr(w.at(idf(d, jt.dof, DF)), -mf, mf);
-        R kk = mode == BSIM_MODE_POSITION ? w.at(ij(d, j, JSTIFF)) : R(0);
-        R cc = mode == BSIM_MODE_FORCE ? R(0) : w.at(ij(d, j, JDAMP));
-        R den = R(1) + h * (h * kk + cc) / ia;
-        R err = w.at(idf(d, jt.dof, DPT)) - w.at(ij(d, j, JQ0));
-        w.at(ij(d, j, JDA)) = h * (kk * err + cc * w.at(idf(d, jt.dof, DVT))) / den;
-        w.at(ij(d, j, JDB)) = h * (kk * h + cc) / den;
-        w.at(ij(d, j, JLF)) = mode == BSIM_MODE_FORCE ? tau * h * meff / ia : R(0);
-        w.at(ij(d, j, JMFH)) = mf * h;
-        R fr = w.at(ij(d, j, JFRIC));
-        w.at(ij(d, j, JFRH)) = fr > R(0) ? fr * h : R(0);
-    }
-    if (jt.has_limits) {  // limit (850-870): q0 in biased passes, start-of-step q otherwise
-        R lo = w.at(ij(d, j, JLO)), hi = w.at(ij(d, j, JHI));
-        R q = biased ? w.at(ij(d, j, JQ0)) : w.at(idf(d, jt.dof, DQ0));
-        R state = R(0), bias = R(0);
-        if (q < lo) {
-            state = R(1);
-            bias = biased ? r_max(lo - q, R(0)) / h : R(0);
-        }
-        if (q > hi) {
-            state = R(2);
-            bias = biased ? r_max(q - hi, R(0)) / h : R(0);
-        }
-        w.at(ij(d, j, JLV)) = state;
-        w.at(ij(d, j, JLB)) = bias;
-    }
-}
+// per-pass contact constants: normal target and stiction (942-973; dpos is
+// fixed during a pass)
 template <class R> BS_HD void plane_pass_constants(const Ctx<R> &c, const Ws<R> &w, int i, bool biased) {
     const Dims &d = c.d;
     const int b = c.L.plane_body[i];
@@ -546,12 +528,12 @@ template <class R> BS_HD void store_bv(const Dims &d, const Ws<R> &w, int b, con
     w.s3(ib(d, b, BW), x.w);
 }
 
-// rate along a 1-DOF joint axis (physics.py:804-810) from the hoisted jacobians
+// rate along a 1-DOF joint axis (physics.py:804-810)
 template <class R>
 BS_HD R axis_rate(const Dims &d, const Ws<R> &w, int j, bool lin, const BV<R> &C, const BV<R> &P) {
-    R qd = dot(w.l3(ij(d, j, JX1)), C.w) - dot(w.l3(ij(d, j, JX2)), P.w);
-    if (lin) qd = qd + dot(w.l3(ij(d, j, JAX)), C.v - P.v);
-    return qd;
+    V3<R> a = w.l3(ij(d, j, JAX));
+    if (!lin) return dot(a, C.w - P.w);
+    return dot(cross(w.l3(ij(d, j, JRC)), a), C.w) - dot(cross(w.l3(ij(d, j, JRP)), a), P.w) + dot(a, C.v - P.v);
 }
 template <class R>
 BS_HD void axis_apply(const Dims &d, const Ws<R> &w, int j, bool lin, R lam, BV<R> &C, BV<R> &P) {
@@ -566,10 +548,10 @@ BS_HD void axis_apply(const Dims &d, const Ws<R> &w, int j, bool lin, R lam, BV<
 
 // PD drive / direct actuation / joint friction (physics.py:812-848)
 template <class R>
-BS_HD void row_drive(const Ctx<R> &c, const Ws<R> &w, int j, int dof, bool lin, BV<R> &C, BV<R> &P) {
+BS_HD void row_drive(const Ctx<R> &c, const Ws<R> &w, int j, int dof, bool lin, R h, BV<R> &C, BV<R> &P) {
     const Dims &d = c.d;
     R qd = axis_rate(d, w, j, lin, C, P);
-    const R mfh = w.at(ij(d, j, JMFH));
+    const R mfh = c.p.max_force * h;
     R lam = w.at(ij(d, j, JLF)) + clampr(w.at(ij(d, j, JDA)) - w.at(ij(d, j, JDB)) * qd, -mfh, mfh);
     R frh = w.at(ij(d, j, JFRH));
     if (frh > R(0)) lam = lam + clampr(-qd * w.at(ij(d, j, JMEFF)), -frh, frh);
@@ -591,33 +573,36 @@ BS_HD void row_limit(const Ctx<R> &c, const Ws<R> &w, int j, int dof, bool lin, 
 }
 
 // point-3 (872-890) or prismatic perpendicular pair (908-928): P = G (tgt - rel)
-template <class R> BS_HD void row_linear(const Dims &d, const Ws<R> &w, int j, BV<R> &C, BV<R> &P) {
-    V3<R> rel = (C.v + cross(C.w, w.l3(ij(d, j, JRC)))) - (P.v + cross(P.w, w.l3(ij(d, j, JRP))));
+template <class R>
+BS_HD void row_linear(const Dims &d, const Ws<R> &w, int j, int pb, int cb, BV<R> &C, BV<R> &P) {
+    V3<R> rc = w.l3(ij(d, j, JRC)), rp = w.l3(ij(d, j, JRP));
+    V3<R> rel = (C.v + cross(C.w, rc)) - (P.v + cross(P.w, rp));
     V3<R> imp = smul(w.lS(ij(d, j, JKI)), w.l3(ij(d, j, JPE)) - rel);
     C.v = C.v + imp * C.m;
-    C.w = C.w + mmul(w.lM(ij(d, j, JMC)), imp);
+    C.w = C.w + smul(w.lS(ib(d, cb, BI)), cross(rc, imp));
     P.v = P.v - imp * P.m;
-    P.w = P.w - mmul(w.lM(ij(d, j, JMP)), imp);
+    P.w = P.w - smul(w.lS(ib(d, pb, BI)), cross(rp, imp));
 }
 
-// angular rows (892-906): omega_c += Hc d, omega_p -= Hp d
-template <class R> BS_HD void row_angular(const Dims &d, const Ws<R> &w, int j, BV<R> &C, BV<R> &P) {
-    V3<R> dv = w.l3(ij(d, j, JRE)) - (C.w - P.w);
-    C.w = C.w + mmul(w.lM(ij(d, j, JHC)), dv);
-    P.w = P.w - mmul(w.lM(ij(d, j, JHP)), dv);
+// angular rows (892-906): L = G (tgt - (w_c - w_p)); w_c += Ic L, w_p -= Ip L
+template <class R>
+BS_HD void row_angular(const Dims &d, const Ws<R> &w, int j, int pb, int cb, BV<R> &C, BV<R> &P) {
+    V3<R> L = smul(w.lS(ij(d, j, JG)), w.l3(ij(d, j, JRE)) - (C.w - P.w));
+    C.w = C.w + smul(w.lS(ib(d, cb, BI)), L);
+    P.w = P.w - smul(w.lS(ib(d, pb, BI)), L);
 }
 
 // all rows of joint j in reference order (physics.py:761-773)
 template <class R>
-BS_HD void joint_rows(const Ctx<R> &c, const Ws<R> &w, int j, int kind, int dof, bool limits, bool biased,
-                      BV<R> &C, BV<R> &P) {
+BS_HD void joint_rows(const Ctx<R> &c, const Ws<R> &w, int j, int kind, int dof, bool limits, int pb, int cb,
+                      R h, bool biased, BV<R> &C, BV<R> &P) {
     const Dims &d = c.d;
     const bool axis = dof >= 0 && kind != BSIM_SPHERICAL;
     const bool lin = kind == BSIM_PRISMATIC;
-    if (biased && axis) row_drive(c, w, j, dof, lin, C, P);
-    if (kind != BSIM_PRISMATIC) row_linear(d, w, j, C, P);
-    if (kind != BSIM_SPHERICAL) row_angular(d, w, j, C, P);
-    if (kind == BSIM_PRISMATIC) row_linear(d, w, j, C, P);
+    if (biased && axis) row_drive(c, w, j, dof, lin, h, C, P);
+    if (kind != BSIM_PRISMATIC) row_linear(d, w, j, pb, cb, C, P);
+    if (kind != BSIM_SPHERICAL) row_angular(d, w, j, pb, cb, C, P);
+    if (kind == BSIM_PRISMATIC) row_linear(d, w, j, pb, cb, C, P);
     if (axis && limits) row_limit(c, w, j, dof, lin, C, P);
 }
 
@@ -625,7 +610,8 @@ BS_HD void joint_rows(const Ctx<R> &c, const Ws<R> &w, int j, int kind, int dof,
 template <class R> BS_HD void row_plane(const Ctx<R> &c, const Ws<R> &w, int i, BV<R> &X) {
     const Dims &d = c.d;
     if (w.at(ipl(d, i, CACT)) == R(0)) return;
-    R vn = X.v.z + dot(w.l3(ipl(d, i, CXN)), X.w);
+    V3<R> r = w.l3(ipl(d, i, CR));
+    R vn = X.v.z + dot(plane_xn(r), X.w);
     R lam_n = w.at(ipl(d, i, CLN));
     R dl = w.at(ipl(d, i, CMN)) * (w.at(ipl(d, i, CTGT)) - vn);
     R nl = r_max(lam_n + dl, R(0));
@@ -635,8 +621,8 @@ template <class R> BS_HD void row_plane(const Ctx<R> &c, const Ws<R> &w, int i, 
     X.v.z = X.v.z + dl * X.m;
     X.w = X.w + w.l3(ipl(d, i, CIXN)) * dl;
     // friction with t1 = (0,-1,0), t2 = (1,0,0)
-    R vt1 = -X.v.y + dot(w.l3(ipl(d, i, CX1)), X.w);
-    R vt2 = X.v.x + dot(w.l3(ipl(d, i, CX2)), X.w);
+    R vt1 = -X.v.y + dot(plane_x1(r), X.w);
+    R vt2 = X.v.x + dot(plane_x2(r), X.w);
     R mu = r_sqrt(vt1 * vt1 + vt2 * vt2) > R(1e-3) ? w.at(d.o_env + EMUD) : w.at(d.o_env + EMUS);
     vt1 = vt1 + w.at(ipl(d, i, CST1));
     vt2 = vt2 + w.at(ipl(d, i, CST2));
@@ -715,7 +701,7 @@ template <class R> BS_HD void sweep(const Ctx<R> &c, const Ws<R> &w, R h, bool b
     for (int j = 0; j < d.J; ++j) {
         const auto &jt = c.joints[j];
         BV<R> C = load_bv(d, w, jt.child), P = load_bv(d, w, jt.parent);
-        joint_rows(c, w, j, jt.kind, jt.dof, jt.has_limits != 0, biased, C, P);
+        joint_rows(c, w, j, jt.kind, jt.dof, jt.has_limits != 0, jt.parent, jt.child, h, biased, C, P);
         store_bv(d, w, jt.child, C);
         store_bv(d, w, jt.parent, P);
     }
@@ -744,24 +730,24 @@ BS_HD void static_joints(const Ctx<R> &c, const Ws<R> &w, R h, bool biased, BV<R
     if constexpr (j < T::J) {
         constexpr int kind = T::kind[j], dof = T::dof[j], ch = T::child[j], pa = T::parent[j];
         constexpr bool lim = T::limits[j] != 0;
-        joint_rows(c, w, j, kind, dof, lim, biased, bv[ch], bv[pa]);
+        joint_rows(c, w, j, kind, dof, lim, pa, ch, h, biased, bv[ch], bv[pa]);
         static_joints<R, T, j + 1>(c, w, h, biased, bv);
     }
 }
 template <class R, class T, int i>
-BS_HD void static_planes(const Ctx<R> &c, const Ws<R> &w, bool biased, BV<R> *bv) {
+BS_HD void static_planes(const Ctx<R> &c, const Ws<R> &w, BV<R> *bv) {
     if constexpr (i < T::P) {
         constexpr int b = T::plane_body[i];
         row_plane(c, w, i, bv[b]);
-        static_planes<R, T, i + 1>(c, w, biased, bv);
+        static_planes<R, T, i + 1>(c, w, bv);
     }
 }
 template <class R, class T, int i>
-BS_HD void static_pairs(const Ctx<R> &c, const Ws<R> &w, bool biased, BV<R> *bv) {
+BS_HD void static_pairs(const Ctx<R> &c, const Ws<R> &w, BV<R> *bv) {
     if constexpr (i < T::Q) {
         constexpr int pa = T::pair_a[i], pb = T::pair_b[i];
         row_pair(c, w, i, bv[pa], bv[pb]);
-        static_pairs<R, T, i + 1>(c, w, biased, bv);
+        static_pairs<R, T, i + 1>(c, w, bv);
     }
 }
 template <class R, class T> BS_HD void sweep_static(const Ctx<R> &c, const Ws<R> &w, R h, bool biased) {
@@ -770,8 +756,8 @@ template <class R, class T> BS_HD void sweep_static(const Ctx<R> &c, const Ws<R>
 #pragma unroll
     for (int b = 0; b < T::B; ++b) bv[b] = load_bv(d, w, b);
     static_joints<R, T, 0>(c, w, h, biased, bv);
-    static_planes<R, T, 0>(c, w, biased, bv);
-    static_pairs<R, T, 0>(c, w, biased, bv);
+    static_planes<R, T, 0>(c, w, bv);
+    static_pairs<R, T, 0>(c, w, bv);
 #pragma unroll
     for (int b = 0; b < T::B; ++b) {
         store_bv(d, w, b, bv[b]);
@@ -906,6 +892,7 @@ template <class R> BS_HD void apply_tendons(const Ctx<R> &c, const Ws<R> &w, int
 }
 
 // ====================================================== the group step
+// ====================================================== the group step
 // Loops over (env, item) pairs distributed over the CTA's threads; on the
 // host (tid 0 of 1) they degenerate to plain sequential loops.
 #define BS_ITEMS(g, count, el, k)                                                   \
@@ -960,18 +947,17 @@ template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> 
             }
             BS_SYNC();
         }
-        // phase A: poses -> inertias -> joint/contact geometry and row constants
-        // (freeze 657-716, refresh 718-756)
-        const int pitem = deltas ? BPE : BP, qitem = deltas ? BQE : BQ;
-        BS_ITEMS(g, d.B, el, b) {
-            Ws<R> w = g.env(el);
-            if (deltas) {
-                w.s3(ib(d, b, BPE), w.l3(ib(d, b, BP)) + w.l3(ib(d, b, BDP)));
-                w.s4(ib(d, b, BQE), qnormalize(qmul(qexp(w.l3(ib(d, b, BDA))), w.l4(ib(d, b, BQ)))));
+        // phase A: orientations -> inertias -> joint/contact geometry and row
+        // constants (freeze 657-716, refresh 718-756)
+        if (!freeze) {
+            BS_ITEMS(g, d.B, el, b) {
+                Ws<R> w = g.env(el);
+                if (deltas)
+                    w.s4(ib(d, b, BQE), qnormalize(qmul(qexp(w.l3(ib(d, b, BDA))), w.l4(ib(d, b, BQ)))));
+                body_inertia(c, w, g.e0 + el, b, deltas ? BQE : BQ);
             }
-            if (!freeze) body_inertia(c, w, g.e0 + el, b, qitem);
+            BS_SYNC();
         }
-        BS_SYNC();
         BS_ITEMS(g, d.J, el, j) {
             Ws<R> w = g.env(el);
             if (freeze) {  // read_dof_states (557): q0 and the unbiased limit rows' q
@@ -983,9 +969,9 @@ template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> 
                 }
                 if (n == 1) w.at(ij(d, j, JQ0)) = q[0];
             }
-            joint_geometry(c, w, j, pitem, qitem, !freeze);
+            joint_geometry(c, w, j, deltas, !freeze);
             joint_constants(c, w, j);
-            joint_pass_constants(c, w, j, h, biased);
+            joint_pass_constants(c, w, g.e0 + el, j, h, biased);
         }
         BS_ITEMS(g, d.P, el, i) {
             Ws<R> w = g.env(el);
@@ -1015,16 +1001,6 @@ template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> 
         R sa = r_min(R(1), p.max_angular_velocity / r_max(norm(av), R(1e-12)));
         w.s3(ib(d, b, BV_), lv * sl);
         w.s3(ib(d, b, BW), av * sa);
-    }
-    // friction anchors (1021-1033)
-    BS_ITEMS(g, d.P, el, i) {
-        Ws<R> w = g.env(el);
-        const R nanv = r_nan(R(0));
-        bool near_ = w.at(ipl(d, i, CD0)) > -p.friction_offset_threshold;
-        int a = d.o_anchor + 3 * i;
-        bool has = !(w.at(a) != w.at(a));
-        if (near_ && !has) w.s3(a, w.l3(ipl(d, i, CPT)));
-        if (!near_) w.s3(a, v3(nanv, nanv, nanv));
     }
     BS_SYNC();
 
@@ -1118,12 +1094,10 @@ template <class R> BS_HD void readout_group(const Ctx<R> &c, const Grp<R> &g) {
     }
 }
 
-// staging of all per-env inputs into the workspace (once per launch)
+// staging of the per-env inputs the rows reuse (once per launch)
 template <class R> BS_HD void stage_group(const Ctx<R> &c, const Grp<R> &g) {
     const Dims &d = c.d;
     BS_ENVS(g, el) { stage_env(c, g.env(el), g.e0 + el); }
-    BS_ITEMS(g, d.J, el, j) { stage_joint(c, g.env(el), g.e0 + el, j); }
-    BS_ITEMS(g, d.D, el, k) { stage_dof(c, g.env(el), g.e0 + el, k); }
     BS_ITEMS(g, d.B, el, b) { g.env(el).at(ib(d, b, BM)) = c.s.inv_mass[(size_t)(g.e0 + el) * d.B + b]; }
     BS_ITEMS(g, d.P, el, i) {
         for (int k = 0; k < 3; ++k)

@@ -1,7 +1,8 @@
 // TEST-ONLY host build of the step kernel's per-env body (bsim_step.cuh),
 // so the CUDA code path's arithmetic can be debugged against the oracle on a
 // CPU-only machine.  Mirrors step_kernel()'s load / stage / substep / store
-// sequence with a one-env workspace (stride 1).  Never used by the product.
+// sequence in CTA-sized env groups (stride NE + 1).  Never used by the product.
+#include <algorithm>
 #include <cstdlib>
 #include <vector>
 
@@ -20,34 +21,41 @@ static void run_t(const bsim_layout_t *L, const typename Abi<R>::Params *p, cons
     c.d = make_dims(*L);
     c.joints = reinterpret_cast<const typename Abi<R>::Joint *>(L->joints);
     const Dims &d = c.d;
-    // the whole batch as one "CTA" with a single thread: stride = E
+    // the batch in CTA-sized groups of Shape<R>::NE envs, one "thread" each
+    constexpr int NE = Shape<R>::NE, STR = Shape<R>::STR;
     const int E = d.E;
-    std::vector<R> buf((size_t)d.items * E, R(1e30));   // poison: catches unstaged reads
-    Grp<R> g{buf.data(), E, 0, E, 0, 1};
-    for (int e = 0; e < E; ++e)
-        for (int b = 0; b < d.B; ++b)
-            for (int k = 0; k < 13; ++k)
-                g.env(e).at(ib(d, b, BP) + k) = s->body_q[13 * ((size_t)e * d.B + b) + k];
-    stage_group(c, g);
-    for (int st = 0; st < n_substeps; ++st) {
-        group_step<R, T>(c, g, st == n_substeps - 1);
-        if (d.T && st != n_substeps - 1) readout_group(c, g);
-    }
-    readout_group(c, g);
-    for (int e = 0; e < E; ++e) {
-        Ws<R> w = g.env(e);
-        for (int i = 0; i < d.P; ++i)
-            for (int k = 0; k < 3; ++k) s->friction_anchor[3 * ((size_t)i * E + e) + k] = w.at(d.o_anchor + 3 * i + k);
-        for (int b = 0; b < d.B; ++b)
-            for (int k = 0; k < 13; ++k) {
-                R x = w.at(ib(d, b, BP) + k);
-                s->body_q[13 * ((size_t)e * d.B + b) + k] = x;
-                s->body_state[13 * ((size_t)e * d.B + b) + k] = k < 3 ? x + s->env_origins[3 * e + k] : x;
-            }
-        for (int a = 0; a < d.A; ++a)
-            for (int k = 0; k < 13; ++k)
-                s->root_state[13 * ((size_t)e * d.A + a) + k] =
-                    s->body_state[13 * ((size_t)e * d.B + L->actor_body_offset[a]) + k];
+    std::vector<R> buf((size_t)d.items * STR);
+    for (int e0 = 0; e0 < E; e0 += NE) {
+        const int ne = E - e0 < NE ? E - e0 : NE;
+        std::fill(buf.begin(), buf.end(), R(1e30));   // poison: catches unstaged reads
+        Grp<R> g{buf.data(), e0, ne, 0, 1};
+        for (int el = 0; el < ne; ++el)
+            for (int b = 0; b < d.B; ++b)
+                for (int k = 0; k < 13; ++k)
+                    g.env(el).at(ib(d, b, BP) + k) = s->body_q[13 * ((size_t)(e0 + el) * d.B + b) + k];
+        stage_group(c, g);
+        for (int st = 0; st < n_substeps; ++st) {
+            group_step<R, T>(c, g, st == n_substeps - 1);
+            if (d.T && st != n_substeps - 1) readout_group(c, g);
+        }
+        readout_group(c, g);
+        for (int el = 0; el < ne; ++el) {
+            const int e = e0 + el;
+            Ws<R> w = g.env(el);
+            for (int i = 0; i < d.P; ++i)
+                for (int k = 0; k < 3; ++k)
+                    s->friction_anchor[3 * ((size_t)i * E + e) + k] = w.at(d.o_anchor + 3 * i + k);
+            for (int b = 0; b < d.B; ++b)
+                for (int k = 0; k < 13; ++k) {
+                    R x = w.at(ib(d, b, BP) + k);
+                    s->body_q[13 * ((size_t)e * d.B + b) + k] = x;
+                    s->body_state[13 * ((size_t)e * d.B + b) + k] = k < 3 ? x + s->env_origins[3 * e + k] : x;
+                }
+            for (int a = 0; a < d.A; ++a)
+                for (int k = 0; k < 13; ++k)
+                    s->root_state[13 * ((size_t)e * d.A + a) + k] =
+                        s->body_state[13 * ((size_t)e * d.B + L->actor_body_offset[a]) + k];
+        }
     }
 }
 
