@@ -249,6 +249,38 @@ int bsim_randomize(const bsim_layout_t *layout, const bsim_state_t *state, const
 int bsim_randomize_f64(const bsim_layout_t *layout, const bsim_state64_t *state, const bsim_dr_t *dr,
                        const uint8_t *env_mask, int64_t step, void *stream);
 
+/* RandomForceState / random_object_force (randomize.py:192-221) on the
+   device.  Per env: a firing probability p ~ logU[p_lo, p_hi] drawn per
+   randomisation episode (bsim_force_resample, which also zeroes the force),
+   and per call a fire test u < p: on a hit the force is resampled from
+   N(0, mass^2) per axis, otherwise it decays by 0.99^(dt / 0.05).  The
+   reference draws from one batch-wide stream; here each env has its own
+   numpy-PCG64 stream keyed (seed, global env, counter) -- same law,
+   independent of the env partition. */
+typedef struct bsim_force_t {
+    int32_t num_envs, env_offset;
+    uint32_t seed;
+    int32_t fp64;               /* real arrays are double when 1, float when 0 */
+    double p_lo, p_hi;
+    void *probability;          /* [E]    firing probability                    */
+    void *force;                /* [E][3] current force                         */
+    int32_t *epoch;             /* [E]    probability-draw counter               */
+    int32_t *count;             /* [E]    per-call draw counter                  */
+} bsim_force_t;
+
+/* RandomForceState.__init__ / resample_probability(env_indices)
+   (randomize.py:200-212): masked envs (NULL = all). */
+int bsim_force_resample(const bsim_force_t *force, const uint8_t *env_mask, void *stream);
+/* random_object_force(state, mass, dt) (randomize.py:215-221).  mass: [E]
+   real.  body_force (nullable): the scene's ctrl_body_force [E*B][3]; when
+   given, row e*bodies_per_env + body receives the new force (the object the
+   disturbance acts on). */
+int bsim_random_object_force(const bsim_force_t *force, const void *mass, double dt, void *body_force,
+                             int32_t bodies_per_env, int32_t body, void *stream);
+
+/* error text of the last failed task / randomisation call */
+const char *bsim_task_last_error(void);
+
 /* EnvBatch.step() tail (envs.py:188-199): call after bsim_step(). */
 int bsim_task_step(const bsim_layout_t *layout, const bsim_state_t *state, const bsim_task_t *task,
                    void *stream);

@@ -15,6 +15,9 @@ def declare(lib):
         f = getattr(lib, "bsim_randomize" + suffix)
         f.argtypes, f.restype = [vp, vp, vp, vp, C.c_int64, vp], C.c_int
     i = C.c_int
+    lib.bsim_force_resample.argtypes, lib.bsim_force_resample.restype = [vp, vp, vp], C.c_int
+    lib.bsim_random_object_force.argtypes = [vp, vp, C.c_double, vp, C.c_int32, C.c_int32, vp]
+    lib.bsim_random_object_force.restype = C.c_int
     lib.bsim_reward_locomotion.argtypes = [i, i, i] + [vp] * 11 + [vp, vp, vp, vp]
     lib.bsim_reward_anymal.argtypes = [i, i, i, i, i] + [vp] * 9 + [vp, i, vp, vp]
     lib.bsim_reward_cube.argtypes = [i, i, i] + [vp] * 5 + [vp, vp, vp, vp, vp]

@@ -44,6 +44,52 @@ template <class R> size_t step_smem_bytes(const Dims &d) {
 }
 
 // ------------------------------------------------------------------ step
+// Sub-partition placement of the serial sweep.  A warp's SM sub-partition
+// (scheduler) is its hardware warp slot % 4; the co-resident CTAs of an SM
+// must not all run their one-warp Gauss-Seidel sweep on the same scheduler.
+// Each CTA claims a free sub-partition in a per-SM bitmask (released at
+// exit) and runs its sweep on its warp that lives there.  Placement only:
+// which lanes execute an env's sweep never changes its arithmetic.
+__device__ unsigned int g_sweep_smsp[1024];
+
+__device__ __forceinline__ unsigned hw_warp_slot() {
+    unsigned w;
+    asm volatile("mov.u32 %0, %%warpid;" : "=r"(w));
+    return w;
+}
+__device__ __forceinline__ unsigned hw_sm_id() {
+    unsigned s;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(s));
+    return s;
+}
+
+// thread 0: claim a sub-partition among those this CTA's warps occupy;
+// returns the claimed bit (0 = none free) and the warp to sweep on.
+template <int NW> __device__ unsigned claim_sweep_smsp(const int *warp_smsp, unsigned *sm_slot, int &warp) {
+    unsigned avail = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) avail |= 1u << warp_smsp[w];
+    unsigned *m = &g_sweep_smsp[*sm_slot = hw_sm_id() & 1023];
+    unsigned old = *(volatile unsigned *)m, bit = 0;
+    for (int tries = 0; tries < 8; ++tries) {
+        unsigned free_ = avail & ~old;
+        if (!free_) break;
+        unsigned b = free_ & (0u - free_);
+        unsigned prev = atomicCAS(m, old, old | b);
+        if (prev == old) {
+            bit = b;
+            break;
+        }
+        old = prev;
+    }
+    warp = 0;
+    if (bit)
+#pragma unroll
+        for (int w = 0; w < NW; ++w)
+            if ((1u << warp_smsp[w]) == bit) warp = w;
+    return bit;
+}
+
 template <class R, class T>
 __global__ void __launch_bounds__(Shape<R>::NTH) step_kernel(const Ctx<R> c, int n_substeps, bsim_actions_t act) {
     constexpr int NE = Shape<R>::NE, NTH = Shape<R>::NTH, STR = Shape<R>::STR;
@@ -54,6 +100,10 @@ __global__ void __launch_bounds__(Shape<R>::NTH) step_kernel(const Ctx<R> c, int
     const int e0 = blockIdx.x * NE;
     const int ne = min(NE, d.E - e0);
     const int per_env = 13 * d.B;
+    constexpr int NW = NTH / 32;
+    __shared__ int s_warp_smsp[NW], s_sweep_warp;
+    __shared__ unsigned s_sweep_bit, s_sm_slot;
+    if ((tid & 31) == 0) s_warp_smsp[tid >> 5] = hw_warp_slot() & 3;
 
     // coalesced load of the CTA's contiguous [ne x B x 13] body slab
     {
@@ -65,7 +115,13 @@ __global__ void __launch_bounds__(Shape<R>::NTH) step_kernel(const Ctx<R> c, int
         }
     }
     __syncthreads();
-    const Grp<R> g{ws, e0, ne, tid, NTH};
+    if (tid == 0) {
+        int w;
+        s_sweep_bit = claim_sweep_smsp<NW>(s_warp_smsp, &s_sm_slot, w);
+        s_sweep_warp = w;
+    }
+    __syncthreads();
+    const Grp<R> g{ws, e0, ne, tid, NTH, 32 * s_sweep_warp};
     stage_group(c, g);
     if (act.actions) {  // fused action mapping (envs.py:180, 421-424)
         BS_ITEMS(g, d.D, el, k) {
@@ -114,6 +170,7 @@ __global__ void __launch_bounds__(Shape<R>::NTH) step_kernel(const Ctx<R> c, int
             dr[i] = k < 3 ? x + c.s.env_origins[3 * (size_t)(e0 + el) + k] : x;
         }
     }
+    if (tid == 0 && s_sweep_bit) atomicAnd(&g_sweep_smsp[s_sm_slot], ~s_sweep_bit);
 }
 
 template <class R>

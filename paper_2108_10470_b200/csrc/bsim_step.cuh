@@ -151,10 +151,11 @@ BS_HD int idf(const Dims &d, int k, int item) { return d.o_dof + k * DOF_ITEMS +
 template <class R> BS_HD V3<R> jv3(const R *a) { return V3<R>{a[0], a[1], a[2]}; }
 template <class R> BS_HD Q4<R> jq4(const R *a) { return Q4<R>{a[0], a[1], a[2], a[3]}; }
 
-// CTA-level view: thread `tid` of `nth`, envs [e0, e0 + ne) in the workspace.
+// CTA-level view: thread `tid` of `nth`, envs [e0, e0 + ne) in the workspace;
+// per-env serial work (the sweep) runs on threads [lane0, lane0 + ne).
 template <class R> struct Grp {
     R *ws;
-    int e0, ne, tid, nth;
+    int e0, ne, tid, nth, lane0;
     BS_HD Ws<R> env(int el) const { return Ws<R>{ws + el}; }
 };
 
@@ -898,7 +899,7 @@ template <class R> BS_HD void apply_tendons(const Ctx<R> &c, const Ws<R> &w, int
 #define BS_ITEMS(g, count, el, k)                                                   \
     for (int it_ = (g).tid, n_ = (g).ne * (count); it_ < n_; it_ += (g).nth)       \
         for (int el = it_ % (g).ne, k = it_ / (g).ne, once_ = 1; once_; once_ = 0)
-#define BS_ENVS(g, el) for (int el = (g).tid; el < (g).ne; el += (g).nth)
+#define BS_ENVS(g, el) for (int el = (g).tid - (g).lane0; el >= 0 && el < (g).ne; el += (g).nth)
 
 // Scene.step() for the CTA's envs on the resident workspace
 // (physics.py:538-592).  `write_outputs`: contact-derived outputs of this

@@ -158,6 +158,97 @@ class DomainRandomizer:
         _ = E
 
 
+class Force(C.Structure):
+    """bsim_force_t (include/batchsim_b200.h)."""
+    _fields_ = [("num_envs", C.c_int32), ("env_offset", C.c_int32), ("seed", C.c_uint32),
+                ("fp64", C.c_int32), ("p_lo", C.c_double), ("p_hi", C.c_double),
+                ("probability", C.c_void_p), ("force", C.c_void_p), ("epoch", C.c_void_p),
+                ("count", C.c_void_p)]
+
+
+def _seed_of(rng):
+    if isinstance(rng, np.random.Generator):
+        return int(rng.integers(0, 2 ** 32))
+    return int(rng) & 0xFFFFFFFF
+
+
+class RandomForceState:
+    """Per-env random disturbance forces (randomize.py:192-212) on the device.
+
+    Same constructor arguments and attributes as the reference (`rng` may be
+    an integer seed or a numpy Generator, from which one seed is drawn);
+    `probability` (E,) and `force` (E, 3) are device tensors that may be
+    edited in place.  Each env draws from its own stream keyed (seed, global
+    env id, counter): the reference's batch-wide stream has the same law but
+    would tie every env's draws to the batch size.
+    """
+
+    def __init__(self, num_envs, rng=0, p_lo=0.001, p_hi=0.1, device="cuda", dtype=torch.float32,
+                 env_offset=0):
+        self.num_envs, self.p_lo, self.p_hi = int(num_envs), float(p_lo), float(p_hi)
+        if self.num_envs < 0 or not 0.0 < self.p_lo <= self.p_hi:
+            raise ValueError("need num_envs >= 0 and 0 < p_lo <= p_hi")
+        self.seed, self.env_offset = _seed_of(rng), int(env_offset)
+        E = self.num_envs
+        self.probability = torch.zeros(E, dtype=dtype, device=device)
+        self.force = torch.zeros((E, 3), dtype=dtype, device=device)
+        self._epoch = torch.zeros(E, dtype=torch.int32, device=device)
+        self._count = torch.zeros(E, dtype=torch.int32, device=device)
+        self._mask = torch.zeros(E, dtype=torch.uint8, device=device)
+        self._lib = N.lib()
+        self.resample_probability(None)
+
+    @property
+    def fp64(self):
+        return self.force.dtype == torch.float64
+
+    def struct(self):
+        return Force(self.num_envs, self.env_offset, self.seed, int(self.fp64), self.p_lo, self.p_hi,
+                     self.probability.data_ptr(), self.force.data_ptr(), self._epoch.data_ptr(),
+                     self._count.data_ptr())
+
+    def resample_probability(self, env_indices):
+        """New firing probability and zero force for the given envs (None = all)."""
+        mptr = None
+        if env_indices is not None:
+            idx = torch.as_tensor(np.atleast_1d(np.asarray(env_indices, dtype=np.int64)),
+                                  device=self.force.device)
+            if idx.numel() == 0:
+                return
+            if int(idx.min()) < 0 or int(idx.max()) >= self.num_envs:
+                raise IndexError("env index out of range")
+            self._mask.zero_()
+            self._mask[idx] = 1
+            mptr = self._mask.data_ptr()
+        f = self.struct()
+        rc = self._lib.bsim_force_resample(C.byref(f), mptr, torch.cuda.current_stream().cuda_stream)
+        if rc != 0:
+            raise N.NativeError(f"bsim_force_resample failed ({rc})")
+
+
+def random_object_force(state, mass, dt, body_force=None, body=0, bodies_per_env=1):
+    """Fire-or-decay update of `state.force` (randomize.py:215-221); returns a
+    copy.  With `body_force` (a scene's ctrl_body_force, (E*B, 3)) the new
+    force is also written to row e*bodies_per_env + body in the same launch."""
+    f = state.force
+    m = mass if isinstance(mass, torch.Tensor) else torch.as_tensor(np.asarray(mass, dtype=np.float64))
+    m = m.to(f.device, f.dtype).reshape(-1).contiguous()
+    if m.numel() != state.num_envs:
+        raise ValueError("mass must have one entry per env")
+    bptr = None
+    if body_force is not None:
+        if body_force.dtype != f.dtype or body_force.device != f.device or not body_force.is_contiguous() \
+                or body_force.numel() != 3 * state.num_envs * bodies_per_env:
+            raise ValueError("body_force must be a contiguous (E*B, 3) tensor of the state's dtype")
+        bptr = body_force.data_ptr()
+    s = state.struct()
+    rc = state._lib.bsim_random_object_force(C.byref(s), m.data_ptr(), float(dt), bptr, int(bodies_per_env),
+                                             int(body), torch.cuda.current_stream().cuda_stream)
+    if rc != 0:
+        raise N.NativeError(f"bsim_random_object_force failed ({rc})")
+    return f.clone()
+
+
 def check_supported(cfg):
     """EnvConfig.randomize / obs_noise are supported on the device."""
     return True
