@@ -100,6 +100,26 @@ class ClockSampler:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons}
 
 
+def ncu_traffic(envs):
+    """dram__bytes_read.sum + dram__bytes_write.sum per step-kernel launch from
+    the newest committed `ncu --set full` summary of this workload
+    (profiles/r*_step_*_ncu.json, written by tools/ncu_summary.py), else None."""
+    import glob
+    best = None
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_step_*_ncu.json"))):
+        try:
+            with open(path) as f:
+                j = json.load(f)
+        except (OSError, ValueError):
+            continue
+        if j.get("envs") != envs:
+            continue
+        for l in j.get("launches", []):
+            if "step_kernel<float" in l.get("kernel", "") and "dram_bytes_per_launch" in l:
+                best = (l["dram_bytes_per_launch"], os.path.basename(path), l.get("fp32_flop_per_env_launch"))
+    return best
+
+
 def kernel_bytes(env):
     """Compulsory HBM bytes of one fused step-kernel launch (reads + writes of
     every array the launch touches, counted once), per env."""
@@ -212,8 +232,13 @@ def run_gpu(args):
     pk, src = peaks()
     bytes_env = kernel_bytes(env)
     achieved = bytes_env * E / (k_ms / 1e3) / 1e9
-    # FP32 issue bound: ~9.3e4 flop per env-sim-step, 2 substeps per launch
-    flops = 9.3e4 * 2 * E
+    tr = ncu_traffic(E) if args.precision == "fp32" else None
+    # FP32 view: flop per env per launch measured by ncu (ffma*2 + fadd + fmul), else the
+    # SURVEY.md 8(d) estimate of 9.3e4 flop per env-sim-step x 2 substeps
+    flop_env = tr[2] if tr and tr[2] else 9.3e4 * 2
+    flops = flop_env * E
+    props = torch.cuda.get_device_properties(dev)
+    fp32_peak = props.multi_processor_count * 128 * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
@@ -226,10 +251,15 @@ def run_gpu(args):
         "gpu_launches": 2 * args.steps,
         "clocks": clocks.summary(),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                     "frac": achieved / pk["hbm_gbs"], "traffic": None, "peak_source": src,
+                     "frac": achieved / pk["hbm_gbs"], "traffic": tr[0] if tr else None,
+                     "traffic_unit": "bytes per launch (ncu dram__bytes_read+write, cold L2)",
+                     "traffic_source": f"profiles/{tr[1]}" if tr else None, "peak_source": src,
                      "kernel": "step_kernel (fused 2 substeps)", "kernel_ms": k_ms,
                      "bytes_per_env": bytes_env,
-                     "fp32_tflops_est": flops / (k_ms / 1e3) / 1e12,
+                     "fp32": {"achieved_tflops": flops / (k_ms / 1e3) / 1e12, "peak_tflops": fp32_peak,
+                              "frac": flops / (k_ms / 1e3) / 1e12 / fp32_peak,
+                              "flop_per_env_launch": flop_env,
+                              "source": "ncu-measured flop count" if tr and tr[2] else "SURVEY 8(d) estimate"},
                      "note": "compulsory bytes; the fused kernel is latency/FP32-issue bound, not HBM bound "
                              "(DESIGN.md)"},
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
@@ -241,30 +271,36 @@ def run_gpu(args):
         dist.destroy_process_group()
 
 
-def cpu_baseline(args, bounded=True):
-    """The C oracle (float64 port of the reference step) on this host's cores,
-    on a bounded sample of the same workload (see DESIGN.md)."""
+def _oracle_scene(n_envs, threads):
     import numpy as np
 
     from oracle.oracle import OracleScene, build
     from paper_2108_10470_b200 import models as M
     from paper_2108_10470_b200.params import SimParams
     build()
-    threads = os.cpu_count() or 1
-    sample = min(args.envs, args.cpu_sample_envs)
-    s = OracleScene([M.quadruped()], sample, SimParams(dt=1 / 120), threads=threads)
+    s = OracleScene([M.quadruped()], n_envs, SimParams(dt=1 / 120), threads=threads)
     s.pos[:, 2] += 0.37
     s.forward_kinematics()
-    rng = np.random.default_rng(0)
-    s.ctrl_dof_pos_target[:] = 0.6 * rng.uniform(-1, 1, s.num_dofs)
+    return s, np.random.default_rng(0)
+
+
+def _oracle_control_step(s, rng):
+    s.ctrl_dof_pos_target[:] = 0.6 * rng.uniform(-1, 1, s.num_dofs)   # envs.py:421-424
     s.step()
     s.step()
+
+
+def cpu_baseline(args, bounded=True):
+    """The C oracle (float64 port of the reference step) on this host's cores,
+    on a bounded sample of the same workload (see DESIGN.md)."""
+    threads = os.cpu_count() or 1
+    sample = min(args.envs, args.cpu_sample_envs)
+    s, rng = _oracle_scene(sample, threads)
+    _oracle_control_step(s, rng)
     n = 0
     t0 = time.perf_counter()
     while True:
-        s.ctrl_dof_pos_target[:] = 0.6 * rng.uniform(-1, 1, s.num_dofs)
-        s.step()
-        s.step()
+        _oracle_control_step(s, rng)
         n += 1
         dt = time.perf_counter() - t0
         if dt > args.cpu_seconds or n >= args.cpu_max_steps:
@@ -276,19 +312,34 @@ def cpu_baseline(args, bounded=True):
 
 
 def run_reference(args):
+    """The reference arm: the reference's algorithm on the host cores.  The
+    reference is pure Python/NumPy and cannot travel to the GPU box, so this
+    times its float64 C restatement (oracle/bso.c, the `port`), which is ~7x
+    faster per core than the NumPy reference: W warm-up and K
+    timed control steps of the same workload (all envs of one GPU's shard)."""
     rank, world, _ = dist_info()
     if rank != 0:
         return
-    base = cpu_baseline(args, bounded=True)
-    # per-step bounded samples: warm-up + K steps of the same sample
-    line = {"metric": METRIC, "value": base["value"], "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
+    threads = os.cpu_count() or 1
+    n_envs = args.envs
+    s, rng = _oracle_scene(n_envs, threads)
+    for _ in range(args.warmup):
+        _oracle_control_step(s, rng)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        _oracle_control_step(s, rng)
+    dt = time.perf_counter() - t0
+    value = n_envs * args.steps / dt
+    base = {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{n_envs} envs x {args.steps} timed control steps (2 substeps each, after "
+                      f"{args.warmup} warm-up), C oracle float64 (oracle/bso.c, OpenMP {threads} threads)"}
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (uniform random actions)", "impl": "reference",
-            "config": {"workload": WORKLOAD, "envs_per_gpu": args.envs, "substeps": 2},
+            "config": {"workload": WORKLOAD, "envs_per_gpu": n_envs, "substeps": 2},
             "cpu_baseline": base,
-            "e2e": {"value": base["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    line["ms_per_step"] = 1e3 * args.envs / base["value"]
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
