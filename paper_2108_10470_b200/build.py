@@ -44,7 +44,8 @@ def build(force=False, verbose=False):
     objs = []
     for src in sources():
         obj = os.path.join(HERE, "_lib", os.path.basename(src)[:-3] + ".o")
-        cmd = ["nvcc", *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
+        extra = os.environ.get("BSIM_NVCC_EXTRA", "").split()   # dev experiments only
+        cmd = ["nvcc", *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)

@@ -29,6 +29,20 @@ BS_HD float r_sin(float x) { return sinf(x); }
 BS_HD double r_sin(double x) { return sin(x); }
 BS_HD float r_cos(float x) { return cosf(x); }
 BS_HD double r_cos(double x) { return cos(x); }
+BS_HD void r_sincos(float x, float &s, float &c) {
+#if defined(__CUDA_ARCH__)
+    sincosf(x, &s, &c);
+#else
+    s = sinf(x); c = cosf(x);
+#endif
+}
+BS_HD void r_sincos(double x, double &s, double &c) {
+#if defined(__CUDA_ARCH__)
+    sincos(x, &s, &c);
+#else
+    s = sin(x); c = cos(x);
+#endif
+}
 BS_HD float r_atan2(float y, float x) { return atan2f(y, x); }
 BS_HD double r_atan2(double y, double x) { return atan2(y, x); }
 BS_HD float r_floor(float x) { return floorf(x); }
@@ -42,6 +56,18 @@ BS_HD double r_min(double a, double b) { return fmin(a, b); }
 BS_HD float exp_r(float x) { return expf(x); }
 BS_HD double exp_r(double x) { return exp(x); }
 BS_HD float r_nan(float) { return nanf(""); }
+// reciprocal / reciprocal square root: one MUFU op (+ multiply) on the fp32
+// device path instead of an IEEE division sequence (<= 2 ulp; the fp32 parity
+// budget is 1e-4); exact IEEE on the host and in the fp64 parity path.
+#if defined(__CUDA_ARCH__)
+BS_HD float r_rcp(float x) { return __fdividef(1.0f, x); }
+BS_HD float r_rsqrt(float x) { return rsqrtf(x); }
+#else
+BS_HD float r_rcp(float x) { return 1.0f / x; }
+BS_HD float r_rsqrt(float x) { return 1.0f / sqrtf(x); }
+#endif
+BS_HD double r_rcp(double x) { return 1.0 / x; }
+BS_HD double r_rsqrt(double x) { return 1.0 / sqrt(x); }
 BS_HD double r_nan(double) { return nan(""); }
 
 template <class R> struct V3 {
@@ -77,9 +103,10 @@ template <class R> BS_HD Q4<R> qmul(Q4<R> a, Q4<R> b) {
 }
 template <class R> BS_HD Q4<R> qconj(Q4<R> q) { return Q4<R>{-q.x, -q.y, -q.z, q.w}; }
 template <class R> BS_HD Q4<R> qnormalize(Q4<R> q) {
-    R n = r_sqrt(q.x * q.x + q.y * q.y + q.z * q.z + q.w * q.w);
-    if (n > R(0)) {
-        q.x = q.x / n; q.y = q.y / n; q.z = q.z / n; q.w = q.w / n;
+    R n2 = q.x * q.x + q.y * q.y + q.z * q.z + q.w * q.w;
+    if (n2 > R(0)) {
+        R in = r_rsqrt(n2);
+        q.x = q.x * in; q.y = q.y * in; q.z = q.z * in; q.w = q.w * in;
     }
     return q;
 }
@@ -94,8 +121,9 @@ template <class R> BS_HD V3<R> qrot(Q4<R> q, V3<R> v) {
 template <class R> BS_HD Q4<R> qexp(V3<R> v) {
     R ang = norm(v);
     V3<R> ax = v3(R(1), R(0), R(0));
-    if (!(ang < R(1e-12))) ax = v * (R(1) / ang);
-    R s = r_sin(R(0.5) * ang), c = r_cos(R(0.5) * ang);
+    if (!(ang < R(1e-12))) ax = v * r_rcp(ang);
+    R s, c;
+    r_sincos(R(0.5) * ang, s, c);
     return Q4<R>{ax.x * s, ax.y * s, ax.z * s, c};
 }
 // log map (spatial.py:155-162)
@@ -158,13 +186,13 @@ template <class R> BS_HD V3<R> ssolve(const S3<R> &K, V3<R> b) {
 template <class R> BS_HD S3<R> sinv(const S3<R> &K) {
     R c00 = K.yy * K.zz - K.yz * K.yz, c01 = K.xz * K.yz - K.xy * K.zz, c02 = K.xy * K.yz - K.xz * K.yy;
     R c11 = K.xx * K.zz - K.xz * K.xz, c12 = K.xy * K.xz - K.xx * K.yz, c22 = K.xx * K.yy - K.xy * K.xy;
-    R det = K.xx * c00 + K.xy * c01 + K.xz * c02;
-    return S3<R>{c00 / det, c01 / det, c02 / det, c11 / det, c12 / det, c22 / det};
+    R id = r_rcp(K.xx * c00 + K.xy * c01 + K.xz * c02);
+    return S3<R>{c00 * id, c01 * id, c02 * id, c11 * id, c12 * id, c22 * id};
 }
 // T^T K^-1 T for T = [t1; t2] and K = [[k00, k01], [k01, k11]]
 template <class R> BS_HD S3<R> proj2(V3<R> t1, V3<R> t2, R k00, R k01, R k11) {
-    R det = k00 * k11 - k01 * k01;
-    R i00 = k11 / det, i01 = -k01 / det, i11 = k00 / det;
+    R id = r_rcp(k00 * k11 - k01 * k01);
+    R i00 = k11 * id, i01 = -k01 * id, i11 = k00 * id;
     auto el = [&](R a1, R b1, R a2, R b2) { return i00 * a1 * b1 + i01 * (a1 * b2 + a2 * b1) + i11 * a2 * b2; };
     return S3<R>{el(t1.x, t1.x, t2.x, t2.x), el(t1.x, t1.y, t2.x, t2.y), el(t1.x, t1.z, t2.x, t2.z),
                  el(t1.y, t1.y, t2.y, t2.y), el(t1.y, t1.z, t2.y, t2.z), el(t1.z, t1.z, t2.z, t2.z)};
@@ -196,8 +224,8 @@ template <class R> BS_HD void ssolve2(R a, R b, R c, R r0, R r1, R &x0, R &x1) {
 template <class R> BS_HD void tangents(V3<R> n, V3<R> &t1, V3<R> &t2) {
     V3<R> ref = r_abs(n.z) < R(0.9) ? v3(R(0), R(0), R(1)) : v3(R(1), R(0), R(0));
     V3<R> t = cross(ref, n);
-    R l = norm(t);
-    t1 = v3(t.x / l, t.y / l, t.z / l);
+    R il = r_rsqrt(dot(t, t));
+    t1 = v3(t.x * il, t.y * il, t.z * il);
     t2 = cross(n, t1);
 }
 
@@ -207,7 +235,7 @@ template <class R> BS_HD R signr(R x) { return x > R(0) ? R(1) : (x < R(0) ? R(-
 template <class R> BS_HD R wrap_pi(R a) {
     const R TWO_PI = R(6.28318530717958647692), PI = R(3.14159265358979323846);
     R r = a + PI;
-    r = r - TWO_PI * r_floor(r / TWO_PI);
+    r = r - TWO_PI * r_floor(r * R(0.15915494309189533577));
     return r - PI;
 }
 template <class R> BS_HD bool finite_r(R x) { return x - x == R(0); }

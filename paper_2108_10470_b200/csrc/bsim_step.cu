@@ -90,15 +90,21 @@ template <int NW> __device__ unsigned claim_sweep_smsp(const int *warp_smsp, uns
     return bit;
 }
 
+#ifndef BSIM_MINB
+#define BSIM_MINB 4   // 4 x 128 threads at <= 128 registers: matches the shared-memory limit
+#endif
+// `epc` envs per CTA (<= NE): chosen by the launcher so the grid is a whole
+// number of waves of resident CTAs (148 SMs x CTAs/SM)
 template <class R, class T>
-__global__ void __launch_bounds__(Shape<R>::NTH) step_kernel(const Ctx<R> c, int n_substeps, bsim_actions_t act) {
-    constexpr int NE = Shape<R>::NE, NTH = Shape<R>::NTH, STR = Shape<R>::STR;
+__global__ void __launch_bounds__(Shape<R>::NTH, BSIM_MINB)
+    step_kernel(const Ctx<R> c, int n_substeps, bsim_actions_t act, int epc) {
+    constexpr int NTH = Shape<R>::NTH, STR = Shape<R>::STR;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const Dims &d = c.d;
     R *ws = reinterpret_cast<R *>(smem_raw);
     const int tid = threadIdx.x;
-    const int e0 = blockIdx.x * NE;
-    const int ne = min(NE, d.E - e0);
+    const int e0 = blockIdx.x * epc;
+    const int ne = min(epc, d.E - e0);
     const int per_env = 13 * d.B;
     constexpr int NW = NTH / 32;
     __shared__ int s_warp_smsp[NW], s_sweep_warp;
@@ -394,16 +400,36 @@ bool bad_layout(const bsim_layout_t *L) {
 
 // ------------------------------------------------------------ launchers
 template <class R, class T>
-int launch_step_t(const Ctx<R> &c, size_t smem, int grid, int n_substeps, const bsim_actions_t &act,
-                  cudaStream_t st) {
+int launch_step_t(const Ctx<R> &c, size_t smem, int n_substeps, const bsim_actions_t &act, cudaStream_t st) {
+    constexpr int NE = Shape<R>::NE;
     static size_t configured = 0;
+    static int slots = 0;   // resident CTAs on the whole device at this smem size
     if (smem > 48 * 1024 && smem > configured) {
         cudaError_t e = cudaFuncSetAttribute(step_kernel<R, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
         if (e != cudaSuccess) return set_err("cudaFuncSetAttribute(step_kernel)", e);
         configured = smem;
+        slots = 0;
     }
-    step_kernel<R, T><<<grid, Shape<R>::NTH, smem, st>>>(c, n_substeps, act);
+    if (slots == 0) {
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<R, T>, Shape<R>::NTH, smem);
+        slots = sms * (per_sm > 0 ? per_sm : 1);
+    }
+    // whole waves: the fewest waves of <= NE envs per CTA, then spread the envs
+    // evenly over waves x slots CTAs (no partial last wave)
+    const int E = c.d.E;
+    int epc = NE;
+#ifndef BSIM_NO_BALANCE
+    const long waves = ((long)E + (long)NE * slots - 1) / ((long)NE * slots);
+    epc = (int)(((long)E + waves * slots - 1) / (waves * slots));
+    if (epc < 1) epc = 1;
+    if (epc > NE) epc = NE;
+#endif
+    const int grid = (E + epc - 1) / epc;
+    step_kernel<R, T><<<grid, Shape<R>::NTH, smem, st>>>(c, n_substeps, act, epc);
     return check_launch("step_kernel");
 }
 
@@ -424,16 +450,15 @@ int launch_step(const bsim_layout_t *layout, const typename Abi<R>::Params *para
     }
     bsim_actions_t act;
     if (actions) act = *actions; else std::memset(&act, 0, sizeof act);
-    int grid = (c.d.E + Shape<R>::NE - 1) / Shape<R>::NE;
     cudaStream_t st = (cudaStream_t)stream;
     switch (layout->topology_id) {
 #define BSIM_LAUNCH_TOPO(ID, TYPE)                                      \
     case ID:                                                            \
-        return launch_step_t<R, TYPE>(c, smem, grid, n_substeps, act, st);
+        return launch_step_t<R, TYPE>(c, smem, n_substeps, act, st);
         BSIM_TOPOLOGIES(BSIM_LAUNCH_TOPO)
 #undef BSIM_LAUNCH_TOPO
     default:
-        return launch_step_t<R, TopoGeneric>(c, smem, grid, n_substeps, act, st);
+        return launch_step_t<R, TopoGeneric>(c, smem, n_substeps, act, st);
     }
 }
 

@@ -52,8 +52,14 @@ template <> struct Abi<double> {
 // CTA shape of the step kernel: NE environments, NTH threads; the workspace
 // stride STR = NE + 1 is odd.
 template <class R> struct Shape;
+#ifndef BSIM_NE32
+#define BSIM_NE32 16
+#endif
+#ifndef BSIM_NTH32
+#define BSIM_NTH32 128
+#endif
 template <> struct Shape<float> {
-    static constexpr int NE = 16, NTH = 128, STR = NE + 1;
+    static constexpr int NE = BSIM_NE32, NTH = BSIM_NTH32, STR = NE + 1;
 };
 template <> struct Shape<double> {
     static constexpr int NE = 8, NTH = 64, STR = NE + 1;
@@ -315,7 +321,7 @@ template <class R> BS_HD void joint_constants(const Ctx<R> &c, const Ws<R> &w, i
         }
         w.s3(ij(d, j, JY1), smul(Ic, x1));
         w.s3(ij(d, j, JY2), smul(Ip, x2));
-        w.at(ij(d, j, JMEFF)) = R(1) / r_max(k, R(1e-12));
+        w.at(ij(d, j, JMEFF)) = r_rcp(r_max(k, R(1e-12)));
     }
 }
 
@@ -326,8 +332,9 @@ template <class R> BS_HD void joint_pass_constants(const Ctx<R> &c, const Ws<R> 
     const Dims &d = c.d;
     const auto &jt = c.joints[j];
     V3<R> pe = w.l3(ij(d, j, JPE)), re = w.l3(ij(d, j, JRE));
-    w.s3(ij(d, j, JPE), biased ? v3(-pe.x / h, -pe.y / h, -pe.z / h) : zero3<R>());   // 881
-    w.s3(ij(d, j, JRE), biased ? v3(-re.x / h, -re.y / h, -re.z / h) : zero3<R>());   // 898
+    const R nih = -r_rcp(h);
+    w.s3(ij(d, j, JPE), biased ? pe * nih : zero3<R>());   // 881
+    w.s3(ij(d, j, JRE), biased ? re * nih : zero3<R>());   // 898
     if (jt.dof < 0 || jt.kind == BSIM_SPHERICAL) return;
     const size_t pj = (size_t)j * d.E + e, pd = (size_t)e * d.D + jt.dof;
     const R meff = w.at(ij(d, j, JMEFF));
@@ -338,11 +345,12 @@ template <class R> BS_HD void joint_pass_constants(const Ctx<R> &c, const Ws<R> 
         R tau = clampr(c.s.ctrl_dof_force[pd], -mf, mf);
         R kk = mode == BSIM_MODE_POSITION ? c.s.joint_stiffness[pj] : R(0);
         R cc = mode == BSIM_MODE_FORCE ? R(0) : c.s.joint_damping[pj];
-        R den = R(1) + h * (h * kk + cc) / ia;
+        const R iia = r_rcp(ia);
+        const R hden = h * r_rcp(R(1) + h * (h * kk + cc) * iia);
         R err = c.s.ctrl_dof_pos_target[pd] - w.at(ij(d, j, JQ0));
-        w.at(ij(d, j, JDA)) = h * (kk * err + cc * c.s.ctrl_dof_vel_target[pd]) / den;
-        w.at(ij(d, j, JDB)) = h * (kk * h + cc) / den;
-        w.at(ij(d, j, JLF)) = mode == BSIM_MODE_FORCE ? tau * h * meff / ia : R(0);
+        w.at(ij(d, j, JDA)) = (kk * err + cc * c.s.ctrl_dof_vel_target[pd]) * hden;
+        w.at(ij(d, j, JDB)) = (kk * h + cc) * hden;
+        w.at(ij(d, j, JLF)) = mode == BSIM_MODE_FORCE ? tau * h * meff * iia : R(0);
         R fr = c.s.joint_friction[pj];
         w.at(ij(d, j, JFRH)) = fr > R(0) ? fr * h : R(0);
     }
@@ -352,11 +360,11 @@ template <class R> BS_HD void joint_pass_constants(const Ctx<R> &c, const Ws<R> 
         R state = R(0), bias = R(0);
         if (q < lo) {
             state = R(1);
-            bias = biased ? r_max(lo - q, R(0)) / h : R(0);
+            bias = biased ? r_max(lo - q, R(0)) * r_rcp(h) : R(0);
         }
         if (q > hi) {
             state = R(2);
-            bias = biased ? r_max(q - hi, R(0)) / h : R(0);
+            bias = biased ? r_max(q - hi, R(0)) * r_rcp(h) : R(0);
         }
         w.at(ij(d, j, JLV)) = state;
         w.at(ij(d, j, JLB)) = bias;
@@ -461,9 +469,9 @@ template <class R> BS_HD void plane_constants(const Ctx<R> &c, const Ws<R> &w, i
     w.s3(ipl(d, i, CIXN), in);
     w.s3(ipl(d, i, CIX1), i1);
     w.s3(ipl(d, i, CIX2), i2);
-    w.at(ipl(d, i, CMN)) = R(1) / r_max(im + dot(xn, in), R(1e-12));
-    w.at(ipl(d, i, CM1)) = R(1) / r_max(im + dot(x1, i1), R(1e-12));
-    w.at(ipl(d, i, CM2)) = R(1) / r_max(im + dot(x2, i2), R(1e-12));
+    w.at(ipl(d, i, CMN)) = r_rcp(r_max(im + dot(xn, in), R(1e-12)));
+    w.at(ipl(d, i, CM1)) = r_rcp(r_max(im + dot(x1, i1), R(1e-12)));
+    w.at(ipl(d, i, CM2)) = r_rcp(r_max(im + dot(x2, i2), R(1e-12)));
 }
 template <class R> BS_HD void pair_constants(const Ctx<R> &c, const Ws<R> &w, int i) {
     const Dims &d = c.d;
@@ -477,7 +485,7 @@ template <class R> BS_HD void pair_constants(const Ctx<R> &c, const Ws<R> &w, in
         V3<R> ix = smul(Ib, xs[k]), iy = smul(Ia, ys[k]);
         w.s3(ipr(d, i, IX[k]), ix);
         w.s3(ipr(d, i, IY[k]), iy);
-        w.at(ipr(d, i, MM[k])) = R(1) / r_max(ma + mb + dot(ys[k], iy) + dot(xs[k], ix), R(1e-12));
+        w.at(ipr(d, i, MM[k])) = r_rcp(r_max(ma + mb + dot(ys[k], iy) + dot(xs[k], ix), R(1e-12)));
     }
 }
 
@@ -486,16 +494,16 @@ template <class R> BS_HD void pair_constants(const Ctx<R> &c, const Ws<R> &w, in
 template <class R> BS_HD void plane_pass_constants(const Ctx<R> &c, const Ws<R> &w, int i, bool biased) {
     const Dims &d = c.d;
     const int b = c.L.plane_body[i];
-    const R dt = c.p.dt;
+    const R idt = r_rcp(c.p.dt);
     R depth = w.at(ipl(d, i, CD0));
     R bias = R(0), st1 = R(0), st2 = R(0);
     if (biased) {
         V3<R> dp = w.l3(ib(d, b, BDP));
         depth = depth + dp.z * R(-1);                       // 942
-        bias = c.p.max_bias * r_max(depth, R(0)) / dt;      // 953
+        bias = c.p.max_bias * r_max(depth, R(0)) * idt;     // 953
         R tex = w.at(ipl(d, i, CTE)) + dp.x, tey = w.at(ipl(d, i, CTE + 1)) + dp.y;
-        st1 = (-tey) / dt;                                  // 971-973, t1 = (0,-1,0)
-        st2 = tex / dt;                                     //           t2 = (1,0,0)
+        st1 = (-tey) * idt;                                 // 971-973, t1 = (0,-1,0)
+        st2 = tex * idt;                                    //           t2 = (1,0,0)
     }
     w.at(ipl(d, i, CTGT)) = r_max(w.at(ipl(d, i, CREST)), bias);
     w.at(ipl(d, i, CST1)) = st1;
@@ -508,7 +516,7 @@ template <class R> BS_HD void pair_pass_constants(const Ctx<R> &c, const Ws<R> &
     if (biased) {
         int pa = c.L.pair_body[2 * i], pb = c.L.pair_body[2 * i + 1];
         depth = depth + dot(w.l3(ipr(d, i, QN)), w.l3(ib(d, pb, BDP)) - w.l3(ib(d, pa, BDP))) * R(-1);  // 949
-        bias = c.p.max_bias * r_max(depth, R(0)) / c.p.dt;
+        bias = c.p.max_bias * r_max(depth, R(0)) * r_rcp(c.p.dt);
     }
     w.at(ipr(d, i, QTGT)) = r_max(w.at(ipr(d, i, QREST)), bias);
 }
@@ -563,12 +571,14 @@ BS_HD void row_drive(const Ctx<R> &c, const Ws<R> &w, int j, int dof, bool lin, 
 // one-sided limit (physics.py:850-870)
 template <class R>
 BS_HD void row_limit(const Ctx<R> &c, const Ws<R> &w, int j, int dof, bool lin, BV<R> &C, BV<R> &P) {
+    // branch-free (an inactive limit applies lam = 0, which leaves the
+    // velocities bit-identical) so the scheduler can overlap independent rows
     const Dims &d = c.d;
     R state = w.at(ij(d, j, JLV));
-    if (state == R(0)) return;
     R qd = axis_rate(d, w, j, lin, C, P);
     R meff = w.at(ij(d, j, JMEFF)), bias = w.at(ij(d, j, JLB));
     R lam = state == R(1) ? r_max(meff * (bias - qd), R(0)) : -r_max(meff * (bias + qd), R(0));
+    lam = state == R(0) ? R(0) : lam;
     axis_apply(d, w, j, lin, lam, C, P);
     w.at(idf(d, dof, DIMP)) += lam;
 }
@@ -608,15 +618,17 @@ BS_HD void joint_rows(const Ctx<R> &c, const Ws<R> &w, int j, int kind, int dof,
 }
 
 // plane contact row (930-983) with the plane's fixed normal / tangents
+// Branch-free: an inactive slot (CACT = 0) applies zero impulses, leaving
+// velocities and accumulators bit-identical, so independent rows overlap.
 template <class R> BS_HD void row_plane(const Ctx<R> &c, const Ws<R> &w, int i, BV<R> &X) {
     const Dims &d = c.d;
-    if (w.at(ipl(d, i, CACT)) == R(0)) return;
+    const bool act = w.at(ipl(d, i, CACT)) != R(0);
     V3<R> r = w.l3(ipl(d, i, CR));
     R vn = X.v.z + dot(plane_xn(r), X.w);
     R lam_n = w.at(ipl(d, i, CLN));
     R dl = w.at(ipl(d, i, CMN)) * (w.at(ipl(d, i, CTGT)) - vn);
     R nl = r_max(lam_n + dl, R(0));
-    dl = nl - lam_n;
+    dl = act ? nl - lam_n : R(0);
     lam_n = lam_n + dl;
     w.at(ipl(d, i, CLN)) = lam_n;
     X.v.z = X.v.z + dl * X.m;
@@ -630,16 +642,11 @@ template <class R> BS_HD void row_plane(const Ctx<R> &c, const Ws<R> &w, int i, 
     R lt0 = w.at(ipl(d, i, CLT)), lt1 = w.at(ipl(d, i, CLT + 1));
     R c0 = lt0 + (-w.at(ipl(d, i, CM1)) * vt1), c1 = lt1 + (-w.at(ipl(d, i, CM2)) * vt2);
     R lim = mu * lam_n;
-    R nrm2 = c0 * c0 + c1 * c1;
-    if (nrm2 > lim * lim) {  // circular cone clamp
-        R nrm = r_sqrt(nrm2);
-        if (nrm > lim) {
-            R sc = lim / r_max(nrm, R(1e-12));
-            c0 = c0 * sc;
-            c1 = c1 * sc;
-        }
-    }
-    R d0 = c0 - lt0, d1 = c1 - lt1;
+    R nrm = r_sqrt(c0 * c0 + c1 * c1);   // circular cone clamp
+    R sc = nrm > lim ? lim * r_rcp(r_max(nrm, R(1e-12))) : R(1);
+    c0 = c0 * sc;
+    c1 = c1 * sc;
+    R d0 = act ? c0 - lt0 : R(0), d1 = act ? c1 - lt1 : R(0);
     w.at(ipl(d, i, CLT)) = lt0 + d0;
     w.at(ipl(d, i, CLT + 1)) = lt1 + d1;
     X.v.x = X.v.x + d1 * X.m;
@@ -726,13 +733,13 @@ template <class R> BS_HD void sweep(const Ctx<R> &c, const Ws<R> &w, R h, bool b
 // The same pass with the topology known at compile time (T = a generated
 // bsim_topologies.cuh entry): every body velocity of the env stays in
 // registers for the whole pass and rows on disjoint bodies can overlap.
-template <class R, class T, int j>
-BS_HD void static_joints(const Ctx<R> &c, const Ws<R> &w, R h, bool biased, BV<R> *bv) {
+template <class R, class T, bool BIASED, int j>
+BS_HD void static_joints(const Ctx<R> &c, const Ws<R> &w, R h, BV<R> *bv) {
     if constexpr (j < T::J) {
         constexpr int kind = T::kind[j], dof = T::dof[j], ch = T::child[j], pa = T::parent[j];
         constexpr bool lim = T::limits[j] != 0;
-        joint_rows(c, w, j, kind, dof, lim, pa, ch, h, biased, bv[ch], bv[pa]);
-        static_joints<R, T, j + 1>(c, w, h, biased, bv);
+        joint_rows(c, w, j, kind, dof, lim, pa, ch, h, BIASED, bv[ch], bv[pa]);
+        static_joints<R, T, BIASED, j + 1>(c, w, h, bv);
     }
 }
 template <class R, class T, int i>
@@ -751,18 +758,21 @@ BS_HD void static_pairs(const Ctx<R> &c, const Ws<R> &w, BV<R> *bv) {
         static_pairs<R, T, i + 1>(c, w, bv);
     }
 }
-template <class R, class T> BS_HD void sweep_static(const Ctx<R> &c, const Ws<R> &w, R h, bool biased) {
+// BIASED is a template parameter so each pass type is one straight-line
+// block (no per-joint uniform branch): the scheduler interleaves rows on
+// disjoint bodies (e.g. a knee row with the next hip row).
+template <class R, class T, bool BIASED> BS_HD void sweep_static(const Ctx<R> &c, const Ws<R> &w, R h) {
     const Dims &d = c.d;
     BV<R> bv[T::B];
 #pragma unroll
     for (int b = 0; b < T::B; ++b) bv[b] = load_bv(d, w, b);
-    static_joints<R, T, 0>(c, w, h, biased, bv);
+    static_joints<R, T, BIASED, 0>(c, w, h, bv);
     static_planes<R, T, 0>(c, w, bv);
     static_pairs<R, T, 0>(c, w, bv);
 #pragma unroll
     for (int b = 0; b < T::B; ++b) {
         store_bv(d, w, b, bv[b]);
-        if (biased) accumulate_deltas(d, w, b, bv[b], h);
+        if (BIASED) accumulate_deltas(d, w, b, bv[b], h);
     }
 }
 
@@ -771,9 +781,12 @@ struct TopoGeneric {
     static constexpr bool is_static = false;
 };
 template <class R, class T> BS_HD void sweep_any(const Ctx<R> &c, const Ws<R> &w, R h, bool biased) {
-    if constexpr (T::is_static)
-        sweep_static<R, T>(c, w, h, biased);
-    else
+    if constexpr (T::is_static) {
+        if (biased)
+            sweep_static<R, T, true>(c, w, h);
+        else
+            sweep_static<R, T, false>(c, w, h);
+    } else
         sweep(c, w, h, biased);
 }
 
@@ -950,6 +963,9 @@ template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> 
         }
         // phase A: orientations -> inertias -> joint/contact geometry and row
         // constants (freeze 657-716, refresh 718-756)
+#ifdef BSIM_EXP_SKIP_A   // timing experiment only: reuse the freeze-time constants
+        if (!freeze && k < N) goto phase_b;
+#endif
         if (!freeze) {
             BS_ITEMS(g, d.B, el, b) {
                 Ws<R> w = g.env(el);
@@ -987,8 +1003,15 @@ template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> 
             pair_pass_constants(c, w, i, biased);
         }
         BS_SYNC();
+#ifdef BSIM_EXP_SKIP_A
+    phase_b:
+#endif
         // phase B: one biased pass (567-572) or the velocity passes (580-581)
+#ifdef BSIM_EXP_SKIP_B   // timing experiment only
+        const int reps = 0;
+#else
         const int reps = biased ? 1 : p.velocity_iterations;
+#endif
         for (int r = 0; r < reps; ++r) {
             BS_ENVS(g, el) { sweep_any<R, T>(c, g.env(el), h, biased); }
             BS_SYNC();
