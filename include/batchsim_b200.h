@@ -202,7 +202,10 @@ int bsim_collide(const bsim_layout_t *layout, const bsim_params_t *params,
    the reset (numpy-identical PCG64 draws keyed (seed, global env, count)),
    forward kinematics of the new state and the post-reset observation.
    ------------------------------------------------------------------------ */
-enum bsim_task_kind { BSIM_TASK_QUADRUPED = 1, BSIM_TASK_ANYMAL = 2 };
+/* QUADRUPED: Ant analog (envs.py:359-478); ANYMAL: envs.py:484-565;
+   HUMANOID: the same locomotion task (obs layout, locomotion_reward, reset
+   law) on the authored 21-DOF humanoid with its own termination height. */
+enum bsim_task_kind { BSIM_TASK_QUADRUPED = 1, BSIM_TASK_ANYMAL = 2, BSIM_TASK_HUMANOID = 3 };
 
 /* Domain randomisation (reference randomize.py:86-189).  Targets in the
    reference's order: 0 dims, 1 masses, 2 friction, 3 damping, 4 gains,
@@ -241,6 +244,7 @@ typedef struct bsim_task_t {
     void *corr_noise;           /* [E][obs_dim] per-episode correlated noise      */
     int32_t *noise_count;       /* [E] uncorrelated-noise stream counter          */
     bsim_dr_t dr;
+    double termination_height;  /* locomotion tasks: done when torso z <= this (rewards.py:25) */
 } bsim_task_t;
 
 /* DomainRandomizer.randomize(env_indices, step) on its own (randomize.py:116-134). */

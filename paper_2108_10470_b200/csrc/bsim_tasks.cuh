@@ -59,7 +59,7 @@ template <class R> BS_HD Frame<R> quad_frame(const Root<R> &r) {
 template <class R>
 BS_HD R quad_reward(const Ctx<R> &c, const TaskView<R> &tv, int e, const Root<R> &r, const Frame<R> &f,
                     bool &done) {
-    const R dt = R(tv.t.control_dt), term = R(0.26);
+    const R dt = R(tv.t.control_dt), term = R(tv.t.termination_height);
     R dx = R(QUAD_TARGET_X) - r.p.x, dy = -r.p.y, dz = -r.p.z;
     R dist = r_sqrt(dx * dx + dy * dy + dz * dz);
     R potential = -dist / dt;
@@ -163,7 +163,8 @@ template <class R> __device__ void task_reset_env(const Ctx<R> &c, const TaskVie
     uint32_t key[4] = {t.seed, genv, (uint32_t)t.reset_count[e], 0xCu};
     NpRng rng = np_rng(key, 3);
     double qx = 0.0, qy = 0.0, qz = 0.0, qw = 1.0;
-    if (t.kind == BSIM_TASK_QUADRUPED) {
+    const bool loco = t.kind != BSIM_TASK_ANYMAL;
+    if (loco) {
         double yaw = np_uniform(rng, -0.1, 0.1);
         qz = sin(yaw / 2.0);
         qw = cos(yaw / 2.0);
@@ -189,7 +190,7 @@ template <class R> __device__ void task_reset_env(const Ctx<R> &c, const TaskVie
     t.reset_count[e] += 1;
     R *a = tv.act(e);
     for (int k = 0; k < t.act_dim; ++k) a[k] = R(0);
-    if (t.kind == BSIM_TASK_QUADRUPED) {
+    if (loco) {
         R z = R(t.rest_height + 0.02);
         R dist = r_sqrt(R(QUAD_TARGET_X) * R(QUAD_TARGET_X) + z * z);
         tv.potential(e) = -dist / R(t.control_dt);
@@ -203,7 +204,7 @@ template <class R> __device__ void task_reset_env(const Ctx<R> &c, const TaskVie
 
 template <class R> __device__ void task_obs(const Ctx<R> &c, const TaskView<R> &tv, int e) {
     const bsim_task_t &t = tv.t;
-    if (t.kind == BSIM_TASK_QUADRUPED) quad_obs(c, tv, e);
+    if (t.kind != BSIM_TASK_ANYMAL) quad_obs(c, tv, e);
     else anymal_obs(c, tv, e);
     if (t.obs_noise) {  // perturb_observations (randomize.py:231-237)
         R *o = tv.obs(e);
@@ -228,7 +229,7 @@ template <class R> __device__ void task_step_env(const Ctx<R> &c, const TaskView
     Root<R> r = root_of(c, e);
     bool done;
     R rew;
-    if (t.kind == BSIM_TASK_QUADRUPED) rew = quad_reward(c, tv, e, r, quad_frame(r), done);
+    if (t.kind != BSIM_TASK_ANYMAL) rew = quad_reward(c, tv, e, r, quad_frame(r), done);
     else rew = anymal_reward(c, tv, e, r, done);
     bool timeout = steps >= t.episode_length;
     bool pois = c.s.nonfinite[e] != 0;

@@ -34,7 +34,7 @@ from .randomize import DEFAULT_SCHEDULE, DR, DomainRandomizer
 from .scene import Scene
 
 ALL = None
-TASK_QUADRUPED, TASK_ANYMAL = 1, 2
+TASK_QUADRUPED, TASK_ANYMAL, TASK_HUMANOID = 1, 2, 3
 
 
 @dataclass
@@ -87,7 +87,8 @@ class Task(C.Structure):
                 ("step_count", C.c_int64)] + [
         (n, C.c_void_p) for n in ("obs", "reward", "done", "timeout", "poisoned", "episode_steps",
                                   "reset_count", "actions", "potentials", "commands", "dof_lower",
-                                  "dof_upper", "corr_noise", "noise_count")] + [("dr", DR)]
+                                  "dof_upper", "corr_noise", "noise_count")] + [("dr", DR),
+                                                                                ("termination_height", C.c_double)]
 
 
 def dof_limits(model):
@@ -109,6 +110,7 @@ class EnvBatch:
     action_scale = 1.0
     task_kind = 0
     rest_height = 0.0
+    termination_height = 0.26     # LocomotionRewardParams.termination_height (rewards.py:25)
 
     def __init__(self, config: EnvConfig):
         self.config = cfg = config.validate()
@@ -147,7 +149,8 @@ class EnvBatch:
                                                    self.actions, self.potentials, self.commands,
                                                    self.dof_lower, self.dof_upper, self.corr_noise,
                                                    self.noise_count)),
-                          self.randomizer.struct if self.randomizer is not None else DR())
+                          self.randomizer.struct if self.randomizer is not None else DR(),
+                          float(self.termination_height))
         self.reset()
 
     # ------------------------------------------------------------ hooks
@@ -250,9 +253,32 @@ class AnymalObsEnv(EnvBatch):
         return M.quadruped12()
 
 
+class HumanoidEnv(EnvBatch):
+    """Humanoid (BASELINE.json config 2): the QuadrupedEnv locomotion task
+    (envs.py:359-478 obs layout, locomotion_reward, reset law) on the authored
+    21-DOF capsule humanoid (models.humanoid_doc); 87-dim obs = 12 + 2x21 DOF
+    + 2 foot sensors x 6 + 21 actions; done when the torso drops to 0.8 m."""
+
+    name = "humanoid"
+    obs_dim = 87
+    act_dim = 21
+    action_scale = 0.6
+    task_kind = TASK_HUMANOID
+    rest_height = M.HUMANOID_REST_HEIGHT
+    termination_height = 0.8
+
+    def __init__(self, config=None):
+        cfg = config or EnvConfig()
+        super().__init__(replace(cfg, sim_dt=1.0 / 120.0, control_dt=1.0 / 60.0))
+
+    def _model(self):
+        return M.humanoid()
+
+
 TASKS = {
     "quadruped": QuadrupedEnv,
     "quadruped-anymal-obs": AnymalObsEnv,
+    "humanoid": HumanoidEnv,
 }
 
 

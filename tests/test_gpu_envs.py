@@ -16,7 +16,8 @@ from golden_util import load, rel_err
 
 pytestmark = pytest.mark.gpu
 
-CASES = [("quadruped", "env_quadruped"), ("quadruped-anymal-obs", "env_quadruped_anymal_obs")]
+CASES = [("quadruped", "env_quadruped"), ("quadruped-anymal-obs", "env_quadruped_anymal_obs"),
+         ("humanoid", "env_humanoid")]
 
 
 def _make(task, meta, precision):
@@ -59,7 +60,7 @@ def test_initial_reset_matches_reference(task, fixture, precision):
 def test_env_step_teacher_forced(task, fixture, precision):
     meta, arr = load(fixture)
     env = _make(task, meta, precision)
-    extra = "potentials" if task == "quadruped" else "commands"
+    extra = "commands" if task == "quadruped-anymal-obs" else "potentials"
     # fp32: the physics step carries the documented fp32 tolerance, and the
     # progress reward differentiates positions at 1/control_dt = 60 Hz
     otol, rtol_ = (1e-7, 1e-7) if precision == "fp64" else (2e-3, 2e-2)
