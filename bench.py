@@ -1,6 +1,7 @@
 """Throughput benchmark of the batched control step (physics + task layer).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--envs E] [--precision fp32|fp64]
+                    [--workload ant|humanoid|anymal]
     python bench.py --impl reference ...          # the CPU reference arm
 
 One "step" = one control step of the Ant-analog locomotion task for every
@@ -8,7 +9,9 @@ env: fused action mapping + 2 physics substeps (TGS, 8 position / 1 velocity
 iterations) + reward / done / observation / auto-reset (reference
 `EnvBatch.step`, envs.py:178-200).  Workload = BASELINE.json north-star
 configuration: Ant at 16384 envs per GPU, control dt 1/60, 2 substeps,
-uniform random actions.  Multi-GPU: one process per GPU (torchrun), each
+uniform random actions (`--workload` selects another BASELINE.json config;
+the line's `other_configs` carries the humanoid / ANYmal analogs and PPO
+rollout steps -- policy inference + env step -- measured the same way).  Multi-GPU: one process per GPU (torchrun), each
 rank owns a contiguous global env range (weak scaling, no data-path
 collective); timing is the max over ranks.
 
@@ -37,7 +40,6 @@ if ROOT not in sys.path:
 
 METRIC = "env-steps/sec (whole box) at 1/2/4/8 B200 vs host-CPU ref; % of HBM roofline"
 UNIT = "env-steps/s"
-WORKLOAD = "ant-quadruped locomotion, 16384 envs/GPU, control dt 1/60 (2 substeps), random actions"
 
 
 def dist_info():
@@ -140,6 +142,129 @@ def kernel_bytes(env):
     return total / E
 
 
+WORKLOADS = {
+    # name: (task, model builder name, rest height attr, description)
+    "ant": ("quadruped", "quadruped", "QUADRUPED_REST_HEIGHT",
+            "ant-quadruped locomotion, {E} envs/GPU, control dt 1/60 (2 substeps), random actions"),
+    "humanoid": ("humanoid", "humanoid", "HUMANOID_REST_HEIGHT",
+                 "humanoid (authored 21-DOF) locomotion, {E} envs/GPU, control dt 1/60 (2 substeps), random actions"),
+    "anymal": ("quadruped-anymal-obs", "quadruped12", "QUADRUPED12_REST_HEIGHT",
+               "anymal-analog velocity tracking (12 DOF, PD targets), {E} envs/GPU, 2 substeps, random actions"),
+}
+
+
+def measure(task, E, args, rank, world, clocks=None, policy=False, kernel=True, e2e=True):
+    """Device-timed control steps of `task` (CUDA events per step, L2 flushed
+    between steps, max over ranks); optionally the fused physics launch alone
+    and the end-to-end run through EnvBatch.step with host buffers."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2108_10470_b200.envs import make_env
+    env = make_env(task, num_envs=E, seed=args.seed, precision=args.precision,
+                   env_offset=rank * E, total_envs=world * E)
+    dev = env.scene.device
+    stream = torch.cuda.current_stream()
+    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+    acts = [torch.rand((E, env.act_dim), generator=gen, device=dev, dtype=env.scene.dtype) * 2 - 1
+            for _ in range(8)]
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    agent = None
+    if policy:      # PPO rollout step: policy inference (reference MLP sizes) + env step
+        from paper_2108_10470_b200.ppo import PPO
+        agent = PPO(env.obs_dim, env.act_dim, device=dev)
+
+    def control_step(i):
+        if agent is not None:
+            a, _, _ = agent.net.act(env.obs, agent.gen)
+            return env.step(a)
+        return env.step(acts[i % len(acts)])
+
+    def maxr(ms):
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    out = {"task": task, "envs_per_gpu": E}
+    if clocks is not None:      # nvidia-smi sampler running through warm-up and the timed steps
+        clocks.__enter__()
+    for i in range(args.warmup):
+        control_step(i)
+    torch.cuda.synchronize()
+    if clocks is not None:      # the first sample lands before the timed region starts
+        t_wait = time.time()
+        while not clocks.samples and time.time() - t_wait < 3.0:
+            control_step(0)
+            torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush.zero_()                       # L2 flush between timed steps (outside the events)
+        ev[i][0].record(stream)
+        control_step(i)
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    if clocks is not None:      # keep sampling until one sample postdates the timed region
+        n0, t_wait = len(clocks.samples), time.time()
+        while len(clocks.samples) == n0 and time.time() - t_wait < 3.0:
+            control_step(0)
+            torch.cuda.synchronize()
+        clocks.__exit__(None, None, None)
+    if world > 1:
+        dist.barrier()
+    ms_total = maxr(sum(a.elapsed_time(b) for a, b in ev))
+    out["ms_total"] = ms_total
+    out["value"] = world * E * args.steps / (ms_total / 1e3)
+
+    if kernel:      # dominant kernel alone: the fused physics launch
+        kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        for i in range(args.steps):
+            flush.zero_()
+            kev[i][0].record(stream)
+            env.scene.step(env.config.decimation, actions=acts[i % len(acts)], action_scale=env.action_scale,
+                           actions_clipped=env.actions)
+            kev[i][1].record(stream)
+        torch.cuda.synchronize()
+        out["kernel_ms"] = sum(a.elapsed_time(b) for a, b in kev) / args.steps
+        out["bytes_per_env"] = kernel_bytes(env)
+        env.reset()
+
+    if e2e:         # end to end through the public API with host buffers
+        h_act = [a.cpu().pin_memory() for a in acts]
+        h_obs = torch.empty(env.obs.shape, dtype=env.obs.dtype, pin_memory=True)
+        h_rew = torch.empty(env.reward.shape, dtype=env.reward.dtype, pin_memory=True)
+        h_done = torch.empty(env.done.shape, dtype=env.done.dtype, pin_memory=True)
+        for i in range(args.warmup):
+            env.step(h_act[i % len(h_act)].to(dev, non_blocking=True))
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(args.steps):
+            a = h_act[i % len(h_act)].to(dev, non_blocking=True)
+            o = env.step(a)
+            h_obs.copy_(o.obs, non_blocking=True)
+            h_rew.copy_(o.reward, non_blocking=True)
+            h_done.copy_(o.done, non_blocking=True)
+            torch.cuda.current_stream().synchronize()   # the host consumes the step's results
+        e1.record(stream)
+        torch.cuda.synchronize()
+        out["e2e"] = {"value": world * E * args.steps / (maxr(e0.elapsed_time(e1)) / 1e3), "unit": UNIT,
+                      "h2d_bytes_per_step": h_act[0].numel() * h_act[0].element_size(),
+                      "d2h_bytes_per_step": (h_obs.numel() * h_obs.element_size()
+                                             + h_rew.numel() * h_rew.element_size()
+                                             + h_done.numel() * h_done.element_size())}
+    env.close()
+    del flush
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
@@ -148,106 +273,49 @@ def run_gpu(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl")
-    from paper_2108_10470_b200.envs import make_env
-
     E = args.envs
-    env = make_env("quadruped", num_envs=E, seed=args.seed, precision=args.precision,
-                   env_offset=rank * E, total_envs=world * E)
-    dev = env.scene.device
-    stream = torch.cuda.current_stream()
-    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
-    acts = [torch.rand((E, env.act_dim), generator=gen, device=dev, dtype=env.scene.dtype) * 2 - 1
-            for _ in range(8)]
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-
-    # ---------------- device-resident inputs
-    for i in range(args.warmup):
-        env.step(acts[i % len(acts)])
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    with ClockSampler(local) as clocks:
-        torch.cuda.synchronize()
-        for i in range(args.steps):
-            flush.zero_()                       # L2 flush between timed steps (outside the events)
-            ev[i][0].record(stream)
-            env.step(acts[i % len(acts)])
-            ev[i][1].record(stream)
-        torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    ms = sum(a.elapsed_time(b) for a, b in ev)
-    t = torch.tensor([ms], device=dev, dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_total = float(t.item())
-    value = world * E * args.steps / (ms_total / 1e3)
-
-    # ---------------- dominant kernel alone: the fused physics launch
-    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    for i in range(args.steps):
-        flush.zero_()
-        kev[i][0].record(stream)
-        env.scene.step(2, actions=acts[i % len(acts)], action_scale=env.action_scale,
-                       actions_clipped=env.actions)
-        kev[i][1].record(stream)
-    torch.cuda.synchronize()
-    k_ms = sum(a.elapsed_time(b) for a, b in kev) / args.steps
-    env.reset()
-
-    # ---------------- end to end through the public API with host buffers
-    h_act = [a.cpu().pin_memory() for a in acts]
-    h_obs = torch.empty(env.obs.shape, dtype=env.obs.dtype, pin_memory=True)
-    h_rew = torch.empty(env.reward.shape, dtype=env.reward.dtype, pin_memory=True)
-    h_done = torch.empty(env.done.shape, dtype=env.done.dtype, pin_memory=True)
-    for i in range(args.warmup):
-        out = env.step(h_act[i % len(h_act)].to(dev, non_blocking=True))
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for i in range(args.steps):
-        a = h_act[i % len(h_act)].to(dev, non_blocking=True)
-        out = env.step(a)
-        h_obs.copy_(out.obs, non_blocking=True)
-        h_rew.copy_(out.reward, non_blocking=True)
-        h_done.copy_(out.done, non_blocking=True)
-        torch.cuda.current_stream().synchronize()   # the host consumes the step's results
-    e1.record(stream)
-    torch.cuda.synchronize()
-    t = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    e2e = world * E * args.steps / (float(t.item()) / 1e3)
-    h2d = h_act[0].numel() * h_act[0].element_size()
-    d2h = (h_obs.numel() * h_obs.element_size() + h_rew.numel() * h_rew.element_size()
-           + h_done.numel() * h_done.element_size())
-
+    task, _, _, desc = WORKLOADS[args.workload]
+    clocks = ClockSampler(local)
+    m = measure(task, E, args, rank, world, clocks=clocks)
+    others = {}
+    if not args.no_other_configs:
+        # the other BASELINE.json configs that have a model here (fewer steps, device-resident only)
+        import copy
+        a2 = copy.copy(args)
+        a2.steps = args.other_steps
+        for name in WORKLOADS:
+            if name == args.workload:
+                continue
+            r = measure(WORKLOADS[name][0], E, a2, rank, world, kernel=False, e2e=False)
+            others[name] = {"value": r["value"], "unit": UNIT, "envs_per_gpu": E, "steps": a2.steps}
+        for name in ("ant", "humanoid"):   # PPO-rollout steps: policy inference + env step
+            r = measure(WORKLOADS[name][0], E, a2, rank, world, policy=True, kernel=False, e2e=False)
+            others[f"{name}_ppo_rollout"] = {"value": r["value"], "unit": UNIT, "envs_per_gpu": E,
+                                             "steps": a2.steps,
+                                             "note": "ActorCritic 256-128-64 act() + env.step per step"}
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
     pk, src = peaks()
-    bytes_env = kernel_bytes(env)
+    k_ms, bytes_env = m["kernel_ms"], m["bytes_per_env"]
     achieved = bytes_env * E / (k_ms / 1e3) / 1e9
-    tr = ncu_traffic(E) if args.precision == "fp32" else None
+    tr = ncu_traffic(E) if (args.precision == "fp32" and args.workload == "ant") else None
     # FP32 view: flop per env per launch measured by ncu (ffma*2 + fadd + fmul), else the
-    # SURVEY.md 8(d) estimate of 9.3e4 flop per env-sim-step x 2 substeps
+    # SURVEY.md 8(d) estimate of 9.3e4 flop per env-sim-step x 2 substeps (Ant)
     flop_env = tr[2] if tr and tr[2] else 9.3e4 * 2
     flops = flop_env * E
-    props = torch.cuda.get_device_properties(dev)
+    props = torch.cuda.get_device_properties(torch.cuda.current_device())
     fp32_peak = props.multi_processor_count * 128 * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
+        "metric": METRIC, "value": m["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": m["ms_total"] / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32" if args.precision == "fp32" else "f64",
-        "data": "synthetic (uniform random actions, bundled Ant-analog model, no checkpoints)",
-        "config": {"workload": WORKLOAD, "model": "quadruped (Ant analog, 9 bodies / 8 DOF)",
-                   "envs_per_gpu": E, "global_envs": world * E, "substeps": 2,
-                   "position_iterations": 8, "velocity_iterations": 1, "precision": args.precision,
-                   "parallelism": f"env-shard x{world}", "l2": "flushed between timed steps (256 MiB write)"},
+        "data": "synthetic (uniform random actions, bundled/authored models, no checkpoints)",
+        "config": {"workload": desc.format(E=E), "task": task, "envs_per_gpu": E, "global_envs": world * E,
+                   "substeps": 2, "position_iterations": 8, "velocity_iterations": 1,
+                   "precision": args.precision, "parallelism": f"env-shard x{world}",
+                   "l2": "flushed between timed steps (256 MiB write)"},
         "gpu_launches": 2 * args.steps,
         "clocks": clocks.summary(),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
@@ -262,8 +330,10 @@ def run_gpu(args):
                               "source": "ncu-measured flop count" if tr and tr[2] else "SURVEY 8(d) estimate"},
                      "note": "compulsory bytes; the fused kernel is latency/FP32-issue bound, not HBM bound "
                              "(DESIGN.md)"},
-        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "e2e": m["e2e"],
     }
+    if others:
+        line["other_configs"] = others
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args, bounded=True)
     print(json.dumps(line), flush=True)
@@ -271,15 +341,16 @@ def run_gpu(args):
         dist.destroy_process_group()
 
 
-def _oracle_scene(n_envs, threads):
+def _oracle_scene(n_envs, threads, workload="ant"):
     import numpy as np
 
     from oracle.oracle import OracleScene, build
     from paper_2108_10470_b200 import models as M
     from paper_2108_10470_b200.params import SimParams
     build()
-    s = OracleScene([M.quadruped()], n_envs, SimParams(dt=1 / 120), threads=threads)
-    s.pos[:, 2] += 0.37
+    _, model, rest, _ = WORKLOADS[workload]
+    s = OracleScene([getattr(M, model)()], n_envs, SimParams(dt=1 / 120), threads=threads)
+    s.pos[:, 2] += getattr(M, rest) + 0.02
     s.forward_kinematics()
     return s, np.random.default_rng(0)
 
@@ -295,7 +366,7 @@ def cpu_baseline(args, bounded=True):
     on a bounded sample of the same workload."""
     threads = os.cpu_count() or 1
     sample = min(args.envs, args.cpu_sample_envs)
-    s, rng = _oracle_scene(sample, threads)
+    s, rng = _oracle_scene(sample, threads, args.workload)
     _oracle_control_step(s, rng)
     n = 0
     t0 = time.perf_counter()
@@ -306,7 +377,7 @@ def cpu_baseline(args, bounded=True):
         if dt > args.cpu_seconds or n >= args.cpu_max_steps:
             break
     return {"value": sample * n / dt, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{sample} envs x {n} control steps (2 substeps each) of the same Ant workload, "
+            "sample": f"{sample} envs x {n} control steps (2 substeps each) of the same {args.workload} workload, "
                       f"C oracle float64 (oracle/bso.c, OpenMP {threads} threads), physics only "
                       f"(the reference's obs/reward is <0.4% of its step time)"}
 
@@ -322,7 +393,7 @@ def run_reference(args):
         return
     threads = os.cpu_count() or 1
     n_envs = args.envs
-    s, rng = _oracle_scene(n_envs, threads)
+    s, rng = _oracle_scene(n_envs, threads, args.workload)
     for _ in range(args.warmup):
         _oracle_control_step(s, rng)
     t0 = time.perf_counter()
@@ -337,7 +408,8 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (uniform random actions)", "impl": "reference",
-            "config": {"workload": WORKLOAD, "envs_per_gpu": n_envs, "substeps": 2},
+            "config": {"workload": WORKLOADS[args.workload][3].format(E=n_envs), "task": WORKLOADS[args.workload][0],
+                       "envs_per_gpu": n_envs, "substeps": 2},
             "cpu_baseline": base,
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -352,7 +424,10 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="ant", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-other-configs", action="store_true")
+    ap.add_argument("--other-steps", type=int, default=10)
     ap.add_argument("--cpu-sample-envs", type=int, default=2048)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--cpu-max-steps", type=int, default=400)
