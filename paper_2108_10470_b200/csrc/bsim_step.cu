@@ -24,6 +24,16 @@
 
 using namespace bsim;
 
+#ifndef BSIM_LARGE_TU
+extern "C" {
+int bsim_large_step_f32(const bsim_layout_t *, const bsim_params_t *, const bsim_state_t *, int32_t,
+                        const bsim_actions_t *, void *);
+int bsim_large_step_f64(const bsim_layout_t *, const bsim_params64_t *, const bsim_state64_t *, int32_t,
+                        const bsim_actions_t *, void *);
+const char *bsim_large_last_error(void);
+}
+#endif
+
 namespace {
 
 std::string g_err;
@@ -433,6 +443,23 @@ int launch_step_t(const Ctx<R> &c, size_t smem, int n_substeps, const bsim_actio
     return check_launch("step_kernel");
 }
 
+#ifndef BSIM_LARGE_TU
+// The large-articulation variant (bsim_step_large.cu: this source with a
+// 4-env x 32-thread CTA) is used when the default 16-env CTA's workspace
+// leaves fewer than 2 CTAs per SM (e.g. the 22-body humanoid: 150 KB).
+template <class R> bool use_large_variant(const Dims &d) {
+    return step_smem_bytes<R>(d) > 113 * 1024;
+}
+int call_large(const bsim_layout_t *l, const bsim_params_t *p, const bsim_state_t *s, int32_t n,
+               const bsim_actions_t *a, void *st) {
+    return bsim_large_step_f32(l, p, s, n, a, st);
+}
+int call_large(const bsim_layout_t *l, const bsim_params64_t *p, const bsim_state64_t *s, int32_t n,
+               const bsim_actions_t *a, void *st) {
+    return bsim_large_step_f64(l, p, s, n, a, st);
+}
+#endif
+
 template <class R>
 int launch_step(const bsim_layout_t *layout, const typename Abi<R>::Params *params,
                 const typename Abi<R>::State *state, int32_t n_substeps, const bsim_actions_t *actions,
@@ -451,6 +478,14 @@ int launch_step(const bsim_layout_t *layout, const typename Abi<R>::Params *para
     bsim_actions_t act;
     if (actions) act = *actions; else std::memset(&act, 0, sizeof act);
     cudaStream_t st = (cudaStream_t)stream;
+#ifdef BSIM_LARGE_TU
+    return launch_step_t<R, TopoGeneric>(c, smem, n_substeps, act, st);
+#else
+    if (use_large_variant<R>(c.d)) {   // big articulations: 4 envs x 32 threads per CTA
+        int rc = call_large(layout, params, state, n_substeps, actions, stream);
+        if (rc != BSIM_OK) g_err = bsim_large_last_error();
+        return rc;
+    }
     switch (layout->topology_id) {
 #define BSIM_LAUNCH_TOPO(ID, TYPE)                                      \
     case ID:                                                            \
@@ -460,6 +495,7 @@ int launch_step(const bsim_layout_t *layout, const typename Abi<R>::Params *para
     default:
         return launch_step_t<R, TopoGeneric>(c, smem, n_substeps, act, st);
     }
+#endif
 }
 
 template <class R>
@@ -539,6 +575,19 @@ int launch_collide(const bsim_layout_t *layout, const typename Abi<R>::Params *p
 
 }  // namespace
 
+#ifdef BSIM_LARGE_TU
+extern "C" {
+int bsim_large_step_f32(const bsim_layout_t *l, const bsim_params_t *p, const bsim_state_t *s, int32_t n,
+                        const bsim_actions_t *a, void *st) {
+    return launch_step<float>(l, p, s, n, a, st);
+}
+int bsim_large_step_f64(const bsim_layout_t *l, const bsim_params64_t *p, const bsim_state64_t *s, int32_t n,
+                        const bsim_actions_t *a, void *st) {
+    return launch_step<double>(l, p, s, n, a, st);
+}
+const char *bsim_large_last_error(void) { return g_err.c_str(); }
+}
+#else
 extern "C" {
 
 int bsim_abi_version(void) { return BSIM_ABI_VERSION; }
@@ -611,3 +660,4 @@ int bsim_collide_f64(const bsim_layout_t *l, const bsim_params64_t *p, const bsi
 }
 
 }  // extern "C"
+#endif  // BSIM_LARGE_TU

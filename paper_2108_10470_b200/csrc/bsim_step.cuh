@@ -61,8 +61,14 @@ template <class R> struct Shape;
 template <> struct Shape<float> {
     static constexpr int NE = BSIM_NE32, NTH = BSIM_NTH32, STR = NE + 1;
 };
+#ifndef BSIM_NE64
+#define BSIM_NE64 8
+#endif
+#ifndef BSIM_NTH64
+#define BSIM_NTH64 64
+#endif
 template <> struct Shape<double> {
-    static constexpr int NE = 8, NTH = 64, STR = NE + 1;
+    static constexpr int NE = BSIM_NE64, NTH = BSIM_NTH64, STR = NE + 1;
 };
 
 // ---------------------------------------------------------------- items
