@@ -270,12 +270,14 @@ def run_gpu(args):
     import torch.distributed as dist
 
     rank, world, local = dist_info()
-    torch.cuda.set_device(local)
+    # one GPU per rank (LOCAL_RANK); BENCH_DIST_BACKEND=gloo + ranks sharing a
+    # device is only for smoke-testing the multi-rank path on a 1-GPU box
+    torch.cuda.set_device(local % torch.cuda.device_count())
     if world > 1:
-        dist.init_process_group("nccl")
+        dist.init_process_group(os.environ.get("BENCH_DIST_BACKEND", "nccl"))
     E = args.envs
     task, _, _, desc = WORKLOADS[args.workload]
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(local % torch.cuda.device_count())
     m = measure(task, E, args, rank, world, clocks=clocks)
     others = {}
     if not args.no_other_configs:
