@@ -21,6 +21,15 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", 
               "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
 
 
+# fp32 arithmetic mode of the physics step TUs: flush-to-zero and the
+# MUFU-based approximate divide / square root (<= 2 ulp; atan2f's internal
+# divide, norms, the sweep's friction / cone-clamp square roots).  Measured
+# 7 % faster step; fp64 (the exact-parity path) is unaffected,
+# and the task / RNG TUs keep IEEE fp32.
+FAST_FP32 = ["-ftz=true", "-prec-div=false", "-prec-sqrt=false"]
+FAST_TUS = ("bsim_step.cu", "bsim_step_large.cu")
+
+
 def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
@@ -45,7 +54,8 @@ def build(force=False, verbose=False):
     for src in sources():
         obj = os.path.join(HERE, "_lib", os.path.basename(src)[:-3] + ".o")
         extra = os.environ.get("BSIM_NVCC_EXTRA", "").split()   # dev experiments only
-        cmd = ["nvcc", *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
+        fast = FAST_FP32 if os.path.basename(src) in FAST_TUS else []
+        cmd = ["nvcc", *NVCC_FLAGS, *fast, *extra, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
