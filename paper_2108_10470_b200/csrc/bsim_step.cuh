@@ -543,70 +543,77 @@ template <class R> BS_HD void store_bv(const Dims &d, const Ws<R> &w, int b, con
     w.s3(ib(d, b, BW), x.w);
 }
 
+// Row operands shared by several rows of one joint, loaded once per joint
+// (the axis rows' jacobians, both bodies' world inverse inertias) and the
+// joint's DOF impulse accumulator kept in a register across its rows.
+template <class R> struct JointOps {
+    V3<R> a, y1, y2;   // world axis, I_c x1, I_p x2
+    S3<R> Ic, Ip;
+    R imp;             // dof_impulse (drive + limit, same addition order)
+};
+
 // rate along a 1-DOF joint axis (physics.py:804-810)
 template <class R>
-BS_HD R axis_rate(const Dims &d, const Ws<R> &w, int j, bool lin, const BV<R> &C, const BV<R> &P) {
-    V3<R> a = w.l3(ij(d, j, JAX));
-    if (!lin) return dot(a, C.w - P.w);
-    return dot(cross(w.l3(ij(d, j, JRC)), a), C.w) - dot(cross(w.l3(ij(d, j, JRP)), a), P.w) + dot(a, C.v - P.v);
+BS_HD R axis_rate(const Dims &d, const Ws<R> &w, int j, bool lin, const JointOps<R> &o, const BV<R> &C,
+                  const BV<R> &P) {
+    if (!lin) return dot(o.a, C.w - P.w);
+    return dot(cross(w.l3(ij(d, j, JRC)), o.a), C.w) - dot(cross(w.l3(ij(d, j, JRP)), o.a), P.w) +
+           dot(o.a, C.v - P.v);
 }
-template <class R>
-BS_HD void axis_apply(const Dims &d, const Ws<R> &w, int j, bool lin, R lam, BV<R> &C, BV<R> &P) {
-    C.w = C.w + w.l3(ij(d, j, JY1)) * lam;
-    P.w = P.w - w.l3(ij(d, j, JY2)) * lam;
+template <class R> BS_HD void axis_apply(bool lin, const JointOps<R> &o, R lam, BV<R> &C, BV<R> &P) {
+    C.w = C.w + o.y1 * lam;
+    P.w = P.w - o.y2 * lam;
     if (lin) {
-        V3<R> a = w.l3(ij(d, j, JAX));
-        C.v = C.v + a * (lam * C.m);
-        P.v = P.v - a * (lam * P.m);
+        C.v = C.v + o.a * (lam * C.m);
+        P.v = P.v - o.a * (lam * P.m);
     }
 }
 
 // PD drive / direct actuation / joint friction (physics.py:812-848)
 template <class R>
-BS_HD void row_drive(const Ctx<R> &c, const Ws<R> &w, int j, int dof, bool lin, R h, BV<R> &C, BV<R> &P) {
+BS_HD void row_drive(const Ctx<R> &c, const Ws<R> &w, int j, bool lin, R h, JointOps<R> &o, BV<R> &C, BV<R> &P) {
     const Dims &d = c.d;
-    R qd = axis_rate(d, w, j, lin, C, P);
+    R qd = axis_rate(d, w, j, lin, o, C, P);
     const R mfh = c.p.max_force * h;
     R lam = w.at(ij(d, j, JLF)) + clampr(w.at(ij(d, j, JDA)) - w.at(ij(d, j, JDB)) * qd, -mfh, mfh);
     R frh = w.at(ij(d, j, JFRH));
     if (frh > R(0)) lam = lam + clampr(-qd * w.at(ij(d, j, JMEFF)), -frh, frh);
-    axis_apply(d, w, j, lin, lam, C, P);
-    w.at(idf(d, dof, DIMP)) += lam;
+    axis_apply(lin, o, lam, C, P);
+    o.imp += lam;
 }
 
 // one-sided limit (physics.py:850-870)
 template <class R>
-BS_HD void row_limit(const Ctx<R> &c, const Ws<R> &w, int j, int dof, bool lin, BV<R> &C, BV<R> &P) {
+BS_HD void row_limit(const Ws<R> &w, const Dims &d, int j, bool lin, JointOps<R> &o, BV<R> &C, BV<R> &P) {
     // branch-free (an inactive limit applies lam = 0, which leaves the
     // velocities bit-identical) so the scheduler can overlap independent rows
-    const Dims &d = c.d;
     R state = w.at(ij(d, j, JLV));
-    R qd = axis_rate(d, w, j, lin, C, P);
+    R qd = axis_rate(d, w, j, lin, o, C, P);
     R meff = w.at(ij(d, j, JMEFF)), bias = w.at(ij(d, j, JLB));
     R lam = state == R(1) ? r_max(meff * (bias - qd), R(0)) : -r_max(meff * (bias + qd), R(0));
     lam = state == R(0) ? R(0) : lam;
-    axis_apply(d, w, j, lin, lam, C, P);
-    w.at(idf(d, dof, DIMP)) += lam;
+    axis_apply(lin, o, lam, C, P);
+    o.imp += lam;
 }
 
 // point-3 (872-890) or prismatic perpendicular pair (908-928): P = G (tgt - rel)
 template <class R>
-BS_HD void row_linear(const Dims &d, const Ws<R> &w, int j, int pb, int cb, BV<R> &C, BV<R> &P) {
+BS_HD void row_linear(const Dims &d, const Ws<R> &w, int j, const JointOps<R> &o, BV<R> &C, BV<R> &P) {
     V3<R> rc = w.l3(ij(d, j, JRC)), rp = w.l3(ij(d, j, JRP));
     V3<R> rel = (C.v + cross(C.w, rc)) - (P.v + cross(P.w, rp));
     V3<R> imp = smul(w.lS(ij(d, j, JKI)), w.l3(ij(d, j, JPE)) - rel);
     C.v = C.v + imp * C.m;
-    C.w = C.w + smul(w.lS(ib(d, cb, BI)), cross(rc, imp));
+    C.w = C.w + smul(o.Ic, cross(rc, imp));
     P.v = P.v - imp * P.m;
-    P.w = P.w - smul(w.lS(ib(d, pb, BI)), cross(rp, imp));
+    P.w = P.w - smul(o.Ip, cross(rp, imp));
 }
 
 // angular rows (892-906): L = G (tgt - (w_c - w_p)); w_c += Ic L, w_p -= Ip L
 template <class R>
-BS_HD void row_angular(const Dims &d, const Ws<R> &w, int j, int pb, int cb, BV<R> &C, BV<R> &P) {
+BS_HD void row_angular(const Dims &d, const Ws<R> &w, int j, const JointOps<R> &o, BV<R> &C, BV<R> &P) {
     V3<R> L = smul(w.lS(ij(d, j, JG)), w.l3(ij(d, j, JRE)) - (C.w - P.w));
-    C.w = C.w + smul(w.lS(ib(d, cb, BI)), L);
-    P.w = P.w - smul(w.lS(ib(d, pb, BI)), L);
+    C.w = C.w + smul(o.Ic, L);
+    P.w = P.w - smul(o.Ip, L);
 }
 
 // all rows of joint j in reference order (physics.py:761-773)
@@ -616,11 +623,21 @@ BS_HD void joint_rows(const Ctx<R> &c, const Ws<R> &w, int j, int kind, int dof,
     const Dims &d = c.d;
     const bool axis = dof >= 0 && kind != BSIM_SPHERICAL;
     const bool lin = kind == BSIM_PRISMATIC;
-    if (biased && axis) row_drive(c, w, j, dof, lin, h, C, P);
-    if (kind != BSIM_PRISMATIC) row_linear(d, w, j, pb, cb, C, P);
-    if (kind != BSIM_SPHERICAL) row_angular(d, w, j, pb, cb, C, P);
-    if (kind == BSIM_PRISMATIC) row_linear(d, w, j, pb, cb, C, P);
-    if (axis && limits) row_limit(c, w, j, dof, lin, C, P);
+    JointOps<R> o;
+    o.Ic = w.lS(ib(d, cb, BI));
+    o.Ip = w.lS(ib(d, pb, BI));
+    if (axis) {
+        o.a = w.l3(ij(d, j, JAX));
+        o.y1 = w.l3(ij(d, j, JY1));
+        o.y2 = w.l3(ij(d, j, JY2));
+        o.imp = w.at(idf(d, dof, DIMP));
+    }
+    if (biased && axis) row_drive(c, w, j, lin, h, o, C, P);
+    if (kind != BSIM_PRISMATIC) row_linear(d, w, j, o, C, P);
+    if (kind != BSIM_SPHERICAL) row_angular(d, w, j, o, C, P);
+    if (kind == BSIM_PRISMATIC) row_linear(d, w, j, o, C, P);
+    if (axis && limits) row_limit(w, d, j, lin, o, C, P);
+    if (axis && (biased || limits)) w.at(idf(d, dof, DIMP)) = o.imp;
 }
 
 // plane contact row (930-983) with the plane's fixed normal / tangents
