@@ -245,6 +245,8 @@ typedef struct bsim_task_t {
     int32_t *noise_count;       /* [E] uncorrelated-noise stream counter          */
     bsim_dr_t dr;
     double termination_height;  /* locomotion tasks: done when torso z <= this (rewards.py:25) */
+    const int64_t *step_count_dev;  /* optional device copy of step_count (CUDA-graph replay);
+                                       NULL: use step_count */
 } bsim_task_t;
 
 /* DomainRandomizer.randomize(env_indices, step) on its own (randomize.py:116-134). */

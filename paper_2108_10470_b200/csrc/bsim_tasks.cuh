@@ -158,7 +158,8 @@ template <class R> __device__ void task_reset_env(const Ctx<R> &c, const TaskVie
     const bsim_task_t &t = tv.t;
     const Dims &d = c.d;
     if (c.s.nonfinite[e]) c.s.nonfinite[e] = 0;   // clear_nonfinite (physics.py:1090)
-    dr_randomize_env(c, t.dr, e, t.step_count);   // randomizer.randomize (envs.py:154-155)
+    const int64_t step_count = t.step_count_dev ? *t.step_count_dev : t.step_count;
+    dr_randomize_env(c, t.dr, e, step_count);     // randomizer.randomize (envs.py:154-155)
     const uint32_t genv = (uint32_t)(c.L.env_offset + e);
     uint32_t key[4] = {t.seed, genv, (uint32_t)t.reset_count[e], 0xCu};
     NpRng rng = np_rng(key, 3);

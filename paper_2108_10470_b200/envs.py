@@ -88,7 +88,8 @@ class Task(C.Structure):
         (n, C.c_void_p) for n in ("obs", "reward", "done", "timeout", "poisoned", "episode_steps",
                                   "reset_count", "actions", "potentials", "commands", "dof_lower",
                                   "dof_upper", "corr_noise", "noise_count")] + [("dr", DR),
-                                                                                ("termination_height", C.c_double)]
+                                                                                ("termination_height", C.c_double),
+                                                                                ("step_count_dev", C.c_void_p)]
 
 
 def dof_limits(model):
@@ -139,6 +140,7 @@ class EnvBatch:
         self.corr_noise = torch.zeros((E, self.obs_dim), dtype=dt, device=dev)
         self.noise_count = torch.zeros(E, dtype=torch.int32, device=dev)
         # domain randomisation (envs.py:94-96): snapshot after scene construction
+        self._graph = None
         self.randomizer = (DomainRandomizer(self.scene, DEFAULT_SCHEDULE, seed=cfg.seed)
                            if cfg.randomize else None)
         self._task = Task(self.task_kind, self.obs_dim, self.act_dim, cfg.episode_length, cfg.seed,
@@ -163,6 +165,7 @@ class EnvBatch:
     # ------------------------------------------------------------ helpers
     def _call(self, name, *args):
         self._task.step_count = int(self.scene.step_count)
+        self._task.step_count_dev = None
         lib = self.scene._lib
         fn = getattr(lib, name + ("_f64" if self.scene.fp64 else ""))
         lay, _, st = self.scene._structs()
@@ -204,13 +207,64 @@ class EnvBatch:
         if tuple(a.shape) != (cfg.num_envs, self.act_dim):
             raise ValueError(f"actions must have shape ({cfg.num_envs}, {self.act_dim})")
         a = a.to(self.scene.device, self.scene.dtype)
-        if not a.is_contiguous():
-            a = a.contiguous()
-        self.scene.step(cfg.decimation, actions=a, action_scale=self.action_scale,
-                        action_mode=MODE_POSITION, actions_clipped=self.actions)
-        self._call("bsim_task_step", self.scene._s)
+        if self._graph is not None:
+            self._graph_in.copy_(a)
+            self._graph.replay()
+            self.scene.step_count += cfg.decimation
+        else:
+            if not a.is_contiguous():
+                a = a.contiguous()
+            self._step_launches(a)
         return StepOutput(self.obs, self.reward, self.done,
                           {"timeout": self.timeout, "poisoned": self.poisoned})
+
+    def _step_launches(self, a, graph=False):
+        """The control step's launches: fused physics (bsim_step) + task layer."""
+        self.scene.step(self.config.decimation, actions=a, action_scale=self.action_scale,
+                        action_mode=MODE_POSITION, actions_clipped=self.actions)
+        if graph:   # the replayed step reads / advances the device step counter
+            self._step_count_dev.add_(self.config.decimation)
+            lib = self.scene._lib
+            fn = getattr(lib, "bsim_task_step" + ("_f64" if self.scene.fp64 else ""))
+            lay, _, st = self.scene._structs()
+            self._task.step_count_dev = self._step_count_dev.data_ptr()
+            rc = fn(C.byref(lay), C.byref(st), C.byref(self._task), self.scene._s)
+            self._task.step_count_dev = None
+            if rc != 0:
+                raise N.NativeError(f"bsim_task_step failed ({rc}): {lib.bsim_task_last_error().decode()}")
+        else:
+            self._call("bsim_task_step", self.scene._s)
+
+    def capture_graph(self, warmup=0):
+        """Capture one control step (physics launch + task launch + the device
+        step counter the DR interval reads) into a CUDA graph; later `step()`
+        calls copy the actions into the graph's static input and replay it --
+        the same launches with the same arguments as the eager path, one graph
+        launch per control step.  `warmup` eager zero-action steps run first
+        (they advance the envs like ordinary steps).  `release_graph()` returns
+        to eager launches."""
+        cfg = self.config
+        dev = self.scene.device
+        self._graph_in = torch.zeros((cfg.num_envs, self.act_dim), dtype=self.scene.dtype, device=dev)
+        for _ in range(warmup):
+            self.step(self._graph_in)
+        self._step_count_dev = torch.full((1,), int(self.scene.step_count), dtype=torch.int64, device=dev)
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        main, count = self.scene.stream, self.scene.step_count
+        g = torch.cuda.CUDAGraph()
+        object.__setattr__(self.scene, "stream", side)
+        try:
+            with torch.cuda.graph(g, stream=side):
+                self._step_launches(self._graph_in, graph=True)
+        finally:
+            object.__setattr__(self.scene, "stream", main)
+            self.scene.step_count = count          # capture executed nothing
+        self._graph = g
+        return g
+
+    def release_graph(self):
+        self._graph = None
 
     def close(self):
         self.scene.close()

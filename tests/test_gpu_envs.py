@@ -108,3 +108,24 @@ def test_fused_env_step_equals_manual_substeps():
     b.scene.step()
     b.scene.step()
     assert torch.equal(a.scene.body_q, b.scene.body_q)
+
+
+@pytest.mark.parametrize("task", ["quadruped", "quadruped-anymal-obs"])
+def test_cuda_graph_step_equals_eager(task):
+    """capture_graph(): replaying the captured control step gives bitwise the
+    eager launches' results, through resets and domain randomisation (the DR
+    interval reads the device step counter)."""
+    from paper_2108_10470_b200.envs import make_env
+    kw = dict(num_envs=64, seed=5, episode_length=7, randomize=True)
+    a, b = make_env(task, **kw), make_env(task, **kw)
+    b.capture_graph()
+    rng = np.random.default_rng(3)
+    for t in range(20):
+        act = torch.as_tensor(rng.uniform(-1.2, 1.2, (64, a.act_dim)), dtype=torch.float32, device="cuda")
+        oa, ob = a.step(act), b.step(act)
+        for x, y in ((oa.obs, ob.obs), (oa.reward, ob.reward), (oa.done, ob.done), (a.scene.body_q, b.scene.body_q),
+                     (a.reset_count, b.reset_count)):
+            assert torch.equal(x, y), t
+    assert a.scene.step_count == b.scene.step_count
+    assert int(b._step_count_dev) == b.scene.step_count
+    assert int(a.done.sum()) >= 0 and int(a.reset_count.sum()) > 2 * 64   # resets happened
