@@ -290,6 +290,16 @@ const char *bsim_task_last_error(void);
 /* EnvBatch.step() tail (envs.py:188-199): call after bsim_step(). */
 int bsim_task_step(const bsim_layout_t *layout, const bsim_state_t *state, const bsim_task_t *task,
                    void *stream);
+/* EnvBatch.step() in ONE launch (envs.py:178-200): the fused physics step
+   (bsim_step) followed, inside the same kernel, by the task tail of
+   bsim_task_step for the CTA's envs -- reward / done / obs / auto-reset read
+   the state the CTA just wrote, so the task layer costs no extra launch and no
+   state re-read from HBM.  task->step_count must be the post-step count. */
+int bsim_env_step(const bsim_layout_t *layout, const bsim_params_t *params, const bsim_state_t *state,
+                  int32_t n_substeps, const bsim_actions_t *actions, const bsim_task_t *task, void *stream);
+int bsim_env_step_f64(const bsim_layout_t *layout, const bsim_params64_t *params,
+                      const bsim_state64_t *state, int32_t n_substeps, const bsim_actions_t *actions,
+                      const bsim_task_t *task, void *stream);
 /* EnvBatch.reset(idx) (envs.py:145-176): reset the masked envs (NULL = all)
    and write the observation of every env. */
 int bsim_task_reset(const bsim_layout_t *layout, const bsim_state_t *state, const bsim_task_t *task,

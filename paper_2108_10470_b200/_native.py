@@ -120,6 +120,7 @@ def _declare(lib):
     for suffix, prm in (("", Params), ("_f64", Params64)):
         sig.update({
             "bsim_step" + suffix: ([P(Layout), P(prm), vp, C.c_int32, P(Actions), vp], C.c_int),
+            "bsim_env_step" + suffix: ([P(Layout), P(prm), vp, C.c_int32, P(Actions), vp, vp], C.c_int),
             "bsim_forward_kinematics" + suffix: ([P(Layout), vp, vp, C.c_uint32, vp], C.c_int),
             "bsim_refresh_buffers" + suffix: ([P(Layout), vp, vp], C.c_int),
             "bsim_set_root_state_indexed" + suffix: ([P(Layout), vp, vp, vp, C.c_int32, vp, vp, vp], C.c_int),

@@ -25,9 +25,10 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", 
 # MUFU-based approximate divide / square root (<= 2 ulp; atan2f's internal
 # divide, norms, the sweep's friction / cone-clamp square roots).  Measured
 # 7 % faster step; fp64 (the exact-parity path) is unaffected,
-# and the task / RNG TUs keep IEEE fp32.
+# the task layer (bsim_tasks.cu) uses the same mode so the fused env step
+# (task tail inside the physics kernel) is bitwise the two-launch path.
 FAST_FP32 = ["-ftz=true", "-prec-div=false", "-prec-sqrt=false"]
-FAST_TUS = ("bsim_step.cu", "bsim_step_large.cu")
+FAST_TUS = ("bsim_step.cu", "bsim_step_large.cu", "bsim_tasks.cu")
 
 
 def sources():

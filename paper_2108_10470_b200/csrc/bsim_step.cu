@@ -21,15 +21,16 @@
 #include "bsim_step.cuh"
 #include "bsim_topologies.cuh"
 #include "bsim_kin.cuh"
+#include "bsim_tasks.cuh"
 
 using namespace bsim;
 
 #ifndef BSIM_LARGE_TU
 extern "C" {
 int bsim_large_step_f32(const bsim_layout_t *, const bsim_params_t *, const bsim_state_t *, int32_t,
-                        const bsim_actions_t *, void *);
+                        const bsim_actions_t *, const bsim_task_t *, void *);
 int bsim_large_step_f64(const bsim_layout_t *, const bsim_params64_t *, const bsim_state64_t *, int32_t,
-                        const bsim_actions_t *, void *);
+                        const bsim_actions_t *, const bsim_task_t *, void *);
 const char *bsim_large_last_error(void);
 }
 #endif
@@ -100,6 +101,10 @@ template <int NW> __device__ unsigned claim_sweep_smsp(const int *warp_smsp, uns
     return bit;
 }
 
+template <class R> __device__ __noinline__ void task_step_env_call(const Ctx<R> &c, const bsim_task_t &t, int e) {
+    task_step_env(c, TaskView<R>{t}, e);
+}
+
 #ifndef BSIM_MINB
 #define BSIM_MINB 4   // 4 x 128 threads at <= 128 registers: matches the shared-memory limit
 #endif
@@ -107,7 +112,8 @@ template <int NW> __device__ unsigned claim_sweep_smsp(const int *warp_smsp, uns
 // number of waves of resident CTAs (148 SMs x CTAs/SM)
 template <class R, class T>
 __global__ void __launch_bounds__(Shape<R>::NTH, BSIM_MINB)
-    step_kernel(const Ctx<R> c, int n_substeps, bsim_actions_t act, int epc) {
+    step_kernel(const __grid_constant__ Ctx<R> c, int n_substeps, bsim_actions_t act, int epc,
+                const __grid_constant__ bsim_task_t task, int with_task) {
     constexpr int NTH = Shape<R>::NTH, STR = Shape<R>::STR;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const Dims &d = c.d;
@@ -187,6 +193,10 @@ __global__ void __launch_bounds__(Shape<R>::NTH, BSIM_MINB)
         }
     }
     if (tid == 0 && s_sweep_bit) atomicAnd(&g_sweep_smsp[s_sm_slot], ~s_sweep_bit);
+    if (with_task) {   // EnvBatch.step tail for this CTA's envs (bsim_env_step)
+        __syncthreads();   // the CTA's state stores above are visible to its threads
+        if (tid < ne) task_step_env_call(c, task, e0 + tid);
+    }
 }
 
 template <class R>
@@ -410,7 +420,8 @@ bool bad_layout(const bsim_layout_t *L) {
 
 // ------------------------------------------------------------ launchers
 template <class R, class T>
-int launch_step_t(const Ctx<R> &c, size_t smem, int n_substeps, const bsim_actions_t &act, cudaStream_t st) {
+int launch_step_t(const Ctx<R> &c, size_t smem, int n_substeps, const bsim_actions_t &act, const bsim_task_t *task,
+                  cudaStream_t st) {
     constexpr int NE = Shape<R>::NE;
     static size_t configured = 0;
     static int slots = 0;   // resident CTAs on the whole device at this smem size
@@ -439,8 +450,17 @@ int launch_step_t(const Ctx<R> &c, size_t smem, int n_substeps, const bsim_actio
     if (epc > NE) epc = NE;
 #endif
     const int grid = (E + epc - 1) / epc;
-    step_kernel<R, T><<<grid, Shape<R>::NTH, smem, st>>>(c, n_substeps, act, epc);
+    bsim_task_t tk;
+    if (task) tk = *task; else std::memset(&tk, 0, sizeof tk);
+    step_kernel<R, T><<<grid, Shape<R>::NTH, smem, st>>>(c, n_substeps, act, epc, tk, task != nullptr);
     return check_launch("step_kernel");
+}
+
+// the task-layer argument rules of bsim_task_step (bsim_tasks.cu)
+bool task_ok(const bsim_layout_t *L, const bsim_task_t *t) {
+    const bool kind_ok = t->kind == BSIM_TASK_QUADRUPED || t->kind == BSIM_TASK_ANYMAL || t->kind == BSIM_TASK_HUMANOID;
+    return kind_ok && t->act_dim == L->dofs_per_env && L->actors_per_env == 1 &&
+           t->obs_dim == 12 + 2 * t->act_dim + (t->kind == BSIM_TASK_ANYMAL ? 0 : 6 * L->sensors_per_env) + t->act_dim;
 }
 
 #ifndef BSIM_LARGE_TU
@@ -451,21 +471,25 @@ template <class R> bool use_large_variant(const Dims &d) {
     return step_smem_bytes<R>(d) > 113 * 1024;
 }
 int call_large(const bsim_layout_t *l, const bsim_params_t *p, const bsim_state_t *s, int32_t n,
-               const bsim_actions_t *a, void *st) {
-    return bsim_large_step_f32(l, p, s, n, a, st);
+               const bsim_actions_t *a, const bsim_task_t *t, void *st) {
+    return bsim_large_step_f32(l, p, s, n, a, t, st);
 }
 int call_large(const bsim_layout_t *l, const bsim_params64_t *p, const bsim_state64_t *s, int32_t n,
-               const bsim_actions_t *a, void *st) {
-    return bsim_large_step_f64(l, p, s, n, a, st);
+               const bsim_actions_t *a, const bsim_task_t *t, void *st) {
+    return bsim_large_step_f64(l, p, s, n, a, t, st);
 }
 #endif
 
 template <class R>
 int launch_step(const bsim_layout_t *layout, const typename Abi<R>::Params *params,
                 const typename Abi<R>::State *state, int32_t n_substeps, const bsim_actions_t *actions,
-                void *stream) {
+                void *stream, const bsim_task_t *task = nullptr) {
     if (bad_layout(layout) || !params || !state || n_substeps < 1) {
         g_err = "bsim_step: invalid arguments";
+        return BSIM_E_INVALID;
+    }
+    if (task && !task_ok(layout, task)) {
+        g_err = "bsim_env_step: invalid task";
         return BSIM_E_INVALID;
     }
     Ctx<R> c = make_ctx<R>(layout, params, state);
@@ -479,21 +503,21 @@ int launch_step(const bsim_layout_t *layout, const typename Abi<R>::Params *para
     if (actions) act = *actions; else std::memset(&act, 0, sizeof act);
     cudaStream_t st = (cudaStream_t)stream;
 #ifdef BSIM_LARGE_TU
-    return launch_step_t<R, TopoGeneric>(c, smem, n_substeps, act, st);
+    return launch_step_t<R, TopoGeneric>(c, smem, n_substeps, act, task, st);
 #else
     if (use_large_variant<R>(c.d)) {   // big articulations: 4 envs x 32 threads per CTA
-        int rc = call_large(layout, params, state, n_substeps, actions, stream);
+        int rc = call_large(layout, params, state, n_substeps, actions, task, stream);
         if (rc != BSIM_OK) g_err = bsim_large_last_error();
         return rc;
     }
     switch (layout->topology_id) {
 #define BSIM_LAUNCH_TOPO(ID, TYPE)                                      \
     case ID:                                                            \
-        return launch_step_t<R, TYPE>(c, smem, n_substeps, act, st);
+        return launch_step_t<R, TYPE>(c, smem, n_substeps, act, task, st);
         BSIM_TOPOLOGIES(BSIM_LAUNCH_TOPO)
 #undef BSIM_LAUNCH_TOPO
     default:
-        return launch_step_t<R, TopoGeneric>(c, smem, n_substeps, act, st);
+        return launch_step_t<R, TopoGeneric>(c, smem, n_substeps, act, task, st);
     }
 #endif
 }
@@ -578,12 +602,12 @@ int launch_collide(const bsim_layout_t *layout, const typename Abi<R>::Params *p
 #ifdef BSIM_LARGE_TU
 extern "C" {
 int bsim_large_step_f32(const bsim_layout_t *l, const bsim_params_t *p, const bsim_state_t *s, int32_t n,
-                        const bsim_actions_t *a, void *st) {
-    return launch_step<float>(l, p, s, n, a, st);
+                        const bsim_actions_t *a, const bsim_task_t *t, void *st) {
+    return launch_step<float>(l, p, s, n, a, st, t);
 }
 int bsim_large_step_f64(const bsim_layout_t *l, const bsim_params64_t *p, const bsim_state64_t *s, int32_t n,
-                        const bsim_actions_t *a, void *st) {
-    return launch_step<double>(l, p, s, n, a, st);
+                        const bsim_actions_t *a, const bsim_task_t *t, void *st) {
+    return launch_step<double>(l, p, s, n, a, st, t);
 }
 const char *bsim_large_last_error(void) { return g_err.c_str(); }
 }
@@ -606,6 +630,16 @@ int bsim_step_smem_per_env(const bsim_layout_t *layout, int32_t fp64, int32_t *b
 int bsim_step(const bsim_layout_t *l, const bsim_params_t *p, const bsim_state_t *s, int32_t n,
               const bsim_actions_t *a, void *st) {
     return launch_step<float>(l, p, s, n, a, st);
+}
+int bsim_env_step(const bsim_layout_t *l, const bsim_params_t *p, const bsim_state_t *s, int32_t n,
+                  const bsim_actions_t *a, const bsim_task_t *t, void *st) {
+    if (!t) return BSIM_E_INVALID;
+    return launch_step<float>(l, p, s, n, a, st, t);
+}
+int bsim_env_step_f64(const bsim_layout_t *l, const bsim_params64_t *p, const bsim_state64_t *s, int32_t n,
+                      const bsim_actions_t *a, const bsim_task_t *t, void *st) {
+    if (!t) return BSIM_E_INVALID;
+    return launch_step<double>(l, p, s, n, a, st, t);
 }
 int bsim_step_f64(const bsim_layout_t *l, const bsim_params64_t *p, const bsim_state64_t *s, int32_t n,
                   const bsim_actions_t *a, void *st) {

@@ -129,3 +129,23 @@ def test_cuda_graph_step_equals_eager(task):
     assert a.scene.step_count == b.scene.step_count
     assert int(b._step_count_dev) == b.scene.step_count
     assert int(a.done.sum()) >= 0 and int(a.reset_count.sum()) > 2 * 64   # resets happened
+
+
+@pytest.mark.parametrize("task", ["quadruped", "quadruped-anymal-obs", "humanoid"])
+def test_fused_env_step_launch_equals_two_launches(task):
+    """bsim_env_step (physics + task tail in one kernel) == bsim_step then
+    bsim_task_step, bitwise, through resets, DR and graph capture."""
+    from paper_2108_10470_b200 import envs as EV
+    kw = dict(num_envs=48, seed=9, episode_length=6, randomize=True)
+    a, b = EV.make_env(task, **kw), EV.make_env(task, **kw)
+    b.fused = True
+    rng = np.random.default_rng(4)
+    for t in range(14):
+        if t == 7:
+            b.capture_graph()
+        act = torch.as_tensor(rng.uniform(-1.2, 1.2, (48, a.act_dim)), dtype=torch.float32, device="cuda")
+        oa, ob = a.step(act), b.step(act)
+        for x, y in ((oa.obs, ob.obs), (oa.reward, ob.reward), (oa.done, ob.done), (a.scene.body_q, b.scene.body_q),
+                     (a.scene.dof_state, b.scene.dof_state), (a.reset_count, b.reset_count)):
+            assert torch.equal(x, y), t
+    assert a.scene.step_count == b.scene.step_count
