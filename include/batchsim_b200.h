@@ -93,7 +93,16 @@ typedef struct bsim_layout_t {
     const void *tendons;                   /* [T]    */
     const void *tendon_elems;
     const int32_t *spatial_paths;          /* per tendon at path_offset: npaths, {len, idx...}* */
+    const int32_t *pair_kind;              /* [Q] BSIM_PAIR_* */
+    const void *pair_ext;                  /* [Q][4] real: PB box half extents of b; PC (0, hh_b);
+                                              CC (hh_a, hh_b); SS unused */
 } bsim_layout_t;
+
+/* Pair-slot narrow phase kinds.  SS is the reference's only pair type
+   (physics.py:481-497); PB / PC / CC extend the slot model to box and capsule
+   pairs (a sphere, capsule end sphere or box corner against a box; a sphere
+   against a capsule segment; capsule against capsule). */
+enum bsim_pair_kind { BSIM_PAIR_SS = 0, BSIM_PAIR_PB = 1, BSIM_PAIR_PC = 2, BSIM_PAIR_CC = 3 };
 
 /* All per-env state, parameters, controls and tensor-API outputs
    (reference parallel.py:24-42 `_SHARED` working set).  DEVICE pointers. */

@@ -607,19 +607,71 @@ static void plane_geometry(const bso_scene *s, int e, int i, const double *pos, 
     point[0] = c[0]; point[1] = c[1]; point[2] = c[2] - rad;
     *active = *depth > -s->params.solver_offset_slop;
 }
+/* Pair slot narrow phase.  Kind 0 (SS) is the reference's sphere-sphere pair
+   (physics.py:481-497).  Kinds 1-3 are NOT in the reference: box / capsule
+   pairs of this build (sphere|corner vs box, sphere|corner vs capsule
+   segment, capsule vs capsule), restated here independently of the CUDA code
+   so the GPU path has a float64 checker (parity unpinned to the reference). */
 static void pair_geometry(const bso_scene *s, int e, int i, const double *pos, const double *quat,
                           double *point, double *n, double *depth, int *active) { /* 481-497 */
     int a = s->pair_body[2 * i], b = s->pair_body[2 * i + 1];
+    int kind = s->pair_kind[i];
+    const double *ext = s->pair_ext + 4 * i;
     const double *off = s->pair_off + 6 * ((size_t)i * s->E + e);
     double ra = s->pair_rad[2 * ((size_t)i * s->E + e)], rb = s->pair_rad[2 * ((size_t)i * s->E + e) + 1];
-    double ca[3], cb[3], d[3];
+    double ca[3], cb[3], d[3], gap;
     qrot(ca, quat + 4 * a, off);
     qrot(cb, quat + 4 * b, off + 3);
-    for (int k = 0; k < 3; ++k) { ca[k] += pos[3 * a + k]; cb[k] += pos[3 * b + k]; d[k] = cb[k] - ca[k]; }
-    double dist = sqrt(dot3(d, d));
-    double dd = dist > 1e-12 ? dist : 1.0;
-    for (int k = 0; k < 3; ++k) n[k] = d[k] / dd;
-    double gap = dist - (ra + rb);
+    for (int k = 0; k < 3; ++k) { ca[k] += pos[3 * a + k]; cb[k] += pos[3 * b + k]; }
+    if (kind == 1) { /* sphere centre ca vs box centred at cb, axes of body b */
+        double rel[3], pl[3], cl[3], dl[3], nl[3] = {0, 0, 0}, qi[4];
+        for (int k = 0; k < 3; ++k) rel[k] = ca[k] - cb[k];
+        qconj(qi, quat + 4 * b);
+        qrot(pl, qi, rel);
+        for (int k = 0; k < 3; ++k) { cl[k] = clampd(pl[k], -ext[k], ext[k]); dl[k] = pl[k] - cl[k]; }
+        double dist = sqrt(dot3(dl, dl));
+        if (dist > 1e-12) {
+            for (int k = 0; k < 3; ++k) nl[k] = dl[k] / dist;
+            gap = dist - ra;
+        } else {
+            int best = 0;
+            double f[3];
+            for (int k = 0; k < 3; ++k) f[k] = ext[k] - fabs(pl[k]);
+            if (f[1] < f[best]) best = 1;
+            if (f[2] < f[best]) best = 2;
+            nl[best] = pl[best] < 0 ? -1.0 : 1.0;
+            gap = -f[best] - ra;
+        }
+        double nw[3];
+        qrot(nw, quat + 4 * b, nl);
+        for (int k = 0; k < 3; ++k) n[k] = -nw[k];
+    } else {
+        if (kind == 2 || kind == 3) { /* segment(s) along the bodies' local z */
+            double ez[3] = {0, 0, 1}, ub[3], ua[3], d0[3];
+            qrot(ub, quat + 4 * b, ez);
+            double hb = ext[1], t;
+            if (kind == 3) {
+                qrot(ua, quat + 4 * a, ez);
+                double ha = ext[0];
+                for (int k = 0; k < 3; ++k) d0[k] = ca[k] - cb[k];
+                double bb = dot3(ua, ub), dA = dot3(ua, d0), dB = dot3(ub, d0);
+                double den = 1.0 - bb * bb;
+                double sa = den > 1e-9 ? clampd((bb * dB - dA) / den, -ha, ha) : 0.0;
+                t = clampd(dB + bb * sa, -hb, hb);
+                sa = clampd(bb * t - dA, -ha, ha);
+                for (int k = 0; k < 3; ++k) ca[k] += ua[k] * sa;
+            } else {
+                for (int k = 0; k < 3; ++k) d0[k] = ca[k] - cb[k];
+                t = clampd(dot3(d0, ub), -hb, hb);
+            }
+            for (int k = 0; k < 3; ++k) cb[k] += ub[k] * t;
+        }
+        for (int k = 0; k < 3; ++k) d[k] = cb[k] - ca[k];
+        double dist = sqrt(dot3(d, d));
+        double dd = dist > 1e-12 ? dist : 1.0;
+        for (int k = 0; k < 3; ++k) n[k] = d[k] / dd;
+        gap = dist - (ra + rb);
+    }
     *depth = s->params.rest_offset - gap;
     for (int k = 0; k < 3; ++k) point[k] = ca[k] + n[k] * (ra + 0.5 * gap);
     *active = *depth > -s->params.solver_offset_slop;

@@ -56,6 +56,8 @@ typedef struct {
     const bso_joint *joints;          /* [J] */
     const int32_t *plane_body;        /* [P] */
     const int32_t *pair_body;         /* [Q][2] */
+    const int32_t *pair_kind;         /* [Q] 0 SS (reference), 1 PB, 2 PC, 3 CC (extension) */
+    const double *pair_ext;           /* [Q][4] box half extents / capsule half heights */
     const int32_t *sensor_body;       /* [S] */
     const int32_t *actor_body_offset; /* [A] */
     const bso_tendon *tendons;        /* [T] */

@@ -81,7 +81,7 @@ LAYOUT_INTS = ("num_envs", "actors_per_env", "bodies_per_env", "dofs_per_env", "
                "planes_per_env", "pairs_per_env", "sensors_per_env", "tendons_per_env", "env_offset",
                "topology_id")
 LAYOUT_PTRS = ("joints", "plane_body", "pair_body", "sensor_body", "actor_body_offset",
-               "actor_dof_offset", "tendons", "tendon_elems", "spatial_paths")
+               "actor_dof_offset", "tendons", "tendon_elems", "spatial_paths", "pair_kind", "pair_ext")
 
 
 class Layout(C.Structure):

@@ -276,16 +276,13 @@ __device__ void slot_geometry(const Ctx<R> &c, int i, int e, bool &active, R &de
         const R *A_ = bq + 13 * c.L.pair_body[2 * q], *B_ = bq + 13 * c.L.pair_body[2 * q + 1];
         const R *off = c.s.pair_off + 6 * ((size_t)q * E + e);
         const R *rr = c.s.pair_rad + 2 * ((size_t)q * E + e);
-        V3<R> arma = qrot(Q4<R>{A_[3], A_[4], A_[5], A_[6]}, jv3(off));
-        V3<R> armb = qrot(Q4<R>{B_[3], B_[4], B_[5], B_[6]}, jv3(off + 3));
         V3<R> pa = V3<R>{A_[0], A_[1], A_[2]};
-        V3<R> dd = (V3<R>{B_[0], B_[1], B_[2]} - pa) + (armb - arma);
-        R dist = norm(dd);
-        R dn = dist > R(1e-12) ? dist : R(1);
-        n = v3(dd.x / dn, dd.y / dn, dd.z / dn);
-        R gap = dist - (rr[0] + rr[1]);
+        V3<R> ra;
+        R gap;
+        pair_shape_contact(c.L.pair_kind[q], Q4<R>{A_[3], A_[4], A_[5], A_[6]}, Q4<R>{B_[3], B_[4], B_[5], B_[6]},
+                           V3<R>{B_[0], B_[1], B_[2]} - pa, off, rr, c.pair_ext() + 4 * q, n, gap, ra);
         depth = c.p.rest_offset - gap;
-        point = pa + arma + n * (rr[0] + R(0.5) * gap) + org;
+        point = pa + ra + org;
     }
     active = depth > -c.p.solver_offset_slop;
 }

@@ -152,6 +152,7 @@ template <class R> struct Ctx {
     const Joint *joints;
     BS_HD const Tendon &tendon(int i) const { return reinterpret_cast<const Tendon *>(L.tendons)[i]; }
     BS_HD const TElem *elems() const { return reinterpret_cast<const TElem *>(L.tendon_elems); }
+    BS_HD const R *pair_ext() const { return reinterpret_cast<const R *>(L.pair_ext); }
 };
 
 BS_HD int ib(const Dims &d, int b, int item) { return d.o_body + b * BODY_ITEMS + item; }
@@ -420,23 +421,91 @@ template <class R> BS_HD void plane_freeze(const Ctx<R> &c, const Ws<R> &w, int 
     w.at(ipl(d, i, CLT + 1)) = R(0);
 }
 
-// Sphere-sphere pair slot i at freeze (physics.py:481-497, 698-712).
+// Narrow phase of one pair slot (contact normal a->b, surface gap, and the
+// arm from body a's origin to the mid-gap contact point).  pab = pos_b - pos_a.
+//   SS sphere-sphere: the reference pair (physics.py:481-497), same arithmetic;
+//   PB sphere (or capsule end sphere / box corner, radius 0) vs box b;
+//   PC sphere vs capsule b (the segment along b's local z, half height ext[1]);
+//   CC capsule vs capsule (clamped segment-segment closest points).
+// The reference has only SS: PB / PC / CC are this build's extension for the
+// box and capsule pair types (parity unpinned -- checked
+// against the C oracle's independent implementation and physics properties).
+template <class R>
+BS_HD void pair_shape_contact(int kind, Q4<R> qa, Q4<R> qb, V3<R> pab, const R *off, const R *rr, const R *ext,
+                              V3<R> &n, R &gap, V3<R> &ra) {
+    V3<R> arma = qrot(qa, jv3(off));
+    if (kind == BSIM_PAIR_SS) {
+        V3<R> armb = qrot(qb, jv3(off + 3));
+        V3<R> dd = pab + (armb - arma);
+        R dist = norm(dd);
+        R dn = dist > R(1e-12) ? dist : R(1);
+        n = v3(dd.x / dn, dd.y / dn, dd.z / dn);
+        gap = dist - (rr[0] + rr[1]);
+        ra = arma + n * (rr[0] + R(0.5) * gap);
+        return;
+    }
+    V3<R> cb = pab + qrot(qb, jv3(off + 3));     // centre of b's box / segment, relative to pos_a
+    V3<R> ca = arma;                             // sphere centre on a
+    R rad = rr[0];
+    if (kind == BSIM_PAIR_PB) {
+        V3<R> pl = qrot(qconj(qb), ca - cb);      // sphere centre in the box frame
+        V3<R> h = v3(ext[0], ext[1], ext[2]);
+        V3<R> cl = v3(clampr(pl.x, -h.x, h.x), clampr(pl.y, -h.y, h.y), clampr(pl.z, -h.z, h.z));
+        V3<R> dl = pl - cl;
+        R dist = norm(dl);
+        V3<R> nl;
+        if (dist > R(1e-12)) {                    // outside: nearest surface point
+            nl = v3(dl.x / dist, dl.y / dist, dl.z / dist);
+            gap = dist - rad;
+        } else {                                  // inside: nearest face
+            R fx = h.x - r_abs(pl.x), fy = h.y - r_abs(pl.y), fz = h.z - r_abs(pl.z);
+            R sx = pl.x < R(0) ? R(-1) : R(1), sy = pl.y < R(0) ? R(-1) : R(1), sz = pl.z < R(0) ? R(-1) : R(1);
+            if (fx <= fy && fx <= fz) { nl = v3(sx, R(0), R(0)); gap = -fx - rad; }
+            else if (fy <= fz) { nl = v3(R(0), sy, R(0)); gap = -fy - rad; }
+            else { nl = v3(R(0), R(0), sz); gap = -fz - rad; }
+        }
+        n = -qrot(qb, nl);                        // from the sphere towards the box
+        ra = ca + n * (rad + R(0.5) * gap);
+        return;
+    }
+    V3<R> ub = qrot(qb, v3(R(0), R(0), R(1)));
+    const R hb = ext[1];
+    if (kind == BSIM_PAIR_CC) {                   // closest points of two clamped segments
+        V3<R> ua = qrot(qa, v3(R(0), R(0), R(1)));
+        const R ha = ext[0];
+        V3<R> d0 = ca - cb;
+        R b_ = dot(ua, ub), dA = dot(ua, d0), dB = dot(ub, d0);
+        R den = R(1) - b_ * b_;
+        R sa = den > R(1e-9) ? clampr((b_ * dB - dA) / den, -ha, ha) : R(0);
+        R tb = clampr(dB + b_ * sa, -hb, hb);
+        sa = clampr(b_ * tb - dA, -ha, ha);
+        ca = ca + ua * sa;
+        cb = cb + ub * tb;
+    } else {                                      // PC: sphere centre vs segment
+        R tb = clampr(dot(ca - cb, ub), -hb, hb);
+        cb = cb + ub * tb;
+    }
+    V3<R> dd = cb - ca;
+    R dist = norm(dd);
+    R dn = dist > R(1e-12) ? dist : R(1);
+    n = v3(dd.x / dn, dd.y / dn, dd.z / dn);
+    gap = dist - (rr[0] + rr[1]);
+    ra = ca + n * (rad + R(0.5) * gap);
+}
+
+// Pair slot i at freeze (physics.py:481-497, 698-712).
 template <class R> BS_HD void pair_freeze(const Ctx<R> &c, const Ws<R> &w, int e, int i) {
     const Dims &d = c.d;
     const auto &p = c.p;
     int pa = c.L.pair_body[2 * i], pb = c.L.pair_body[2 * i + 1];
     const R *off = c.s.pair_off + 6 * ((size_t)i * d.E + e);
     const R *rr = c.s.pair_rad + 2 * ((size_t)i * d.E + e);
-    V3<R> arma = qrot(w.l4(ib(d, pa, BQ)), jv3(off));
-    V3<R> armb = qrot(w.l4(ib(d, pb, BQ)), jv3(off + 3));
     V3<R> pa0 = w.l3(ib(d, pa, BP));
-    V3<R> dd = (w.l3(ib(d, pb, BP)) - pa0) + (armb - arma);
-    R dist = norm(dd);
-    R dn = dist > R(1e-12) ? dist : R(1);
-    V3<R> n = v3(dd.x / dn, dd.y / dn, dd.z / dn);
-    R gap = dist - (rr[0] + rr[1]);
+    V3<R> n, ra;
+    R gap;
+    pair_shape_contact(c.L.pair_kind[i], w.l4(ib(d, pa, BQ)), w.l4(ib(d, pb, BQ)), w.l3(ib(d, pb, BP)) - pa0, off,
+                       rr, c.pair_ext() + 4 * i, n, gap, ra);
     R depth = p.rest_offset - gap;
-    V3<R> ra = arma + n * (rr[0] + R(0.5) * gap);
     V3<R> r = (pa0 - w.l3(ib(d, pb, BP))) + ra;
     V3<R> va = w.l3(ib(d, pa, BV_)) + cross(w.l3(ib(d, pa, BW)), ra);
     V3<R> vb = w.l3(ib(d, pb, BV_)) + cross(w.l3(ib(d, pb, BW)), r);

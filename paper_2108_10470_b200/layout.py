@@ -62,10 +62,68 @@ class JointRow:
     limit_hi: float
 
 
+PAIR_SS, PAIR_PB, PAIR_PC, PAIR_CC = 0, 1, 2, 3      # bsim_pair_kind (include/batchsim_b200.h)
+
+
+def _corners(sh):
+    hx, hy, hz = sh.params
+    off = np.asarray(sh.offset, float)
+    return [off + [sx * hx, sy * hy, sz * hz] for sx in (-1, 1) for sy in (-1, 1) for sz in (-1, 1)]
+
+
+def _ends(sh):
+    r, hh = sh.params
+    off = np.asarray(sh.offset, float)
+    return [off + [0.0, 0.0, s * hh] for s in (-1.0, 1.0)]
+
+
+def pair_slots(b1, s1, b2, s2):
+    """Candidate contact slots of one shape pair between two actors:
+    (kind, body_a, off_a, rad_a, body_b, off_b, rad_b, ext4).
+
+    sphere-sphere is the reference's pair (physics.py:330-338, one SS slot,
+    a = the first shape).  The box / capsule pairs extend the same static-slot
+    model the reference uses for the ground (physics.py:314-327: capsule ->
+    two end spheres, box -> eight corner points): sphere-box one PB slot;
+    capsule-box the capsule's end spheres against the box (2 PB) and the box
+    corners against the capsule (8 PC); box-box each box's corners against
+    the other box (16 PB); sphere-capsule one PC slot; capsule-capsule one CC
+    slot (segment-segment)."""
+    z4 = (0.0, 0.0, 0.0, 0.0)
+    off = lambda sh: np.asarray(sh.offset, float)  # noqa: E731
+
+    def pb(ba, pa_, ra_, bb, sb):          # point/sphere on ba vs box sb on bb
+        return (PAIR_PB, ba, pa_, ra_, bb, off(sb), 0.0, (*sb.params, 0.0))
+
+    def pc(ba, pa_, ra_, bb, sb):          # point/sphere on ba vs capsule sb on bb
+        return (PAIR_PC, ba, pa_, ra_, bb, off(sb), sb.params[0], (0.0, sb.params[1], 0.0, 0.0))
+
+    k1, k2 = s1.kind, s2.kind
+    if k1 == "sphere" and k2 == "sphere":
+        return [(PAIR_SS, b1, off(s1), s1.params[0], b2, off(s2), s2.params[0], z4)]
+    if k1 == "box" and k2 != "box":        # order so that a box, if any, is the second shape
+        return pair_slots(b2, s2, b1, s1)
+    if k1 == "capsule" and k2 == "sphere":
+        return pair_slots(b2, s2, b1, s1)
+    if k1 == "sphere" and k2 == "box":
+        return [pb(b1, off(s1), s1.params[0], b2, s2)]
+    if k1 == "sphere" and k2 == "capsule":
+        return [pc(b1, off(s1), s1.params[0], b2, s2)]
+    if k1 == "capsule" and k2 == "capsule":
+        return [(PAIR_CC, b1, off(s1), s1.params[0], b2, off(s2), s2.params[0], (s1.params[1], s2.params[1], 0.0, 0.0))]
+    if k1 == "capsule" and k2 == "box":
+        return ([pb(b1, e, s1.params[0], b2, s2) for e in _ends(s1)] +
+                [pc(b2, c, 0.0, b1, s1) for c in _corners(s2)])
+    if k1 == "box" and k2 == "box":
+        return ([pb(b1, c, 0.0, b2, s2) for c in _corners(s1)] +
+                [pb(b2, c, 0.0, b1, s1) for c in _corners(s2)])
+    return []
+
+
 class SceneLayout:
     """Per-env tables for a list of actors replicated over all envs."""
 
-    def __init__(self, models, ground=True):
+    def __init__(self, models, ground=True, shape_pairs="spheres"):
         if isinstance(models, ArticulationModel):
             models = [models]
         self.models = list(models)
@@ -151,12 +209,20 @@ class SceneLayout:
         for i in range(len(shapes)):
             for k in range(i + 1, len(shapes)):
                 (ai, bi, si), (ak, bk, sk) = shapes[i], shapes[k]
-                if ai != ak and si.kind == "sphere" and sk.kind == "sphere":
-                    pairs.append((bi, si, bk, sk))
-        self.pair_body = np.array([[p[0], p[2]] for p in pairs], np.int32).reshape(-1, 2)
-        self.pair_off = np.array([[p[1].offset, p[3].offset] for p in pairs], float).reshape(-1, 2, 3)
-        self.pair_rad = np.array([[p[1].params[0], p[3].params[0]] for p in pairs],
-                                 float).reshape(-1, 2)
+                if ai == ak:          # self-collision within an actor is off (physics.py:333-334)
+                    continue
+                if shape_pairs == "spheres":   # the reference's pair set (physics.py:335-338)
+                    if si.kind == "sphere" and sk.kind == "sphere":
+                        pairs += pair_slots(bi, si, bk, sk)
+                elif shape_pairs == "all":     # + box / capsule pair types (extension)
+                    pairs += pair_slots(bi, si, bk, sk)
+                else:
+                    raise ValueError("shape_pairs must be 'spheres' (reference) or 'all'")
+        self.pair_kind = np.array([p[0] for p in pairs], np.int32)
+        self.pair_body = np.array([[p[1], p[4]] for p in pairs], np.int32).reshape(-1, 2)
+        self.pair_off = np.array([[p[2], p[5]] for p in pairs], float).reshape(-1, 2, 3)
+        self.pair_rad = np.array([[p[3], p[6]] for p in pairs], float).reshape(-1, 2)
+        self.pair_ext = np.array([p[7] for p in pairs], float).reshape(-1, 4)
         self.planes_per_env = len(plane)
         self.pairs_per_env = len(pairs)
 

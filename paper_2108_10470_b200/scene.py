@@ -54,7 +54,7 @@ class Scene:
 
     def __init__(self, models, num_envs, params: SimParams | None = None, spacing=4.0,
                  ground=True, env_origins=None, device=None, precision="fp32",
-                 env_offset=0, total_envs=None, stream=None, specialize=True):
+                 env_offset=0, total_envs=None, stream=None, specialize=True, shape_pairs="spheres"):
         if not torch.cuda.is_available():
             raise N.NativeError("paper_2108_10470_b200.Scene needs a CUDA device (no CPU fallback)")
         if isinstance(models, ArticulationModel):
@@ -75,7 +75,9 @@ class Scene:
         self.env_offset = int(env_offset)
         self.total_envs = int(total_envs) if total_envs is not None else self.env_offset + E
 
-        L = self.layout = SceneLayout(self.models, ground)
+        # shape_pairs: "spheres" = the reference's contact set (sphere-sphere
+        # pairs between actors); "all" adds the box / capsule pair types
+        L = self.layout = SceneLayout(self.models, ground, shape_pairs)
         # AOT-specialised step kernel for known topologies (codegen.py), else generic
         from .codegen import topology_id
         self.topology_id = topology_id(L) if specialize else 0

@@ -65,6 +65,9 @@ def pack_tables(L: SceneLayout, fp64: bool = False):
         "tendons": as_bytes(tendons),
         "tendon_elems": as_bytes(elems),
         "spatial_paths": np.array(flat_paths or [0], np.int32),
+        "pair_kind": np.ascontiguousarray(L.pair_kind, np.int32) if L.pairs_per_env else np.zeros(1, np.int32),
+        "pair_ext": (np.ascontiguousarray(L.pair_ext, np.float64 if fp64 else np.float32).reshape(-1)
+                     if L.pairs_per_env else np.zeros(4, np.float64 if fp64 else np.float32)),
     }
 
 

@@ -1,0 +1,100 @@
+"""Authored scenes for the box / capsule pair types (shape_pairs="all"), which
+the reference does not have (parity unpinned).  Traces are
+produced by the float64 C oracle (oracle/bso.c, an independent restatement of
+the same narrow phase) in the golden-fixture format of tests/golden_util.py,
+so the host build of the kernel body and the CUDA path are compared against
+it exactly like the reference-generated fixtures."""
+
+import numpy as np
+
+from paper_2108_10470_b200 import models as M
+from paper_2108_10470_b200.model import load_model
+from paper_2108_10470_b200.models import capsule_inertia
+from paper_2108_10470_b200.params import SimParams
+
+G = 9.81
+
+
+def capsule(name, m, r, hh, fixed=False):
+    return load_model({"name": name, "fixed_base": fixed,
+                       "links": [{"name": "c", "mass": m, "inertia": list(capsule_inertia(m, r, hh)),
+                                  "shape": {"kind": "capsule", "params": [r, hh]}}]})
+
+
+def q_axis(ax, ang):
+    ax = np.asarray(ax, float)
+    ax = ax / np.linalg.norm(ax)
+    return np.r_[ax * np.sin(ang / 2), np.cos(ang / 2)]
+
+
+SCENES = {
+    # box B (rotated) resting on box A resting on the ground: 16 PB corner slots
+    "box_stack": (lambda: [M.free_box((0.2, 0.2, 0.1), 2.0), M.free_box((0.1, 0.1, 0.1), 1.0)],
+                  [((0, 0, 0.1), (0, 0, 1), 0.0), ((0.05, 0.02, 0.3), (0, 0, 1), 0.3)]),
+    # sphere on a box: 1 PB slot
+    "sphere_on_box": (lambda: [M.free_box((0.2, 0.2, 0.1), 2.0), M.free_sphere(0.1, 1.0)],
+                      [((0, 0, 0.1), (0, 0, 1), 0.0), ((0.05, 0.0, 0.3), (0, 0, 1), 0.0)]),
+    # two horizontal capsules crossing: 1 CC slot
+    "capsule_cross": (lambda: [capsule("a", 1.0, 0.05, 0.2), capsule("b", 0.5, 0.05, 0.2)],
+                      [((0, 0, 0.05), (0, 1, 0), np.pi / 2), ((0, 0, 0.15), (1, 0, 0), np.pi / 2)]),
+    # horizontal capsule on a box: 2 PB (capsule ends) + 8 PC (box corners)
+    "capsule_on_box": (lambda: [M.free_box((0.2, 0.2, 0.1), 2.0), capsule("b", 0.5, 0.05, 0.1)],
+                       [((0, 0, 0.1), (0, 0, 1), 0.0), ((0, 0, 0.2505), (1, 0, 0), np.pi / 2)]),
+    # sphere cradled between two static horizontal capsule rails: 2 PC slots
+    "sphere_in_cradle": (lambda: [capsule("rail_a", 1.0, 0.05, 0.25, fixed=True),
+                                  capsule("rail_b", 1.0, 0.05, 0.25, fixed=True), M.free_sphere(0.08, 0.4)],
+                         [((0, -0.06, 0.2), (0, 1, 0), np.pi / 2), ((0, 0.06, 0.2), (0, 1, 0), np.pi / 2),
+                          ((0.02, 0.0, 0.3153), (0, 0, 1), 0.0)]),
+}
+
+
+def setup(name, s, jitter=0.0, seed=0):
+    """Place the actors of scene `name` (env-local poses + the env origins);
+    `jitter` adds per-env random velocities."""
+    _, poses = SCENES[name]
+    B, E = s.bodies_per_env, s.num_envs
+    rng = np.random.default_rng(seed)
+    gpu = hasattr(s, "env_origins_host")       # the CUDA Scene keeps env-local positions
+    org = np.zeros((E, 3)) if gpu else s.env_origins
+    put = (lambda v: __import__("torch").as_tensor(v, dtype=s.dtype)) if gpu else (lambda v: v)  # noqa: E731
+    for e in range(E):
+        for a, (p, ax, ang) in enumerate(poses):
+            s.pos[e * B + a] = put(org[e] + np.asarray(p, float))
+            s.quat[e * B + a] = put(q_axis(ax, ang))
+            if jitter:
+                s.linvel[e * B + a] = put(rng.uniform(-jitter, jitter, 3))
+                s.angvel[e * B + a] = put(rng.uniform(-jitter, jitter, 3))
+
+
+STATE = ("pos", "quat", "linvel", "angvel", "_friction_anchor", "nonfinite", "dof_state",
+         "ctrl_dof_force", "ctrl_dof_pos_target", "ctrl_dof_vel_target", "ctrl_body_force",
+         "ctrl_body_torque", "dof_mode")
+OUTPUTS = ("root_state", "body_state", "dof_state", "net_contact", "dof_force", "sensor_forces", "nonfinite",
+           "pos", "quat", "linvel", "angvel", "_friction_anchor")
+
+
+def oracle_trace(name, E=4, steps=12, warm=30, dt=1 / 120, jitter=0.3):
+    """(meta, arrays) in the golden-fixture format: the oracle's state before
+    / after each of `steps` steps, after `warm` steps of settling."""
+    from oracle.oracle import OracleScene
+    models = SCENES[name][0]()
+    p = SimParams(dt=dt)
+    s = OracleScene(models, E, p, shape_pairs="all")
+    setup(name, s, jitter=jitter)
+    for _ in range(warm):
+        s.step()
+    arr = {f"param_{k}": np.array(getattr(s, k)) for k in
+           ("inv_mass", "inertia_local", "inv_inertia_local", "gravity", "mu_static", "mu_dynamic",
+            "joint_stiffness", "joint_damping", "joint_armature", "joint_friction", "joint_limit_lo",
+            "joint_limit_hi", "plane_off", "plane_rad", "pair_off", "pair_rad", "env_origins")}
+    rec = {f"in_{k}": [] for k in STATE}
+    rec.update({f"out_{k}": [] for k in OUTPUTS})
+    for _ in range(steps):
+        for k in STATE:
+            rec[f"in_{k}"].append(np.array(getattr(s, k), copy=True))
+        s.step()
+        for k in OUTPUTS:
+            rec[f"out_{k}"].append(np.array(getattr(s, k), copy=True))
+    arr.update({k: np.stack(v) for k, v in rec.items()})
+    meta = {"kind": "physics", "num_envs": E, "steps": steps, "params": {"dt": dt}, "spacing": 4.0, "ground": True}
+    return models, p, meta, arr

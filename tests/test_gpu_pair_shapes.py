@@ -1,0 +1,79 @@
+"""Box / capsule pair contacts on the CUDA path (shape_pairs="all"; parity
+unpinned to the reference, which has none): teacher-forced steps against the
+float64 C oracle's independent narrow phase, contact-query masks, and
+resting-contact properties (the stacked bodies' reported contact force equals
+their weight, as the reference's plane test_physics.py:208-214)."""
+
+import numpy as np
+import pytest
+import torch
+
+from golden_util import gpu_outputs, load_gpu_state, rel_err
+from pair_scenes import G, SCENES, oracle_trace, setup
+
+pytestmark = pytest.mark.gpu
+
+
+def _gpu(models, p, E, precision, arr=None):
+    from paper_2108_10470_b200.scene import Scene
+    s = Scene(models, E, p, precision=precision, shape_pairs="all",
+              env_origins=None if arr is None else arr["param_env_origins"])
+    return s
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+@pytest.mark.parametrize("name", sorted(SCENES))
+def test_step_matches_oracle_teacher_forced(name, precision):
+    models, p, meta, arr = oracle_trace(name)
+    s = _gpu(models, p, meta["num_envs"], precision, arr)
+    tol = 1e-8 if precision == "fp64" else 2e-3
+    for t in range(meta["steps"]):
+        load_gpu_state(s, arr, t)
+        s.step()
+        got = gpu_outputs(s)
+        for k in ("root_state", "body_state", "net_contact"):
+            e = rel_err(got[k], arr[f"out_{k}"][t], tol, tol)
+            assert e <= 1.0, (name, precision, t, k, e)
+
+
+@pytest.mark.parametrize("name", sorted(SCENES))
+def test_contact_geometry_masks_match_oracle(name):
+    """Active masks of every plane / pair slot are identical to the oracle's
+    (depths / points / normals within fp64 rounding)."""
+    from oracle.oracle import OracleScene
+    models, p, meta, arr = oracle_trace(name, steps=2)
+    ref = OracleScene(models, meta["num_envs"], p, shape_pairs="all", env_origins=arr["param_env_origins"])
+    for k in ("pos", "quat", "linvel", "angvel"):
+        getattr(ref, k)[...] = arr[f"out_{k}"][-1]
+    s = _gpu(models, p, meta["num_envs"], "fp64", arr)
+    load_gpu_state(s, arr, 1, prefix="out_")
+    ga, gd, gp, gn = (x.cpu().numpy() if isinstance(x, torch.Tensor) else x for x in s.contact_geometry())
+    ra, rd, rp, rn = ref.contact_geometry()
+    assert np.array_equal(np.asarray(ga, bool), np.asarray(ra, bool))
+    np.testing.assert_allclose(gd, rd, atol=1e-9)
+    np.testing.assert_allclose(gp, rp, atol=1e-9)
+    np.testing.assert_allclose(gn, rn, atol=1e-9)
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+@pytest.mark.parametrize("name", sorted(SCENES))
+def test_resting_pair_contact_carries_weight(name, precision):
+    """After settling, each body's reported net contact force, averaged over
+    1 s, equals its own weight (the lower body's ground force minus the load
+    on top), and the stack holds its height."""
+    from paper_2108_10470_b200.params import SimParams
+    models = SCENES[name][0]()
+    E = 4
+    s = _gpu(models, SimParams(dt=1 / 120), E, precision)
+    setup(name, s)
+    z0 = s.pos[:, 2].double().clone()
+    s.step(240)
+    B = s.bodies_per_env
+    acc = torch.zeros(E * B, dtype=torch.float64, device=s.device)
+    for _ in range(120):
+        s.step()
+        acc += s.net_contact[:, 2].double()
+    w = torch.as_tensor(np.tile([sum(l.mass for l in m.links) * G for m in models], E), device=s.device)
+    dyn = s.inv_mass > 0                       # static rails carry no weight of their own
+    assert float(((acc / 120 - w).abs() / w)[dyn].max()) < 0.05, (acc / 120 / w)
+    assert float((s.pos[:, 2].double() - z0).abs().max()) < 0.01
