@@ -265,6 +265,60 @@ def measure(task, E, args, rank, world, clocks=None, policy=False, kernel=True, 
     return out
 
 
+def measure_franka(E, args, rank, world):
+    """Franka cube-stack (BASELINE.json config 4, physics + reward): the
+    authored arm + gripper and two cubes with box / capsule pair contacts
+    (shape_pairs="all"), random PD targets around the home pose, 2 substeps,
+    and the reference franka_stack_reward kernel on the new state per step.
+    There is no reference env for this config: no obs /
+    reset layer."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2108_10470_b200 import models as M
+    from paper_2108_10470_b200 import rewards as RW
+    from paper_2108_10470_b200.params import SimParams
+    from paper_2108_10470_b200.scene import Scene
+    s = Scene([M.franka(), M.cube("cubeA", M.CUBE_A_HALF, 0.3), M.cube("cubeB", M.CUBE_B_HALF, 0.5)], E,
+              SimParams(dt=1 / 120), shape_pairs="all", env_offset=rank * E, total_envs=world * E)
+    B, D = s.bodies_per_env, s.dofs_per_env
+    roots = s.body_q.view(E, B, 13)
+    roots[:, 10, 0:3] = torch.tensor([0.45, 0.0, M.CUBE_A_HALF], dtype=s.dtype)
+    roots[:, 11, 0:3] = torch.tensor([0.45, 0.15, M.CUBE_B_HALF], dtype=s.dtype)
+    home = torch.tensor(M.FRANKA_HOME, dtype=s.dtype, device=s.device).repeat(E)
+    s.dof_state[:, 0] = home
+    s.forward_kinematics()
+    scale = torch.tensor([0.4] * 7 + [0.04, 0.04], dtype=s.dtype, device=s.device).repeat(E)
+    gen = torch.Generator(device=s.device).manual_seed(99 + rank)
+    prm = RW.FrankaStackParams()
+    st = s.body_state.view(E, B, 13)
+
+    def step():
+        s.ctrl_dof_pos_target.copy_(home + scale * (torch.rand(E * D, generator=gen, device=s.device,
+                                                               dtype=s.dtype) * 2 - 1))
+        s.step(2)
+        return RW.franka_stack_reward(st[:, 10, 0:3], st[:, 11, 0:3], st[:, 7, 0:3], st[:, 8, 0:3],
+                                      st[:, 9, 0:3], prm)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        r = step()
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1)], device=s.device, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ok = bool(torch.isfinite(r).all()) and int(s.nonfinite.sum()) == 0
+    s.close()
+    return world * E * args.steps / (float(t.item()) / 1e3), ok
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
@@ -290,6 +344,11 @@ def run_gpu(args):
                 continue
             r = measure(WORKLOADS[name][0], E, a2, rank, world, kernel=False, e2e=False)
             others[name] = {"value": r["value"], "unit": UNIT, "envs_per_gpu": E, "steps": a2.steps}
+        fv, fok = measure_franka(8192, a2, rank, world)
+        others["franka_cube_stack"] = {"value": fv, "unit": UNIT, "envs_per_gpu": 8192, "steps": a2.steps,
+                                       "finite": fok,
+                                       "note": "physics (arm + 2 cubes, box pair contacts) + franka_stack_reward; "
+                                               "no reference env exists for this config"}
         for name in ("ant", "humanoid"):   # PPO-rollout steps: policy inference + env step
             r = measure(WORKLOADS[name][0], E, a2, rank, world, policy=True, kernel=False, e2e=False)
             others[f"{name}_ppo_rollout"] = {"value": r["value"], "unit": UNIT, "envs_per_gpu": E,

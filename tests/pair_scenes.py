@@ -40,6 +40,12 @@ SCENES = {
     # horizontal capsule on a box: 2 PB (capsule ends) + 8 PC (box corners)
     "capsule_on_box": (lambda: [M.free_box((0.2, 0.2, 0.1), 2.0), capsule("b", 0.5, 0.05, 0.1)],
                        [((0, 0, 0.1), (0, 0, 1), 0.0), ((0, 0, 0.2505), (1, 0, 0), np.pi / 2)]),
+    # Franka cube-stack (BASELINE config 4): arm + gripper pads vs two cubes
+    # (4 PB pad-cube slots, 16 PB cube-cube slots), cubes on the ground
+    "franka_cube_stack": (lambda: [M.franka(), M.cube("cubeA", M.CUBE_A_HALF, 0.3),
+                                   M.cube("cubeB", M.CUBE_B_HALF, 0.5)],
+                          [((0, 0, 0), (0, 0, 1), 0.0), ((0.45, 0.0, 0.025), (0, 0, 1), 0.3),
+                           ((0.45, 0.15, 0.035), (0, 0, 1), -0.2)]),
     # sphere cradled between two static horizontal capsule rails: 2 PC slots
     "sphere_in_cradle": (lambda: [capsule("rail_a", 1.0, 0.05, 0.25, fixed=True),
                                   capsule("rail_b", 1.0, 0.05, 0.25, fixed=True), M.free_sphere(0.08, 0.4)],
@@ -57,13 +63,22 @@ def setup(name, s, jitter=0.0, seed=0):
     gpu = hasattr(s, "env_origins_host")       # the CUDA Scene keeps env-local positions
     org = np.zeros((E, 3)) if gpu else s.env_origins
     put = (lambda v: __import__("torch").as_tensor(v, dtype=s.dtype)) if gpu else (lambda v: v)  # noqa: E731
+    roots = [s.actor_body_offset[a] for a in range(len(poses))] if hasattr(s, "actor_body_offset") \
+        else list(s.layout.actor_body_offset)
     for e in range(E):
         for a, (p, ax, ang) in enumerate(poses):
-            s.pos[e * B + a] = put(org[e] + np.asarray(p, float))
-            s.quat[e * B + a] = put(q_axis(ax, ang))
-            if jitter:
-                s.linvel[e * B + a] = put(rng.uniform(-jitter, jitter, 3))
-                s.angvel[e * B + a] = put(rng.uniform(-jitter, jitter, 3))
+            r = e * B + roots[a]
+            s.pos[r] = put(org[e] + np.asarray(p, float))
+            s.quat[r] = put(q_axis(ax, ang))
+            if jitter and name != "franka_cube_stack":
+                s.linvel[r] = put(rng.uniform(-jitter, jitter, 3))
+                s.angvel[r] = put(rng.uniform(-jitter, jitter, 3))
+    if name == "franka_cube_stack":            # arm at its home pose, PD-held
+        home = np.tile(M.FRANKA_HOME, E)
+        s.dof_state[:, 0] = put(home)
+        s.ctrl_dof_pos_target[:] = put(home)
+    if s.dofs_per_env:
+        s.forward_kinematics()
 
 
 STATE = ("pos", "quat", "linvel", "angvel", "_friction_anchor", "nonfinite", "dof_state",
@@ -81,8 +96,11 @@ def oracle_trace(name, E=4, steps=12, warm=30, dt=1 / 120, jitter=0.3):
     p = SimParams(dt=dt)
     s = OracleScene(models, E, p, shape_pairs="all")
     setup(name, s, jitter=jitter)
+    rng = np.random.default_rng(11)
     for _ in range(warm):
         s.step()
+    if s.dofs_per_env:                        # random PD targets around the start pose from here on
+        s.ctrl_dof_pos_target[:] = s.ctrl_dof_pos_target + 0.3 * rng.uniform(-1, 1, s.num_dofs)
     arr = {f"param_{k}": np.array(getattr(s, k)) for k in
            ("inv_mass", "inertia_local", "inv_inertia_local", "gravity", "mu_static", "mu_dynamic",
             "joint_stiffness", "joint_damping", "joint_armature", "joint_friction", "joint_limit_lo",

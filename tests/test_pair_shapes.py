@@ -46,7 +46,9 @@ def test_host_build_matches_oracle(name):
         hk.arr["body_q"][...] = np.concatenate([arr["in_pos"][t] - org[be], arr["in_quat"][t], arr["in_linvel"][t],
                                                 arr["in_angvel"][t]], 1)
         hk.arr["friction_anchor"][...] = arr["in__friction_anchor"][t] - org[None]
-        hk.arr["dof_state"][...] = arr["in_dof_state"][t]
+        for k in ("dof_state", "ctrl_dof_force", "ctrl_dof_pos_target", "ctrl_dof_vel_target", "ctrl_body_force",
+                  "ctrl_body_torque", "dof_mode", "nonfinite"):
+            hk.arr[k][...] = arr[f"in_{k}"][t]
         hk.step()
         for k in ("body_state", "net_contact"):
             assert rel_err(hk.arr[k], arr[f"out_{k}"][t], 1e-8, 1e-8) <= 1, (name, t, k)
