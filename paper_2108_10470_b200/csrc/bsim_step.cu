@@ -492,20 +492,24 @@ int launch_step(const bsim_layout_t *layout, const typename Abi<R>::Params *para
     Ctx<R> c = make_ctx<R>(layout, params, state);
     if (c.d.E == 0) return BSIM_OK;
     size_t smem = step_smem_bytes<R>(c.d);
-    if (smem > 227 * 1024) {
-        g_err = "bsim_step: model too large for the step kernel's shared-memory workspace";
-        return BSIM_E_TOO_LARGE;
-    }
     bsim_actions_t act;
     if (actions) act = *actions; else std::memset(&act, 0, sizeof act);
     cudaStream_t st = (cudaStream_t)stream;
 #ifdef BSIM_LARGE_TU
+    if (smem > 227 * 1024) {
+        g_err = "bsim_step: model too large for the step kernel's shared-memory workspace";
+        return BSIM_E_TOO_LARGE;
+    }
     return launch_step_t<R, TopoGeneric>(c, smem, n_substeps, act, task, st);
 #else
     if (use_large_variant<R>(c.d)) {   // big articulations: 4 envs x 32 threads per CTA
         int rc = call_large(layout, params, state, n_substeps, actions, task, stream);
         if (rc != BSIM_OK) g_err = bsim_large_last_error();
         return rc;
+    }
+    if (smem > 227 * 1024) {
+        g_err = "bsim_step: model too large for the step kernel's shared-memory workspace";
+        return BSIM_E_TOO_LARGE;
     }
     switch (layout->topology_id) {
 #define BSIM_LAUNCH_TOPO(ID, TYPE)                                      \
@@ -618,9 +622,12 @@ int bsim_step_smem_per_env(const bsim_layout_t *layout, int32_t fp64, int32_t *b
                            int32_t *envs_per_cta) {
     if (bad_layout(layout)) return BSIM_E_INVALID;
     Dims d = make_dims(*layout);
-    size_t total = fp64 ? step_smem_bytes<double>(d) : step_smem_bytes<float>(d);
+    const bool large = fp64 ? use_large_variant<double>(d) : use_large_variant<float>(d);
+    // the large-articulation TU's CTA: 4 envs (fp32) / 2 envs (fp64), stride NE + 1
+    const int ne = large ? (fp64 ? 2 : 4) : (fp64 ? Shape<double>::NE : Shape<float>::NE);
+    size_t total = (size_t)d.items * (ne + 1) * (fp64 ? 8 : 4);
     if (bytes_per_env) *bytes_per_env = (int32_t)(d.items * (fp64 ? 8 : 4));
-    if (envs_per_cta) *envs_per_cta = fp64 ? Shape<double>::NE : Shape<float>::NE;
+    if (envs_per_cta) *envs_per_cta = ne;
     return total > 227 * 1024 ? BSIM_E_TOO_LARGE : BSIM_OK;
 }
 

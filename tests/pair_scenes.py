@@ -46,6 +46,11 @@ SCENES = {
                                    M.cube("cubeB", M.CUBE_B_HALF, 0.5)],
                           [((0, 0, 0), (0, 0, 1), 0.0), ((0.45, 0.0, 0.025), (0, 0, 1), 0.3),
                            ((0.45, 0.15, 0.035), (0, 0, 1), -0.2)]),
+    # Shadow Hand (BASELINE config 5): 24-DOF hand with coupling tendons, a
+    # cube on the palm (16 PB palm-cube + 5 PB fingertip-cube slots)
+    "shadow_hand_cube": (lambda: [M.shadow_hand(), M.cube("cube", M.SHADOW_CUBE_HALF, 0.1)],
+                         [(M.SHADOW_HAND_ROOT, (0, 0, 1), 0.0),
+                          ((0.145, 0.0, M.SHADOW_HAND_ROOT[2] + 0.012 + M.SHADOW_CUBE_HALF + 0.001), (0, 0, 1), 0.2)]),
     # sphere cradled between two static horizontal capsule rails: 2 PC slots
     "sphere_in_cradle": (lambda: [capsule("rail_a", 1.0, 0.05, 0.25, fixed=True),
                                   capsule("rail_b", 1.0, 0.05, 0.25, fixed=True), M.free_sphere(0.08, 0.4)],
@@ -70,7 +75,7 @@ def setup(name, s, jitter=0.0, seed=0):
             r = e * B + roots[a]
             s.pos[r] = put(org[e] + np.asarray(p, float))
             s.quat[r] = put(q_axis(ax, ang))
-            if jitter and name != "franka_cube_stack":
+            if jitter and name not in ("franka_cube_stack", "shadow_hand_cube"):
                 s.linvel[r] = put(rng.uniform(-jitter, jitter, 3))
                 s.angvel[r] = put(rng.uniform(-jitter, jitter, 3))
     if name == "franka_cube_stack":            # arm at its home pose, PD-held
