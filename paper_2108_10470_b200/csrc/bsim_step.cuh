@@ -207,21 +207,28 @@ template <class R> BS_HD void body_external(const Ctx<R> &c, const Ws<R> &w, int
 
 // Reduced coordinates of joint j from the pose/velocity in the workspace
 // (physics.py:427-459).  Writes q[k], qd[k] for its 1 or 3 DOFs.
-template <class R> BS_HD int joint_dofs(const Ctx<R> &c, const Ws<R> &w, int j, R *q, R *qd) {
+// REV = every joint of the scene is revolute (a compile-time property of the
+// AOT topology): the joint kind folds to a constant and the other kinds' code
+// leaves the binary (smaller kernel, fewer instruction-cache misses).
+// IDF = every joint frame has identity orientation (origin / child quats):
+// the frame products fold away.
+template <class R, bool REV = false, bool IDF = false>
+BS_HD int joint_dofs(const Ctx<R> &c, const Ws<R> &w, int j, R *q, R *qd) {
     const auto &jt = c.joints[j];
+    const int kind = REV ? (int)BSIM_REVOLUTE : jt.kind;
     const Dims &d = c.d;
     int p = jt.parent, ch = jt.child;
     Q4<R> qp = w.l4(ib(d, p, BQ)), qc = w.l4(ib(d, ch, BQ));
-    Q4<R> jqp = qmul(qp, jq4(jt.origin_quat)), jqc = qmul(qc, jq4(jt.child_quat));
+    Q4<R> jqp = IDF ? qp : qmul(qp, jq4(jt.origin_quat)), jqc = IDF ? qc : qmul(qc, jq4(jt.child_quat));
     V3<R> wp = w.l3(ib(d, p, BW)), wc = w.l3(ib(d, ch, BW));
-    if (jt.kind == BSIM_REVOLUTE) {
+    if (kind == BSIM_REVOLUTE) {
         Q4<R> qr = qmul(qconj(jqp), jqc);
         V3<R> ax = jv3(jt.axis);
         q[0] = wrap_pi(R(2) * r_atan2(dot(qvec(qr), ax), qr.w));
         qd[0] = dot(qrot(jqp, ax), wc - wp);
         return 1;
     }
-    if (jt.kind == BSIM_PRISMATIC) {
+    if (kind == BSIM_PRISMATIC) {
         V3<R> rp = qrot(qp, jv3(jt.origin_pos)), rc = qrot(qc, jv3(jt.child_pos));
         V3<R> sep = (w.l3(ib(d, ch, BP)) - w.l3(ib(d, p, BP))) + (rc - rp);
         V3<R> aw = qrot(jqp, jv3(jt.axis));
@@ -230,7 +237,7 @@ template <class R> BS_HD int joint_dofs(const Ctx<R> &c, const Ws<R> &w, int j, 
         qd[0] = dot(aw, vac - vap);
         return 1;
     }
-    if (jt.kind == BSIM_SPHERICAL) {
+    if (kind == BSIM_SPHERICAL) {
         Q4<R> qr = qmul(qconj(jqp), jqc);
         V3<R> rv = qlog(qr);
         V3<R> wr = qrot(qconj(jqp), wc - wp);
@@ -243,14 +250,15 @@ template <class R> BS_HD int joint_dofs(const Ctx<R> &c, const Ws<R> &w, int j, 
 
 // Anchor arms, errors and axis of joint j (freeze physics.py:660-680,
 // refresh 733-756).  deltas: effective pose (pos + dpos, BQE).
-template <class R>
+template <class R, bool REV = false, bool IDF = false>
 BS_HD void joint_geometry(const Ctx<R> &c, const Ws<R> &w, int j, bool deltas, bool refresh_q0) {
     const Dims &d = c.d;
     const auto &jt = c.joints[j];
+    const int kind = REV ? (int)BSIM_REVOLUTE : jt.kind;
     int p = jt.parent, ch = jt.child;
     const int qitem = deltas ? BQE : BQ;
     Q4<R> qp = w.l4(ib(d, p, qitem)), qc = w.l4(ib(d, ch, qitem));
-    Q4<R> jqp = qmul(qp, jq4(jt.origin_quat)), jqc = qmul(qc, jq4(jt.child_quat));
+    Q4<R> jqp = IDF ? qp : qmul(qp, jq4(jt.origin_quat)), jqc = IDF ? qc : qmul(qc, jq4(jt.child_quat));
     V3<R> rp = qrot(qp, jv3(jt.origin_pos)), rc = qrot(qc, jv3(jt.child_pos));
     // ac - ap with the body-origin difference taken first (env-local)
     V3<R> sep = w.l3(ib(d, ch, BP)) - w.l3(ib(d, p, BP));
@@ -265,10 +273,10 @@ BS_HD void joint_geometry(const Ctx<R> &c, const Ws<R> &w, int j, bool deltas, b
     w.s3(ij(d, j, JRE), qvec(qe) * (R(2) * sg));
     w.s3(ij(d, j, JAX), aw);
     if (refresh_q0 && jt.dof >= 0) {
-        if (jt.kind == BSIM_REVOLUTE) {
+        if (kind == BSIM_REVOLUTE) {
             Q4<R> qr = qmul(qconj(jqp), jqc);
             w.at(ij(d, j, JQ0)) = wrap_pi(R(2) * r_atan2(dot(qvec(qr), jv3(jt.axis)), qr.w));
-        } else if (jt.kind == BSIM_PRISMATIC) {
+        } else if (kind == BSIM_PRISMATIC) {
             w.at(ij(d, j, JQ0)) = dot(aw, perr);
         }
     }
@@ -277,14 +285,14 @@ BS_HD void joint_geometry(const Ctx<R> &c, const Ws<R> &w, int j, bool deltas, b
 // Velocity-independent constants of every row of joint j (needs the current
 // world inverse inertias): the algebra of physics.py:777-928 with everything
 // that does not involve a velocity hoisted out of the serial sweep.
-template <class R> BS_HD void joint_constants(const Ctx<R> &c, const Ws<R> &w, int j) {
+template <class R, bool REV = false> BS_HD void joint_constants(const Ctx<R> &c, const Ws<R> &w, int j) {
     const Dims &d = c.d;
     const auto &jt = c.joints[j];
     int p = jt.parent, ch = jt.child;
     R mp = w.at(ib(d, p, BM)), mc = w.at(ib(d, ch, BM));
     S3<R> Ip = w.lS(ib(d, p, BI)), Ic = w.lS(ib(d, ch, BI));
     V3<R> rp = w.l3(ij(d, j, JRP)), rc = w.l3(ij(d, j, JRC)), a = w.l3(ij(d, j, JAX));
-    const int kind = jt.kind;
+    const int kind = REV ? (int)BSIM_REVOLUTE : jt.kind;
     V3<R> t1, t2;
     tangents(a, t1, t2);
     // linear block: point-3 K^-1 (872-890) or the prismatic perpendicular pair (908-928)
@@ -335,14 +343,15 @@ template <class R> BS_HD void joint_constants(const Ctx<R> &c, const Ws<R> &w, i
 // Per-pass constants of joint j: targets (-perr/h, -rerr/h), the PD drive's
 // affine impulse law, limit activation and bias.  Per-env gains / limits /
 // controls are read from HBM here (L1/L2 resident) instead of being staged.
-template <class R> BS_HD void joint_pass_constants(const Ctx<R> &c, const Ws<R> &w, int e, int j, R h, bool biased) {
+template <class R, bool REV = false>
+BS_HD void joint_pass_constants(const Ctx<R> &c, const Ws<R> &w, int e, int j, R h, bool biased) {
     const Dims &d = c.d;
     const auto &jt = c.joints[j];
     V3<R> pe = w.l3(ij(d, j, JPE)), re = w.l3(ij(d, j, JRE));
     const R nih = -r_rcp(h);
     w.s3(ij(d, j, JPE), biased ? pe * nih : zero3<R>());   // 881
     w.s3(ij(d, j, JRE), biased ? re * nih : zero3<R>());   // 898
-    if (jt.dof < 0 || jt.kind == BSIM_SPHERICAL) return;
+    if (jt.dof < 0 || (!REV && jt.kind == BSIM_SPHERICAL)) return;
     const size_t pj = (size_t)j * d.E + e, pd = (size_t)e * d.D + jt.dof;
     const R meff = w.at(ij(d, j, JMEFF));
     if (biased) {  // drive (812-848): lam = LF + clip(DA - DB qd, +-mf h) [+ friction]
@@ -997,7 +1006,20 @@ template <class R> BS_HD void apply_tendons(const Ctx<R> &c, const Ws<R> &w, int
     }
 }
 
-// ====================================================== the group step
+// compile-time properties of an AOT topology (the generic kernel: none)
+template <class T> constexpr bool topo_rev() {
+    if constexpr (T::is_static) return T::all_revolute; else return false;
+}
+template <class T> constexpr bool topo_idf() {
+    if constexpr (T::is_static) return T::identity_frames; else return false;
+}
+template <class T> constexpr bool topo_pairs() {
+    if constexpr (T::is_static) return T::Q > 0; else return true;
+}
+template <class T> constexpr bool topo_tendons() {
+    if constexpr (T::is_static) return T::has_tendons; else return true;
+}
+
 // ====================================================== the group step
 // Loops over (env, item) pairs distributed over the CTA's threads; on the
 // host (tid 0 of 1) they degenerate to plain sequential loops.
@@ -1029,7 +1051,7 @@ template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> 
         w.s3(ib(d, b, BDA), zero3<R>());
     }
     BS_SYNC();
-    if (d.T) {
+    if (topo_tendons<T>() && d.T) {
         BS_ENVS(g, el) { apply_tendons(c, g.env(el), g.e0 + el); }
         BS_SYNC();
     }
@@ -1071,16 +1093,16 @@ template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> 
             Ws<R> w = g.env(el);
             if (freeze) {  // read_dof_states (557): q0 and the unbiased limit rows' q
                 R q[3], qd[3];
-                int n = joint_dofs(c, w, j, q, qd);
+                int n = joint_dofs<R, topo_rev<T>(), topo_idf<T>()>(c, w, j, q, qd);
                 for (int kk = 0; kk < n; ++kk) {
                     w.at(idf(d, c.joints[j].dof + kk, DQ0)) = q[kk];
                     w.at(idf(d, c.joints[j].dof + kk, DIMP)) = R(0);
                 }
                 if (n == 1) w.at(ij(d, j, JQ0)) = q[0];
             }
-            joint_geometry(c, w, j, deltas, !freeze);
-            joint_constants(c, w, j);
-            joint_pass_constants(c, w, g.e0 + el, j, h, biased);
+            joint_geometry<R, topo_rev<T>(), topo_idf<T>()>(c, w, j, deltas, !freeze);
+            joint_constants<R, topo_rev<T>()>(c, w, j);
+            joint_pass_constants<R, topo_rev<T>()>(c, w, g.e0 + el, j, h, biased);
         }
         BS_ITEMS(g, d.P, el, i) {
             Ws<R> w = g.env(el);
@@ -1088,11 +1110,13 @@ template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> 
             plane_constants(c, w, i);
             plane_pass_constants(c, w, i, biased);
         }
-        BS_ITEMS(g, d.Q, el, i) {
-            Ws<R> w = g.env(el);
-            if (freeze) pair_freeze(c, w, g.e0 + el, i);
-            pair_constants(c, w, i);
-            pair_pass_constants(c, w, i, biased);
+        if (topo_pairs<T>()) {
+            BS_ITEMS(g, d.Q, el, i) {
+                Ws<R> w = g.env(el);
+                if (freeze) pair_freeze(c, w, g.e0 + el, i);
+                pair_constants(c, w, i);
+                pair_pass_constants(c, w, i, biased);
+            }
         }
         BS_SYNC();
 #ifdef BSIM_EXP_SKIP_A
