@@ -51,7 +51,7 @@ int check_launch(const char *what) {
 }
 
 template <class R> size_t step_smem_bytes(const Dims &d) {
-    return (size_t)d.items * Shape<R>::STR * sizeof(R);
+    return (size_t)d.pad * Shape<R>::NE * sizeof(R);
 }
 
 // ------------------------------------------------------------------ step
@@ -114,7 +114,7 @@ template <class R, class T>
 __global__ void __launch_bounds__(Shape<R>::NTH, BSIM_MINB)
     step_kernel(const __grid_constant__ Ctx<R> c, int n_substeps, bsim_actions_t act, int epc,
                 const __grid_constant__ bsim_task_t task, int with_task) {
-    constexpr int NTH = Shape<R>::NTH, STR = Shape<R>::STR;
+    constexpr int NTH = Shape<R>::NTH;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const Dims &d = c.d;
     R *ws = reinterpret_cast<R *>(smem_raw);
@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(Shape<R>::NTH, BSIM_MINB)
         for (int i = tid; i < ne * per_env; i += NTH) {
             int el = i / per_env, item = i - el * per_env;
             int b = item / 13, k = item - b * 13;
-            ws[(d.o_body + b * BODY_ITEMS + k) * STR + el] = src[i];
+            ws[(size_t)el * d.pad + d.o_body + b * BODY_ITEMS + body_item13(k)] = src[i];
         }
     }
     __syncthreads();
@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(Shape<R>::NTH, BSIM_MINB)
         s_sweep_warp = w;
     }
     __syncthreads();
-    const Grp<R> g{ws, e0, ne, tid, NTH, 32 * s_sweep_warp};
+    const Grp<R> g{ws, e0, ne, tid, NTH, 32 * s_sweep_warp, d.pad};
     stage_group(c, g);
     if (act.actions) {  // fused action mapping (envs.py:180, 421-424)
         BS_ITEMS(g, d.D, el, k) {
@@ -168,7 +168,8 @@ __global__ void __launch_bounds__(Shape<R>::NTH, BSIM_MINB)
     readout_group(c, g);
     BS_ITEMS(g, d.P, el, i) {
         for (int k = 0; k < 3; ++k)
-            c.s.friction_anchor[3 * ((size_t)i * d.E + e0 + el) + k] = g.env(el).at(d.o_anchor + 3 * i + k);
+            c.s.friction_anchor[3 * ((size_t)i * d.E + e0 + el) + k] =
+                g.env(el).at(d.o_anchor + ANCHOR_ITEMS * i + k);
     }
     __syncthreads();
     // coalesced stores: canonical env-local state, world-frame body_state / root_state
@@ -178,7 +179,7 @@ __global__ void __launch_bounds__(Shape<R>::NTH, BSIM_MINB)
         for (int i = tid; i < ne * per_env; i += NTH) {
             int el = i / per_env, item = i - el * per_env;
             int b = item / 13, k = item - b * 13;
-            R x = ws[(d.o_body + b * BODY_ITEMS + k) * STR + el];
+            R x = ws[(size_t)el * d.pad + d.o_body + b * BODY_ITEMS + body_item13(k)];
             dq[i] = x;
             db[i] = k < 3 ? x + c.s.env_origins[3 * (size_t)(e0 + el) + k] : x;
         }
@@ -188,7 +189,7 @@ __global__ void __launch_bounds__(Shape<R>::NTH, BSIM_MINB)
             int el = i / per_root, item = i - el * per_root;
             int a = item / 13, k = item - a * 13;
             int b = c.L.actor_body_offset[a];
-            R x = ws[(d.o_body + b * BODY_ITEMS + k) * STR + el];
+            R x = ws[(size_t)el * d.pad + d.o_body + b * BODY_ITEMS + body_item13(k)];
             dr[i] = k < 3 ? x + c.s.env_origins[3 * (size_t)(e0 + el) + k] : x;
         }
     }
@@ -405,7 +406,7 @@ Ctx<R> make_ctx(const bsim_layout_t *L, const typename Abi<R>::Params *p, const 
     c.L = *L;
     if (p) c.p = *p; else std::memset(&c.p, 0, sizeof c.p);
     c.s = *s;
-    c.d = make_dims(*L);
+    c.d = make_dims(*L, sizeof(R) == 8);
     c.joints = reinterpret_cast<const typename Abi<R>::Joint *>(L->joints);
     return c;
 }
@@ -621,12 +622,12 @@ const char *bsim_last_error(void) { return g_err.c_str(); }
 int bsim_step_smem_per_env(const bsim_layout_t *layout, int32_t fp64, int32_t *bytes_per_env,
                            int32_t *envs_per_cta) {
     if (bad_layout(layout)) return BSIM_E_INVALID;
-    Dims d = make_dims(*layout);
+    Dims d = make_dims(*layout, fp64 != 0);
     const bool large = fp64 ? use_large_variant<double>(d) : use_large_variant<float>(d);
-    // the large-articulation TU's CTA: 4 envs (fp32) / 2 envs (fp64), stride NE + 1
+    // the large-articulation TU's CTA: 4 envs (fp32) / 2 envs (fp64)
     const int ne = large ? (fp64 ? 2 : 4) : (fp64 ? Shape<double>::NE : Shape<float>::NE);
-    size_t total = (size_t)d.items * (ne + 1) * (fp64 ? 8 : 4);
-    if (bytes_per_env) *bytes_per_env = (int32_t)(d.items * (fp64 ? 8 : 4));
+    size_t total = (size_t)d.pad * ne * (fp64 ? 8 : 4);
+    if (bytes_per_env) *bytes_per_env = (int32_t)(d.pad * (fp64 ? 8 : 4));
     if (envs_per_cta) *envs_per_cta = ne;
     return total > 227 * 1024 ? BSIM_E_TOO_LARGE : BSIM_OK;
 }

@@ -49,8 +49,8 @@ template <> struct Abi<double> {
     using State = bsim_state64_t;
 };
 
-// CTA shape of the step kernel: NE environments, NTH threads; the workspace
-// stride STR = NE + 1 is odd.
+// CTA shape of the step kernel: NE environments, NTH threads; the envs'
+// workspace records are PAD words apart (make_dims).
 template <class R> struct Shape;
 #ifndef BSIM_NE32
 #define BSIM_NE32 16
@@ -59,7 +59,7 @@ template <class R> struct Shape;
 #define BSIM_NTH32 128
 #endif
 template <> struct Shape<float> {
-    static constexpr int NE = BSIM_NE32, NTH = BSIM_NTH32, STR = NE + 1;
+    static constexpr int NE = BSIM_NE32, NTH = BSIM_NTH32;
 };
 #ifndef BSIM_NE64
 #define BSIM_NE64 8
@@ -68,50 +68,64 @@ template <> struct Shape<float> {
 #define BSIM_NTH64 64
 #endif
 template <> struct Shape<double> {
-    static constexpr int NE = BSIM_NE64, NTH = BSIM_NTH64, STR = NE + 1;
+    static constexpr int NE = BSIM_NE64, NTH = BSIM_NTH64;
 };
 
 // ---------------------------------------------------------------- items
-// per body: pose, velocity, TGS deltas, world inverse inertia (sym), inverse
-// mass, effective orientation scratch
-enum { BP = 0, BQ = 3, BV_ = 7, BW = 10, BDP = 13, BDA = 16, BI = 19, BM = 25, BQE = 26, BODY_ITEMS = 30 };
+// Per-env workspace items.  v8 layout: ENV-MAJOR records (one env's items are
+// contiguous, envs PAD words apart) with every vector field 16-byte aligned,
+// so a 3-vector / quaternion / symmetric 3x3 moves with one or two 128 / 64-bit
+// shared-memory accesses (LDS.128 / STS.64) instead of 3-6 scalar ones.  PAD
+// is = 4 (mod 8) words for fp32: the 8 lanes of each quarter-warp phase of a
+// 128-bit access hit distinct 16-byte bank groups; odd for fp64 (scalar).
+// Scalars live in the spare .w slots of the 3-vectors.
+//
+// per body: pose (+ inverse mass), velocity, TGS deltas, world inverse
+// inertia (sym), effective orientation scratch
+enum { BP = 0, BM = 3, BQ = 4, BV_ = 8, BW = 12, BDP = 16, BDA = 20, BI = 24, BQE = 32, BODY_ITEMS = 36 };
 // per joint: geometry and the row constants of phase A
 enum {
-    JRP = 0, JRC = 3,     // anchor arms (parent / child)
-    JPE = 6,              // perr0 after geometry; the linear target -perr0/h after pass constants
-    JRE = 9,              // rerr0 after geometry; the angular target -rerr0/h after pass constants
-    JAX = 12, JQ0 = 15,   // world joint axis, joint coordinate q0
-    JKI = 16,             // point-3: K^-1 ; prismatic-perp: T^T K^-1 T            (sym, 6)
-    JG = 22,              // angular rows: T^T (T Isum T^T)^-1 T                   (sym, 6)
-    JY1 = 28, JY2 = 31,   // axis rows: I_c x1 / I_p x2 per unit impulse
-    JMEFF = 34,
-    // per-pass constants of the drive / limit rows (so the sweep divides nothing)
-    JDA = 35, JDB = 36,   // PD impulse = DA - DB * qd  (812-848, implicit discretisation)
-    JLF = 37,             // direct-actuation impulse (FORCE mode)
-    JFRH = 38,            // joint friction bound fr * h (0 = off)
-    JLV = 39,             // limit state this pass: 0 none, 1 below lo, 2 above hi
-    JLB = 40,             // limit bias velocity this pass
-    JOINT_ITEMS = 41
+    JRP = 0, JQ0 = 3,     // parent anchor arm | joint coordinate q0
+    JRC = 4, JMEFF = 7,   // child anchor arm  | axis-row effective mass
+    JPE = 8, JDA = 11,    // perr0 after geometry, the linear target -perr0/h after pass constants |
+                          // PD impulse = DA - DB * qd  (812-848, implicit discretisation)
+    JRE = 12, JDB = 15,   // rerr0 after geometry, the angular target -rerr0/h after pass constants
+    JAX = 16, JLF = 19,   // world joint axis | direct-actuation impulse (FORCE mode)
+    JKI = 20,             // point-3: K^-1 ; prismatic-perp: T^T K^-1 T            (sym, 6)
+    JFRH = 26,            // joint friction bound fr * h (0 = off)
+    JLV = 27,             // limit state this pass: 0 none, 1 below lo, 2 above hi
+    JG = 28,              // angular rows: T^T (T Isum T^T)^-1 T                   (sym, 6)
+    JLB = 34,             // limit bias velocity this pass
+    JY1 = 36, JY2 = 40,   // axis rows: I_c x1 / I_p x2 per unit impulse
+    JOINT_ITEMS = 44
 };
 // per plane contact slot (normal z, tangents (0,-1,0) and (1,0,0): every
 // jacobian is a permutation of the arm r, so only r is stored)
-enum { CR = 0, CD0 = 3, CREST = 4, CLN = 5, CLT = 6, CTE = 8, CACT = 10, CIXN = 11, CIX1 = 14, CIX2 = 17,
-       CMN = 20, CM1 = 21, CM2 = 22, CTGT = 23, CST1 = 24, CST2 = 25, PLANE_ITEMS = 26 };
-// per sphere-sphere pair slot
-enum { QR = 0, QRA = 3, QN = 6, QT1 = 9, QT2 = 12, QD0 = 15, QREST = 16, QLN = 17, QLT = 18, QACT = 20,
-       QPT = 21, QXN = 24, QX1 = 27, QX2 = 30, QYN = 33, QY1 = 36, QY2 = 39, QIXN = 42, QIX1 = 45,
-       QIX2 = 48, QIYN = 51, QIY1 = 54, QIY2 = 57, QMN = 60, QM1 = 61, QM2 = 62, QTGT = 63, PAIR_ITEMS = 64 };
+enum { CR = 0, CACT = 3, CIXN = 4, CMN = 7, CIX1 = 8, CM1 = 11, CIX2 = 12, CM2 = 15, CLN = 16, CLT = 17,
+       CTGT = 19, CST1 = 20, CST2 = 21, CD0 = 22, CREST = 23, CTE = 24, PLANE_ITEMS = 28 };
+// per pair slot
+enum { QR = 0, QD0 = 3, QRA = 4, QREST = 7, QN = 8, QLN = 11, QT1 = 12, QACT = 15, QT2 = 16, QMN = 19,
+       QPT = 20, QM1 = 23, QXN = 24, QM2 = 27, QX1 = 28, QTGT = 31, QX2 = 32, QYN = 36, QY1 = 40, QY2 = 44,
+       QIXN = 48, QIX1 = 52, QIX2 = 56, QIYN = 60, QIY1 = 64, QIY2 = 68, QLT = 72, PAIR_ITEMS = 76 };
 // per dof: impulse accumulator, start-of-step readout
 enum { DIMP = 0, DQ0 = 1, DOF_ITEMS = 2 };
 // per env
-enum { EMUS = 0, EMUD = 1, EGX = 2, EGY = 3, EGZ = 4, EBAD = 5, ENV_ITEMS = 6 };
+enum { EMUS = 0, EMUD = 1, EGX = 2, EGY = 3, EGZ = 4, EBAD = 5, ENV_ITEMS = 8 };
+// per friction anchor (xyz + pad)
+enum { ANCHOR_ITEMS = 4 };
+
+// canonical 13-float body row (pos3 quat4 linvel3 angvel3) -> body item
+BS_HD int body_item13(int k) { return k < 3 ? BP + k : (k < 7 ? BQ + k - 3 : (k < 10 ? BV_ + k - 7 : BW + k - 10)); }
 
 struct Dims {
     int E, A, B, D, J, P, Q, S, T;
-    int o_body, o_joint, o_plane, o_pair, o_anchor, o_dof, o_env, items;
+    int o_body, o_joint, o_plane, o_pair, o_anchor, o_dof, o_env, items, pad;
 };
 
-BS_HD Dims make_dims(const bsim_layout_t &L) {
+BS_HD int round4(int x) { return (x + 3) & ~3; }
+
+// pad_mod8: fp32 -> PAD = 4 (mod 8); fp64 -> PAD odd
+BS_HD Dims make_dims(const bsim_layout_t &L, bool fp64 = false) {
     Dims d;
     d.E = L.num_envs; d.A = L.actors_per_env; d.B = L.bodies_per_env; d.D = L.dofs_per_env;
     d.J = L.joints_per_env; d.P = L.planes_per_env; d.Q = L.pairs_per_env;
@@ -121,16 +135,24 @@ BS_HD Dims make_dims(const bsim_layout_t &L) {
     d.o_plane = d.o_joint + JOINT_ITEMS * d.J;
     d.o_pair = d.o_plane + PLANE_ITEMS * d.P;
     d.o_anchor = d.o_pair + PAIR_ITEMS * d.Q;
-    d.o_dof = d.o_anchor + 3 * d.P;
-    d.o_env = d.o_dof + DOF_ITEMS * d.D;
+    d.o_dof = d.o_anchor + ANCHOR_ITEMS * d.P;
+    d.o_env = round4(d.o_dof + DOF_ITEMS * d.D);
     d.items = d.o_env + ENV_ITEMS;
+    if (fp64) {
+        d.pad = d.items | 1;
+    } else {
+        d.pad = d.items;
+        while ((d.pad & 7) != 4) ++d.pad;
+    }
     return d;
 }
 
-// One env's column of the shared workspace (compile-time stride).
+// One env's record of the shared workspace.  Vector accessors use 128 / 64-bit
+// shared-memory accesses on the fp32 device path (every vector item offset is
+// a multiple of 4 and the record base is 16-byte aligned: PAD = 4 mod 8).
 template <class R> struct Ws {
     R *base;
-    BS_HD R &at(int i) const { return base[i * Shape<R>::STR]; }
+    BS_HD R &at(int i) const { return base[i]; }
     BS_HD V3<R> l3(int i) const { return V3<R>{at(i), at(i + 1), at(i + 2)}; }
     BS_HD void s3(int i, V3<R> v) const { at(i) = v.x; at(i + 1) = v.y; at(i + 2) = v.z; }
     BS_HD Q4<R> l4(int i) const { return Q4<R>{at(i), at(i + 1), at(i + 2), at(i + 3)}; }
@@ -140,6 +162,36 @@ template <class R> struct Ws {
         at(i) = m.xx; at(i + 1) = m.xy; at(i + 2) = m.xz; at(i + 3) = m.yy; at(i + 4) = m.yz; at(i + 5) = m.zz;
     }
 };
+#if defined(__CUDA_ARCH__)
+template <> struct Ws<float> {
+    float *base;
+    __device__ __forceinline__ float &at(int i) const { return base[i]; }
+    __device__ __forceinline__ V3<float> l3(int i) const {
+        float4 v = *reinterpret_cast<const float4 *>(base + i);
+        return V3<float>{v.x, v.y, v.z};
+    }
+    __device__ __forceinline__ void s3(int i, V3<float> v) const {
+        *reinterpret_cast<float2 *>(base + i) = make_float2(v.x, v.y);
+        base[i + 2] = v.z;
+    }
+    __device__ __forceinline__ Q4<float> l4(int i) const {
+        float4 v = *reinterpret_cast<const float4 *>(base + i);
+        return Q4<float>{v.x, v.y, v.z, v.w};
+    }
+    __device__ __forceinline__ void s4(int i, Q4<float> q) const {
+        *reinterpret_cast<float4 *>(base + i) = make_float4(q.x, q.y, q.z, q.w);
+    }
+    __device__ __forceinline__ S3<float> lS(int i) const {
+        float4 a = *reinterpret_cast<const float4 *>(base + i);
+        float2 b = *reinterpret_cast<const float2 *>(base + i + 4);
+        return S3<float>{a.x, a.y, a.z, a.w, b.x, b.y};
+    }
+    __device__ __forceinline__ void sS(int i, const S3<float> &m) const {
+        *reinterpret_cast<float4 *>(base + i) = make_float4(m.xx, m.xy, m.xz, m.yy);
+        *reinterpret_cast<float2 *>(base + i + 4) = make_float2(m.yz, m.zz);
+    }
+};
+#endif
 
 template <class R> struct Ctx {
     using Joint = typename Abi<R>::Joint;
@@ -168,8 +220,8 @@ template <class R> BS_HD Q4<R> jq4(const R *a) { return Q4<R>{a[0], a[1], a[2], 
 // per-env serial work (the sweep) runs on threads [lane0, lane0 + ne).
 template <class R> struct Grp {
     R *ws;
-    int e0, ne, tid, nth, lane0;
-    BS_HD Ws<R> env(int el) const { return Ws<R>{ws + el}; }
+    int e0, ne, tid, nth, lane0, pad;
+    BS_HD Ws<R> env(int el) const { return Ws<R>{ws + (size_t)el * pad}; }
 };
 
 // ====================================================== phase A pieces
@@ -408,7 +460,7 @@ template <class R> BS_HD void plane_freeze(const Ctx<R> &c, const Ws<R> &w, int 
     R depth = p.rest_offset - gap;
     V3<R> r = v3(arm.x, arm.y, arm.z - rad);
     V3<R> point = pos + r;
-    const int an = d.o_anchor + 3 * i;
+    const int an = d.o_anchor + ANCHOR_ITEMS * i;
     R ax = w.at(an), ay = w.at(an + 1);
     bool has = !(ax != ax);
     w.at(ipl(d, i, CTE)) = has ? point.x - ax : R(0);
@@ -1195,7 +1247,7 @@ template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> 
     BS_ITEMS(g, d.B, el, b) {
         Ws<R> w = g.env(el);
         bool ok = true;
-        for (int k = 0; k < 13; ++k) ok = ok && finite_r(w.at(ib(d, b, BP) + k));
+        for (int k = 0; k < 13; ++k) ok = ok && finite_r(w.at(ib(d, b, body_item13(k))));
         if (!ok) w.at(d.o_env + EBAD) = R(1);
     }
     BS_SYNC();
@@ -1205,7 +1257,7 @@ template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> 
             int e = g.e0 + el;
             if (b == 0) c.s.nonfinite[e] = 1;
             for (int k = 0; k < 13; ++k) {
-                R &x = w.at(ib(d, b, BP) + k);
+                R &x = w.at(ib(d, b, body_item13(k)));
                 // the reference zeroes the WORLD position (physics.py:1081)
                 if (!finite_r(x)) x = k < 3 ? -c.s.env_origins[3 * (size_t)e + k] : R(0);
             }
@@ -1241,7 +1293,7 @@ template <class R> BS_HD void stage_group(const Ctx<R> &c, const Grp<R> &g) {
     BS_ITEMS(g, d.B, el, b) { g.env(el).at(ib(d, b, BM)) = c.s.inv_mass[(size_t)(g.e0 + el) * d.B + b]; }
     BS_ITEMS(g, d.P, el, i) {
         for (int k = 0; k < 3; ++k)
-            g.env(el).at(d.o_anchor + 3 * i + k) = c.s.friction_anchor[3 * ((size_t)i * d.E + g.e0 + el) + k];
+            g.env(el).at(d.o_anchor + ANCHOR_ITEMS * i + k) = c.s.friction_anchor[3 * ((size_t)i * d.E + g.e0 + el) + k];
     }
 }
 

@@ -18,21 +18,21 @@ static void run_t(const bsim_layout_t *L, const typename Abi<R>::Params *p, cons
     c.L = *L;
     c.p = *p;
     c.s = *s;
-    c.d = make_dims(*L);
+    c.d = make_dims(*L, sizeof(R) == 8);
     c.joints = reinterpret_cast<const typename Abi<R>::Joint *>(L->joints);
     const Dims &d = c.d;
     // the batch in CTA-sized groups of Shape<R>::NE envs, one "thread" each
-    constexpr int NE = Shape<R>::NE, STR = Shape<R>::STR;
+    constexpr int NE = Shape<R>::NE;
     const int E = d.E;
-    std::vector<R> buf((size_t)d.items * STR);
+    std::vector<R> buf((size_t)d.pad * NE);
     for (int e0 = 0; e0 < E; e0 += NE) {
         const int ne = E - e0 < NE ? E - e0 : NE;
         std::fill(buf.begin(), buf.end(), R(1e30));   // poison: catches unstaged reads
-        Grp<R> g{buf.data(), e0, ne, 0, 1, 0};
+        Grp<R> g{buf.data(), e0, ne, 0, 1, 0, d.pad};
         for (int el = 0; el < ne; ++el)
             for (int b = 0; b < d.B; ++b)
                 for (int k = 0; k < 13; ++k)
-                    g.env(el).at(ib(d, b, BP) + k) = s->body_q[13 * ((size_t)(e0 + el) * d.B + b) + k];
+                    g.env(el).at(ib(d, b, body_item13(k))) = s->body_q[13 * ((size_t)(e0 + el) * d.B + b) + k];
         stage_group(c, g);
         for (int st = 0; st < n_substeps; ++st) {
             group_step<R, T>(c, g, st == n_substeps - 1);
@@ -44,10 +44,10 @@ static void run_t(const bsim_layout_t *L, const typename Abi<R>::Params *p, cons
             Ws<R> w = g.env(el);
             for (int i = 0; i < d.P; ++i)
                 for (int k = 0; k < 3; ++k)
-                    s->friction_anchor[3 * ((size_t)i * E + e) + k] = w.at(d.o_anchor + 3 * i + k);
+                    s->friction_anchor[3 * ((size_t)i * E + e) + k] = w.at(d.o_anchor + ANCHOR_ITEMS * i + k);
             for (int b = 0; b < d.B; ++b)
                 for (int k = 0; k < 13; ++k) {
-                    R x = w.at(ib(d, b, BP) + k);
+                    R x = w.at(ib(d, b, body_item13(k)));
                     s->body_q[13 * ((size_t)e * d.B + b) + k] = x;
                     s->body_state[13 * ((size_t)e * d.B + b) + k] = k < 3 ? x + s->env_origins[3 * e + k] : x;
                 }
