@@ -85,7 +85,7 @@ template <> struct Shape<double> {
 enum { BP = 0, BM = 3, BQ = 4, BV_ = 8, BW = 12, BDP = 16, BDA = 20, BI = 24, BQE = 32, BODY_ITEMS = 36 };
 // per joint: geometry and the row constants of phase A
 enum {
-    JRP = 0, JQ0 = 3,     // parent anchor arm | joint coordinate q0
+    JRP = 0,              // parent anchor arm (.w unused: q0 lives in registers)
     JRC = 4, JMEFF = 7,   // child anchor arm  | axis-row effective mass
     JPE = 8, JDA = 11,    // perr0 after geometry, the linear target -perr0/h after pass constants |
                           // PD impulse = DA - DB * qd  (812-848, implicit discretisation)
@@ -300,14 +300,34 @@ BS_HD int joint_dofs(const Ctx<R> &c, const Ws<R> &w, int j, R *q, R *qd) {
     return 0;
 }
 
-// Anchor arms, errors and axis of joint j (freeze physics.py:660-680,
-// refresh 733-756).  deltas: effective pose (pos + dpos, BQE).
+// Phase A of joint j for one pass, fused: geometry (freeze physics.py:660-680,
+// refresh 733-756; `deltas`: the effective pose pos + dpos / BQE), the
+// velocity-independent row constants (the algebra of physics.py:777-928 with
+// everything that does not involve a velocity hoisted out of the serial
+// sweep), and the per-pass constants (targets -perr/h, -rerr/h, the PD
+// drive's affine impulse law, limit activation and bias).  Everything stays
+// in registers and leaves as eleven whole 16-byte record groups (one STS.128
+// each on the fp32 device path).  At freeze the reduced coordinates
+// (read_dof_states, physics.py:557) seed q0, the unbiased limit rows' q and
+// the DOF impulse accumulators.  Per-env gains / limits / controls are read
+// from HBM (L1/L2 resident).
 template <class R, bool REV = false, bool IDF = false>
-BS_HD void joint_geometry(const Ctx<R> &c, const Ws<R> &w, int j, bool deltas, bool refresh_q0) {
+BS_HD void joint_item(const Ctx<R> &c, const Ws<R> &w, int e, int j, R h, bool biased, bool freeze, bool deltas) {
     const Dims &d = c.d;
     const auto &jt = c.joints[j];
     const int kind = REV ? (int)BSIM_REVOLUTE : jt.kind;
-    int p = jt.parent, ch = jt.child;
+    const int p = jt.parent, ch = jt.child;
+    R q0 = R(0);
+    if (freeze) {
+        R q[3], qd[3];
+        int n = joint_dofs<R, REV, IDF>(c, w, j, q, qd);
+        for (int kk = 0; kk < n; ++kk) {
+            w.at(idf(d, jt.dof + kk, DQ0)) = q[kk];
+            w.at(idf(d, jt.dof + kk, DIMP)) = R(0);
+        }
+        if (n == 1) q0 = q[0];
+    }
+    // ---- geometry
     const int qitem = deltas ? BQE : BQ;
     Q4<R> qp = w.l4(ib(d, p, qitem)), qc = w.l4(ib(d, ch, qitem));
     Q4<R> jqp = IDF ? qp : qmul(qp, jq4(jt.origin_quat)), jqc = IDF ? qc : qmul(qc, jq4(jt.child_quat));
@@ -317,64 +337,51 @@ BS_HD void joint_geometry(const Ctx<R> &c, const Ws<R> &w, int j, bool deltas, b
     if (deltas) sep = (w.l3(ib(d, ch, BP)) + w.l3(ib(d, ch, BDP))) - (w.l3(ib(d, p, BP)) + w.l3(ib(d, p, BDP)));
     V3<R> perr = sep + (rc - rp);
     Q4<R> qe = qmul(jqc, qconj(jqp));
-    R sg = signr(qe.w);
-    V3<R> aw = qrot(jqp, jv3(jt.axis));
-    w.s3(ij(d, j, JRP), rp);
-    w.s3(ij(d, j, JRC), rc);
-    w.s3(ij(d, j, JPE), perr);
-    w.s3(ij(d, j, JRE), qvec(qe) * (R(2) * sg));
-    w.s3(ij(d, j, JAX), aw);
-    if (refresh_q0 && jt.dof >= 0) {
+    V3<R> rerr = qvec(qe) * (R(2) * signr(qe.w));
+    V3<R> a = qrot(jqp, jv3(jt.axis));
+    if (!freeze && jt.dof >= 0) {
         if (kind == BSIM_REVOLUTE) {
             Q4<R> qr = qmul(qconj(jqp), jqc);
-            w.at(ij(d, j, JQ0)) = wrap_pi(R(2) * r_atan2(dot(qvec(qr), jv3(jt.axis)), qr.w));
+            q0 = wrap_pi(R(2) * r_atan2(dot(qvec(qr), jv3(jt.axis)), qr.w));
         } else if (kind == BSIM_PRISMATIC) {
-            w.at(ij(d, j, JQ0)) = dot(aw, perr);
+            q0 = dot(a, perr);
         }
     }
-}
-
-// Velocity-independent constants of every row of joint j (needs the current
-// world inverse inertias): the algebra of physics.py:777-928 with everything
-// that does not involve a velocity hoisted out of the serial sweep.
-template <class R, bool REV = false> BS_HD void joint_constants(const Ctx<R> &c, const Ws<R> &w, int j) {
-    const Dims &d = c.d;
-    const auto &jt = c.joints[j];
-    int p = jt.parent, ch = jt.child;
+    // ---- row constants from the current world inverse inertias
     R mp = w.at(ib(d, p, BM)), mc = w.at(ib(d, ch, BM));
     S3<R> Ip = w.lS(ib(d, p, BI)), Ic = w.lS(ib(d, ch, BI));
-    V3<R> rp = w.l3(ij(d, j, JRP)), rc = w.l3(ij(d, j, JRC)), a = w.l3(ij(d, j, JAX));
-    const int kind = REV ? (int)BSIM_REVOLUTE : jt.kind;
     V3<R> t1, t2;
     tangents(a, t1, t2);
-    // linear block: point-3 K^-1 (872-890) or the prismatic perpendicular pair (908-928)
-    if (kind != BSIM_PRISMATIC) {
+    S3<R> KI, G{R(0), R(0), R(0), R(0), R(0), R(0)};
+    if (kind != BSIM_PRISMATIC) {   // point-3 K^-1 (872-890)
         R m = mp + mc;
         S3<R> K{m, R(0), R(0), m, R(0), m};
         add_rIr(K, rp, Ip);
         add_rIr(K, rc, Ic);
-        w.sS(ij(d, j, JKI), sinv(K));
-    } else {
+        KI = sinv(K);
+    } else {                        // prismatic perpendicular pair (908-928)
         R m = mp + mc;
         V3<R> p1 = cross(rp, t1), p2 = cross(rp, t2), c1 = cross(rc, t1), c2 = cross(rc, t2);
         V3<R> Ip1 = smul(Ip, p1), Ip2 = smul(Ip, p2), Ic1 = smul(Ic, c1), Ic2 = smul(Ic, c2);
         R k00 = dot(t1, t1) * m + dot(p1, Ip1) + dot(c1, Ic1);
         R k01 = dot(t1, t2) * m + dot(p1, Ip2) + dot(c1, Ic2);
         R k11 = dot(t2, t2) * m + dot(p2, Ip2) + dot(c2, Ic2);
-        w.sS(ij(d, j, JKI), proj2(t1, t2, k00, k01, k11));
+        KI = proj2(t1, t2, k00, k01, k11);
     }
-    // angular block (892-906): G = T^T (T Isum T^T)^-1 T
-    if (kind != BSIM_SPHERICAL) {
+    if (kind != BSIM_SPHERICAL) {   // angular block (892-906): G = T^T (T Isum T^T)^-1 T
         S3<R> Isum = sadd(Ip, Ic);
         if (kind == BSIM_REVOLUTE) {
             V3<R> i1 = smul(Isum, t1), i2 = smul(Isum, t2);
-            w.sS(ij(d, j, JG), proj2(t1, t2, dot(t1, i1), dot(t1, i2), dot(t2, i2)));
+            G = proj2(t1, t2, dot(t1, i1), dot(t1, i2), dot(t2, i2));
         } else {
-            w.sS(ij(d, j, JG), proj3(t1, t2, a, Isum));
+            G = proj3(t1, t2, a, Isum);
         }
     }
     // axis rows: drive (812-848) and limit (850-870), meff (777-788)
-    if (jt.dof >= 0 && kind != BSIM_SPHERICAL) {
+    V3<R> y1 = zero3<R>(), y2 = zero3<R>();
+    R meff = R(0), DA = R(0), DB = R(0), LF = R(0), FRH = R(0), LV = R(0), LB = R(0);
+    const bool axis = jt.dof >= 0 && kind != BSIM_SPHERICAL;
+    if (axis) {
         R k;
         V3<R> x1, x2;
         if (kind == BSIM_REVOLUTE) {
@@ -386,57 +393,52 @@ template <class R, bool REV = false> BS_HD void joint_constants(const Ctx<R> &c,
             x2 = cross(rp, a);
             k = mp + mc + dot(x2, smul(Ip, x2)) + dot(x1, smul(Ic, x1));
         }
-        w.s3(ij(d, j, JY1), smul(Ic, x1));
-        w.s3(ij(d, j, JY2), smul(Ip, x2));
-        w.at(ij(d, j, JMEFF)) = r_rcp(r_max(k, R(1e-12)));
+        y1 = smul(Ic, x1);
+        y2 = smul(Ip, x2);
+        meff = r_rcp(r_max(k, R(1e-12)));
+        const size_t pj = (size_t)j * d.E + e, pd = (size_t)e * d.D + jt.dof;
+        if (biased) {  // drive: lam = LF + clip(DA - DB qd, +-mf h) [+ friction]
+            const int mode = (int)c.s.dof_mode[pd];
+            const R ia = meff + c.s.joint_armature[pj];
+            const R mf = c.p.max_force;
+            R tau = clampr(c.s.ctrl_dof_force[pd], -mf, mf);
+            R kk = mode == BSIM_MODE_POSITION ? c.s.joint_stiffness[pj] : R(0);
+            R cc = mode == BSIM_MODE_FORCE ? R(0) : c.s.joint_damping[pj];
+            const R iia = r_rcp(ia);
+            const R hden = h * r_rcp(R(1) + h * (h * kk + cc) * iia);
+            R err = c.s.ctrl_dof_pos_target[pd] - q0;
+            DA = (kk * err + cc * c.s.ctrl_dof_vel_target[pd]) * hden;
+            DB = (kk * h + cc) * hden;
+            LF = mode == BSIM_MODE_FORCE ? tau * h * meff * iia : R(0);
+            R fr = c.s.joint_friction[pj];
+            FRH = fr > R(0) ? fr * h : R(0);
+        }
+        if (jt.has_limits) {  // limit: q0 in biased passes, start-of-step q otherwise
+            R lo = c.s.joint_limit_lo[pj], hi = c.s.joint_limit_hi[pj];
+            R q = biased ? q0 : w.at(idf(d, jt.dof, DQ0));
+            if (q < lo) {
+                LV = R(1);
+                LB = biased ? r_max(lo - q, R(0)) * r_rcp(h) : R(0);
+            }
+            if (q > hi) {
+                LV = R(2);
+                LB = biased ? r_max(q - hi, R(0)) * r_rcp(h) : R(0);
+            }
+        }
     }
-}
-
-// Per-pass constants of joint j: targets (-perr/h, -rerr/h), the PD drive's
-// affine impulse law, limit activation and bias.  Per-env gains / limits /
-// controls are read from HBM here (L1/L2 resident) instead of being staged.
-template <class R, bool REV = false>
-BS_HD void joint_pass_constants(const Ctx<R> &c, const Ws<R> &w, int e, int j, R h, bool biased) {
-    const Dims &d = c.d;
-    const auto &jt = c.joints[j];
-    V3<R> pe = w.l3(ij(d, j, JPE)), re = w.l3(ij(d, j, JRE));
     const R nih = -r_rcp(h);
-    w.s3(ij(d, j, JPE), biased ? pe * nih : zero3<R>());   // 881
-    w.s3(ij(d, j, JRE), biased ? re * nih : zero3<R>());   // 898
-    if (jt.dof < 0 || (!REV && jt.kind == BSIM_SPHERICAL)) return;
-    const size_t pj = (size_t)j * d.E + e, pd = (size_t)e * d.D + jt.dof;
-    const R meff = w.at(ij(d, j, JMEFF));
-    if (biased) {  // drive (812-848): lam = LF + clip(DA - DB qd, +-mf h) [+ friction]
-        const int mode = (int)c.s.dof_mode[pd];
-        const R ia = meff + c.s.joint_armature[pj];
-        const R mf = c.p.max_force;
-        R tau = clampr(c.s.ctrl_dof_force[pd], -mf, mf);
-        R kk = mode == BSIM_MODE_POSITION ? c.s.joint_stiffness[pj] : R(0);
-        R cc = mode == BSIM_MODE_FORCE ? R(0) : c.s.joint_damping[pj];
-        const R iia = r_rcp(ia);
-        const R hden = h * r_rcp(R(1) + h * (h * kk + cc) * iia);
-        R err = c.s.ctrl_dof_pos_target[pd] - w.at(ij(d, j, JQ0));
-        w.at(ij(d, j, JDA)) = (kk * err + cc * c.s.ctrl_dof_vel_target[pd]) * hden;
-        w.at(ij(d, j, JDB)) = (kk * h + cc) * hden;
-        w.at(ij(d, j, JLF)) = mode == BSIM_MODE_FORCE ? tau * h * meff * iia : R(0);
-        R fr = c.s.joint_friction[pj];
-        w.at(ij(d, j, JFRH)) = fr > R(0) ? fr * h : R(0);
-    }
-    if (jt.has_limits) {  // limit (850-870): q0 in biased passes, start-of-step q otherwise
-        R lo = c.s.joint_limit_lo[pj], hi = c.s.joint_limit_hi[pj];
-        R q = biased ? w.at(ij(d, j, JQ0)) : w.at(idf(d, jt.dof, DQ0));
-        R state = R(0), bias = R(0);
-        if (q < lo) {
-            state = R(1);
-            bias = biased ? r_max(lo - q, R(0)) * r_rcp(h) : R(0);
-        }
-        if (q > hi) {
-            state = R(2);
-            bias = biased ? r_max(q - hi, R(0)) * r_rcp(h) : R(0);
-        }
-        w.at(ij(d, j, JLV)) = state;
-        w.at(ij(d, j, JLB)) = bias;
-    }
+    V3<R> pt = biased ? perr * nih : zero3<R>(), rt = biased ? rerr * nih : zero3<R>();   // 881, 898
+    w.s4(ij(d, j, JRP), Q4<R>{rp.x, rp.y, rp.z, R(0)});
+    w.s4(ij(d, j, JRC), Q4<R>{rc.x, rc.y, rc.z, meff});
+    w.s4(ij(d, j, JPE), Q4<R>{pt.x, pt.y, pt.z, DA});
+    w.s4(ij(d, j, JRE), Q4<R>{rt.x, rt.y, rt.z, DB});
+    w.s4(ij(d, j, JAX), Q4<R>{a.x, a.y, a.z, LF});
+    w.s4(ij(d, j, JKI), Q4<R>{KI.xx, KI.xy, KI.xz, KI.yy});
+    w.s4(ij(d, j, JKI) + 4, Q4<R>{KI.yz, KI.zz, FRH, LV});
+    w.s4(ij(d, j, JG), Q4<R>{G.xx, G.xy, G.xz, G.yy});
+    w.s4(ij(d, j, JG) + 4, Q4<R>{G.yz, G.zz, LB, R(0)});
+    w.s4(ij(d, j, JY1), Q4<R>{y1.x, y1.y, y1.z, R(0)});
+    w.s4(ij(d, j, JY2), Q4<R>{y2.x, y2.y, y2.z, R(0)});
 }
 
 // plane-contact jacobians: xn = r x z, x1 = r x (0,-1,0), x2 = r x (1,0,0)
@@ -602,12 +604,10 @@ template <class R> BS_HD void plane_constants(const Ctx<R> &c, const Ws<R> &w, i
     V3<R> r = w.l3(ipl(d, i, CR));
     V3<R> xn = plane_xn(r), x1 = plane_x1(r), x2 = plane_x2(r);
     V3<R> in = smul(I, xn), i1 = smul(I, x1), i2 = smul(I, x2);
-    w.s3(ipl(d, i, CIXN), in);
-    w.s3(ipl(d, i, CIX1), i1);
-    w.s3(ipl(d, i, CIX2), i2);
-    w.at(ipl(d, i, CMN)) = r_rcp(r_max(im + dot(xn, in), R(1e-12)));
-    w.at(ipl(d, i, CM1)) = r_rcp(r_max(im + dot(x1, i1), R(1e-12)));
-    w.at(ipl(d, i, CM2)) = r_rcp(r_max(im + dot(x2, i2), R(1e-12)));
+    // whole 16-byte groups: [I xn | m_n], [I x1 | m_1], [I x2 | m_2]
+    w.s4(ipl(d, i, CIXN), Q4<R>{in.x, in.y, in.z, r_rcp(r_max(im + dot(xn, in), R(1e-12)))});
+    w.s4(ipl(d, i, CIX1), Q4<R>{i1.x, i1.y, i1.z, r_rcp(r_max(im + dot(x1, i1), R(1e-12)))});
+    w.s4(ipl(d, i, CIX2), Q4<R>{i2.x, i2.y, i2.z, r_rcp(r_max(im + dot(x2, i2), R(1e-12)))});
 }
 template <class R> BS_HD void pair_constants(const Ctx<R> &c, const Ws<R> &w, int i) {
     const Dims &d = c.d;
@@ -641,9 +641,9 @@ template <class R> BS_HD void plane_pass_constants(const Ctx<R> &c, const Ws<R> 
         st1 = (-tey) * idt;                                 // 971-973, t1 = (0,-1,0)
         st2 = tex * idt;                                    //           t2 = (1,0,0)
     }
-    w.at(ipl(d, i, CTGT)) = r_max(w.at(ipl(d, i, CREST)), bias);
-    w.at(ipl(d, i, CST1)) = st1;
-    w.at(ipl(d, i, CST2)) = st2;
+    const R rest = w.at(ipl(d, i, CREST));
+    w.at(ipl(d, i, CTGT)) = r_max(rest, bias);
+    w.s4(ipl(d, i, CST1), Q4<R>{st1, st2, w.at(ipl(d, i, CD0)), rest});   // [st1 st2 | d0 rest]
 }
 template <class R> BS_HD void pair_pass_constants(const Ctx<R> &c, const Ws<R> &w, int i, bool biased) {
     const Dims &d = c.d;
@@ -1142,19 +1142,7 @@ template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> 
             BS_SYNC();
         }
         BS_ITEMS(g, d.J, el, j) {
-            Ws<R> w = g.env(el);
-            if (freeze) {  // read_dof_states (557): q0 and the unbiased limit rows' q
-                R q[3], qd[3];
-                int n = joint_dofs<R, topo_rev<T>(), topo_idf<T>()>(c, w, j, q, qd);
-                for (int kk = 0; kk < n; ++kk) {
-                    w.at(idf(d, c.joints[j].dof + kk, DQ0)) = q[kk];
-                    w.at(idf(d, c.joints[j].dof + kk, DIMP)) = R(0);
-                }
-                if (n == 1) w.at(ij(d, j, JQ0)) = q[0];
-            }
-            joint_geometry<R, topo_rev<T>(), topo_idf<T>()>(c, w, j, deltas, !freeze);
-            joint_constants<R, topo_rev<T>()>(c, w, j);
-            joint_pass_constants<R, topo_rev<T>()>(c, w, g.e0 + el, j, h, biased);
+            joint_item<R, topo_rev<T>(), topo_idf<T>()>(c, g.env(el), g.e0 + el, j, h, biased, freeze, deltas);
         }
         BS_ITEMS(g, d.P, el, i) {
             Ws<R> w = g.env(el);
