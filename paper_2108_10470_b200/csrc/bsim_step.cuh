@@ -680,6 +680,8 @@ template <class R> struct JointOps {
     V3<R> a, y1, y2;   // world axis, I_c x1, I_p x2
     S3<R> Ic, Ip;
     R imp;             // dof_impulse (drive + limit, same addition order)
+    // row scalars carried in the .w slots of the joint's record groups
+    R lf, meff, da, db, frh, lv, lb;
 };
 
 // rate along a 1-DOF joint axis (physics.py:804-810)
@@ -702,12 +704,10 @@ template <class R> BS_HD void axis_apply(bool lin, const JointOps<R> &o, R lam, 
 // PD drive / direct actuation / joint friction (physics.py:812-848)
 template <class R>
 BS_HD void row_drive(const Ctx<R> &c, const Ws<R> &w, int j, bool lin, R h, JointOps<R> &o, BV<R> &C, BV<R> &P) {
-    const Dims &d = c.d;
-    R qd = axis_rate(d, w, j, lin, o, C, P);
+    R qd = axis_rate(c.d, w, j, lin, o, C, P);
     const R mfh = c.p.max_force * h;
-    R lam = w.at(ij(d, j, JLF)) + clampr(w.at(ij(d, j, JDA)) - w.at(ij(d, j, JDB)) * qd, -mfh, mfh);
-    R frh = w.at(ij(d, j, JFRH));
-    if (frh > R(0)) lam = lam + clampr(-qd * w.at(ij(d, j, JMEFF)), -frh, frh);
+    R lam = o.lf + clampr(o.da - o.db * qd, -mfh, mfh);
+    if (o.frh > R(0)) lam = lam + clampr(-qd * o.meff, -o.frh, o.frh);
     axis_apply(lin, o, lam, C, P);
     o.imp += lam;
 }
@@ -717,11 +717,9 @@ template <class R>
 BS_HD void row_limit(const Ws<R> &w, const Dims &d, int j, bool lin, JointOps<R> &o, BV<R> &C, BV<R> &P) {
     // branch-free (an inactive limit applies lam = 0, which leaves the
     // velocities bit-identical) so the scheduler can overlap independent rows
-    R state = w.at(ij(d, j, JLV));
     R qd = axis_rate(d, w, j, lin, o, C, P);
-    R meff = w.at(ij(d, j, JMEFF)), bias = w.at(ij(d, j, JLB));
-    R lam = state == R(1) ? r_max(meff * (bias - qd), R(0)) : -r_max(meff * (bias + qd), R(0));
-    lam = state == R(0) ? R(0) : lam;
+    R lam = o.lv == R(1) ? r_max(o.meff * (o.lb - qd), R(0)) : -r_max(o.meff * (o.lb + qd), R(0));
+    lam = o.lv == R(0) ? R(0) : lam;
     axis_apply(lin, o, lam, C, P);
     o.imp += lam;
 }
@@ -757,9 +755,20 @@ BS_HD void joint_rows(const Ctx<R> &c, const Ws<R> &w, int j, int kind, int dof,
     o.Ic = w.lS(ib(d, cb, BI));
     o.Ip = w.lS(ib(d, pb, BI));
     if (axis) {
-        o.a = w.l3(ij(d, j, JAX));
+        // whole record groups: [axis | LF], [Y1], [Y2], [RC | MEFF], [PE | DA],
+        // [RE | DB], [KI4 KI5 FRH LV], [G4 G5 LB -]
+        Q4<R> ax = w.l4(ij(d, j, JAX));
+        o.a = qvec(ax);
+        o.lf = ax.w;
         o.y1 = w.l3(ij(d, j, JY1));
         o.y2 = w.l3(ij(d, j, JY2));
+        o.meff = w.l4(ij(d, j, JRC)).w;
+        o.da = w.l4(ij(d, j, JPE)).w;
+        o.db = w.l4(ij(d, j, JRE)).w;
+        Q4<R> k4 = w.l4(ij(d, j, JKI) + 4);
+        o.frh = k4.z;
+        o.lv = k4.w;
+        o.lb = w.l4(ij(d, j, JG) + 4).z;
         o.imp = w.at(idf(d, dof, DIMP));
     }
     if (biased && axis) row_drive(c, w, j, lin, h, o, C, P);
@@ -775,36 +784,39 @@ BS_HD void joint_rows(const Ctx<R> &c, const Ws<R> &w, int j, int kind, int dof,
 // velocities and accumulators bit-identical, so independent rows overlap.
 template <class R> BS_HD void row_plane(const Ctx<R> &c, const Ws<R> &w, int i, BV<R> &X) {
     const Dims &d = c.d;
-    const bool act = w.at(ipl(d, i, CACT)) != R(0);
-    V3<R> r = w.l3(ipl(d, i, CR));
+    // whole record groups: [r | act], [I xn | m_n], [I x1 | m_1], [I x2 | m_2],
+    // [lam_n lt0 lt1 | tgt], [st1 st2 | d0 rest]
+    const Q4<R> ra = w.l4(ipl(d, i, CR)), gn = w.l4(ipl(d, i, CIXN));
+    const Q4<R> acc = w.l4(ipl(d, i, CLN)), stc = w.l4(ipl(d, i, CST1));
+    const bool act = ra.w != R(0);
+    V3<R> r = qvec(ra);
     R vn = X.v.z + dot(plane_xn(r), X.w);
-    R lam_n = w.at(ipl(d, i, CLN));
-    R dl = w.at(ipl(d, i, CMN)) * (w.at(ipl(d, i, CTGT)) - vn);
+    R lam_n = acc.x;
+    R dl = gn.w * (acc.w - vn);
     R nl = r_max(lam_n + dl, R(0));
     dl = act ? nl - lam_n : R(0);
     lam_n = lam_n + dl;
-    w.at(ipl(d, i, CLN)) = lam_n;
     X.v.z = X.v.z + dl * X.m;
-    X.w = X.w + w.l3(ipl(d, i, CIXN)) * dl;
+    X.w = X.w + qvec(gn) * dl;
     // friction with t1 = (0,-1,0), t2 = (1,0,0)
     R vt1 = -X.v.y + dot(plane_x1(r), X.w);
     R vt2 = X.v.x + dot(plane_x2(r), X.w);
     R mu = r_sqrt(vt1 * vt1 + vt2 * vt2) > R(1e-3) ? w.at(d.o_env + EMUD) : w.at(d.o_env + EMUS);
-    vt1 = vt1 + w.at(ipl(d, i, CST1));
-    vt2 = vt2 + w.at(ipl(d, i, CST2));
-    R lt0 = w.at(ipl(d, i, CLT)), lt1 = w.at(ipl(d, i, CLT + 1));
-    R c0 = lt0 + (-w.at(ipl(d, i, CM1)) * vt1), c1 = lt1 + (-w.at(ipl(d, i, CM2)) * vt2);
+    vt1 = vt1 + stc.x;
+    vt2 = vt2 + stc.y;
+    const Q4<R> g1 = w.l4(ipl(d, i, CIX1)), g2 = w.l4(ipl(d, i, CIX2));
+    R lt0 = acc.y, lt1 = acc.z;
+    R c0 = lt0 + (-g1.w * vt1), c1 = lt1 + (-g2.w * vt2);
     R lim = mu * lam_n;
     R nrm = r_sqrt(c0 * c0 + c1 * c1);   // circular cone clamp
     R sc = nrm > lim ? lim * r_rcp(r_max(nrm, R(1e-12))) : R(1);
     c0 = c0 * sc;
     c1 = c1 * sc;
     R d0 = act ? c0 - lt0 : R(0), d1 = act ? c1 - lt1 : R(0);
-    w.at(ipl(d, i, CLT)) = lt0 + d0;
-    w.at(ipl(d, i, CLT + 1)) = lt1 + d1;
+    w.s4(ipl(d, i, CLN), Q4<R>{lam_n, lt0 + d0, lt1 + d1, acc.w});
     X.v.x = X.v.x + d1 * X.m;
     X.v.y = X.v.y + (-d0) * X.m;
-    X.w = X.w + w.l3(ipl(d, i, CIX1)) * d0 + w.l3(ipl(d, i, CIX2)) * d1;
+    X.w = X.w + qvec(g1) * d0 + qvec(g2) * d1;
 }
 
 // sphere-sphere pair row (930-983, pair branches); A = body a, X = body b
