@@ -501,7 +501,15 @@ int launch_step(const bsim_layout_t *layout, const typename Abi<R>::Params *para
         g_err = "bsim_step: model too large for the step kernel's shared-memory workspace";
         return BSIM_E_TOO_LARGE;
     }
-    return launch_step_t<R, TopoGeneric>(c, smem, n_substeps, act, task, st);
+    switch (layout->topology_id) {
+#define BSIM_LAUNCH_TOPO(ID, TYPE)                                      \
+    case ID:                                                            \
+        return launch_step_t<R, TYPE>(c, smem, n_substeps, act, task, st);
+        BSIM_TOPOLOGIES_LARGE(BSIM_LAUNCH_TOPO)
+#undef BSIM_LAUNCH_TOPO
+    default:
+        return launch_step_t<R, TopoGeneric>(c, smem, n_substeps, act, task, st);
+    }
 #else
     if (use_large_variant<R>(c.d)) {   // big articulations: 4 envs x 32 threads per CTA
         int rc = call_large(layout, params, state, n_substeps, actions, task, stream);

@@ -945,8 +945,11 @@ template <class R, class T, bool BIASED> BS_HD void sweep_static(const Ctx<R> &c
 struct TopoGeneric {
     static constexpr bool is_static = false;
 };
+template <class T> constexpr bool topo_register_sweep() {
+    if constexpr (T::is_static) return T::register_sweep; else return false;
+}
 template <class R, class T> BS_HD void sweep_any(const Ctx<R> &c, const Ws<R> &w, R h, bool biased) {
-    if constexpr (T::is_static) {
+    if constexpr (topo_register_sweep<T>()) {
         if (biased)
             sweep_static<R, T, true>(c, w, h);
         else

@@ -12,6 +12,6 @@
 #define BSIM_NTH32 128
 #define BSIM_NE64 2
 #define BSIM_NTH64 64
-#define BSIM_MINB 4
+#define BSIM_MINB 5   // 5 x 128 threads: the 20-env-per-SM occupancy the record size allows
 #define bsim bsim_large
 #include "bsim_step.cu"

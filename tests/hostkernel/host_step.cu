@@ -66,6 +66,7 @@ static void run(const bsim_layout_t *L, const typename Abi<R>::Params *p, const 
     case ID:              \
         return run_t<R, TYPE>(L, p, s, n);
         BSIM_TOPOLOGIES(HK_TOPO)
+        BSIM_TOPOLOGIES_LARGE(HK_TOPO)
 #undef HK_TOPO
     default:
         return run_t<R, TopoGeneric>(L, p, s, n);
