@@ -941,12 +941,78 @@ template <class R, class T, bool BIASED> BS_HD void sweep_static(const Ctx<R> &c
     }
 }
 
+#if defined(__CUDA_ARCH__)
+// Two-lane pipelined sweep for a root with L legs that are 2-joint chains
+// (codegen's `star_chain` = 2 trait, the Ant analog: joint 2l = root ->
+// hip_l = link 2l+1, joint 2l+1 = hip_l -> knee_l = link 2l+2, all revolute
+// with limits, dof = joint index, plane slots on the root then on each knee,
+// no pairs).  Each env gets two lanes of the sweep warp: lane 0 runs the root
+// chain j_0, j_2, ..., lane 1 the knee rows j_1, j_3, ... one step behind,
+// receiving each hip's velocity from lane 0 by a shuffle.  Only rows on
+// disjoint bodies run side by side and every row's arithmetic is unchanged,
+// so the result is the reference's Gauss-Seidel order (physics.py:761-775):
+// j_2s+1 and j_2s+2 share no body, and a plane row may run as soon as its
+// body's last joint row is done because no later joint row touches it.
+// 8 joint + 5 plane row times become 5 + 3.  (The same pipeline for 3-joint
+// legs -- the ANYmal analog -- measured slower than the register-resident
+// sequential sweep, so codegen only marks 2-joint stars.)
+template <class R, class T>
+__device__ void sweep_star(const Ctx<R> &c, const Ws<R> &w, R h, bool biased, int p, unsigned mask) {
+    const Dims &d = c.d;
+    constexpr int L = T::J / 2;
+    BV<R> P = load_bv(d, w, 0), C;              // lane 0 keeps the root in P
+    for (int s = 0; s <= L; ++s) {
+        // lane 0: joint 2s (root -> hip s); lane 1: joint 2s - 1 (hip s-1 -> knee s-1)
+        const bool active = p == 0 ? s < L : s >= 1;
+        const int j = p == 0 ? 2 * s : 2 * s - 1;
+        const int cb = j + 1, pb = p == 0 ? 0 : j;
+        if (active) {
+            C = load_bv(d, w, cb);
+            if (biased)
+                joint_rows(c, w, j, BSIM_REVOLUTE, j, true, pb, cb, h, true, C, P);
+            else
+                joint_rows(c, w, j, BSIM_REVOLUTE, j, true, pb, cb, h, false, C, P);
+        }
+        // lane 1 is done with hip s-1 (P) and knee s-1 (C): both final for the joints
+        if (p == 1 && active) {
+            store_bv(d, w, pb, P);
+            store_bv(d, w, cb, C);
+        }
+        // hand hip s (lane 0's C after joint 2s) to lane 1 for joint 2s+1
+        BV<R> hip;
+        hip.v.x = __shfl_xor_sync(mask, C.v.x, 1);
+        hip.v.y = __shfl_xor_sync(mask, C.v.y, 1);
+        hip.v.z = __shfl_xor_sync(mask, C.v.z, 1);
+        hip.w.x = __shfl_xor_sync(mask, C.w.x, 1);
+        hip.w.y = __shfl_xor_sync(mask, C.w.y, 1);
+        hip.w.z = __shfl_xor_sync(mask, C.w.z, 1);
+        hip.m = __shfl_xor_sync(mask, C.m, 1);
+        if (p == 1) P = hip;
+    }
+    if (p == 0) store_bv(d, w, 0, P);
+    __syncwarp(mask);
+    // plane rows: slot q on the root (q = 0) or on knee q-1, round-robin over the lanes
+    for (int q = p; q < T::P; q += 2) {
+        const int b = q == 0 ? 0 : 2 * q;
+        BV<R> X = load_bv(d, w, b);
+        row_plane(c, w, q, X);
+        store_bv(d, w, b, X);
+    }
+    __syncwarp(mask);
+    if (biased)   // dpos += v h, dang += w h (physics.py:571-572) from the final velocities
+        for (int b = p; b < T::B; b += 2) accumulate_deltas(d, w, b, load_bv(d, w, b), h);
+}
+#endif
+
 // no compile-time topology: use the generic sweep
 struct TopoGeneric {
     static constexpr bool is_static = false;
 };
 template <class T> constexpr bool topo_register_sweep() {
     if constexpr (T::is_static) return T::register_sweep; else return false;
+}
+template <class T> constexpr bool topo_star() {
+    if constexpr (T::is_static) return T::star_chain > 0; else return false;
 }
 template <class R, class T> BS_HD void sweep_any(const Ctx<R> &c, const Ws<R> &w, R h, bool biased) {
     if constexpr (topo_register_sweep<T>()) {
@@ -1184,7 +1250,18 @@ template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> 
         const int reps = biased ? 1 : p.velocity_iterations;
 #endif
         for (int r = 0; r < reps; ++r) {
-            BS_ENVS(g, el) { sweep_any<R, T>(c, g.env(el), h, biased); }
+#if defined(__CUDA_ARCH__)
+            if constexpr (topo_star<T>()) {   // two lanes per env (sweep_star)
+                const int t = g.tid - g.lane0;
+                if (t >= 0 && t < 2 * g.ne) {
+                    const unsigned mask = 2 * g.ne >= 32 ? 0xffffffffu : ((1u << (2 * g.ne)) - 1u);
+                    sweep_star<R, T>(c, g.env(t >> 1), h, biased, t & 1, mask);
+                }
+            } else
+#endif
+            {
+                BS_ENVS(g, el) { sweep_any<R, T>(c, g.env(el), h, biased); }
+            }
             BS_SYNC();
         }
     }
