@@ -350,8 +350,8 @@ BS_HD void joint_item(const Ctx<R> &c, const Ws<R> &w, int e, int j, R h, bool b
     // ---- row constants from the current world inverse inertias
     R mp = w.at(ib(d, p, BM)), mc = w.at(ib(d, ch, BM));
     S3<R> Ip = w.lS(ib(d, p, BI)), Ic = w.lS(ib(d, ch, BI));
-    V3<R> t1, t2;
-    tangents(a, t1, t2);
+    V3<R> t1{R(0), R(0), R(0)}, t2{R(0), R(0), R(0)};
+    if (kind != BSIM_REVOLUTE) tangents(a, t1, t2);
     S3<R> KI, G{R(0), R(0), R(0), R(0), R(0), R(0)};
     if (kind != BSIM_PRISMATIC) {   // point-3 K^-1 (872-890)
         R m = mp + mc;
@@ -371,8 +371,14 @@ BS_HD void joint_item(const Ctx<R> &c, const Ws<R> &w, int e, int j, R h, bool b
     if (kind != BSIM_SPHERICAL) {   // angular block (892-906): G = T^T (T Isum T^T)^-1 T
         S3<R> Isum = sadd(Ip, Ic);
         if (kind == BSIM_REVOLUTE) {
-            V3<R> i1 = smul(Isum, t1), i2 = smul(Isum, t2);
-            G = proj2(t1, t2, dot(t1, i1), dot(t1, i2), dot(t2, i2));
+            // T^T (T M T^T)^-1 T for the two directions normal to the axis a,
+            // M = Isum: the same matrix as M^-1 - (M^-1 a)(M^-1 a)^T / (a . M^-1 a)
+            // (the projected inverse), which needs no tangent basis
+            S3<R> Mi = sinv(Isum);
+            V3<R> u = smul(Mi, a);
+            R is = r_rcp(dot(a, u));
+            G = S3<R>{Mi.xx - u.x * u.x * is, Mi.xy - u.x * u.y * is, Mi.xz - u.x * u.z * is,
+                      Mi.yy - u.y * u.y * is, Mi.yz - u.y * u.z * is, Mi.zz - u.z * u.z * is};
         } else {
             G = proj3(t1, t2, a, Isum);
         }
