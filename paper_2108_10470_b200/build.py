@@ -51,19 +51,24 @@ def build(force=False, verbose=False):
     if not force and up_to_date():
         return OUT
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
-    objs = []
-    for src in sources():
+    from concurrent.futures import ThreadPoolExecutor
+
+    def compile_one(src):
         obj = os.path.join(HERE, "_lib", os.path.basename(src)[:-3] + ".o")
         extra = os.environ.get("BSIM_NVCC_EXTRA", "").split()   # dev experiments only
         fast = FAST_FP32 if os.path.basename(src) in FAST_TUS else []
         cmd = ["nvcc", *NVCC_FLAGS, *fast, *extra, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        if r.returncode != 0:
-            sys.stderr.write(r.stdout + r.stderr)
-            raise RuntimeError(f"nvcc failed on {src}")
-        if verbose:
-            sys.stderr.write(r.stderr)
-        objs.append(obj)
+        return src, obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    objs = []
+    with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as pool:   # one nvcc per TU
+        for src, obj, r in pool.map(compile_one, sources()):
+            if r.returncode != 0:
+                sys.stderr.write(r.stdout + r.stderr)
+                raise RuntimeError(f"nvcc failed on {src}")
+            if verbose:
+                sys.stderr.write(r.stderr)
+            objs.append(obj)
     cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", *objs, "-o", OUT]
     subprocess.check_call(cmd)
     return OUT
