@@ -19,7 +19,7 @@ Timed-region rules: W untimed warm-up steps; K timed steps, each bracketed by
 CUDA events on the launching stream, an L2 flush (256 MiB write) between
 steps outside the events; barrier + synchronize on both sides.  `value` uses
 device-resident inputs; `e2e` repeats the run through the public EnvBatch API
-with the actions copied from pinned host memory and obs / reward / done
+(step_host) with the actions copied from pinned host memory and obs / reward / done
 copied back every step.
 """
 
@@ -233,32 +233,26 @@ def measure(task, E, args, rank, world, clocks=None, policy=False, kernel=True, 
         out["bytes_per_env"] = kernel_bytes(env)
         env.reset()
 
-    if e2e:         # end to end through the public API with host buffers
+    if e2e:         # end to end through the public API with host buffers (EnvBatch.step_host:
+        # pinned actions in, pinned obs / reward / done / info out, the host
+        # consumes each step's results before issuing the next)
         h_act = [a.cpu().pin_memory() for a in acts]
-        h_obs = torch.empty(env.obs.shape, dtype=env.obs.dtype, pin_memory=True)
-        h_rew = torch.empty(env.reward.shape, dtype=env.reward.dtype, pin_memory=True)
-        h_done = torch.empty(env.done.shape, dtype=env.done.dtype, pin_memory=True)
         for i in range(args.warmup):
-            env.step(h_act[i % len(h_act)].to(dev, non_blocking=True))
+            env.step_host(h_act[i % len(h_act)])
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for i in range(args.steps):
-            a = h_act[i % len(h_act)].to(dev, non_blocking=True)
-            o = env.step(a)
-            h_obs.copy_(o.obs, non_blocking=True)
-            h_rew.copy_(o.reward, non_blocking=True)
-            h_done.copy_(o.done, non_blocking=True)
-            torch.cuda.current_stream().synchronize()   # the host consumes the step's results
+            o = env.step_host(h_act[i % len(h_act)])
         e1.record(stream)
         torch.cuda.synchronize()
+        d2h = sum(t.numel() * t.element_size() for t in (o.obs, o.reward, o.done, *o.info.values()))
         out["e2e"] = {"value": world * E * args.steps / (maxr(e0.elapsed_time(e1)) / 1e3), "unit": UNIT,
                       "h2d_bytes_per_step": h_act[0].numel() * h_act[0].element_size(),
-                      "d2h_bytes_per_step": (h_obs.numel() * h_obs.element_size()
-                                             + h_rew.numel() * h_rew.element_size()
-                                             + h_done.numel() * h_done.element_size())}
+                      "d2h_bytes_per_step": d2h, "chunks": env.host_chunk_count(),
+                      "api": "EnvBatch.step_host (wave-sized env chunks, copies overlapped on a copy stream)"}
     env.close()
     del flush
     torch.cuda.empty_cache()

@@ -318,6 +318,78 @@ int bsim_task_step_f64(const bsim_layout_t *layout, const bsim_state64_t *state,
 int bsim_task_reset_f64(const bsim_layout_t *layout, const bsim_state64_t *state, const bsim_task_t *task,
                         const uint8_t *env_mask, void *stream);
 
+/* Env-range forms for the pipelined host-buffer step (EnvBatch.step with
+   host arrays, envs.py:178-200 called with numpy actions): the same launches
+   restricted to envs [env_begin, env_begin + env_count) of the scene, so a
+   wave-sized chunk's device->host copy overlaps the next chunk's step.
+   Every per-env result equals the whole-batch launch's (envs are independent). */
+int bsim_step_range(const bsim_layout_t *layout, const bsim_params_t *params, const bsim_state_t *state,
+                    int32_t n_substeps, const bsim_actions_t *actions, int32_t env_begin, int32_t env_count,
+                    void *stream);
+int bsim_step_range_f64(const bsim_layout_t *layout, const bsim_params64_t *params, const bsim_state64_t *state,
+                        int32_t n_substeps, const bsim_actions_t *actions, int32_t env_begin, int32_t env_count,
+                        void *stream);
+int bsim_env_step_range(const bsim_layout_t *layout, const bsim_params_t *params, const bsim_state_t *state,
+                        int32_t n_substeps, const bsim_actions_t *actions, const bsim_task_t *task,
+                        int32_t env_begin, int32_t env_count, void *stream);
+int bsim_env_step_range_f64(const bsim_layout_t *layout, const bsim_params64_t *params,
+                            const bsim_state64_t *state, int32_t n_substeps, const bsim_actions_t *actions,
+                            const bsim_task_t *task, int32_t env_begin, int32_t env_count, void *stream);
+int bsim_task_step_range(const bsim_layout_t *layout, const bsim_state_t *state, const bsim_task_t *task,
+                         int32_t env_begin, int32_t env_count, void *stream);
+int bsim_task_step_range_f64(const bsim_layout_t *layout, const bsim_state64_t *state, const bsim_task_t *task,
+                             int32_t env_begin, int32_t env_count, void *stream);
+/* Host buffers of one pipelined host-buffer control step (EnvBatch.step with
+   numpy arrays, envs.py:178-200).  Host arrays should be page-locked (pinned)
+   for the copies to be asynchronous. */
+typedef struct bsim_host_io_t {
+    const void *actions;        /* [E][act_dim] host, the entry point's precision */
+    void *obs, *reward;         /* [E][obs_dim], [E] host                          */
+    uint8_t *done, *timeout, *poisoned;   /* [E] host                             */
+    int32_t n_chunks;           /* env chunks; <= 0: one per step-kernel wave     */
+    int32_t fused;              /* 1: one bsim_env_step_range launch per chunk;
+                                   0: bsim_step_range + bsim_task_step_range      */
+} bsim_host_io_t;
+/* One control step from and to host memory, pipelined in ONE call: the envs
+   are split into n_chunks ranges; every chunk's actions go host->device on a
+   copy stream, chunk c steps (physics + task tail) on its own stream once its
+   actions landed, and its obs / reward / done / timeout / poisoned go
+   device->host on the copy stream while chunk c+1 is still stepping.  The
+   work is ordered after everything already queued on `stream`, and `stream`
+   waits for all of it, so synchronising `stream` makes the host buffers valid.
+   actions->actions is the DEVICE staging array the uploaded actions land in
+   ([E][act_dim]); scale / mode / actions_clipped as for bsim_step.
+   task->step_count must be the post-step count (as for bsim_env_step). */
+int bsim_env_step_host(const bsim_layout_t *layout, const bsim_params_t *params, const bsim_state_t *state,
+                       int32_t n_substeps, const bsim_actions_t *actions, const bsim_task_t *task,
+                       const bsim_host_io_t *io, void *stream);
+/* error text of the last failed bsim_env_step_host call */
+const char *bsim_host_last_error(void);
+int bsim_env_step_host_f64(const bsim_layout_t *layout, const bsim_params64_t *params,
+                           const bsim_state64_t *state, int32_t n_substeps, const bsim_actions_t *actions,
+                           const bsim_task_t *task, const bsim_host_io_t *io, void *stream);
+/* The pipelined host step captured once as a CUDA graph (one launch per
+   control step).  task->step_count_dev must point at a device int64 the
+   graph fills from *count_host (a pinned host slot) before the step, so the
+   DR interval keeps advancing; the graph bakes every other pointer and the
+   params, so rebuild it if any of them change.  Launch: re-points the action
+   uploads at `host_actions` (same size and layout as io->actions), writes
+   step_count (the post-step count) to *count_host, and launches on `stream`;
+   the previous launch must have completed. */
+typedef struct bsim_host_graph bsim_host_graph_t;
+int bsim_env_step_host_graph(const bsim_layout_t *layout, const bsim_params_t *params, const bsim_state_t *state,
+                             int32_t n_substeps, const bsim_actions_t *actions, const bsim_task_t *task,
+                             const bsim_host_io_t *io, int64_t *count_host, bsim_host_graph_t **graph);
+int bsim_env_step_host_graph_f64(const bsim_layout_t *layout, const bsim_params64_t *params,
+                                 const bsim_state64_t *state, int32_t n_substeps, const bsim_actions_t *actions,
+                                 const bsim_task_t *task, const bsim_host_io_t *io, int64_t *count_host,
+                                 bsim_host_graph_t **graph);
+int bsim_host_graph_launch(bsim_host_graph_t *graph, const void *host_actions, int64_t step_count, void *stream);
+void bsim_host_graph_destroy(bsim_host_graph_t *graph);
+/* Envs one full wave of the step kernel keeps resident on the current device
+   (SMs x CTAs/SM x envs/CTA) -- the chunk size of the pipelined step. */
+int bsim_step_envs_per_wave(const bsim_layout_t *layout, int32_t fp64, int32_t *envs);
+
 /* ------------------------------------------------------------------------
    Batched reward kernels (reference rewards.py:78-219), one thread per env.
    Arrays are float (fp64 = 0) or double (fp64 = 1) device arrays. */

@@ -106,6 +106,12 @@ class Actions(C.Structure):
                 ("mode", C.c_int32), ("pad", C.c_int32)]
 
 
+class HostIO(C.Structure):
+    """bsim_host_io_t."""
+    _fields_ = [("actions", C.c_void_p), ("obs", C.c_void_p), ("reward", C.c_void_p), ("done", C.c_void_p),
+                ("timeout", C.c_void_p), ("poisoned", C.c_void_p), ("n_chunks", C.c_int32), ("fused", C.c_int32)]
+
+
 _lib = None
 
 
@@ -116,11 +122,23 @@ def _declare(lib):
         "bsim_abi_version": ([], C.c_int),
         "bsim_last_error": ([], C.c_char_p),
         "bsim_step_smem_per_env": ([P(Layout), C.c_int32, P(C.c_int32), P(C.c_int32)], C.c_int),
+        "bsim_step_envs_per_wave": ([P(Layout), C.c_int32, P(C.c_int32)], C.c_int),
+        "bsim_host_last_error": ([], C.c_char_p),
+        "bsim_host_graph_launch": ([vp, vp, C.c_int64, vp], C.c_int),
+        "bsim_host_graph_destroy": ([vp], None),
     }
     for suffix, prm in (("", Params), ("_f64", Params64)):
         sig.update({
             "bsim_step" + suffix: ([P(Layout), P(prm), vp, C.c_int32, P(Actions), vp], C.c_int),
             "bsim_env_step" + suffix: ([P(Layout), P(prm), vp, C.c_int32, P(Actions), vp, vp], C.c_int),
+            "bsim_env_step_host" + suffix: ([P(Layout), P(prm), vp, C.c_int32, P(Actions), vp, P(HostIO), vp],
+                                            C.c_int),
+            "bsim_env_step_host_graph" + suffix: ([P(Layout), P(prm), vp, C.c_int32, P(Actions), vp, P(HostIO),
+                                                   vp, P(vp)], C.c_int),
+            "bsim_step_range" + suffix: ([P(Layout), P(prm), vp, C.c_int32, P(Actions), C.c_int32, C.c_int32, vp],
+                                         C.c_int),
+            "bsim_env_step_range" + suffix: ([P(Layout), P(prm), vp, C.c_int32, P(Actions), vp,
+                                              C.c_int32, C.c_int32, vp], C.c_int),
             "bsim_forward_kinematics" + suffix: ([P(Layout), vp, vp, C.c_uint32, vp], C.c_int),
             "bsim_refresh_buffers" + suffix: ([P(Layout), vp, vp], C.c_int),
             "bsim_set_root_state_indexed" + suffix: ([P(Layout), vp, vp, vp, C.c_int32, vp, vp, vp], C.c_int),

@@ -10,6 +10,8 @@ def declare(lib):
         f.argtypes, f.restype = [vp, vp, vp, vp], C.c_int
         f = getattr(lib, "bsim_task_reset" + suffix)
         f.argtypes, f.restype = [vp, vp, vp, vp, vp], C.c_int
+        f = getattr(lib, "bsim_task_step_range" + suffix)
+        f.argtypes, f.restype = [vp, vp, vp, C.c_int32, C.c_int32, vp], C.c_int
     lib.bsim_task_last_error.argtypes, lib.bsim_task_last_error.restype = [], C.c_char_p
     for suffix in ("", "_f64"):
         f = getattr(lib, "bsim_randomize" + suffix)

@@ -28,9 +28,10 @@ using namespace bsim;
 #ifndef BSIM_LARGE_TU
 extern "C" {
 int bsim_large_step_f32(const bsim_layout_t *, const bsim_params_t *, const bsim_state_t *, int32_t,
-                        const bsim_actions_t *, const bsim_task_t *, void *);
+                        const bsim_actions_t *, const bsim_task_t *, int32_t, int32_t, void *);
 int bsim_large_step_f64(const bsim_layout_t *, const bsim_params64_t *, const bsim_state64_t *, int32_t,
-                        const bsim_actions_t *, const bsim_task_t *, void *);
+                        const bsim_actions_t *, const bsim_task_t *, int32_t, int32_t, void *);
+int bsim_large_envs_per_wave(const bsim_layout_t *, int32_t, int32_t *);
 const char *bsim_large_last_error(void);
 }
 #endif
@@ -109,18 +110,20 @@ template <class R> __device__ __noinline__ void task_step_env_call(const Ctx<R> 
 #define BSIM_MINB 4   // 4 x 128 threads at <= 128 registers: matches the shared-memory limit
 #endif
 // `epc` envs per CTA (<= NE): chosen by the launcher so the grid is a whole
-// number of waves of resident CTAs (148 SMs x CTAs/SM)
+// number of waves of resident CTAs (148 SMs x CTAs/SM).  The grid covers envs
+// [e_begin, e_end) -- all of them, or one wave-sized chunk of the pipelined
+// host-buffer step (bsim_env_step_range).
 template <class R, class T>
 __global__ void __launch_bounds__(Shape<R>::NTH, BSIM_MINB)
-    step_kernel(const __grid_constant__ Ctx<R> c, int n_substeps, bsim_actions_t act, int epc,
-                const __grid_constant__ bsim_task_t task, int with_task) {
+    step_kernel(const __grid_constant__ Ctx<R> c, int n_substeps, bsim_actions_t act, int epc, int e_begin,
+                int e_end, const __grid_constant__ bsim_task_t task, int with_task) {
     constexpr int NTH = Shape<R>::NTH;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const Dims &d = c.d;
     R *ws = reinterpret_cast<R *>(smem_raw);
     const int tid = threadIdx.x;
-    const int e0 = blockIdx.x * epc;
-    const int ne = min(epc, d.E - e0);
+    const int e0 = e_begin + blockIdx.x * epc;   // envs [e_begin, e_end) of the scene's E
+    const int ne = min(epc, e_end - e0);
     const int per_env = 13 * d.B;
     constexpr int NW = NTH / 32;
     __shared__ int s_warp_smsp[NW], s_sweep_warp;
@@ -417,12 +420,10 @@ bool bad_layout(const bsim_layout_t *L) {
 }
 
 // ------------------------------------------------------------ launchers
-template <class R, class T>
-int launch_step_t(const Ctx<R> &c, size_t smem, int n_substeps, const bsim_actions_t &act, const bsim_task_t *task,
-                  cudaStream_t st) {
-    constexpr int NE = Shape<R>::NE;
+// resident CTAs of step_kernel<R, T> on the whole device at `smem` bytes
+template <class R, class T> int device_slots(size_t smem, int *slots_out) {
     static size_t configured = 0;
-    static int slots = 0;   // resident CTAs on the whole device at this smem size
+    static int slots = 0;
     if (smem > 48 * 1024 && smem > configured) {
         cudaError_t e = cudaFuncSetAttribute(step_kernel<R, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
@@ -437,8 +438,20 @@ int launch_step_t(const Ctx<R> &c, size_t smem, int n_substeps, const bsim_actio
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<R, T>, Shape<R>::NTH, smem);
         slots = sms * (per_sm > 0 ? per_sm : 1);
     }
+    *slots_out = slots;
+    return BSIM_OK;
+}
+
+template <class R, class T>
+int launch_step_t(const Ctx<R> &c, size_t smem, int n_substeps, const bsim_actions_t &act, const bsim_task_t *task,
+                  int e_begin, int e_count, cudaStream_t st) {
+    constexpr int NE = Shape<R>::NE;
+    int slots = 0;
+    if (int rc = device_slots<R, T>(smem, &slots)) return rc;
     // whole waves: the fewest waves of <= NE envs per CTA, then spread the envs
-    // evenly over waves x slots CTAs (no partial last wave)
+    // evenly over waves x slots CTAs (no partial last wave).  Balanced on the
+    // scene's E: the chunks of a pipelined step (bsim_env_step_host) keep the
+    // whole batch's CTA size, so n concurrent chunk grids fill the same waves.
     const int E = c.d.E;
     int epc = NE;
 #ifndef BSIM_NO_BALANCE
@@ -447,10 +460,11 @@ int launch_step_t(const Ctx<R> &c, size_t smem, int n_substeps, const bsim_actio
     if (epc < 1) epc = 1;
     if (epc > NE) epc = NE;
 #endif
-    const int grid = (E + epc - 1) / epc;
+    const int grid = (e_count + epc - 1) / epc;
     bsim_task_t tk;
     if (task) tk = *task; else std::memset(&tk, 0, sizeof tk);
-    step_kernel<R, T><<<grid, Shape<R>::NTH, smem, st>>>(c, n_substeps, act, epc, tk, task != nullptr);
+    step_kernel<R, T><<<grid, Shape<R>::NTH, smem, st>>>(c, n_substeps, act, epc, e_begin, e_begin + e_count, tk,
+                                                           task != nullptr);
     return check_launch("step_kernel");
 }
 
@@ -469,21 +483,26 @@ template <class R> bool use_large_variant(const Dims &d) {
     return step_smem_bytes<R>(d) > 113 * 1024;
 }
 int call_large(const bsim_layout_t *l, const bsim_params_t *p, const bsim_state_t *s, int32_t n,
-               const bsim_actions_t *a, const bsim_task_t *t, void *st) {
-    return bsim_large_step_f32(l, p, s, n, a, t, st);
+               const bsim_actions_t *a, const bsim_task_t *t, int32_t eb, int32_t en, void *st) {
+    return bsim_large_step_f32(l, p, s, n, a, t, eb, en, st);
 }
 int call_large(const bsim_layout_t *l, const bsim_params64_t *p, const bsim_state64_t *s, int32_t n,
-               const bsim_actions_t *a, const bsim_task_t *t, void *st) {
-    return bsim_large_step_f64(l, p, s, n, a, t, st);
+               const bsim_actions_t *a, const bsim_task_t *t, int32_t eb, int32_t en, void *st) {
+    return bsim_large_step_f64(l, p, s, n, a, t, eb, en, st);
 }
 #endif
 
 template <class R>
 int launch_step(const bsim_layout_t *layout, const typename Abi<R>::Params *params,
                 const typename Abi<R>::State *state, int32_t n_substeps, const bsim_actions_t *actions,
-                void *stream, const bsim_task_t *task = nullptr) {
+                void *stream, const bsim_task_t *task = nullptr, int32_t env_begin = 0, int32_t env_count = -1) {
     if (bad_layout(layout) || !params || !state || n_substeps < 1) {
         g_err = "bsim_step: invalid arguments";
+        return BSIM_E_INVALID;
+    }
+    if (env_count < 0) env_count = layout->num_envs - env_begin;
+    if (env_begin < 0 || env_begin + env_count > layout->num_envs) {
+        g_err = "bsim_step: env range out of bounds";
         return BSIM_E_INVALID;
     }
     if (task && !task_ok(layout, task)) {
@@ -491,7 +510,7 @@ int launch_step(const bsim_layout_t *layout, const typename Abi<R>::Params *para
         return BSIM_E_INVALID;
     }
     Ctx<R> c = make_ctx<R>(layout, params, state);
-    if (c.d.E == 0) return BSIM_OK;
+    if (c.d.E == 0 || env_count == 0) return BSIM_OK;
     size_t smem = step_smem_bytes<R>(c.d);
     bsim_actions_t act;
     if (actions) act = *actions; else std::memset(&act, 0, sizeof act);
@@ -504,15 +523,15 @@ int launch_step(const bsim_layout_t *layout, const typename Abi<R>::Params *para
     switch (layout->topology_id) {
 #define BSIM_LAUNCH_TOPO(ID, TYPE)                                      \
     case ID:                                                            \
-        return launch_step_t<R, TYPE>(c, smem, n_substeps, act, task, st);
+        return launch_step_t<R, TYPE>(c, smem, n_substeps, act, task, env_begin, env_count, st);
         BSIM_TOPOLOGIES_LARGE(BSIM_LAUNCH_TOPO)
 #undef BSIM_LAUNCH_TOPO
     default:
-        return launch_step_t<R, TopoGeneric>(c, smem, n_substeps, act, task, st);
+        return launch_step_t<R, TopoGeneric>(c, smem, n_substeps, act, task, env_begin, env_count, st);
     }
 #else
     if (use_large_variant<R>(c.d)) {   // big articulations: 4 envs x 32 threads per CTA
-        int rc = call_large(layout, params, state, n_substeps, actions, task, stream);
+        int rc = call_large(layout, params, state, n_substeps, actions, task, env_begin, env_count, stream);
         if (rc != BSIM_OK) g_err = bsim_large_last_error();
         return rc;
     }
@@ -523,11 +542,11 @@ int launch_step(const bsim_layout_t *layout, const typename Abi<R>::Params *para
     switch (layout->topology_id) {
 #define BSIM_LAUNCH_TOPO(ID, TYPE)                                      \
     case ID:                                                            \
-        return launch_step_t<R, TYPE>(c, smem, n_substeps, act, task, st);
+        return launch_step_t<R, TYPE>(c, smem, n_substeps, act, task, env_begin, env_count, st);
         BSIM_TOPOLOGIES(BSIM_LAUNCH_TOPO)
 #undef BSIM_LAUNCH_TOPO
     default:
-        return launch_step_t<R, TopoGeneric>(c, smem, n_substeps, act, task, st);
+        return launch_step_t<R, TopoGeneric>(c, smem, n_substeps, act, task, env_begin, env_count, st);
     }
 #endif
 }
@@ -607,17 +626,44 @@ int launch_collide(const bsim_layout_t *layout, const typename Abi<R>::Params *p
     return check_launch("collide_write_kernel");
 }
 
+// resident envs of one full wave of step_kernel CTAs for this layout (the
+// chunk size of the pipelined host-buffer step)
+template <class R> int envs_per_wave(const bsim_layout_t *l, int32_t *envs) {
+    Dims d = make_dims(*l, sizeof(R) == 8);
+    size_t smem = step_smem_bytes<R>(d);
+    if (smem > 227 * 1024) return BSIM_E_TOO_LARGE;
+    int slots = 0, rc = BSIM_OK;
+    switch (l->topology_id) {
+#define BSIM_WAVE_TOPO(ID, TYPE) \
+    case ID:                     \
+        rc = device_slots<R, TYPE>(smem, &slots); break;
+#ifdef BSIM_LARGE_TU
+        BSIM_TOPOLOGIES_LARGE(BSIM_WAVE_TOPO)
+#else
+        BSIM_TOPOLOGIES(BSIM_WAVE_TOPO)
+#endif
+#undef BSIM_WAVE_TOPO
+    default:
+        rc = device_slots<R, TopoGeneric>(smem, &slots);
+    }
+    *envs = slots * Shape<R>::NE;
+    return rc;
+}
+
 }  // namespace
 
 #ifdef BSIM_LARGE_TU
 extern "C" {
 int bsim_large_step_f32(const bsim_layout_t *l, const bsim_params_t *p, const bsim_state_t *s, int32_t n,
-                        const bsim_actions_t *a, const bsim_task_t *t, void *st) {
-    return launch_step<float>(l, p, s, n, a, st, t);
+                        const bsim_actions_t *a, const bsim_task_t *t, int32_t eb, int32_t en, void *st) {
+    return launch_step<float>(l, p, s, n, a, st, t, eb, en);
 }
 int bsim_large_step_f64(const bsim_layout_t *l, const bsim_params64_t *p, const bsim_state64_t *s, int32_t n,
-                        const bsim_actions_t *a, const bsim_task_t *t, void *st) {
-    return launch_step<double>(l, p, s, n, a, st, t);
+                        const bsim_actions_t *a, const bsim_task_t *t, int32_t eb, int32_t en, void *st) {
+    return launch_step<double>(l, p, s, n, a, st, t, eb, en);
+}
+int bsim_large_envs_per_wave(const bsim_layout_t *l, int32_t fp64, int32_t *envs) {
+    return fp64 ? envs_per_wave<double>(l, envs) : envs_per_wave<float>(l, envs);
 }
 const char *bsim_large_last_error(void) { return g_err.c_str(); }
 }
@@ -657,6 +703,35 @@ int bsim_env_step_f64(const bsim_layout_t *l, const bsim_params64_t *p, const bs
 int bsim_step_f64(const bsim_layout_t *l, const bsim_params64_t *p, const bsim_state64_t *s, int32_t n,
                   const bsim_actions_t *a, void *st) {
     return launch_step<double>(l, p, s, n, a, st);
+}
+int bsim_step_range(const bsim_layout_t *l, const bsim_params_t *p, const bsim_state_t *s, int32_t n,
+                    const bsim_actions_t *a, int32_t env_begin, int32_t env_count, void *st) {
+    if (env_count < 0) return BSIM_E_INVALID;
+    return launch_step<float>(l, p, s, n, a, st, nullptr, env_begin, env_count);
+}
+int bsim_step_range_f64(const bsim_layout_t *l, const bsim_params64_t *p, const bsim_state64_t *s, int32_t n,
+                        const bsim_actions_t *a, int32_t env_begin, int32_t env_count, void *st) {
+    if (env_count < 0) return BSIM_E_INVALID;
+    return launch_step<double>(l, p, s, n, a, st, nullptr, env_begin, env_count);
+}
+int bsim_env_step_range(const bsim_layout_t *l, const bsim_params_t *p, const bsim_state_t *s, int32_t n,
+                        const bsim_actions_t *a, const bsim_task_t *t, int32_t env_begin, int32_t env_count,
+                        void *st) {
+    if (!t || env_count < 0) return BSIM_E_INVALID;
+    return launch_step<float>(l, p, s, n, a, st, t, env_begin, env_count);
+}
+int bsim_env_step_range_f64(const bsim_layout_t *l, const bsim_params64_t *p, const bsim_state64_t *s, int32_t n,
+                            const bsim_actions_t *a, const bsim_task_t *t, int32_t env_begin, int32_t env_count,
+                            void *st) {
+    if (!t || env_count < 0) return BSIM_E_INVALID;
+    return launch_step<double>(l, p, s, n, a, st, t, env_begin, env_count);
+}
+int bsim_step_envs_per_wave(const bsim_layout_t *l, int32_t fp64, int32_t *envs) {
+    if (bad_layout(l) || !envs) return BSIM_E_INVALID;
+    Dims d = make_dims(*l, fp64 != 0);
+    const bool large = fp64 ? use_large_variant<double>(d) : use_large_variant<float>(d);
+    if (large) return bsim_large_envs_per_wave(l, fp64, envs);
+    return fp64 ? envs_per_wave<double>(l, envs) : envs_per_wave<float>(l, envs);
 }
 int bsim_forward_kinematics(const bsim_layout_t *l, const bsim_state_t *s, const uint8_t *m, uint32_t am,
                             void *st) {

@@ -19,18 +19,38 @@ int t_set_err(const char *what, cudaError_t e) {
     return BSIM_E_CUDA;
 }
 
-template <class R> __global__ void task_step_kernel(const Ctx<R> c, const bsim_task_t t) {
-    int e = blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= c.d.E) return;
-    task_step_env(c, TaskView<R>{t}, e);
+// One thread per env over envs [e_begin, e_end).  The CTA's observation rows
+// are built in shared memory and leave with one coalesced copy (a thread-per-
+// env row store is a 240-348 B stride across the warp).
+template <class R> __device__ void obs_copy_out(const bsim_task_t &t, const R *stage, int cta_e0, int e_end) {
+    __syncthreads();
+    const int n = max(0, min((int)blockDim.x, e_end - cta_e0)) * t.obs_dim;
+    R *dst = reinterpret_cast<R *>(t.obs) + (size_t)cta_e0 * t.obs_dim;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = stage[i];
 }
 
-template <class R> __global__ void task_reset_kernel(const Ctx<R> c, const bsim_task_t t, const uint8_t *mask) {
-    int e = blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= c.d.E) return;
-    TaskView<R> tv{t};
-    if (!mask || mask[e]) task_reset_env(c, tv, e);
-    task_obs(c, tv, e);
+template <class R>
+__global__ void task_step_kernel(const __grid_constant__ Ctx<R> c, const __grid_constant__ bsim_task_t t, int e_begin,
+                                 int e_end) {
+    extern __shared__ __align__(16) unsigned char task_smem[];
+    R *stage = reinterpret_cast<R *>(task_smem);
+    const int cta_e0 = e_begin + blockIdx.x * blockDim.x, e = cta_e0 + threadIdx.x;
+    if (e < e_end) task_step_env(c, TaskView<R>{t, stage, cta_e0}, e);
+    obs_copy_out(t, stage, cta_e0, e_end);
+}
+
+template <class R>
+__global__ void task_reset_kernel(const __grid_constant__ Ctx<R> c, const __grid_constant__ bsim_task_t t,
+                                  const uint8_t *mask) {
+    extern __shared__ __align__(16) unsigned char task_smem[];
+    R *stage = reinterpret_cast<R *>(task_smem);
+    const int cta_e0 = blockIdx.x * blockDim.x, e = cta_e0 + threadIdx.x;
+    if (e < c.d.E) {
+        TaskView<R> tv{t, stage, cta_e0};
+        if (!mask || mask[e]) task_reset_env(c, tv, e);
+        task_obs(c, tv, e);
+    }
+    obs_copy_out(t, stage, cta_e0, c.d.E);
 }
 
 template <class R>
@@ -60,19 +80,32 @@ bool bad(const bsim_layout_t *L, const void *s, const bsim_task_t *t) {
 
 template <class R>
 int launch_task(const bsim_layout_t *L, const typename Abi<R>::State *s, const bsim_task_t *t, bool reset,
-                const uint8_t *mask, void *stream) {
+                const uint8_t *mask, int env_begin, int env_count, void *stream) {
     if (bad(L, s, t)) {
         t_err = "bsim_task: invalid arguments";
         return BSIM_E_INVALID;
     }
+    if (env_count < 0) env_count = L->num_envs - env_begin;
+    if (env_begin < 0 || env_begin + env_count > L->num_envs) {
+        t_err = "bsim_task: env range out of bounds";
+        return BSIM_E_INVALID;
+    }
     Ctx<R> c = task_ctx<R>(L, s);
-    if (c.d.E == 0) return BSIM_OK;
-    const int TPB = 128;
-    int grid = (c.d.E + TPB - 1) / TPB;
+    if (env_count == 0) return BSIM_OK;
+    // obs staging rows: up to 128 envs per CTA within the default 48 KB
+    const size_t row = (size_t)t->obs_dim * sizeof(R);
+    int tpb = 128;
+    while (tpb > 32 && tpb * row > 48 * 1024) tpb -= 32;
+    if (tpb * row > 48 * 1024) {
+        t_err = "bsim_task: observation too wide";
+        return BSIM_E_TOO_LARGE;
+    }
+    const int grid = (env_count + tpb - 1) / tpb;
+    const size_t smem = tpb * row;
     if (reset)
-        task_reset_kernel<R><<<grid, TPB, 0, (cudaStream_t)stream>>>(c, *t, mask);
+        task_reset_kernel<R><<<grid, tpb, smem, (cudaStream_t)stream>>>(c, *t, mask);
     else
-        task_step_kernel<R><<<grid, TPB, 0, (cudaStream_t)stream>>>(c, *t);
+        task_step_kernel<R><<<grid, tpb, smem, (cudaStream_t)stream>>>(c, *t, env_begin, env_begin + env_count);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? BSIM_OK : t_set_err(reset ? "task_reset_kernel" : "task_step_kernel", e);
 }
@@ -105,18 +138,28 @@ int bsim_randomize_f64(const bsim_layout_t *l, const bsim_state64_t *s, const bs
 }
 
 int bsim_task_step(const bsim_layout_t *l, const bsim_state_t *s, const bsim_task_t *t, void *st) {
-    return launch_task<float>(l, s, t, false, nullptr, st);
+    return launch_task<float>(l, s, t, false, nullptr, 0, -1, st);
 }
 int bsim_task_step_f64(const bsim_layout_t *l, const bsim_state64_t *s, const bsim_task_t *t, void *st) {
-    return launch_task<double>(l, s, t, false, nullptr, st);
+    return launch_task<double>(l, s, t, false, nullptr, 0, -1, st);
 }
 int bsim_task_reset(const bsim_layout_t *l, const bsim_state_t *s, const bsim_task_t *t, const uint8_t *m,
                     void *st) {
-    return launch_task<float>(l, s, t, true, m, st);
+    return launch_task<float>(l, s, t, true, m, 0, -1, st);
 }
 int bsim_task_reset_f64(const bsim_layout_t *l, const bsim_state64_t *s, const bsim_task_t *t, const uint8_t *m,
                         void *st) {
-    return launch_task<double>(l, s, t, true, m, st);
+    return launch_task<double>(l, s, t, true, m, 0, -1, st);
+}
+int bsim_task_step_range(const bsim_layout_t *l, const bsim_state_t *s, const bsim_task_t *t, int32_t env_begin,
+                         int32_t env_count, void *st) {
+    if (env_count < 0) return BSIM_E_INVALID;
+    return launch_task<float>(l, s, t, false, nullptr, env_begin, env_count, st);
+}
+int bsim_task_step_range_f64(const bsim_layout_t *l, const bsim_state64_t *s, const bsim_task_t *t,
+                             int32_t env_begin, int32_t env_count, void *st) {
+    if (env_count < 0) return BSIM_E_INVALID;
+    return launch_task<double>(l, s, t, false, nullptr, env_begin, env_count, st);
 }
 const char *bsim_task_last_error(void) { return t_err.c_str(); }
 

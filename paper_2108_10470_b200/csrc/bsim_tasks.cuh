@@ -14,7 +14,11 @@ namespace bsim {
 
 template <class R> struct TaskView {
     const bsim_task_t &t;
-    BS_HD R *obs(int e) const { return reinterpret_cast<R *>(t.obs) + (size_t)e * t.obs_dim; }
+    R *stage = nullptr;   // optional shared-memory obs rows of envs [stage_e0, ...) (coalesced copy-out)
+    int stage_e0 = 0;
+    BS_HD R *obs(int e) const {
+        return stage ? stage + (size_t)(e - stage_e0) * t.obs_dim : reinterpret_cast<R *>(t.obs) + (size_t)e * t.obs_dim;
+    }
     BS_HD R &reward(int e) const { return reinterpret_cast<R *>(t.reward)[e]; }
     BS_HD R *act(int e) const { return reinterpret_cast<R *>(t.actions) + (size_t)e * t.act_dim; }
     BS_HD R &potential(int e) const { return reinterpret_cast<R *>(t.potentials)[e]; }

@@ -149,3 +149,53 @@ def test_fused_env_step_launch_equals_two_launches(task):
                      (a.scene.dof_state, b.scene.dof_state), (a.reset_count, b.reset_count)):
             assert torch.equal(x, y), t
     assert a.scene.step_count == b.scene.step_count
+
+
+@pytest.mark.parametrize("task,fused,chunks,graph", [("quadruped", False, 3, True), ("quadruped", True, 16, False),
+                                                     ("quadruped", False, 0, False), ("quadruped-anymal-obs", False, 16, True),
+                                                     ("humanoid", False, 3, False), ("humanoid", True, 0, True)])
+def test_host_buffer_step_equals_device_step(task, fused, chunks, graph):
+    """EnvBatch.step_host (numpy actions in, pinned obs / reward / done out;
+    bsim_env_step_host splits the batch into env chunks, each stepped on its
+    own stream while the previous chunk's outputs cross PCIe) == EnvBatch.step,
+    bitwise, through resets and DR, at ragged chunk bounds (131 envs), eager
+    and replayed as the captured graph (bsim_env_step_host_graph; the action
+    uploads re-pointed as the host buffer alternates)."""
+    from paper_2108_10470_b200 import envs as EV
+    kw = dict(num_envs=131, seed=5, episode_length=5, randomize=True)
+    a, b = EV.make_env(task, **kw), EV.make_env(task, **kw)
+    b.host_fused, b.host_chunks, b.host_graph = fused, chunks, graph
+    rng = np.random.default_rng(8)
+    pinned = torch.empty((131, a.act_dim), pin_memory=True)
+    for t in range(12):
+        act = rng.uniform(-1.2, 1.2, (131, a.act_dim)).astype(np.float32)
+        oa = a.step(torch.as_tensor(act, device="cuda"))
+        if t % 2:
+            ob = b.step_host(act)                                  # numpy: staged through the pinned buffer
+        else:
+            pinned.copy_(torch.from_numpy(act))
+            ob = b.step_host(pinned)                               # pinned: read in place
+        assert ob.obs.device.type == "cpu" and ob.obs.is_pinned()
+        for x, y in ((oa.obs, ob.obs), (oa.reward, ob.reward), (oa.done, ob.done),
+                     (oa.info["timeout"], ob.info["timeout"]), (oa.info["poisoned"], ob.info["poisoned"])):
+            assert torch.equal(x.cpu(), y), t
+        assert torch.equal(a.scene.body_q, b.scene.body_q), t
+        assert torch.equal(a.actions, b.actions), t
+    assert a.scene.step_count == b.scene.step_count
+    assert int(a.reset_count.sum()) > 131     # resets happened
+    assert (b._host["graph"] is not None) == graph
+    b.close()
+
+
+def test_envs_per_wave_is_a_whole_wave():
+    """bsim_step_envs_per_wave = SMs x resident CTAs x envs per CTA; the
+    default host-step chunking of 16384 Ant-analog envs is one chunk per wave."""
+    import ctypes as C
+    from paper_2108_10470_b200 import envs as EV
+    env = EV.make_env("quadruped", num_envs=16384)
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    w = C.c_int32(0)
+    lay, _, _ = env.scene._structs()
+    assert env.scene._lib.bsim_step_envs_per_wave(C.byref(lay), 0, C.byref(w)) == 0
+    assert w.value % sms == 0 and w.value >= sms * 16
+    assert env.host_chunk_count() == -(-16384 // w.value)
