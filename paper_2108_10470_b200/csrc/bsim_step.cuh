@@ -318,6 +318,31 @@ BS_HD void joint_item(const Ctx<R> &c, const Ws<R> &w, int e, int j, R h, bool b
     const int kind = REV ? (int)BSIM_REVOLUTE : jt.kind;
     const int p = jt.parent, ch = jt.child;
     R q0 = R(0);
+    // per-env gains / limits / controls: issued first so their L1/L2 latency
+    // hides behind the geometry below (they were the kernel's top long-
+    // scoreboard stalls when loaded at their use)
+    const bool axis = jt.dof >= 0 && kind != BSIM_SPHERICAL;
+    const bool lim = axis && jt.has_limits;
+    int g_mode = 0;
+    R g_arm = R(0), g_tau = R(0), g_kp = R(0), g_kd = R(0), g_tgt = R(0), g_vt = R(0), g_fr = R(0);
+    R g_lo = R(0), g_hi = R(0);
+    if (axis) {
+        const size_t pj = (size_t)j * d.E + e, pd = (size_t)e * d.D + jt.dof;
+        if (biased) {
+            g_mode = (int)c.s.dof_mode[pd];
+            g_arm = c.s.joint_armature[pj];
+            g_tau = c.s.ctrl_dof_force[pd];
+            g_kp = c.s.joint_stiffness[pj];
+            g_kd = c.s.joint_damping[pj];
+            g_tgt = c.s.ctrl_dof_pos_target[pd];
+            g_vt = c.s.ctrl_dof_vel_target[pd];
+            g_fr = c.s.joint_friction[pj];
+        }
+        if (lim) {
+            g_lo = c.s.joint_limit_lo[pj];
+            g_hi = c.s.joint_limit_hi[pj];
+        }
+    }
     if (freeze) {
         R q[3], qd[3];
         int n = joint_dofs<R, REV, IDF>(c, w, j, q, qd);
@@ -386,7 +411,6 @@ BS_HD void joint_item(const Ctx<R> &c, const Ws<R> &w, int e, int j, R h, bool b
     // axis rows: drive (812-848) and limit (850-870), meff (777-788)
     V3<R> y1 = zero3<R>(), y2 = zero3<R>();
     R meff = R(0), DA = R(0), DB = R(0), LF = R(0), FRH = R(0), LV = R(0), LB = R(0);
-    const bool axis = jt.dof >= 0 && kind != BSIM_SPHERICAL;
     if (axis) {
         R k;
         V3<R> x1, x2;
@@ -402,25 +426,23 @@ BS_HD void joint_item(const Ctx<R> &c, const Ws<R> &w, int e, int j, R h, bool b
         y1 = smul(Ic, x1);
         y2 = smul(Ip, x2);
         meff = r_rcp(r_max(k, R(1e-12)));
-        const size_t pj = (size_t)j * d.E + e, pd = (size_t)e * d.D + jt.dof;
         if (biased) {  // drive: lam = LF + clip(DA - DB qd, +-mf h) [+ friction]
-            const int mode = (int)c.s.dof_mode[pd];
-            const R ia = meff + c.s.joint_armature[pj];
+            const int mode = g_mode;
+            const R ia = meff + g_arm;
             const R mf = c.p.max_force;
-            R tau = clampr(c.s.ctrl_dof_force[pd], -mf, mf);
-            R kk = mode == BSIM_MODE_POSITION ? c.s.joint_stiffness[pj] : R(0);
-            R cc = mode == BSIM_MODE_FORCE ? R(0) : c.s.joint_damping[pj];
+            R tau = clampr(g_tau, -mf, mf);
+            R kk = mode == BSIM_MODE_POSITION ? g_kp : R(0);
+            R cc = mode == BSIM_MODE_FORCE ? R(0) : g_kd;
             const R iia = r_rcp(ia);
             const R hden = h * r_rcp(R(1) + h * (h * kk + cc) * iia);
-            R err = c.s.ctrl_dof_pos_target[pd] - q0;
-            DA = (kk * err + cc * c.s.ctrl_dof_vel_target[pd]) * hden;
+            R err = g_tgt - q0;
+            DA = (kk * err + cc * g_vt) * hden;
             DB = (kk * h + cc) * hden;
             LF = mode == BSIM_MODE_FORCE ? tau * h * meff * iia : R(0);
-            R fr = c.s.joint_friction[pj];
-            FRH = fr > R(0) ? fr * h : R(0);
+            FRH = g_fr > R(0) ? g_fr * h : R(0);
         }
-        if (jt.has_limits) {  // limit: q0 in biased passes, start-of-step q otherwise
-            R lo = c.s.joint_limit_lo[pj], hi = c.s.joint_limit_hi[pj];
+        if (lim) {  // limit: q0 in biased passes, start-of-step q otherwise
+            R lo = g_lo, hi = g_hi;
             R q = biased ? q0 : w.at(idf(d, jt.dof, DQ0));
             if (q < lo) {
                 LV = R(1);
