@@ -71,6 +71,21 @@ def _arr(vals):
     return "{" + ", ".join(str(int(v)) for v in vals) + "}"
 
 
+def _packed(vals):
+    """8-bit fields, 8 per 64-bit word (entry i in byte i % 8 of word i // 8):
+    the kernel unpacks entry j with a shift and a mask instead of a dependent
+    load from the joint table (csrc/bsim_step.cuh unpack_u8)."""
+    vals = [int(v) for v in vals] or [0]
+    assert all(0 <= v < 256 for v in vals), vals
+    words = []
+    for w in range(0, len(vals), 8):
+        x = 0
+        for i, v in enumerate(vals[w:w + 8]):
+            x |= v << (8 * i)
+        words.append(f"{x:#x}ull")
+    return "{" + ", ".join(words) + "}"
+
+
 def generate():
     structs, entries, entries_large, sigs = [], [], [], []
     items = [(n, b, False) for n, b in SPECIALISED.items()] + [(n, b, True) for n, b in SPECIALISED_LARGE.items()]
@@ -87,6 +102,7 @@ def generate():
     static constexpr bool has_tendons = {str(L.tendons_per_env > 0).lower()};
     static constexpr bool identity_frames = {str(_identity_frames(L)).lower()};
     static constexpr int star_chain = {_star_chain(L)};
+    static constexpr bool packed_meta = {str(L.joints_per_env <= 16).lower()};   // joint_meta from the packed tables
     static constexpr int kind[] = {_arr(j.kind for j in J)};
     static constexpr int parent[] = {_arr(j.parent for j in J)};
     static constexpr int child[] = {_arr(j.child for j in J)};
@@ -95,6 +111,12 @@ def generate():
     static constexpr int plane_body[] = {_arr(L.plane_body)};
     static constexpr int pair_a[] = {_arr(p[0] for p in L.pair_body)};
     static constexpr int pair_b[] = {_arr(p[1] for p in L.pair_body)};
+    // the same tables bit-packed (8-bit entries; dof stored + 1, kl = kind | limits << 2)
+    static constexpr unsigned long long parent_w[] = {_packed(j.parent for j in J)};
+    static constexpr unsigned long long child_w[] = {_packed(j.child for j in J)};
+    static constexpr unsigned long long dof1_w[] = {_packed(j.dof + 1 for j in J)};
+    static constexpr unsigned long long kl_w[] = {_packed(j.kind | int(j.has_limits) << 2 for j in J)};
+    static constexpr unsigned long long plane_body_w[] = {_packed(L.plane_body)};
 }};""")
         (entries_large if large else entries).append(f"X({tid}, {cname})")
         sigs.append((tid, name, signature(L)))

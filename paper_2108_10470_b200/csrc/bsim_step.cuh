@@ -264,12 +264,17 @@ template <class R> BS_HD void body_external(const Ctx<R> &c, const Ws<R> &w, int
 // leaves the binary (smaller kernel, fewer instruction-cache misses).
 // IDF = every joint frame has identity orientation (origin / child quats):
 // the frame products fold away.
+// a joint's topology fields (joint_meta below)
+struct JMeta {
+    int kind, parent, child, dof, limits;
+};
+
 template <class R, bool REV = false, bool IDF = false>
-BS_HD int joint_dofs(const Ctx<R> &c, const Ws<R> &w, int j, R *q, R *qd) {
+BS_HD int joint_dofs(const Ctx<R> &c, const Ws<R> &w, int j, R *q, R *qd, const JMeta *jm = nullptr) {
     const auto &jt = c.joints[j];
-    const int kind = REV ? (int)BSIM_REVOLUTE : jt.kind;
+    const int kind = REV ? (int)BSIM_REVOLUTE : (jm ? jm->kind : jt.kind);
     const Dims &d = c.d;
-    int p = jt.parent, ch = jt.child;
+    int p = jm ? jm->parent : jt.parent, ch = jm ? jm->child : jt.child;
     Q4<R> qp = w.l4(ib(d, p, BQ)), qc = w.l4(ib(d, ch, BQ));
     Q4<R> jqp = IDF ? qp : qmul(qp, jq4(jt.origin_quat)), jqc = IDF ? qc : qmul(qc, jq4(jt.child_quat));
     V3<R> wp = w.l3(ib(d, p, BW)), wc = w.l3(ib(d, ch, BW));
@@ -300,6 +305,52 @@ BS_HD int joint_dofs(const Ctx<R> &c, const Ws<R> &w, int j, R *q, R *qd) {
     return 0;
 }
 
+// Joint j's topology fields.  AOT topologies unpack them from the bit-packed
+// compile-time tables of bsim_topologies.cuh (a shift and a mask, no memory
+// access); the generic kernel reads the joint table (a dependent global load
+// the slot's geometry has to wait for).
+enum { TF_PARENT = 0, TF_CHILD = 1, TF_DOF1 = 2, TF_KL = 3, TF_PLANE = 4 };
+template <class T, int F, int K> BS_HD unsigned long long topo_word() {
+    if constexpr (F == TF_PARENT) { constexpr unsigned long long v = T::parent_w[K]; return v; }
+    else if constexpr (F == TF_CHILD) { constexpr unsigned long long v = T::child_w[K]; return v; }
+    else if constexpr (F == TF_DOF1) { constexpr unsigned long long v = T::dof1_w[K]; return v; }
+    else if constexpr (F == TF_KL) { constexpr unsigned long long v = T::kl_w[K]; return v; }
+    else { constexpr unsigned long long v = T::plane_body_w[K]; return v; }
+}
+template <class T, int F> constexpr int topo_words() {
+    if constexpr (F == TF_PARENT) return sizeof(T::parent_w) / 8;
+    else if constexpr (F == TF_CHILD) return sizeof(T::child_w) / 8;
+    else if constexpr (F == TF_DOF1) return sizeof(T::dof1_w) / 8;
+    else if constexpr (F == TF_KL) return sizeof(T::kl_w) / 8;
+    else return sizeof(T::plane_body_w) / 8;
+}
+template <class T, int F, int K = 0> BS_HD unsigned long long topo_select(int word) {
+    if constexpr (K + 1 >= topo_words<T, F>()) return topo_word<T, F, K>();
+    else return word == K ? topo_word<T, F, K>() : topo_select<T, F, K + 1>(word);
+}
+template <class T, int F> BS_HD int topo_entry(int i) {
+    return (int)((topo_select<T, F>(i >> 3) >> ((i & 7) << 3)) & 0xffull);
+}
+template <class T> constexpr bool topo_packed() {
+    if constexpr (T::is_static) return T::packed_meta; else return false;
+}
+// (more than two words per field measured slower for the 21-joint humanoid:
+// the select chain and its registers cost more than the load it replaces)
+template <class T, class R> BS_HD JMeta joint_meta(const Ctx<R> &c, int j) {
+    if constexpr (topo_packed<T>()) {
+        const int kl = topo_entry<T, TF_KL>(j);
+        return JMeta{kl & 3, topo_entry<T, TF_PARENT>(j), topo_entry<T, TF_CHILD>(j), topo_entry<T, TF_DOF1>(j) - 1,
+                     kl >> 2};
+    } else {
+        const auto &jt = c.joints[j];
+        return JMeta{jt.kind, jt.parent, jt.child, jt.dof, jt.has_limits};
+    }
+}
+template <class T, class R> BS_HD int plane_body_of(const Ctx<R> &c, int i) {
+    if constexpr (topo_packed<T>()) return topo_entry<T, TF_PLANE>(i);
+    else return c.L.plane_body[i];
+}
+
 // Phase A of joint j for one pass, fused: geometry (freeze physics.py:660-680,
 // refresh 733-756; `deltas`: the effective pose pos + dpos / BQE), the
 // velocity-independent row constants (the algebra of physics.py:777-928 with
@@ -311,23 +362,24 @@ BS_HD int joint_dofs(const Ctx<R> &c, const Ws<R> &w, int j, R *q, R *qd) {
 // (read_dof_states, physics.py:557) seed q0, the unbiased limit rows' q and
 // the DOF impulse accumulators.  Per-env gains / limits / controls are read
 // from HBM (L1/L2 resident).
-template <class R, bool REV = false, bool IDF = false>
+template <class R, class T, bool REV = false, bool IDF = false>
 BS_HD void joint_item(const Ctx<R> &c, const Ws<R> &w, int e, int j, R h, bool biased, bool freeze, bool deltas) {
     const Dims &d = c.d;
     const auto &jt = c.joints[j];
-    const int kind = REV ? (int)BSIM_REVOLUTE : jt.kind;
-    const int p = jt.parent, ch = jt.child;
+    const JMeta jm = joint_meta<T>(c, j);
+    const int kind = REV ? (int)BSIM_REVOLUTE : jm.kind;
+    const int p = jm.parent, ch = jm.child, jdof = jm.dof;
     R q0 = R(0);
     // per-env gains / limits / controls: issued first so their L1/L2 latency
     // hides behind the geometry below (they were the kernel's top long-
     // scoreboard stalls when loaded at their use)
-    const bool axis = jt.dof >= 0 && kind != BSIM_SPHERICAL;
-    const bool lim = axis && jt.has_limits;
+    const bool axis = jdof >= 0 && kind != BSIM_SPHERICAL;
+    const bool lim = axis && jm.limits;
     int g_mode = 0;
     R g_arm = R(0), g_tau = R(0), g_kp = R(0), g_kd = R(0), g_tgt = R(0), g_vt = R(0), g_fr = R(0);
     R g_lo = R(0), g_hi = R(0);
     if (axis) {
-        const size_t pj = (size_t)j * d.E + e, pd = (size_t)e * d.D + jt.dof;
+        const size_t pj = (size_t)j * d.E + e, pd = (size_t)e * d.D + jdof;
         if (biased) {
             g_mode = (int)c.s.dof_mode[pd];
             g_arm = c.s.joint_armature[pj];
@@ -345,10 +397,10 @@ BS_HD void joint_item(const Ctx<R> &c, const Ws<R> &w, int e, int j, R h, bool b
     }
     if (freeze) {
         R q[3], qd[3];
-        int n = joint_dofs<R, REV, IDF>(c, w, j, q, qd);
+        int n = joint_dofs<R, REV, IDF>(c, w, j, q, qd, &jm);
         for (int kk = 0; kk < n; ++kk) {
-            w.at(idf(d, jt.dof + kk, DQ0)) = q[kk];
-            w.at(idf(d, jt.dof + kk, DIMP)) = R(0);
+            w.at(idf(d, jdof + kk, DQ0)) = q[kk];
+            w.at(idf(d, jdof + kk, DIMP)) = R(0);
         }
         if (n == 1) q0 = q[0];
     }
@@ -364,7 +416,7 @@ BS_HD void joint_item(const Ctx<R> &c, const Ws<R> &w, int e, int j, R h, bool b
     Q4<R> qe = qmul(jqc, qconj(jqp));
     V3<R> rerr = qvec(qe) * (R(2) * signr(qe.w));
     V3<R> a = qrot(jqp, jv3(jt.axis));
-    if (!freeze && jt.dof >= 0) {
+    if (!freeze && jdof >= 0) {
         if (kind == BSIM_REVOLUTE) {
             Q4<R> qr = qmul(qconj(jqp), jqc);
             q0 = wrap_pi(R(2) * r_atan2(dot(qvec(qr), jv3(jt.axis)), qr.w));
@@ -443,7 +495,7 @@ BS_HD void joint_item(const Ctx<R> &c, const Ws<R> &w, int e, int j, R h, bool b
         }
         if (lim) {  // limit: q0 in biased passes, start-of-step q otherwise
             R lo = g_lo, hi = g_hi;
-            R q = biased ? q0 : w.at(idf(d, jt.dof, DQ0));
+            R q = biased ? q0 : w.at(idf(d, jdof, DQ0));
             if (q < lo) {
                 LV = R(1);
                 LB = biased ? r_max(lo - q, R(0)) * r_rcp(h) : R(0);
@@ -478,10 +530,10 @@ template <class R> BS_HD V3<R> plane_x2(V3<R> r) { return v3(R(0), r.z, -r.y); }
 // friction anchor of this slot is consumed here (terr0) and immediately
 // replaced by its end-of-step value (physics.py:1021-1033 depends only on
 // frozen quantities).
-template <class R> BS_HD void plane_freeze(const Ctx<R> &c, const Ws<R> &w, int e, int i) {
+template <class R> BS_HD void plane_freeze(const Ctx<R> &c, const Ws<R> &w, int e, int i, int b = -1) {
     const Dims &d = c.d;
     const auto &p = c.p;
-    int b = c.L.plane_body[i];
+    if (b < 0) b = c.L.plane_body[i];
     const R *off = c.s.plane_off + 3 * ((size_t)i * d.E + e);
     R rad = c.s.plane_rad[(size_t)i * d.E + e];
     V3<R> arm = qrot(w.l4(ib(d, b, BQ)), jv3(off));
@@ -624,9 +676,9 @@ template <class R> BS_HD void pair_freeze(const Ctx<R> &c, const Ws<R> &w, int e
 }
 
 // contact row constants from the current inertia (physics.py:993-1006)
-template <class R> BS_HD void plane_constants(const Ctx<R> &c, const Ws<R> &w, int i) {
+template <class R> BS_HD void plane_constants(const Ctx<R> &c, const Ws<R> &w, int i, int b = -1) {
     const Dims &d = c.d;
-    int b = c.L.plane_body[i];
+    if (b < 0) b = c.L.plane_body[i];
     R im = w.at(ib(d, b, BM));
     S3<R> I = w.lS(ib(d, b, BI));
     V3<R> r = w.l3(ipl(d, i, CR));
@@ -655,9 +707,9 @@ template <class R> BS_HD void pair_constants(const Ctx<R> &c, const Ws<R> &w, in
 
 // per-pass contact constants: normal target and stiction (942-973; dpos is
 // fixed during a pass)
-template <class R> BS_HD void plane_pass_constants(const Ctx<R> &c, const Ws<R> &w, int i, bool biased) {
+template <class R> BS_HD void plane_pass_constants(const Ctx<R> &c, const Ws<R> &w, int i, bool biased, int b = -1) {
     const Dims &d = c.d;
-    const int b = c.L.plane_body[i];
+    if (b < 0) b = c.L.plane_body[i];
     const R idt = r_rcp(c.p.dt);
     R depth = w.at(ipl(d, i, CD0));
     R bias = R(0), st1 = R(0), st2 = R(0);
@@ -1251,13 +1303,14 @@ template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> 
             BS_SYNC();
         }
         BS_ITEMS(g, d.J, el, j) {
-            joint_item<R, topo_rev<T>(), topo_idf<T>()>(c, g.env(el), g.e0 + el, j, h, biased, freeze, deltas);
+            joint_item<R, T, topo_rev<T>(), topo_idf<T>()>(c, g.env(el), g.e0 + el, j, h, biased, freeze, deltas);
         }
         BS_ITEMS(g, d.P, el, i) {
             Ws<R> w = g.env(el);
-            if (freeze) plane_freeze(c, w, g.e0 + el, i);
-            plane_constants(c, w, i);
-            plane_pass_constants(c, w, i, biased);
+            const int pb = plane_body_of<T>(c, i);
+            if (freeze) plane_freeze(c, w, g.e0 + el, i, pb);
+            plane_constants(c, w, i, pb);
+            plane_pass_constants(c, w, i, biased, pb);
         }
         if (topo_pairs<T>()) {
             BS_ITEMS(g, d.Q, el, i) {
