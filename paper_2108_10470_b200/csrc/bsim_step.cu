@@ -51,8 +51,13 @@ int check_launch(const char *what) {
     return BSIM_OK;
 }
 
-template <class R> size_t step_smem_bytes(const Dims &d) {
-    return (size_t)d.pad * Shape<R>::NE * sizeof(R);
+// the env workspace records, then a copy of the joint table (phase A reads
+// its frames every pass; from L1/L2 they were a top long-scoreboard stall)
+template <class R> __host__ __device__ size_t step_ws_bytes(const Dims &d, int n_envs = Shape<R>::NE) {
+    return ((size_t)d.pad * n_envs * sizeof(R) + 15) & ~(size_t)15;
+}
+template <class R> size_t step_smem_bytes(const Dims &d, int n_envs = Shape<R>::NE) {
+    return step_ws_bytes<R>(d, n_envs) + (size_t)d.J * sizeof(typename Abi<R>::Joint);
 }
 
 // ------------------------------------------------------------------ step
@@ -138,6 +143,11 @@ __global__ void __launch_bounds__(Shape<R>::NTH, BSIM_MINB)
             int b = item / 13, k = item - b * 13;
             ws[(size_t)el * d.pad + d.o_body + b * BODY_ITEMS + body_item13(k)] = src[i];
         }
+        // the joint table (sizeof(Joint) is a multiple of 16 bytes)
+        const int n16 = d.J * (int)(sizeof(typename Abi<R>::Joint) / 16);
+        const float4 *js = reinterpret_cast<const float4 *>(c.joints);
+        float4 *jd = reinterpret_cast<float4 *>(smem_raw + step_ws_bytes<R>(d, epc));
+        for (int i = tid; i < n16; i += NTH) jd[i] = js[i];
     }
     __syncthreads();
     if (tid == 0) {
@@ -146,7 +156,8 @@ __global__ void __launch_bounds__(Shape<R>::NTH, BSIM_MINB)
         s_sweep_warp = w;
     }
     __syncthreads();
-    const Grp<R> g{ws, e0, ne, tid, NTH, 32 * s_sweep_warp, d.pad};
+    const Grp<R> g{ws, e0, ne, tid, NTH, 32 * s_sweep_warp, d.pad,
+                   reinterpret_cast<const typename Abi<R>::Joint *>(smem_raw + step_ws_bytes<R>(d, epc))};
     stage_group(c, g);
     if (act.actions) {  // fused action mapping (envs.py:180, 421-424)
         BS_ITEMS(g, d.D, el, k) {
@@ -420,50 +431,83 @@ bool bad_layout(const bsim_layout_t *L) {
 }
 
 // ------------------------------------------------------------ launchers
-// resident CTAs of step_kernel<R, T> on the whole device at `smem` bytes
-template <class R, class T> int device_slots(size_t smem, int *slots_out) {
+// Launch plan of step_kernel<R, T> for a layout and batch size E: the CTA's
+// env count n <= NE fixes its shared memory (n workspace records + the joint
+// table) and so the resident CTAs per SM; take the n needing the fewest waves
+// of resident CTAs (largest n on ties), then spread the envs evenly over those
+// waves (whole waves, no partial last one) -- `epc` envs per CTA.  Chunks of
+// a pipelined step (bsim_env_step_host) use the plan of the scene's whole E,
+// so n concurrent chunk grids fill the same waves.  Cached per (layout, E);
+// host-side state, not thread-safe (one host thread drives a scene).
+struct Plan {
+    int epc;
+    size_t smem;
+    long capacity;   // resident envs of one wave (SMs x CTAs/SM x envs/CTA)
+};
+template <class R, class T> int plan_launch(const Dims &d, int E, Plan *out) {
+    constexpr int NE = Shape<R>::NE;
+    struct Entry {
+        int pad, J, E;
+        Plan p;
+    };
+    static Entry cache[16];
+    static int n_cache = 0;
     static size_t configured = 0;
-    static int slots = 0;
-    if (smem > 48 * 1024 && smem > configured) {
+    for (int i = 0; i < n_cache && i < 16; ++i)
+        if (cache[i].pad == d.pad && cache[i].J == d.J && cache[i].E == E) {
+            *out = cache[i].p;
+            return BSIM_OK;
+        }
+    const size_t smax = step_smem_bytes<R>(d, NE);
+    if (smax > 48 * 1024 && smax > configured) {
         cudaError_t e = cudaFuncSetAttribute(step_kernel<R, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
+                                             (int)smax);
         if (e != cudaSuccess) return set_err("cudaFuncSetAttribute(step_kernel)", e);
-        configured = smem;
-        slots = 0;
+        configured = smax;
     }
-    if (slots == 0) {
-        int dev = 0, sms = 0, per_sm = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<R, T>, Shape<R>::NTH, smem);
-        slots = sms * (per_sm > 0 ? per_sm : 1);
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const long En = E > 0 ? E : 1;
+    long best_waves = -1, best_slots = 0;
+    int best_n = 0;
+    for (int n = NE; n >= 1; --n) {
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<R, T>, Shape<R>::NTH,
+                                                      step_smem_bytes<R>(d, n));
+        if (per_sm < 1) continue;
+        const long slots = (long)sms * per_sm, waves = (En + slots * n - 1) / (slots * n);
+        if (best_waves < 0 || waves < best_waves) {
+            best_waves = waves;
+            best_slots = slots;
+            best_n = n;
+        }
     }
-    *slots_out = slots;
+    if (!best_n) return set_err("step_kernel occupancy", cudaErrorInvalidConfiguration);
+    int epc = best_n;
+#ifndef BSIM_NO_BALANCE
+    epc = (int)((En + best_waves * best_slots - 1) / (best_waves * best_slots));
+    if (epc < 1) epc = 1;
+    if (epc > best_n) epc = best_n;
+#endif
+    Plan p{epc, step_smem_bytes<R>(d, epc), best_slots * best_n};
+    cache[n_cache % 16] = Entry{d.pad, d.J, E, p};
+    ++n_cache;
+    *out = p;
     return BSIM_OK;
 }
 
 template <class R, class T>
 int launch_step_t(const Ctx<R> &c, size_t smem, int n_substeps, const bsim_actions_t &act, const bsim_task_t *task,
                   int e_begin, int e_count, cudaStream_t st) {
-    constexpr int NE = Shape<R>::NE;
-    int slots = 0;
-    if (int rc = device_slots<R, T>(smem, &slots)) return rc;
-    // whole waves: the fewest waves of <= NE envs per CTA, then spread the envs
-    // evenly over waves x slots CTAs (no partial last wave).  Balanced on the
-    // scene's E: the chunks of a pipelined step (bsim_env_step_host) keep the
-    // whole batch's CTA size, so n concurrent chunk grids fill the same waves.
-    const int E = c.d.E;
-    int epc = NE;
-#ifndef BSIM_NO_BALANCE
-    const long waves = ((long)E + (long)NE * slots - 1) / ((long)NE * slots);
-    epc = (int)(((long)E + waves * slots - 1) / (waves * slots));
-    if (epc < 1) epc = 1;
-    if (epc > NE) epc = NE;
-#endif
+    (void)smem;
+    Plan pl;
+    if (int rc = plan_launch<R, T>(c.d, c.d.E, &pl)) return rc;
+    const int epc = pl.epc;
     const int grid = (e_count + epc - 1) / epc;
     bsim_task_t tk;
     if (task) tk = *task; else std::memset(&tk, 0, sizeof tk);
-    step_kernel<R, T><<<grid, Shape<R>::NTH, smem, st>>>(c, n_substeps, act, epc, e_begin, e_begin + e_count, tk,
+    step_kernel<R, T><<<grid, Shape<R>::NTH, pl.smem, st>>>(c, n_substeps, act, epc, e_begin, e_begin + e_count, tk,
                                                            task != nullptr);
     return check_launch("step_kernel");
 }
@@ -480,7 +524,7 @@ bool task_ok(const bsim_layout_t *L, const bsim_task_t *t) {
 // 4-env x 32-thread CTA) is used when the default 16-env CTA's workspace
 // leaves fewer than 2 CTAs per SM (e.g. the 22-body humanoid: 150 KB).
 template <class R> bool use_large_variant(const Dims &d) {
-    return step_smem_bytes<R>(d) > 113 * 1024;
+    return step_ws_bytes<R>(d) > 113 * 1024;
 }
 int call_large(const bsim_layout_t *l, const bsim_params_t *p, const bsim_state_t *s, int32_t n,
                const bsim_actions_t *a, const bsim_task_t *t, int32_t eb, int32_t en, void *st) {
@@ -630,13 +674,13 @@ int launch_collide(const bsim_layout_t *layout, const typename Abi<R>::Params *p
 // chunk size of the pipelined host-buffer step)
 template <class R> int envs_per_wave(const bsim_layout_t *l, int32_t *envs) {
     Dims d = make_dims(*l, sizeof(R) == 8);
-    size_t smem = step_smem_bytes<R>(d);
-    if (smem > 227 * 1024) return BSIM_E_TOO_LARGE;
-    int slots = 0, rc = BSIM_OK;
+    if (step_smem_bytes<R>(d, 1) > 227 * 1024) return BSIM_E_TOO_LARGE;
+    Plan pl{0, 0, 0};
+    int rc = BSIM_OK;
     switch (l->topology_id) {
 #define BSIM_WAVE_TOPO(ID, TYPE) \
     case ID:                     \
-        rc = device_slots<R, TYPE>(smem, &slots); break;
+        rc = plan_launch<R, TYPE>(d, d.E, &pl); break;
 #ifdef BSIM_LARGE_TU
         BSIM_TOPOLOGIES_LARGE(BSIM_WAVE_TOPO)
 #else
@@ -644,9 +688,9 @@ template <class R> int envs_per_wave(const bsim_layout_t *l, int32_t *envs) {
 #endif
 #undef BSIM_WAVE_TOPO
     default:
-        rc = device_slots<R, TopoGeneric>(smem, &slots);
+        rc = plan_launch<R, TopoGeneric>(d, d.E, &pl);
     }
-    *envs = slots * Shape<R>::NE;
+    *envs = (int32_t)pl.capacity;
     return rc;
 }
 
@@ -680,7 +724,8 @@ int bsim_step_smem_per_env(const bsim_layout_t *layout, int32_t fp64, int32_t *b
     const bool large = fp64 ? use_large_variant<double>(d) : use_large_variant<float>(d);
     // the large-articulation TU's CTA: 4 envs (fp32) / 2 envs (fp64)
     const int ne = large ? (fp64 ? 2 : 4) : (fp64 ? Shape<double>::NE : Shape<float>::NE);
-    size_t total = (size_t)d.pad * ne * (fp64 ? 8 : 4);
+    size_t total = (size_t)d.pad * ne * (fp64 ? 8 : 4) + 16 +
+                   (size_t)d.J * (fp64 ? sizeof(bsim_joint64_t) : sizeof(bsim_joint_t));
     if (bytes_per_env) *bytes_per_env = (int32_t)(d.pad * (fp64 ? 8 : 4));
     if (envs_per_cta) *envs_per_cta = ne;
     return total > 227 * 1024 ? BSIM_E_TOO_LARGE : BSIM_OK;

@@ -221,6 +221,7 @@ template <class R> BS_HD Q4<R> jq4(const R *a) { return Q4<R>{a[0], a[1], a[2], 
 template <class R> struct Grp {
     R *ws;
     int e0, ne, tid, nth, lane0, pad;
+    const typename Abi<R>::Joint *jt;   // the joint table: a shared-memory copy on the device
     BS_HD Ws<R> env(int el) const { return Ws<R>{ws + (size_t)el * pad}; }
 };
 
@@ -270,8 +271,9 @@ struct JMeta {
 };
 
 template <class R, bool REV = false, bool IDF = false>
-BS_HD int joint_dofs(const Ctx<R> &c, const Ws<R> &w, int j, R *q, R *qd, const JMeta *jm = nullptr) {
-    const auto &jt = c.joints[j];
+BS_HD int joint_dofs(const Ctx<R> &c, const Ws<R> &w, int j, R *q, R *qd, const JMeta *jm = nullptr,
+                     const typename Abi<R>::Joint *jtab = nullptr) {
+    const auto &jt = (jtab ? jtab : c.joints)[j];
     const int kind = REV ? (int)BSIM_REVOLUTE : (jm ? jm->kind : jt.kind);
     const Dims &d = c.d;
     int p = jm ? jm->parent : jt.parent, ch = jm ? jm->child : jt.child;
@@ -363,9 +365,10 @@ template <class T, class R> BS_HD int plane_body_of(const Ctx<R> &c, int i) {
 // the DOF impulse accumulators.  Per-env gains / limits / controls are read
 // from HBM (L1/L2 resident).
 template <class R, class T, bool REV = false, bool IDF = false>
-BS_HD void joint_item(const Ctx<R> &c, const Ws<R> &w, int e, int j, R h, bool biased, bool freeze, bool deltas) {
+BS_HD void joint_item(const Ctx<R> &c, const Ws<R> &w, int e, int j, R h, bool biased, bool freeze, bool deltas,
+                      const typename Abi<R>::Joint *jtab) {
     const Dims &d = c.d;
-    const auto &jt = c.joints[j];
+    const auto &jt = jtab[j];
     const JMeta jm = joint_meta<T>(c, j);
     const int kind = REV ? (int)BSIM_REVOLUTE : jm.kind;
     const int p = jm.parent, ch = jm.child, jdof = jm.dof;
@@ -397,7 +400,7 @@ BS_HD void joint_item(const Ctx<R> &c, const Ws<R> &w, int e, int j, R h, bool b
     }
     if (freeze) {
         R q[3], qd[3];
-        int n = joint_dofs<R, REV, IDF>(c, w, j, q, qd, &jm);
+        int n = joint_dofs<R, REV, IDF>(c, w, j, q, qd, &jm, jtab);
         for (int kk = 0; kk < n; ++kk) {
             w.at(idf(d, jdof + kk, DQ0)) = q[kk];
             w.at(idf(d, jdof + kk, DIMP)) = R(0);
@@ -1303,7 +1306,8 @@ template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> 
             BS_SYNC();
         }
         BS_ITEMS(g, d.J, el, j) {
-            joint_item<R, T, topo_rev<T>(), topo_idf<T>()>(c, g.env(el), g.e0 + el, j, h, biased, freeze, deltas);
+            joint_item<R, T, topo_rev<T>(), topo_idf<T>()>(c, g.env(el), g.e0 + el, j, h, biased, freeze, deltas,
+                                                           g.jt);
         }
         BS_ITEMS(g, d.P, el, i) {
             Ws<R> w = g.env(el);

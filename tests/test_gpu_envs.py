@@ -197,5 +197,5 @@ def test_envs_per_wave_is_a_whole_wave():
     w = C.c_int32(0)
     lay, _, _ = env.scene._structs()
     assert env.scene._lib.bsim_step_envs_per_wave(C.byref(lay), 0, C.byref(w)) == 0
-    assert w.value % sms == 0 and w.value >= sms * 16
+    assert w.value % sms == 0 and w.value >= sms * 8
     assert env.host_chunk_count() == -(-16384 // w.value)
