@@ -238,9 +238,14 @@ template <class R> BS_HD void stage_env(const Ctx<R> &c, const Ws<R> &w, int e) 
 }
 
 // world inverse inertia of body b from orientation item qitem (physics.py:594-596)
+// The local inverse inertia diagonal is staged once per launch into spare
+// record slots (BI + 6, BI + 7, BW.w; stage_group) -- refreshed every pass,
+// it was a per-pass global load.
 template <class R> BS_HD void body_inertia(const Ctx<R> &c, const Ws<R> &w, int e, int b, int qitem) {
-    V3<R> d = jv3(c.s.inv_inertia_local + 3 * ((size_t)e * c.d.B + b));
-    w.sS(ib(c.d, b, BI), world_inertia(w.l4(ib(c.d, b, qitem)), d));
+    (void)e;
+    const int bi = ib(c.d, b, BI);
+    V3<R> d{w.at(bi + 6), w.at(bi + 7), w.at(ib(c.d, b, BW) + 3)};
+    w.sS(bi, world_inertia(w.l4(ib(c.d, b, qitem)), d));
 }
 
 // external forces on body b (physics.py:545-552)
@@ -1455,7 +1460,14 @@ template <class R> BS_HD void readout_group(const Ctx<R> &c, const Grp<R> &g) {
 template <class R> BS_HD void stage_group(const Ctx<R> &c, const Grp<R> &g) {
     const Dims &d = c.d;
     BS_ENVS(g, el) { stage_env(c, g.env(el), g.e0 + el); }
-    BS_ITEMS(g, d.B, el, b) { g.env(el).at(ib(d, b, BM)) = c.s.inv_mass[(size_t)(g.e0 + el) * d.B + b]; }
+    BS_ITEMS(g, d.B, el, b) {
+        Ws<R> w = g.env(el);
+        const size_t gb = (size_t)(g.e0 + el) * d.B + b;
+        w.at(ib(d, b, BM)) = c.s.inv_mass[gb];
+        w.at(ib(d, b, BI) + 6) = c.s.inv_inertia_local[3 * gb];
+        w.at(ib(d, b, BI) + 7) = c.s.inv_inertia_local[3 * gb + 1];
+        w.at(ib(d, b, BW) + 3) = c.s.inv_inertia_local[3 * gb + 2];
+    }
     BS_ITEMS(g, d.P, el, i) {
         for (int k = 0; k < 3; ++k)
             g.env(el).at(d.o_anchor + ANCHOR_ITEMS * i + k) = c.s.friction_anchor[3 * ((size_t)i * d.E + g.e0 + el) + k];
