@@ -57,7 +57,7 @@ template <class R> __host__ __device__ size_t step_ws_bytes(const Dims &d, int n
     return ((size_t)d.pad * n_envs * sizeof(R) + 15) & ~(size_t)15;
 }
 template <class R> size_t step_smem_bytes(const Dims &d, int n_envs = Shape<R>::NE) {
-    return step_ws_bytes<R>(d, n_envs) + (size_t)d.J * sizeof(typename Abi<R>::Joint);
+    return step_ws_bytes<R>(d, n_envs) + (size_t)d.J * jtab_stride_smem<R>();
 }
 
 // ------------------------------------------------------------------ step
@@ -144,10 +144,10 @@ __global__ void __launch_bounds__(Shape<R>::NTH, BSIM_MINB)
             ws[(size_t)el * d.pad + d.o_body + b * BODY_ITEMS + body_item13(k)] = src[i];
         }
         // the joint table (sizeof(Joint) is a multiple of 16 bytes)
-        const int n16 = d.J * (int)(sizeof(typename Abi<R>::Joint) / 16);
+        constexpr int rec16 = (int)(sizeof(typename Abi<R>::Joint) / 16), str16 = jtab_stride_smem<R>() / 16;
         const float4 *js = reinterpret_cast<const float4 *>(c.joints);
         float4 *jd = reinterpret_cast<float4 *>(smem_raw + step_ws_bytes<R>(d, epc));
-        for (int i = tid; i < n16; i += NTH) jd[i] = js[i];
+        for (int i = tid; i < d.J * rec16; i += NTH) jd[(i / rec16) * str16 + i % rec16] = js[i];
     }
     __syncthreads();
     if (tid == 0) {
@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(Shape<R>::NTH, BSIM_MINB)
     }
     __syncthreads();
     const Grp<R> g{ws, e0, ne, tid, NTH, 32 * s_sweep_warp, d.pad,
-                   reinterpret_cast<const typename Abi<R>::Joint *>(smem_raw + step_ws_bytes<R>(d, epc))};
+                   JTab<R>{smem_raw + step_ws_bytes<R>(d, epc), jtab_stride_smem<R>()}};
     stage_group(c, g);
     if (act.actions) {  // fused action mapping (envs.py:180, 421-424)
         BS_ITEMS(g, d.D, el, k) {
@@ -725,7 +725,7 @@ int bsim_step_smem_per_env(const bsim_layout_t *layout, int32_t fp64, int32_t *b
     // the large-articulation TU's CTA: 4 envs (fp32) / 2 envs (fp64)
     const int ne = large ? (fp64 ? 2 : 4) : (fp64 ? Shape<double>::NE : Shape<float>::NE);
     size_t total = (size_t)d.pad * ne * (fp64 ? 8 : 4) + 16 +
-                   (size_t)d.J * (fp64 ? sizeof(bsim_joint64_t) : sizeof(bsim_joint_t));
+                   (size_t)d.J * (fp64 ? sizeof(bsim_joint64_t) + 16 : sizeof(bsim_joint_t) + 16);
     if (bytes_per_env) *bytes_per_env = (int32_t)(d.pad * (fp64 ? 8 : 4));
     if (envs_per_cta) *envs_per_cta = ne;
     return total > 227 * 1024 ? BSIM_E_TOO_LARGE : BSIM_OK;

@@ -218,10 +218,22 @@ template <class R> BS_HD Q4<R> jq4(const R *a) { return Q4<R>{a[0], a[1], a[2], 
 
 // CTA-level view: thread `tid` of `nth`, envs [e0, e0 + ne) in the workspace;
 // per-env serial work (the sweep) runs on threads [lane0, lane0 + ne).
+// A joint table with a byte stride: the device copy in shared memory pads
+// each 128 / 224-byte record by 16 bytes so the different joints a warp's
+// lanes read fall in different banks.
+template <class R> struct JTab {
+    const unsigned char *base;
+    int stride;
+    BS_HD const typename Abi<R>::Joint &operator[](int j) const {
+        return *reinterpret_cast<const typename Abi<R>::Joint *>(base + (size_t)j * stride);
+    }
+};
+template <class R> constexpr int jtab_stride_smem() { return (int)sizeof(typename Abi<R>::Joint) + 16; }
+
 template <class R> struct Grp {
     R *ws;
     int e0, ne, tid, nth, lane0, pad;
-    const typename Abi<R>::Joint *jt;   // the joint table: a shared-memory copy on the device
+    JTab<R> jt;   // the joint table: a shared-memory copy on the device
     BS_HD Ws<R> env(int el) const { return Ws<R>{ws + (size_t)el * pad}; }
 };
 
@@ -277,8 +289,8 @@ struct JMeta {
 
 template <class R, bool REV = false, bool IDF = false>
 BS_HD int joint_dofs(const Ctx<R> &c, const Ws<R> &w, int j, R *q, R *qd, const JMeta *jm = nullptr,
-                     const typename Abi<R>::Joint *jtab = nullptr) {
-    const auto &jt = (jtab ? jtab : c.joints)[j];
+                     const JTab<R> *jtab = nullptr) {
+    const auto &jt = jtab ? (*jtab)[j] : c.joints[j];
     const int kind = REV ? (int)BSIM_REVOLUTE : (jm ? jm->kind : jt.kind);
     const Dims &d = c.d;
     int p = jm ? jm->parent : jt.parent, ch = jm ? jm->child : jt.child;
@@ -371,7 +383,7 @@ template <class T, class R> BS_HD int plane_body_of(const Ctx<R> &c, int i) {
 // from HBM (L1/L2 resident).
 template <class R, class T, bool REV = false, bool IDF = false>
 BS_HD void joint_item(const Ctx<R> &c, const Ws<R> &w, int e, int j, R h, bool biased, bool freeze, bool deltas,
-                      const typename Abi<R>::Joint *jtab) {
+                      const JTab<R> &jtab) {
     const Dims &d = c.d;
     const auto &jt = jtab[j];
     const JMeta jm = joint_meta<T>(c, j);
@@ -405,7 +417,7 @@ BS_HD void joint_item(const Ctx<R> &c, const Ws<R> &w, int e, int j, R h, bool b
     }
     if (freeze) {
         R q[3], qd[3];
-        int n = joint_dofs<R, REV, IDF>(c, w, j, q, qd, &jm, jtab);
+        int n = joint_dofs<R, REV, IDF>(c, w, j, q, qd, &jm, &jtab);
         for (int kk = 0; kk < n; ++kk) {
             w.at(idf(d, jdof + kk, DQ0)) = q[kk];
             w.at(idf(d, jdof + kk, DIMP)) = R(0);

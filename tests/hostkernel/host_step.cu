@@ -28,7 +28,8 @@ static void run_t(const bsim_layout_t *L, const typename Abi<R>::Params *p, cons
     for (int e0 = 0; e0 < E; e0 += NE) {
         const int ne = E - e0 < NE ? E - e0 : NE;
         std::fill(buf.begin(), buf.end(), R(1e30));   // poison: catches unstaged reads
-        Grp<R> g{buf.data(), e0, ne, 0, 1, 0, d.pad, c.joints};
+        Grp<R> g{buf.data(), e0, ne, 0, 1, 0, d.pad,
+                 JTab<R>{reinterpret_cast<const unsigned char *>(c.joints), (int)sizeof(*c.joints)}};
         for (int el = 0; el < ne; ++el)
             for (int b = 0; b < d.B; ++b)
                 for (int k = 0; k < 13; ++k)
