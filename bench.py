@@ -107,8 +107,14 @@ def ncu_traffic(envs):
     the newest committed `ncu --set full` summary of this workload
     (profiles/r*_step_*_ncu.json, written by tools/ncu_summary.py), else None."""
     import glob
+    import re
+
+    def version(path):      # r01_step_v13_ncu.json -> (1, 13): newest round, then kernel version
+        m = re.search(r"r(\d+)_step_v(\d+)", os.path.basename(path))
+        return (int(m.group(1)), int(m.group(2))) if m else (-1, -1)
+
     best = None
-    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_step_*_ncu.json"))):
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_step_*_ncu.json")), key=version):
         try:
             with open(path) as f:
                 j = json.load(f)

@@ -107,8 +107,8 @@ template <int NW> __device__ unsigned claim_sweep_smsp(const int *warp_smsp, uns
     return bit;
 }
 
-template <class R> __device__ __noinline__ void task_step_env_call(const Ctx<R> &c, const bsim_task_t &t, int e) {
-    task_step_env(c, TaskView<R>{t}, e);
+template <class R> __device__ __noinline__ void task_step_env_call(const Ctx<R> &c, const bsim_task_t &t, int e, int sl) {
+    task_step_env_g<R, BSIM_TASK_G>(c, TaskView<R>{t}, e, sl);
 }
 
 #ifndef BSIM_MINB
@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(Shape<R>::NTH, BSIM_MINB)
     if (tid == 0 && s_sweep_bit) atomicAnd(&g_sweep_smsp[s_sm_slot], ~s_sweep_bit);
     if (with_task) {   // EnvBatch.step tail for this CTA's envs (bsim_env_step)
         __syncthreads();   // the CTA's state stores above are visible to its threads
-        if (tid < ne) task_step_env_call(c, task, e0 + tid);
+        if (tid < BSIM_TASK_G * ne) task_step_env_call(c, task, e0 + tid / BSIM_TASK_G, tid % BSIM_TASK_G);
     }
 }
 

@@ -24,19 +24,24 @@ int t_set_err(const char *what, cudaError_t e) {
 // env row store is a 240-348 B stride across the warp).
 template <class R> __device__ void obs_copy_out(const bsim_task_t &t, const R *stage, int cta_e0, int e_end) {
     __syncthreads();
-    const int n = max(0, min((int)blockDim.x, e_end - cta_e0)) * t.obs_dim;
+    const int n = max(0, e_end - cta_e0) * t.obs_dim;
     R *dst = reinterpret_cast<R *>(t.obs) + (size_t)cta_e0 * t.obs_dim;
     for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = stage[i];
 }
+
+// TASK_G lanes per env (bsim_tasks.cuh group form; the fused tail of
+// bsim_env_step uses the same G, so both paths agree bitwise)
+constexpr int TASK_G = BSIM_TASK_G;
 
 template <class R>
 __global__ void task_step_kernel(const __grid_constant__ Ctx<R> c, const __grid_constant__ bsim_task_t t, int e_begin,
                                  int e_end) {
     extern __shared__ __align__(16) unsigned char task_smem[];
     R *stage = reinterpret_cast<R *>(task_smem);
-    const int cta_e0 = e_begin + blockIdx.x * blockDim.x, e = cta_e0 + threadIdx.x;
-    if (e < e_end) task_step_env(c, TaskView<R>{t, stage, cta_e0}, e);
-    obs_copy_out(t, stage, cta_e0, e_end);
+    const int epc = blockDim.x / TASK_G;
+    const int cta_e0 = e_begin + blockIdx.x * epc, e = cta_e0 + threadIdx.x / TASK_G;
+    if (e < e_end) task_step_env_g<R, TASK_G>(c, TaskView<R>{t, stage, cta_e0}, e, threadIdx.x % TASK_G);
+    obs_copy_out(t, stage, cta_e0, min(e_end, cta_e0 + epc));
 }
 
 template <class R>
@@ -48,9 +53,9 @@ __global__ void task_reset_kernel(const __grid_constant__ Ctx<R> c, const __grid
     if (e < c.d.E) {
         TaskView<R> tv{t, stage, cta_e0};
         if (!mask || mask[e]) task_reset_env(c, tv, e);
-        task_obs(c, tv, e);
+        task_obs_g<R, 1>(c, tv, e, 0);
     }
-    obs_copy_out(t, stage, cta_e0, c.d.E);
+    obs_copy_out(t, stage, cta_e0, min(c.d.E, cta_e0 + (int)blockDim.x));
 }
 
 template <class R>
@@ -100,12 +105,14 @@ int launch_task(const bsim_layout_t *L, const typename Abi<R>::State *s, const b
         t_err = "bsim_task: observation too wide";
         return BSIM_E_TOO_LARGE;
     }
-    const int grid = (env_count + tpb - 1) / tpb;
-    const size_t smem = tpb * row;
-    if (reset)
-        task_reset_kernel<R><<<grid, tpb, smem, (cudaStream_t)stream>>>(c, *t, mask);
-    else
-        task_step_kernel<R><<<grid, tpb, smem, (cudaStream_t)stream>>>(c, *t, env_begin, env_begin + env_count);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (reset) {
+        task_reset_kernel<R><<<(env_count + tpb - 1) / tpb, tpb, tpb * row, st>>>(c, *t, mask);
+    } else {   // TASK_G lanes per env: 128 / TASK_G envs per CTA
+        const int epc = 128 / TASK_G;
+        task_step_kernel<R><<<(env_count + epc - 1) / epc, 128, epc * row, st>>>(c, *t, env_begin,
+                                                                               env_begin + env_count);
+    }
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? BSIM_OK : t_set_err(reset ? "task_reset_kernel" : "task_step_kernel", e);
 }

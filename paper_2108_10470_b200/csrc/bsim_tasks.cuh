@@ -1,10 +1,14 @@
-// bsim_tasks.cuh -- per-env task logic of the two locomotion tasks
-// (host+device): reward, termination, observation and reset, fused so one
-// thread per env finishes a whole EnvBatch.step() tail.
+// bsim_tasks.cuh -- per-env task logic of the locomotion tasks: reward,
+// termination, observation and reset, fused so one group of G lanes per env
+// (task_step_env_g) finishes a whole EnvBatch.step() tail.
 //
 // QuadrupedEnv: reference envs.py:359-478, locomotion_reward rewards.py:78-112.
 // AnymalObsEnv: reference envs.py:484-565, anymal_reward (flat) rewards.py:129-158.
 #pragma once
+
+#ifndef BSIM_TASK_G
+#define BSIM_TASK_G 8   // lanes per env of the task tail (task_step_env_g)
+#endif
 
 #include "bsim_dr.cuh"
 #include "bsim_kin.cuh"
@@ -59,102 +63,6 @@ template <class R> BS_HD Frame<R> quad_frame(const Root<R> &r) {
     return f;
 }
 
-// locomotion_reward (rewards.py:78-112); returns reward, writes the new potential
-template <class R>
-BS_HD R quad_reward(const Ctx<R> &c, const TaskView<R> &tv, int e, const Root<R> &r, const Frame<R> &f,
-                    bool &done) {
-    const R dt = R(tv.t.control_dt), term = R(tv.t.termination_height);
-    R dx = R(QUAD_TARGET_X) - r.p.x, dy = -r.p.y, dz = -r.p.z;
-    R dist = r_sqrt(dx * dx + dy * dy + dz * dz);
-    R potential = -dist / dt;
-    R rew = potential - tv.potential(e);
-    R height = r.p.z;
-    rew = rew + (height >= term ? R(0.5) : R(0));
-    rew = rew + (height <= term ? R(-1) : R(0));
-    rew = rew + (f.up_z > R(0.93) ? R(0.1) : R(0));
-    rew = rew + R(0.5) * (f.heading_proj >= R(0.8) ? R(1) : f.heading_proj / R(0.8));
-    const R *a = tv.act(e);
-    const R *dof = c.s.dof_state + 2 * (size_t)e * c.d.D;
-    R sa = R(0), se = R(0), near_ = R(0);
-    for (int k = 0; k < tv.t.act_dim; ++k) {
-        sa = sa + a[k] * a[k];
-        se = se + a[k] * R(1) * dof[2 * k + 1];
-        R lo = tv.lo(k), hi = tv.hi(k);
-        if (finite_r(lo) && finite_r(hi)) {
-            R frac = (dof[2 * k] - lo) / (hi - lo);
-            if (frac < R(0.01) || frac > R(0.99)) near_ = near_ + R(1);
-        }
-    }
-    rew = rew - R(0.005) * sa;
-    rew = rew + R(0.05) * se;
-    rew = rew - R(0.1) * near_;
-    tv.potential(e) = potential;
-    done = height <= term;
-    return rew;
-}
-
-// 60-dim observation (envs.py:441-461)
-template <class R> BS_HD void quad_obs(const Ctx<R> &c, const TaskView<R> &tv, int e) {
-    Root<R> r = root_of(c, e);
-    Frame<R> f = quad_frame(r);
-    R *o = tv.obs(e);
-    R x = r.q.x, y = r.q.y, z = r.q.z, w = r.q.w;
-    R yaw = r_atan2(R(2) * (w * z + x * y), R(1) - R(2) * (y * y + z * z));
-    R roll = r_atan2(R(2) * (w * x + y * z), R(1) - R(2) * (x * x + y * y));
-    R ang = r_atan2(-r.p.y, R(QUAD_TARGET_X) - r.p.x) - yaw;
-    ang = r_atan2(r_sin(ang), r_cos(ang));
-    o[0] = r.p.z;
-    o[1] = f.lin_b.x; o[2] = f.lin_b.y; o[3] = f.lin_b.z;
-    o[4] = f.ang_b.x; o[5] = f.ang_b.y; o[6] = f.ang_b.z;
-    o[7] = yaw; o[8] = roll; o[9] = ang; o[10] = f.up_z; o[11] = f.heading_proj;
-    const int A = tv.t.act_dim, S = c.d.S;
-    const R *dof = c.s.dof_state + 2 * (size_t)e * c.d.D;
-    for (int k = 0; k < A; ++k) {
-        o[12 + k] = R(2) * (dof[2 * k] - tv.lo(k)) / (tv.hi(k) - tv.lo(k)) - R(1);
-        o[12 + A + k] = dof[2 * k + 1] * R(0.05);
-    }
-    const R *sf = c.s.sensor_forces + 6 * (size_t)e * S;
-    for (int k = 0; k < 6 * S; ++k) o[12 + 2 * A + k] = sf[k] * R(0.01);
-    const R *a = tv.act(e);
-    for (int k = 0; k < A; ++k) o[12 + 2 * A + 6 * S + k] = a[k];
-}
-
-// ------------------------------------------------------------ anymal
-template <class R> BS_HD R anymal_reward(const Ctx<R> &c, const TaskView<R> &tv, int e, const Root<R> &r, bool &done) {
-    const R dt = R(tv.t.control_dt);
-    V3<R> lin_b = rot_inv(r.q, r.v), ang_b = rot_inv(r.q, r.w);
-    const R *cmd = tv.cmd(e);
-    R ex = cmd[0] - lin_b.x, ey = cmd[1] - lin_b.y, ez = cmd[2] - ang_b.z;
-    R err_xy = ex * ex + ey * ey, err_yaw = ez * ez;
-    R tq = R(0);
-    const R *df = c.s.dof_force + (size_t)e * c.d.D;
-    for (int k = 0; k < tv.t.act_dim; ++k) tq = tq + df[k] * df[k];
-    R rew = R(1) * dt * exp_r(-err_xy / R(0.25)) + R(0.5) * dt * exp_r(-err_yaw / R(0.25)) - R(0.00002) * dt * tq;
-    R up_z = qrot(r.q, v3(R(0), R(0), R(1))).z;
-    done = up_z < R(0.3) || r.p.z < R(0.18);
-    return rew;
-}
-
-// 48-dim observation (envs.py:538-550)
-template <class R> BS_HD void anymal_obs(const Ctx<R> &c, const TaskView<R> &tv, int e) {
-    Root<R> r = root_of(c, e);
-    R *o = tv.obs(e);
-    V3<R> lin_b = rot_inv(r.q, r.v), ang_b = rot_inv(r.q, r.w), gb = rot_inv(r.q, v3(R(0), R(0), R(-1)));
-    o[0] = lin_b.x; o[1] = lin_b.y; o[2] = lin_b.z;
-    o[3] = ang_b.x; o[4] = ang_b.y; o[5] = ang_b.z;
-    o[6] = gb.x; o[7] = gb.y; o[8] = gb.z;
-    const R *cmd = tv.cmd(e);
-    o[9] = cmd[0]; o[10] = cmd[1]; o[11] = cmd[2];
-    const int A = tv.t.act_dim;
-    const R *dof = c.s.dof_state + 2 * (size_t)e * c.d.D;
-    for (int k = 0; k < A; ++k) {
-        o[12 + k] = dof[2 * k];
-        o[12 + A + k] = dof[2 * k + 1] * R(0.05);
-    }
-    const R *a = tv.act(e);
-    for (int k = 0; k < A; ++k) o[12 + 2 * A + k] = a[k];
-}
-
 // ------------------------------------------------------------ reset
 // EnvBatch.reset for one env (envs.py:145-166) with the task's _reset_envs
 // (404-419 / 517-531) and _post_reset (385-397 / 506-515).
@@ -207,44 +115,181 @@ template <class R> __device__ void task_reset_env(const Ctx<R> &c, const TaskVie
     }
 }
 
-template <class R> __device__ void task_obs(const Ctx<R> &c, const TaskView<R> &tv, int e) {
-    const bsim_task_t &t = tv.t;
-    if (t.kind != BSIM_TASK_ANYMAL) quad_obs(c, tv, e);
-    else anymal_obs(c, tv, e);
-    if (t.obs_noise) {  // perturb_observations (randomize.py:231-237)
-        R *o = tv.obs(e);
-        const R *cn = reinterpret_cast<const R *>(t.corr_noise) + (size_t)e * t.obs_dim;
-        if (t.obs_noise_uncorr > 0.0) {
-            // numpy draws this from one batch-wide stream; a per-env stream
-            // keyed (seed, 0xE7, env, count) keeps it parallel (same law)
-            uint32_t key[4] = {t.seed, 0xE7u, (uint32_t)(c.L.env_offset + e), (uint32_t)t.noise_count[e]};
-            NpRng r = np_rng(key, 4);
-            for (int k = 0; k < t.obs_dim; ++k) o[k] = o[k] + R(0.0 + t.obs_noise_uncorr * np_std_normal(r));
-            t.noise_count[e] += 1;
+// ------------------------------------------------------------ group form
+// The same tail with G lanes per env (an aligned group of a warp, s = lane
+// in the group): the per-DOF / per-sensor loops are strided over the group
+// and the reward's DOF sums reduced with a fixed xor tree; everything else is
+// computed redundantly by the group's lanes (one SIMT instruction stream) and
+// written by lane 0.  Resets and observation noise (sequential RNG streams)
+// run on lane 0.  G = 1 is the serial form.  Device only.
+#if defined(__CUDACC__)
+template <int G> __device__ __forceinline__ unsigned group_mask() {
+    if constexpr (G >= 32) return 0xffffffffu;
+    else return ((1u << G) - 1u) << ((threadIdx.x & 31u) & ~(unsigned)(G - 1));
+}
+template <int G, class R> __device__ __forceinline__ R group_sum(R v) {
+    const unsigned m = group_mask<G>();
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(m, v, o);
+    return v;
+}
+
+// locomotion_reward (rewards.py:78-112); returns the reward, lane 0 writes the new potential
+template <class R, int G>
+__device__ R quad_reward_g(const Ctx<R> &c, const TaskView<R> &tv, int e, int sl, const Root<R> &r, const Frame<R> &f,
+                           bool &done) {
+    const R dt = R(tv.t.control_dt), term = R(tv.t.termination_height);
+    R dx = R(QUAD_TARGET_X) - r.p.x, dy = -r.p.y, dz = -r.p.z;
+    R dist = r_sqrt(dx * dx + dy * dy + dz * dz);
+    R potential = -dist / dt;
+    R rew = potential - tv.potential(e);
+    R height = r.p.z;
+    rew = rew + (height >= term ? R(0.5) : R(0));
+    rew = rew + (height <= term ? R(-1) : R(0));
+    rew = rew + (f.up_z > R(0.93) ? R(0.1) : R(0));
+    rew = rew + R(0.5) * (f.heading_proj >= R(0.8) ? R(1) : f.heading_proj / R(0.8));
+    const R *a = tv.act(e);
+    const R *dof = c.s.dof_state + 2 * (size_t)e * c.d.D;
+    R sa = R(0), se = R(0), near_ = R(0);
+    for (int k = sl; k < tv.t.act_dim; k += G) {
+        sa = sa + a[k] * a[k];
+        se = se + a[k] * R(1) * dof[2 * k + 1];
+        R lo = tv.lo(k), hi = tv.hi(k);
+        if (finite_r(lo) && finite_r(hi)) {
+            R frac = (dof[2 * k] - lo) / (hi - lo);
+            if (frac < R(0.01) || frac > R(0.99)) near_ = near_ + R(1);
         }
-        for (int k = 0; k < t.obs_dim; ++k) o[k] = o[k] + cn[k];
+    }
+    sa = group_sum<G>(sa);
+    se = group_sum<G>(se);
+    near_ = group_sum<G>(near_);
+    rew = rew - R(0.005) * sa;
+    rew = rew + R(0.05) * se;
+    rew = rew - R(0.1) * near_;
+    __syncwarp(group_mask<G>());           // every lane read the old potential
+    if (sl == 0) tv.potential(e) = potential;
+    done = height <= term;
+    return rew;
+}
+
+// 60-dim observation (envs.py:441-461)
+template <class R, int G> __device__ void quad_obs_g(const Ctx<R> &c, const TaskView<R> &tv, int e, int sl) {
+    Root<R> r = root_of(c, e);
+    R *o = tv.obs(e);
+    if (sl == 0) {
+        Frame<R> f = quad_frame(r);
+        R x = r.q.x, y = r.q.y, z = r.q.z, w = r.q.w;
+        R yaw = r_atan2(R(2) * (w * z + x * y), R(1) - R(2) * (y * y + z * z));
+        R roll = r_atan2(R(2) * (w * x + y * z), R(1) - R(2) * (x * x + y * y));
+        R ang = r_atan2(-r.p.y, R(QUAD_TARGET_X) - r.p.x) - yaw;
+        ang = r_atan2(r_sin(ang), r_cos(ang));
+        o[0] = r.p.z;
+        o[1] = f.lin_b.x; o[2] = f.lin_b.y; o[3] = f.lin_b.z;
+        o[4] = f.ang_b.x; o[5] = f.ang_b.y; o[6] = f.ang_b.z;
+        o[7] = yaw; o[8] = roll; o[9] = ang; o[10] = f.up_z; o[11] = f.heading_proj;
+    }
+    const int A = tv.t.act_dim, S = c.d.S;
+    const R *dof = c.s.dof_state + 2 * (size_t)e * c.d.D;
+    for (int k = sl; k < A; k += G) {
+        o[12 + k] = R(2) * (dof[2 * k] - tv.lo(k)) / (tv.hi(k) - tv.lo(k)) - R(1);
+        o[12 + A + k] = dof[2 * k + 1] * R(0.05);
+    }
+    const R *sf = c.s.sensor_forces + 6 * (size_t)e * S;
+    for (int k = sl; k < 6 * S; k += G) o[12 + 2 * A + k] = sf[k] * R(0.01);
+    const R *a = tv.act(e);
+    for (int k = sl; k < A; k += G) o[12 + 2 * A + 6 * S + k] = a[k];
+}
+
+// anymal_reward, flat terrain (rewards.py:129-158)
+template <class R, int G>
+__device__ R anymal_reward_g(const Ctx<R> &c, const TaskView<R> &tv, int e, int sl, const Root<R> &r, bool &done) {
+    const R dt = R(tv.t.control_dt);
+    V3<R> lin_b = rot_inv(r.q, r.v), ang_b = rot_inv(r.q, r.w);
+    const R *cmd = tv.cmd(e);
+    R ex = cmd[0] - lin_b.x, ey = cmd[1] - lin_b.y, ez = cmd[2] - ang_b.z;
+    R err_xy = ex * ex + ey * ey, err_yaw = ez * ez;
+    R tq = R(0);
+    const R *df = c.s.dof_force + (size_t)e * c.d.D;
+    for (int k = sl; k < tv.t.act_dim; k += G) tq = tq + df[k] * df[k];
+    tq = group_sum<G>(tq);
+    R rew = R(1) * dt * exp_r(-err_xy / R(0.25)) + R(0.5) * dt * exp_r(-err_yaw / R(0.25)) - R(0.00002) * dt * tq;
+    R up_z = qrot(r.q, v3(R(0), R(0), R(1))).z;
+    done = up_z < R(0.3) || r.p.z < R(0.18);
+    return rew;
+}
+
+// 48-dim observation (envs.py:538-550)
+template <class R, int G> __device__ void anymal_obs_g(const Ctx<R> &c, const TaskView<R> &tv, int e, int sl) {
+    Root<R> r = root_of(c, e);
+    R *o = tv.obs(e);
+    if (sl == 0) {
+        V3<R> lin_b = rot_inv(r.q, r.v), ang_b = rot_inv(r.q, r.w), gb = rot_inv(r.q, v3(R(0), R(0), R(-1)));
+        o[0] = lin_b.x; o[1] = lin_b.y; o[2] = lin_b.z;
+        o[3] = ang_b.x; o[4] = ang_b.y; o[5] = ang_b.z;
+        o[6] = gb.x; o[7] = gb.y; o[8] = gb.z;
+        const R *cmd = tv.cmd(e);
+        o[9] = cmd[0]; o[10] = cmd[1]; o[11] = cmd[2];
+    }
+    const int A = tv.t.act_dim;
+    const R *dof = c.s.dof_state + 2 * (size_t)e * c.d.D;
+    for (int k = sl; k < A; k += G) {
+        o[12 + k] = dof[2 * k];
+        o[12 + A + k] = dof[2 * k + 1] * R(0.05);
+    }
+    const R *a = tv.act(e);
+    for (int k = sl; k < A; k += G) o[12 + 2 * A + k] = a[k];
+}
+
+template <class R, int G> __device__ void task_obs_g(const Ctx<R> &c, const TaskView<R> &tv, int e, int sl) {
+    const bsim_task_t &t = tv.t;
+    if (t.kind != BSIM_TASK_ANYMAL) quad_obs_g<R, G>(c, tv, e, sl);
+    else anymal_obs_g<R, G>(c, tv, e, sl);
+    if (t.obs_noise) {  // perturb_observations (randomize.py:231-237): one sequential stream per env
+        __syncwarp(group_mask<G>());
+        if (sl == 0) {
+            R *o = tv.obs(e);
+            const R *cn = reinterpret_cast<const R *>(t.corr_noise) + (size_t)e * t.obs_dim;
+            if (t.obs_noise_uncorr > 0.0) {
+                uint32_t key[4] = {t.seed, 0xE7u, (uint32_t)(c.L.env_offset + e), (uint32_t)t.noise_count[e]};
+                NpRng rr = np_rng(key, 4);
+                for (int k = 0; k < t.obs_dim; ++k) o[k] = o[k] + R(0.0 + t.obs_noise_uncorr * np_std_normal(rr));
+                t.noise_count[e] += 1;
+            }
+            for (int k = 0; k < t.obs_dim; ++k) o[k] = o[k] + cn[k];
+        }
     }
 }
 
-// EnvBatch.step tail after the decimated physics (envs.py:188-199)
-template <class R> __device__ void task_step_env(const Ctx<R> &c, const TaskView<R> &tv, int e) {
+// the reset path out of line: the tail's hot path stays small (inlined, the
+// FK / DR / RNG code made instruction-fetch stalls the tail's top stall)
+template <class R> __device__ __noinline__ void task_reset_env_call(const Ctx<R> &c, const TaskView<R> &tv, int e) {
+    task_reset_env(c, tv, e);
+}
+
+// EnvBatch.step tail after the decimated physics (envs.py:188-199), G lanes per env
+template <class R, int G> __device__ void task_step_env_g(const Ctx<R> &c, const TaskView<R> &tv, int e, int sl) {
     const bsim_task_t &t = tv.t;
-    int steps = t.episode_steps[e] + 1;
-    t.episode_steps[e] = steps;
+    const int steps = t.episode_steps[e] + 1;
     Root<R> r = root_of(c, e);
     bool done;
     R rew;
-    if (t.kind != BSIM_TASK_ANYMAL) rew = quad_reward(c, tv, e, r, quad_frame(r), done);
-    else rew = anymal_reward(c, tv, e, r, done);
-    bool timeout = steps >= t.episode_length;
-    bool pois = c.s.nonfinite[e] != 0;
+    if (t.kind != BSIM_TASK_ANYMAL) rew = quad_reward_g<R, G>(c, tv, e, sl, r, quad_frame(r), done);
+    else rew = anymal_reward_g<R, G>(c, tv, e, sl, r, done);
+    const bool timeout = steps >= t.episode_length;
+    const bool pois = c.s.nonfinite[e] != 0;
     done = done || timeout || pois;
-    tv.reward(e) = pois ? R(0) : rew;
-    t.done[e] = done;
-    t.timeout[e] = timeout;
-    t.poisoned[e] = pois;
-    if (done) task_reset_env(c, tv, e);
-    task_obs(c, tv, e);   // reset rows get the post-reset observation (envs.py:195-198)
+    __syncwarp(group_mask<G>());           // every lane read the pre-step state
+    if (sl == 0) {
+        t.episode_steps[e] = steps;
+        tv.reward(e) = pois ? R(0) : rew;
+        t.done[e] = done;
+        t.timeout[e] = timeout;
+        t.poisoned[e] = pois;
+        if (done) task_reset_env_call(c, tv, e);
+    }
+    __syncwarp(group_mask<G>());           // the reset state is visible to the group
+    task_obs_g<R, G>(c, tv, e, sl);        // reset rows get the post-reset observation (envs.py:195-198)
 }
+#endif
 
 }  // namespace bsim
