@@ -1300,22 +1300,18 @@ template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> 
 
     for (int k = 0; k <= N; ++k) {
         const bool biased = k < N, freeze = k == 0, deltas = k > 0 && k < N;
-        if (k == N) {  // integrate (574-575)
-            BS_ITEMS(g, d.B, el, b) {
-                Ws<R> w = g.env(el);
-                w.s3(ib(d, b, BP), w.l3(ib(d, b, BP)) + w.l3(ib(d, b, BDP)));
-                w.s4(ib(d, b, BQ), qnormalize(qmul(qexp(w.l3(ib(d, b, BDA))), w.l4(ib(d, b, BQ)))));
-            }
-            BS_SYNC();
-        }
         // phase A: orientations -> inertias -> joint/contact geometry and row
         // constants (freeze 657-716, refresh 718-756)
 #ifdef BSIM_EXP_SKIP_A   // timing experiment only: reuse the freeze-time constants
         if (!freeze && k < N) goto phase_b;
 #endif
-        if (!freeze) {
+        if (!freeze) {   // per body: [integrate (574-575) at k = N,] orientation, world inverse inertia
             BS_ITEMS(g, d.B, el, b) {
                 Ws<R> w = g.env(el);
+                if (k == N) {
+                    w.s3(ib(d, b, BP), w.l3(ib(d, b, BP)) + w.l3(ib(d, b, BDP)));
+                    w.s4(ib(d, b, BQ), qnormalize(qmul(qexp(w.l3(ib(d, b, BDA))), w.l4(ib(d, b, BQ)))));
+                }
                 if (deltas)
                     w.s4(ib(d, b, BQE), qnormalize(qmul(qexp(w.l3(ib(d, b, BDA))), w.l4(ib(d, b, BQ)))));
                 body_inertia(c, w, g.e0 + el, b, deltas ? BQE : BQ);
@@ -1375,6 +1371,10 @@ template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> 
         R sa = r_min(R(1), p.max_angular_velocity / r_max(norm(av), R(1e-12)));
         w.s3(ib(d, b, BV_), lv * sl);
         w.s3(ib(d, b, BW), av * sa);
+        // _flag_nonfinite (1073-1088) check on the final state of this body
+        bool ok = true;
+        for (int kk = 0; kk < 13; ++kk) ok = ok && finite_r(w.at(ib(d, b, body_item13(kk))));
+        if (!ok) w.at(d.o_env + EBAD) = R(1);
     }
     BS_SYNC();
 
@@ -1425,14 +1425,9 @@ template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> 
         }
     }
 
-    // _flag_nonfinite (1073-1088): sanitize poisoned envs (sticky flag)
-    BS_ITEMS(g, d.B, el, b) {
-        Ws<R> w = g.env(el);
-        bool ok = true;
-        for (int k = 0; k < 13; ++k) ok = ok && finite_r(w.at(ib(d, b, body_item13(k))));
-        if (!ok) w.at(d.o_env + EBAD) = R(1);
-    }
-    BS_SYNC();
+    // _flag_nonfinite (1073-1088): sanitize poisoned envs (sticky flag; the
+    // check ran with the velocity clamps)
+    if (write_outputs) BS_SYNC();   // the output stage above reads the pre-sanitize state
     BS_ITEMS(g, d.B, el, b) {
         Ws<R> w = g.env(el);
         if (w.at(d.o_env + EBAD) != R(0)) {
