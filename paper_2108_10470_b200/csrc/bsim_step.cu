@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(Shape<R>::NTH, BSIM_MINB)
     }
     __syncthreads();
     for (int s = 0; s < n_substeps; ++s) {
-        group_step<R, T>(c, g, s == n_substeps - 1);
+        group_step<R, T>(c, g, s == n_substeps - 1, s);
         if (d.T && s != n_substeps - 1) {  // fixed tendons read dof_state next substep
             readout_group(c, g);
             __syncthreads();

@@ -110,6 +110,8 @@ enum { QR = 0, QD0 = 3, QRA = 4, QREST = 7, QN = 8, QLN = 11, QT1 = 12, QACT = 1
 // per dof: impulse accumulator, start-of-step readout
 enum { DIMP = 0, DQ0 = 1, DOF_ITEMS = 2 };
 // per env
+// EBAD / EBAD + 1: the per-env non-finite flag of even / odd substeps (each
+// cleared during the following substep, so no barrier-separated clear)
 enum { EMUS = 0, EMUD = 1, EGX = 2, EGY = 3, EGZ = 4, EBAD = 5, ENV_ITEMS = 8 };
 // per friction anchor (xyz + pad)
 enum { ANCHOR_ITEMS = 4 };
@@ -247,6 +249,7 @@ template <class R> BS_HD void stage_env(const Ctx<R> &c, const Ws<R> &w, int e) 
     w.at(d.o_env + EGY) = s.gravity[3 * (size_t)e + 1];
     w.at(d.o_env + EGZ) = s.gravity[3 * (size_t)e + 2];
     w.at(d.o_env + EBAD) = R(0);
+    w.at(d.o_env + EBAD + 1) = R(0);
 }
 
 // world inverse inertia of body b from orientation item qitem (physics.py:594-596)
@@ -1268,8 +1271,9 @@ template <class T> constexpr bool topo_tendons() {
 // The N biased passes and the final velocity stage share one phase-A body
 // (freeze at k = 0, refresh-with-deltas at 0 < k < N, integrate + refresh at
 // k = N), so every piece of the step appears once in the binary.
-template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> &g, bool write_outputs) {
+template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> &g, bool write_outputs, int sub) {
     const Dims &d = c.d;
+    const int ebad = d.o_env + EBAD + (sub & 1);
     const auto &p = c.p;
     const R dt = p.dt;
     const int N = p.position_iterations;
@@ -1282,6 +1286,7 @@ template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> 
         body_external(c, w, g.e0 + el, b);
         w.s3(ib(d, b, BDP), zero3<R>());
         w.s3(ib(d, b, BDA), zero3<R>());
+        if (b == 0) w.at(d.o_env + EBAD + ((sub + 1) & 1)) = R(0);   // the previous substep's flag
     }
     BS_SYNC();
     if (topo_tendons<T>() && d.T) {
@@ -1374,7 +1379,7 @@ template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> 
         // _flag_nonfinite (1073-1088) check on the final state of this body
         bool ok = true;
         for (int kk = 0; kk < 13; ++kk) ok = ok && finite_r(w.at(ib(d, b, body_item13(kk))));
-        if (!ok) w.at(d.o_env + EBAD) = R(1);
+        if (!ok) w.at(ebad) = R(1);
     }
     BS_SYNC();
 
@@ -1430,7 +1435,7 @@ template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> 
     if (write_outputs) BS_SYNC();   // the output stage above reads the pre-sanitize state
     BS_ITEMS(g, d.B, el, b) {
         Ws<R> w = g.env(el);
-        if (w.at(d.o_env + EBAD) != R(0)) {
+        if (w.at(ebad) != R(0)) {
             int e = g.e0 + el;
             if (b == 0) c.s.nonfinite[e] = 1;
             for (int k = 0; k < 13; ++k) {
@@ -1443,8 +1448,6 @@ template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> 
             w.s4(ib(d, b, BQ), qnormalize(q));
         }
     }
-    BS_SYNC();
-    BS_ENVS(g, el) { g.env(el).at(d.o_env + EBAD) = R(0); }
     BS_SYNC();
 }
 

@@ -36,7 +36,7 @@ static void run_t(const bsim_layout_t *L, const typename Abi<R>::Params *p, cons
                     g.env(el).at(ib(d, b, body_item13(k))) = s->body_q[13 * ((size_t)(e0 + el) * d.B + b) + k];
         stage_group(c, g);
         for (int st = 0; st < n_substeps; ++st) {
-            group_step<R, T>(c, g, st == n_substeps - 1);
+            group_step<R, T>(c, g, st == n_substeps - 1, st);
             if (d.T && st != n_substeps - 1) readout_group(c, g);
         }
         readout_group(c, g);
