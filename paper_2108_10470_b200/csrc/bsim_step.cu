@@ -2,14 +2,14 @@
 // indexed state setters, contact queries, and their C-ABI entry points
 // (declared in include/batchsim_b200.h).
 //
-// Step kernel mapping: one CTA owns NE envs
-// (Shape<R> in bsim_step.cuh: 16 fp32 / 8 fp64) with 8 threads per env for
-// the lane-parallel phase A and one thread per env for the Gauss-Seidel
-// sweep.  The CTA's per-env workspace is dynamic shared memory laid out
-// item-major with the compile-time odd stride NE + 1 (per-thread column
-// accesses and the cooperative row-contiguous global loads/stores are both
-// bank-conflict free).  Body state is moved HBM <-> shared memory with fully
-// coalesced loads/stores of the CTA's contiguous [NE envs x B bodies x 13]
+// Step kernel mapping: one CTA owns up to NE envs (Shape<R>
+// in bsim_step.cuh: 16 fp32 / 8 fp64; the launch plan picks `epc` <= NE for
+// whole waves) with 8 threads per env for the lane-parallel phase A and one
+// thread (two for the Ant's star sweep) per env for the Gauss-Seidel sweep.
+// The CTA's workspace is dynamic shared memory: one env-major record per env
+// (16-byte aligned vector items, PAD = 4 mod 8 words apart) followed by a
+// padded copy of the joint table.  Body state moves HBM <-> shared memory
+// with coalesced loads / stores of the CTA's contiguous [envs x B bodies x 13]
 // slab; all substeps of a control step run on the resident workspace, so HBM
 // sees the state once per control step.
 #include <cuda_runtime.h>
