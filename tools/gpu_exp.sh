@@ -8,7 +8,7 @@ OUT=gpurun_out/exp.log
 for v in "$@"; do
   echo "=== variant: [$v]" >> $OUT
   BSIM_NVCC_EXTRA="$v" timeout 600 python -m paper_2108_10470_b200.build --force >> $OUT 2>&1 || { echo "build failed" >> $OUT; continue; }
-  timeout 300 python tools/quick_step_bench.py --envs 4096,16384 --prec fp32 --generic --tag "[$v] " >> $OUT 2>&1
-  timeout 600 python -m pytest tests/test_gpu_step.py -x -q -m gpu 2>&1 | tail -2 >> $OUT
+  timeout 300 python tools/quick_step_bench.py --envs ${QENVS:-4096,16384} --prec fp32 ${QGEN---generic} --tag "[$v] " >> $OUT 2>&1
+  [ -z "$NOTEST" ] && timeout 600 python -m pytest tests/test_gpu_step.py -x -q -m gpu 2>&1 | tail -2 >> $OUT
 done
 cat $OUT
