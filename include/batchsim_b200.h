@@ -429,6 +429,21 @@ int bsim_reward_cube(int n, int A, int fp64, const void *object_pos, const void 
 int bsim_reward_franka(int n, int fp64, const void *cubeA_pos, const void *cubeB_pos,
                        const void *gripper_pos, const void *lfinger_pos, const void *rfinger_pos,
                        const bsim_franka_params_t *params, void *reward, void *stream);
+typedef struct bsim_trifinger_params_t {
+    double w_og, w_fo, w_fv, kernel_a, kernel_b, fingertip_term_cutoff;
+} bsim_trifinger_params_t;
+/* trifinger_reward (rewards.py:179-197): F fingertips per env, positions /
+   velocities [n][F][3]; timestep is int64 [n] */
+int bsim_reward_trifinger(int n, int F, int fp64, const void *cube_pos, const void *prev_cube_pos,
+                          const void *cube_quat, const void *target_pos, const void *target_quat,
+                          const void *fingertip_pos, const void *prev_fingertip_pos,
+                          const void *fingertip_vel, const int64_t *timestep,
+                          const bsim_trifinger_params_t *params, void *reward, void *stream);
+/* ingenuity_reward (rewards.py:115-121): S spin-rate components per env */
+int bsim_reward_ingenuity(int n, int S, int fp64, const void *pos, const void *target,
+                          const void *local_up_z, const void *spin_rate, void *reward, void *stream);
+/* amp_imitation_reward (rewards.py:222-225): r = -ln(1 - clip(D, 1e-4, 1 - 1e-4)) elementwise */
+int bsim_reward_amp(int n, int fp64, const void *d_score, void *reward, void *stream);
 
 /* float64 variants (same semantics, double tables / params / state). */
 int bsim_step_f64(const bsim_layout_t *layout, const bsim_params64_t *params,

@@ -24,6 +24,10 @@ def declare(lib):
     lib.bsim_reward_anymal.argtypes = [i, i, i, i, i] + [vp] * 9 + [vp, i, vp, vp]
     lib.bsim_reward_cube.argtypes = [i, i, i] + [vp] * 5 + [vp, vp, vp, vp, vp]
     lib.bsim_reward_franka.argtypes = [i, i] + [vp] * 5 + [vp, vp, vp]
-    for n in ("bsim_reward_locomotion", "bsim_reward_anymal", "bsim_reward_cube", "bsim_reward_franka"):
+    lib.bsim_reward_trifinger.argtypes = [i, i, i] + [vp] * 9 + [vp, vp, vp]
+    lib.bsim_reward_ingenuity.argtypes = [i, i, i] + [vp] * 4 + [vp, vp]
+    lib.bsim_reward_amp.argtypes = [i, i, vp, vp, vp]
+    for n in ("bsim_reward_locomotion", "bsim_reward_anymal", "bsim_reward_cube", "bsim_reward_franka",
+              "bsim_reward_trifinger", "bsim_reward_ingenuity", "bsim_reward_amp"):
         getattr(lib, n).restype = C.c_int
     return lib

@@ -132,6 +132,56 @@ __global__ void franka_kernel(int n, const R *ca, const R *cb, const R *gp, cons
     out[i] = rs > alt ? rs : alt;
 }
 
+// trifinger_reward (rewards.py:179-197): logistic position kernel + rotation
+// term, fingertip-to-cube progress (until the cutoff) and fingertip speed
+template <class R>
+__global__ void trifinger_kernel(int n, int F, const R *cp, const R *pcp, const R *cq, const R *tp, const R *tq,
+                                 const R *ft, const R *pft, const R *fv, const int64_t *ts,
+                                 bsim_trifinger_params_t p, R *out) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const R *c = cp + 3 * i, *pc = pcp + 3 * i;
+    R x = norm3(c, tp + 3 * i);
+    R ka = R(p.kernel_a) * x;
+    R kern = R(1) / (exp(ka) + R(p.kernel_b) + exp(-ka));
+    R rd = rot_dist(cq + 4 * i, tq + 4 * i);
+    R rog = kern + R(1) / (R(3) * fabs(rd) + R(0.01));
+    R delta = 0, speed = 0;
+    for (int f = 0; f < F; ++f) {
+        size_t o = ((size_t)i * F + f) * 3;
+        delta = delta + (norm3(ft + o, c) - norm3(pft + o, pc));
+        speed = speed + sq(fv[o]) + sq(fv[o + 1]) + sq(fv[o + 2]);
+    }
+    R rfo = (double)ts[i] <= p.fingertip_term_cutoff ? delta : R(0);
+    out[i] = R(p.w_og) * rog + R(p.w_fo) * rfo + R(p.w_fv) * speed;
+}
+
+// ingenuity_reward (rewards.py:115-121): R_pos (1 + R_upright + R_spin)
+template <class R>
+__global__ void ingenuity_kernel(int n, int S, const R *pos, const R *tgt, const R *upz, const R *spin, R *out) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const R *a = pos + 3 * i, *b = tgt + 3 * i;
+    R d2 = sq(a[0] - b[0]) + sq(a[1] - b[1]) + sq(a[2] - b[2]);
+    R s2 = 0;
+    for (int k = 0; k < S; ++k) s2 = s2 + sq(spin[(size_t)i * S + k]);
+    R rpos = R(1) / (R(1) + d2);
+    R rspin = R(1) / (R(1) + s2);
+    R rup = R(1) / (R(1) + sq(upz[i]));
+    out[i] = rpos * (R(1) + rup + rspin);
+}
+
+// amp_imitation_reward (rewards.py:222-225)
+template <class R>
+__global__ void amp_kernel(int n, const R *d, R *out) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    R v = d[i];
+    const R lo = R(1e-4), hi = R(1) - R(1e-4);
+    v = v < lo ? lo : (v > hi ? hi : v);  // np.clip; NaN passes through
+    out[i] = -log(R(1) - v);
+}
+
 int done(const char *) { return cudaGetLastError() == cudaSuccess ? 0 : -2; }
 constexpr int TPB = 256;
 inline int grid(int n) { return (n + TPB - 1) / TPB; }
@@ -201,6 +251,45 @@ int bsim_reward_franka(int n, int fp64, const void *ca, const void *cb, const vo
         franka_kernel<float><<<grid(n), TPB, 0, s>>>(n, (const float *)ca, (const float *)cb, (const float *)gp,
             (const float *)lf, (const float *)rf, *p, (float *)out);
     return done("franka");
+}
+
+int bsim_reward_trifinger(int n, int F, int fp64, const void *cp, const void *pcp, const void *cq, const void *tp,
+                          const void *tq, const void *ft, const void *pft, const void *fv, const int64_t *ts,
+                          const bsim_trifinger_params_t *p, void *out, void *stream) {
+    if (n <= 0) return 0;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (fp64)
+        trifinger_kernel<double><<<grid(n), TPB, 0, s>>>(n, F, (const double *)cp, (const double *)pcp,
+            (const double *)cq, (const double *)tp, (const double *)tq, (const double *)ft, (const double *)pft,
+            (const double *)fv, ts, *p, (double *)out);
+    else
+        trifinger_kernel<float><<<grid(n), TPB, 0, s>>>(n, F, (const float *)cp, (const float *)pcp,
+            (const float *)cq, (const float *)tp, (const float *)tq, (const float *)ft, (const float *)pft,
+            (const float *)fv, ts, *p, (float *)out);
+    return done("trifinger");
+}
+
+int bsim_reward_ingenuity(int n, int S, int fp64, const void *pos, const void *tgt, const void *upz,
+                          const void *spin, void *out, void *stream) {
+    if (n <= 0) return 0;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (fp64)
+        ingenuity_kernel<double><<<grid(n), TPB, 0, s>>>(n, S, (const double *)pos, (const double *)tgt,
+            (const double *)upz, (const double *)spin, (double *)out);
+    else
+        ingenuity_kernel<float><<<grid(n), TPB, 0, s>>>(n, S, (const float *)pos, (const float *)tgt,
+            (const float *)upz, (const float *)spin, (float *)out);
+    return done("ingenuity");
+}
+
+int bsim_reward_amp(int n, int fp64, const void *d, void *out, void *stream) {
+    if (n <= 0) return 0;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (fp64)
+        amp_kernel<double><<<grid(n), TPB, 0, s>>>(n, (const double *)d, (double *)out);
+    else
+        amp_kernel<float><<<grid(n), TPB, 0, s>>>(n, (const float *)d, (float *)out);
+    return done("amp");
 }
 
 }  // extern "C"

@@ -68,6 +68,16 @@ class FrankaStackParams:
     away_distance: float = 0.04
 
 
+@dataclass
+class TrifingerRewardParams:
+    w_og: float = 1.0
+    w_fo: float = 0.2
+    w_fv: float = -0.05
+    kernel_a: float = 50.0
+    kernel_b: float = 2.0
+    fingertip_term_cutoff: int = int(5e7)
+
+
 def _struct(p):
     fields = [(k, C.c_double) for k in p.__dataclass_fields__]
     S = type("P", (C.Structure,), {"_fields_": fields})
@@ -178,4 +188,48 @@ def franka_stack_reward(cubeA_pos, cubeB_pos, gripper_pos, lfinger_pos, rfinger_
     _check(N.lib().bsim_reward_franka(n, a.fp64, ca.data_ptr(), a(cubeB_pos).data_ptr(), a(gripper_pos).data_ptr(),
                                       a(lfinger_pos).data_ptr(), a(rfinger_pos).data_ptr(), C.byref(p),
                                       out.data_ptr(), _stream()), "franka_stack_reward")
+    return out
+
+
+def trifinger_reward(cube_pos, prev_cube_pos, cube_quat, target_pos, target_quat, fingertip_pos,
+                     prev_fingertip_pos, fingertip_vel, timestep, params):
+    """rewards.py:179-197; fingertip arrays are (n, F, 3), timestep (n,) integer steps."""
+    a = _Args()
+    cp = a(cube_pos)
+    n = cp.shape[0]
+    ft = a(fingertip_pos)
+    F = ft.shape[1] if ft.dim() == 3 else 0
+    ts = timestep if isinstance(timestep, torch.Tensor) else torch.as_tensor(np.asarray(timestep))
+    ts = torch.broadcast_to(ts.to(cp.device, torch.int64), (n,)).contiguous()
+    a.keep.append(ts)
+    args = [cp, a(prev_cube_pos), a(cube_quat), a(target_pos), a(target_quat), ft, a(prev_fingertip_pos),
+            a(fingertip_vel)]
+    out = torch.empty(n, dtype=a.dtype, device=cp.device)
+    p = _struct(params)
+    _check(N.lib().bsim_reward_trifinger(n, F, a.fp64, *(t.data_ptr() for t in args), ts.data_ptr(), C.byref(p),
+                                         out.data_ptr(), _stream()), "trifinger_reward")
+    return out
+
+
+def ingenuity_reward(pos, target, local_up_z, spin_rate):
+    """rewards.py:115-121: R_pos * (1 + R_upright + R_spin)."""
+    a = _Args()
+    ps = a(pos)
+    n = ps.shape[0]
+    spin = a(spin_rate)
+    spin = spin.reshape(n, -1)
+    out = torch.empty(n, dtype=a.dtype, device=ps.device)
+    _check(N.lib().bsim_reward_ingenuity(n, spin.shape[1], a.fp64, ps.data_ptr(), a(target).data_ptr(),
+                                         a(local_up_z).data_ptr(), spin.data_ptr(), out.data_ptr(), _stream()),
+           "ingenuity_reward")
+    return out
+
+
+def amp_imitation_reward(d_score):
+    """rewards.py:222-225: -ln(1 - clip(D, 1e-4, 1 - 1e-4)), same shape as d_score."""
+    a = _Args()
+    d = a(d_score)
+    out = torch.empty_like(d)
+    _check(N.lib().bsim_reward_amp(d.numel(), a.fp64, d.data_ptr(), out.data_ptr(), _stream()),
+           "amp_imitation_reward")
     return out

@@ -306,6 +306,7 @@ def main():
     env_cases()
     buffer_cases()
     reward_cases()
+    reward_extra_cases()
     randomize_cases()
 
 
@@ -473,6 +474,48 @@ def reward_cases():
               "cube_success": csucc, **{f"franka_{k}": v for k, v in fr.items()},
               "franka_reward": frr}
     save("rewards", {"kind": "rewards", "n": N}, arrays)
+
+
+def reward_extra_cases():
+    """The remaining reward kernels: trifinger (rewards.py:179-197, both sides
+    of the fingertip-term cutoff), ingenuity (115-121), AMP (222-225, incl.
+    the clip edges) and the nine-term rough ANYmal variant (129-158)."""
+    rng = np.random.default_rng(2025)
+    N, F = 512, 3
+    tp = RR.TrifingerRewardParams()
+    q1 = rng.normal(size=(N, 4)); q1 /= np.linalg.norm(q1, axis=1, keepdims=True)
+    q2 = rng.normal(size=(N, 4)); q2 /= np.linalg.norm(q2, axis=1, keepdims=True)
+    q2[: N // 4] = q1[: N // 4] + rng.normal(size=(N // 4, 4), scale=0.02)
+    q2 /= np.linalg.norm(q2, axis=1, keepdims=True)
+    tri = dict(cube=rng.normal(size=(N, 3), scale=0.05), prev_cube=rng.normal(size=(N, 3), scale=0.05),
+               cube_quat=q1, target=rng.normal(size=(N, 3), scale=0.05), target_quat=q2,
+               tip=rng.normal(size=(N, F, 3), scale=0.1), prev_tip=rng.normal(size=(N, F, 3), scale=0.1),
+               tip_vel=rng.normal(size=(N, F, 3)),
+               timestep=np.where(rng.uniform(size=N) < 0.5, tp.fingertip_term_cutoff - 3,
+                                 tp.fingertip_term_cutoff + 3).astype(np.int64))
+    tri["timestep"][0] = tp.fingertip_term_cutoff
+    tri["target"][: N // 8] = tri["cube"][: N // 8]
+    trr = RR.trifinger_reward(tri["cube"], tri["prev_cube"], tri["cube_quat"], tri["target"],
+                              tri["target_quat"], tri["tip"], tri["prev_tip"], tri["tip_vel"],
+                              tri["timestep"], tp)
+    ing = dict(pos=rng.normal(size=(N, 3)), target=rng.normal(size=(N, 3)),
+               up=rng.uniform(-1, 1, N), spin=rng.normal(size=(N, 3)))
+    igr = RR.ingenuity_reward(ing["pos"], ing["target"], ing["up"], ing["spin"])
+    d = rng.uniform(-0.2, 1.2, N)
+    d[:4] = [0.0, 1.0, 1e-4, 1.0 - 1e-4]
+    amr = RR.amp_imitation_reward(d)
+    ap = RR.AnymalRewardParams()
+    ro = dict(lin=rng.normal(size=(N, 3)), ang=rng.normal(size=(N, 3)), cmd=rng.uniform(-1, 1, (N, 3)),
+              qvel=rng.normal(size=(N, 12)), qacc=rng.normal(size=(N, 12), scale=10),
+              torques=rng.normal(size=(N, 12), scale=20), arate=rng.normal(size=(N, 12)),
+              coll=rng.integers(0, 4, N).astype(float), air=rng.uniform(0, 1, (N, 4)))
+    ror = RR.anymal_reward(ro["lin"], ro["ang"], ro["cmd"], ro["qvel"], ro["qacc"], ro["torques"],
+                           ro["arate"], ro["coll"], ro["air"], ap, variant="rough")
+    arrays = {**{f"tri_{k}": v for k, v in tri.items()}, "tri_reward": trr,
+              **{f"ing_{k}": v for k, v in ing.items()}, "ing_reward": igr,
+              "amp_d": d, "amp_reward": amr,
+              **{f"rough_{k}": v for k, v in ro.items()}, "rough_reward": ror}
+    save("rewards_extra", {"kind": "rewards", "n": N}, arrays)
 
 
 if __name__ == "__main__":
