@@ -320,40 +320,24 @@ def measure_franka(E, args, rank, world):
 
 
 def measure_shadow_hand(E, args, rank, world):
-    """Shadow Hand cube reorientation (BASELINE.json config 5, physics +
-    reward + domain randomisation): the authored 24-DOF hand with coupling
-    tendons and a cube (box pair contacts), Table-12 domain randomisation of
-    every env at the start, random PD targets, 2 substeps, and the reference
-    cube_reorientation_reward kernel per step.  No reference env exists for
-    this config: no obs / reset layer."""
+    """Shadow Hand cube reorientation (BASELINE.json config 5): ShadowHandEnv
+    -- the authored 24-DOF hand with coupling tendons and a cube (box pair
+    contacts), Table-12 domain randomisation at every reset, 2 substeps, and
+    the fused cube task tail (cube_reorientation_reward, fall / timeout,
+    goal resets on success, 96-dim obs, auto-reset) per control step, uniform
+    random actions.  The reference has the reward but no env for this config
+    (SURVEY.md 8(d)): the env layer is ours (envs.ShadowHandEnv)."""
     import torch
     import torch.distributed as dist
 
-    from paper_2108_10470_b200 import models as M
-    from paper_2108_10470_b200 import rewards as RW
-    from paper_2108_10470_b200.params import SimParams
-    from paper_2108_10470_b200.randomize import DEFAULT_SCHEDULE, DomainRandomizer
-    from paper_2108_10470_b200.scene import Scene
-    s = Scene([M.shadow_hand(), M.cube("cube", M.SHADOW_CUBE_HALF, 0.1)], E, SimParams(dt=1 / 120),
-              shape_pairs="all", env_offset=rank * E, total_envs=world * E)
-    B, D = s.bodies_per_env, s.dofs_per_env
-    roots = s.body_q.view(E, B, 13)
-    roots[:, 0, 0:3] = torch.tensor(M.SHADOW_HAND_ROOT, dtype=s.dtype)
-    roots[:, B - 1, 0:3] = torch.tensor([0.145, 0.0, M.SHADOW_HAND_ROOT[2] + 0.012 + M.SHADOW_CUBE_HALF + 0.001],
-                                        dtype=s.dtype)
-    s.forward_kinematics()
-    DomainRandomizer(s, DEFAULT_SCHEDULE, seed=7).randomize(list(range(E)), 10 ** 6)
-    gen = torch.Generator(device=s.device).manual_seed(77 + rank)
-    prm = RW.CubeRewardParams()
-    st = s.body_state.view(E, B, 13)
-    tgt_pos = st[:, B - 1, 0:3].clone()
-    tgt_quat = torch.tensor([0.0, 0.0, 0.0, 1.0], dtype=s.dtype, device=s.device).repeat(E, 1)
+    from paper_2108_10470_b200.envs import make_env
+    env = make_env("shadow-hand", num_envs=E, seed=0, randomize=True, env_offset=rank * E, total_envs=world * E)
+    gen = torch.Generator(device=env.obs.device).manual_seed(77 + rank)
+    s = env.scene
 
     def step():
-        a = torch.rand((E, D), generator=gen, device=s.device, dtype=s.dtype) * 2 - 1
-        s.ctrl_dof_pos_target.copy_(0.4 * a.reshape(-1))
-        s.step(2)
-        return RW.cube_reorientation_reward(st[:, B - 1, 0:3], st[:, B - 1, 3:7], tgt_pos, tgt_quat, a, prm)[0]
+        a = torch.rand((E, env.act_dim), generator=gen, device=env.obs.device, dtype=s.dtype) * 2 - 1
+        return env.step(a).reward
 
     for _ in range(args.warmup):
         step()
@@ -370,7 +354,7 @@ def measure_shadow_hand(E, args, rank, world):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ok = bool(torch.isfinite(r).all()) and int(s.nonfinite.sum()) == 0
-    s.close()
+    env.close()
     return world * E * args.steps / (float(t.item()) / 1e3), ok
 
 
@@ -407,8 +391,10 @@ def run_gpu(args):
         hv, hok = measure_shadow_hand(16384, a2, rank, world)
         others["shadow_hand"] = {"value": hv, "unit": UNIT, "envs_per_gpu": 16384, "steps": a2.steps,
                                  "finite": hok,
-                                 "note": "physics (24-DOF hand, tendons, cube, box pair contacts) + domain "
-                                         "randomisation + cube_reorientation_reward; no reference env exists"}
+                                 "note": "ShadowHandEnv: physics (24-DOF hand, tendons, cube, box pair contacts) "
+                                         "+ domain randomisation at resets + fused cube task tail (reward, fall / "
+                                         "timeout, goal resets, obs, auto-reset); the reference has the reward "
+                                         "but no env for this config"}
         for name in ("ant", "humanoid"):   # PPO-rollout steps: policy inference + env step
             r = measure(WORKLOADS[name][0], E, a2, rank, world, policy=True, kernel=False, e2e=False)
             others[f"{name}_ppo_rollout"] = {"value": r["value"], "unit": UNIT, "envs_per_gpu": E,

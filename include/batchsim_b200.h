@@ -213,8 +213,16 @@ int bsim_collide(const bsim_layout_t *layout, const bsim_params_t *params,
    ------------------------------------------------------------------------ */
 /* QUADRUPED: Ant analog (envs.py:359-478); ANYMAL: envs.py:484-565;
    HUMANOID: the same locomotion task (obs layout, locomotion_reward, reset
-   law) on the authored 21-DOF humanoid with its own termination height. */
-enum bsim_task_kind { BSIM_TASK_QUADRUPED = 1, BSIM_TASK_ANYMAL = 2, BSIM_TASK_HUMANOID = 3 };
+   law) on the authored 21-DOF humanoid with its own termination height.
+   CUBE: in-hand cube reorientation (BASELINE.json config "Shadow Hand"; the
+   reference has the reward, rewards.py:161-176, but no env): a fixed-base
+   hand (actor 0) and a single-body cube (actor 1, the env's last body);
+   obs = [2(q-lo)/(hi-lo)-1 (D), 0.2 qd (D), cube pos 3, quat 4, linvel 3,
+   0.2 angvel 3, goal pos 3, goal quat 4, cube quat (x) conj(goal quat) 4,
+   actions (A)]; reward = cube_reorientation_reward with the reference's
+   CubeRewardParams defaults; done = cube farther than fall_dist from the
+   goal | timeout | poisoned; a success draws a new goal orientation. */
+enum bsim_task_kind { BSIM_TASK_QUADRUPED = 1, BSIM_TASK_ANYMAL = 2, BSIM_TASK_HUMANOID = 3, BSIM_TASK_CUBE = 4 };
 
 /* Domain randomisation (reference randomize.py:86-189).  Targets in the
    reference's order: 0 dims, 1 masses, 2 friction, 3 damping, 4 gains,
@@ -256,6 +264,8 @@ typedef struct bsim_task_t {
     double termination_height;  /* locomotion tasks: done when torso z <= this (rewards.py:25) */
     const int64_t *step_count_dev;  /* optional device copy of step_count (CUDA-graph replay);
                                        NULL: use step_count */
+    void *goals;                /* CUBE: [E][8] goal pos xyz (the cube's spawn point, set by the
+                                   caller), goal quat xyzw, consecutive successes; NULL otherwise */
 } bsim_task_t;
 
 /* DomainRandomizer.randomize(env_indices, step) on its own (randomize.py:116-134). */

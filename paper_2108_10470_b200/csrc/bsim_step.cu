@@ -513,11 +513,7 @@ int launch_step_t(const Ctx<R> &c, size_t smem, int n_substeps, const bsim_actio
 }
 
 // the task-layer argument rules of bsim_task_step (bsim_tasks.cu)
-bool task_ok(const bsim_layout_t *L, const bsim_task_t *t) {
-    const bool kind_ok = t->kind == BSIM_TASK_QUADRUPED || t->kind == BSIM_TASK_ANYMAL || t->kind == BSIM_TASK_HUMANOID;
-    return kind_ok && t->act_dim == L->dofs_per_env && L->actors_per_env == 1 &&
-           t->obs_dim == 12 + 2 * t->act_dim + (t->kind == BSIM_TASK_ANYMAL ? 0 : 6 * L->sensors_per_env) + t->act_dim;
-}
+bool task_ok(const bsim_layout_t *L, const bsim_task_t *t) { return task_args_ok(L, t); }
 
 #ifndef BSIM_LARGE_TU
 // The large-articulation variant (bsim_step_large.cu: this source with a

@@ -77,10 +77,7 @@ Ctx<R> task_ctx(const bsim_layout_t *L, const typename Abi<R>::State *s) {
 }
 
 bool bad(const bsim_layout_t *L, const void *s, const bsim_task_t *t) {
-    return !L || !s || !t || (t->kind != BSIM_TASK_QUADRUPED && t->kind != BSIM_TASK_ANYMAL && t->kind != BSIM_TASK_HUMANOID) ||
-           t->act_dim != L->dofs_per_env || L->actors_per_env != 1 ||
-           t->obs_dim != 12 + 2 * t->act_dim + (t->kind == BSIM_TASK_ANYMAL ? 0 : 6 * L->sensors_per_env) +
-                             t->act_dim;
+    return !L || !s || !t || !task_args_ok(L, t);
 }
 
 template <class R>

@@ -16,6 +16,16 @@
 
 namespace bsim {
 
+// the task-layer argument rules shared by bsim_task_* and bsim_env_step*
+inline bool task_args_ok(const bsim_layout_t *L, const bsim_task_t *t) {
+    if (t->kind == BSIM_TASK_CUBE)
+        return t->goals && t->act_dim == L->dofs_per_env && L->actors_per_env == 2 &&
+               t->obs_dim == 2 * L->dofs_per_env + 24 + t->act_dim;
+    const bool kind_ok = t->kind == BSIM_TASK_QUADRUPED || t->kind == BSIM_TASK_ANYMAL || t->kind == BSIM_TASK_HUMANOID;
+    return kind_ok && t->act_dim == L->dofs_per_env && L->actors_per_env == 1 &&
+           t->obs_dim == 12 + 2 * t->act_dim + (t->kind == BSIM_TASK_ANYMAL ? 0 : 6 * L->sensors_per_env) + t->act_dim;
+}
+
 template <class R> struct TaskView {
     const bsim_task_t &t;
     R *stage = nullptr;   // optional shared-memory obs rows of envs [stage_e0, ...) (coalesced copy-out)
@@ -27,6 +37,7 @@ template <class R> struct TaskView {
     BS_HD R *act(int e) const { return reinterpret_cast<R *>(t.actions) + (size_t)e * t.act_dim; }
     BS_HD R &potential(int e) const { return reinterpret_cast<R *>(t.potentials)[e]; }
     BS_HD R *cmd(int e) const { return reinterpret_cast<R *>(t.commands) + 3 * (size_t)e; }
+    BS_HD R *goal(int e) const { return reinterpret_cast<R *>(t.goals) + 8 * (size_t)e; }
     BS_HD R lo(int k) const { return reinterpret_cast<const R *>(t.dof_lower)[k]; }
     BS_HD R hi(int k) const { return reinterpret_cast<const R *>(t.dof_upper)[k]; }
 };
@@ -63,6 +74,45 @@ template <class R> BS_HD Frame<R> quad_frame(const Root<R> &r) {
     return f;
 }
 
+// ------------------------------------------------------------ cube reorientation
+// The env's last body is the cube (actor 1); tv.goal(e) = goal pos 3, quat 4, successes.
+template <class R> BS_HD const R *cube_row(const Ctx<R> &c, int e) {
+    return c.s.body_q + ((size_t)e * c.d.B + c.d.B - 1) * 13;
+}
+
+// hand DOFs U(+-0.1) clamped into their limits, zero rates; the cube at the
+// goal position (its spawn point above the palm) with a random yaw, at rest
+template <class R> __device__ void cube_reset_state(const Ctx<R> &c, const TaskView<R> &tv, int e, NpRng &rng) {
+    const Dims &d = c.d;
+    R *hand = c.s.body_q + (size_t)e * d.B * 13;   // fixed-base root: the pose stays, the twist is zeroed
+    for (int k = 7; k < 13; ++k) hand[k] = R(0);
+    R *dof = c.s.dof_state + 2 * (size_t)e * d.D;
+    for (int k = 0; k < tv.t.act_dim; ++k) {
+        double q = np_uniform(rng, -0.1, 0.1);
+        const double lo = (double)tv.lo(k), hi = (double)tv.hi(k);
+        dof[2 * k] = R(q < lo ? lo : (q > hi ? hi : q));
+        dof[2 * k + 1] = R(0);
+    }
+    const double yaw = np_uniform(rng, -3.141592653589793, 3.141592653589793);
+    const R *g = tv.goal(e);
+    R *cb = hand + (size_t)(d.B - 1) * 13;
+    cb[0] = g[0]; cb[1] = g[1]; cb[2] = g[2];
+    cb[3] = R(0); cb[4] = R(0); cb[5] = R(sin(yaw / 2.0)); cb[6] = R(cos(yaw / 2.0));
+    for (int k = 7; k < 13; ++k) cb[k] = R(0);
+}
+
+// a new goal orientation, uniform on SO(3) (Shoemake), from the stream keyed
+// (seed, global env, reset count, successes)
+template <class R> __device__ void cube_new_goal(const Ctx<R> &c, const TaskView<R> &tv, int e) {
+    R *g = tv.goal(e);
+    uint32_t key[4] = {tv.t.seed, (uint32_t)(c.L.env_offset + e), (uint32_t)tv.t.reset_count[e],
+                       0xD000u + (uint32_t)g[7]};
+    NpRng r = np_rng(key, 4);
+    const double u1 = np_uniform(r, 0.0, 1.0), u2 = np_uniform(r, 0.0, 1.0), u3 = np_uniform(r, 0.0, 1.0);
+    const double a = sqrt(1.0 - u1), b = sqrt(u1), tp = 6.283185307179586;
+    g[3] = R(a * sin(tp * u2)); g[4] = R(a * cos(tp * u2)); g[5] = R(b * sin(tp * u3)); g[6] = R(b * cos(tp * u3));
+}
+
 // ------------------------------------------------------------ reset
 // EnvBatch.reset for one env (envs.py:145-166) with the task's _reset_envs
 // (404-419 / 517-531) and _post_reset (385-397 / 506-515).
@@ -75,22 +125,27 @@ template <class R> __device__ void task_reset_env(const Ctx<R> &c, const TaskVie
     const uint32_t genv = (uint32_t)(c.L.env_offset + e);
     uint32_t key[4] = {t.seed, genv, (uint32_t)t.reset_count[e], 0xCu};
     NpRng rng = np_rng(key, 3);
-    double qx = 0.0, qy = 0.0, qz = 0.0, qw = 1.0;
-    const bool loco = t.kind != BSIM_TASK_ANYMAL;
-    if (loco) {
-        double yaw = np_uniform(rng, -0.1, 0.1);
-        qz = sin(yaw / 2.0);
-        qw = cos(yaw / 2.0);
-    }
-    double n = sqrt(qx * qx + qy * qy + qz * qz + qw * qw);  // set_root_state renormalises (buffers.py:145)
-    R *root = c.s.body_q + (size_t)e * d.B * 13;
-    root[0] = R(0); root[1] = R(0); root[2] = R(t.rest_height + 0.02);
-    root[3] = R(qx / n); root[4] = R(qy / n); root[5] = R(qz / n); root[6] = R(qw / n);
-    for (int k = 7; k < 13; ++k) root[k] = R(0);
-    R *dof = c.s.dof_state + 2 * (size_t)e * d.D;
-    for (int k = 0; k < t.act_dim; ++k) {
-        dof[2 * k] = R(np_uniform(rng, -0.1, 0.1));
-        dof[2 * k + 1] = R(0);
+    const bool cube = t.kind == BSIM_TASK_CUBE;
+    const bool loco = t.kind != BSIM_TASK_ANYMAL && !cube;
+    if (cube) {
+        cube_reset_state(c, tv, e, rng);
+    } else {
+        double qx = 0.0, qy = 0.0, qz = 0.0, qw = 1.0;
+        if (loco) {
+            double yaw = np_uniform(rng, -0.1, 0.1);
+            qz = sin(yaw / 2.0);
+            qw = cos(yaw / 2.0);
+        }
+        double n = sqrt(qx * qx + qy * qy + qz * qz + qw * qw);  // set_root_state renormalises (buffers.py:145)
+        R *root = c.s.body_q + (size_t)e * d.B * 13;
+        root[0] = R(0); root[1] = R(0); root[2] = R(t.rest_height + 0.02);
+        root[3] = R(qx / n); root[4] = R(qy / n); root[5] = R(qz / n); root[6] = R(qw / n);
+        for (int k = 7; k < 13; ++k) root[k] = R(0);
+        R *dof = c.s.dof_state + 2 * (size_t)e * d.D;
+        for (int k = 0; k < t.act_dim; ++k) {
+            dof[2 * k] = R(np_uniform(rng, -0.1, 0.1));
+            dof[2 * k + 1] = R(0);
+        }
     }
     if (t.obs_noise) {  // per-episode correlated noise continues the reset stream (envs.py:161-164)
         R *cn = reinterpret_cast<R *>(t.corr_noise) + (size_t)e * t.obs_dim;
@@ -103,7 +158,10 @@ template <class R> __device__ void task_reset_env(const Ctx<R> &c, const TaskVie
     t.reset_count[e] += 1;
     R *a = tv.act(e);
     for (int k = 0; k < t.act_dim; ++k) a[k] = R(0);
-    if (loco) {
+    if (cube) {
+        tv.goal(e)[7] = R(0);
+        cube_new_goal(c, tv, e);
+    } else if (loco) {
         R z = R(t.rest_height + 0.02);
         R dist = r_sqrt(R(QUAD_TARGET_X) * R(QUAD_TARGET_X) + z * z);
         tv.potential(e) = -dist / R(t.control_dt);
@@ -240,9 +298,55 @@ template <class R, int G> __device__ void anymal_obs_g(const Ctx<R> &c, const Ta
     for (int k = sl; k < A; k += G) o[12 + 2 * A + k] = a[k];
 }
 
+// cube_reorientation_reward (rewards.py:161-176) with the CubeRewardParams
+// defaults (rewards.py:31-40); done = the cube fell (goal distance >= fall_dist)
+template <class R, int G>
+__device__ R cube_reward_g(const Ctx<R> &c, const TaskView<R> &tv, int e, int sl, bool &done, bool &success) {
+    const R *cb = cube_row(c, e), *g = tv.goal(e);
+    R dx = cb[0] - g[0], dy = cb[1] - g[1], dz = cb[2] - g[2];
+    R gd = r_sqrt(dx * dx + dy * dy + dz * dz);
+    Q4<R> dq = qmul(Q4<R>{cb[3], cb[4], cb[5], cb[6]}, qconj(Q4<R>{g[3], g[4], g[5], g[6]}));
+    R nn = r_sqrt(dq.x * dq.x + dq.y * dq.y + dq.z * dq.z);
+    nn = nn > R(1) ? R(1) : nn;
+    R rd = R(2) * asin(nn);                   // rot_dist (spatial.py:125-132)
+    const R *a = tv.act(e);
+    R sa = R(0);
+    for (int k = sl; k < tv.t.act_dim; k += G) sa = sa + a[k] * a[k];
+    sa = group_sum<G>(sa);
+    R rew = gd * R(-10.0) + (R(1) / (fabs(rd) + R(0.1))) * R(1.0) + sa * R(-0.0002);
+    success = fabs(rd) <= R(0.4);
+    if (success) rew = rew + R(250.0);
+    done = gd >= R(0.24);                     // + fall_penalty 0
+    return rew;
+}
+
+// cube task observation (layout in include/batchsim_b200.h, BSIM_TASK_CUBE)
+template <class R, int G> __device__ void cube_obs_g(const Ctx<R> &c, const TaskView<R> &tv, int e, int sl) {
+    const int D = c.d.D, A = tv.t.act_dim;
+    R *o = tv.obs(e);
+    const R *dof = c.s.dof_state + 2 * (size_t)e * D;
+    for (int k = sl; k < D; k += G) {
+        R lo = tv.lo(k), hi = tv.hi(k), q = dof[2 * k];
+        o[k] = finite_r(lo) && finite_r(hi) ? R(2) * (q - lo) / (hi - lo) - R(1) : q;
+        o[D + k] = dof[2 * k + 1] * R(0.2);
+    }
+    if (sl == 0) {
+        const R *cb = cube_row(c, e), *g = tv.goal(e);
+        R *p = o + 2 * D;
+        for (int k = 0; k < 10; ++k) p[k] = cb[k];
+        for (int k = 10; k < 13; ++k) p[k] = cb[k] * R(0.2);
+        for (int k = 0; k < 7; ++k) p[13 + k] = g[k];
+        Q4<R> dq = qmul(Q4<R>{cb[3], cb[4], cb[5], cb[6]}, qconj(Q4<R>{g[3], g[4], g[5], g[6]}));
+        p[20] = dq.x; p[21] = dq.y; p[22] = dq.z; p[23] = dq.w;
+    }
+    const R *a = tv.act(e);
+    for (int k = sl; k < A; k += G) o[2 * D + 24 + k] = a[k];
+}
+
 template <class R, int G> __device__ void task_obs_g(const Ctx<R> &c, const TaskView<R> &tv, int e, int sl) {
     const bsim_task_t &t = tv.t;
-    if (t.kind != BSIM_TASK_ANYMAL) quad_obs_g<R, G>(c, tv, e, sl);
+    if (t.kind == BSIM_TASK_CUBE) cube_obs_g<R, G>(c, tv, e, sl);
+    else if (t.kind != BSIM_TASK_ANYMAL) quad_obs_g<R, G>(c, tv, e, sl);
     else anymal_obs_g<R, G>(c, tv, e, sl);
     if (t.obs_noise) {  // perturb_observations (randomize.py:231-237): one sequential stream per env
         __syncwarp(group_mask<G>());
@@ -265,15 +369,21 @@ template <class R, int G> __device__ void task_obs_g(const Ctx<R> &c, const Task
 template <class R> __device__ __noinline__ void task_reset_env_call(const Ctx<R> &c, const TaskView<R> &tv, int e) {
     task_reset_env(c, tv, e);
 }
+// goal reset after a success (cube task): successes + 1, a new goal orientation
+template <class R> __device__ __noinline__ void cube_goal_call(const Ctx<R> &c, const TaskView<R> &tv, int e) {
+    tv.goal(e)[7] = tv.goal(e)[7] + R(1);
+    cube_new_goal(c, tv, e);
+}
 
 // EnvBatch.step tail after the decimated physics (envs.py:188-199), G lanes per env
 template <class R, int G> __device__ void task_step_env_g(const Ctx<R> &c, const TaskView<R> &tv, int e, int sl) {
     const bsim_task_t &t = tv.t;
     const int steps = t.episode_steps[e] + 1;
     Root<R> r = root_of(c, e);
-    bool done;
+    bool done, success = false;
     R rew;
-    if (t.kind != BSIM_TASK_ANYMAL) rew = quad_reward_g<R, G>(c, tv, e, sl, r, quad_frame(r), done);
+    if (t.kind == BSIM_TASK_CUBE) rew = cube_reward_g<R, G>(c, tv, e, sl, done, success);
+    else if (t.kind != BSIM_TASK_ANYMAL) rew = quad_reward_g<R, G>(c, tv, e, sl, r, quad_frame(r), done);
     else rew = anymal_reward_g<R, G>(c, tv, e, sl, r, done);
     const bool timeout = steps >= t.episode_length;
     const bool pois = c.s.nonfinite[e] != 0;
@@ -286,6 +396,7 @@ template <class R, int G> __device__ void task_step_env_g(const Ctx<R> &c, const
         t.timeout[e] = timeout;
         t.poisoned[e] = pois;
         if (done) task_reset_env_call(c, tv, e);
+        else if (success) cube_goal_call(c, tv, e);
     }
     __syncwarp(group_mask<G>());           // the reset state is visible to the group
     task_obs_g<R, G>(c, tv, e, sl);        // reset rows get the post-reset observation (envs.py:195-198)

@@ -34,7 +34,7 @@ from .randomize import DEFAULT_SCHEDULE, DR, DomainRandomizer
 from .scene import Scene
 
 ALL = None
-TASK_QUADRUPED, TASK_ANYMAL, TASK_HUMANOID = 1, 2, 3
+TASK_QUADRUPED, TASK_ANYMAL, TASK_HUMANOID, TASK_CUBE = 1, 2, 3, 4
 
 
 @dataclass
@@ -89,7 +89,8 @@ class Task(C.Structure):
                                   "reset_count", "actions", "potentials", "commands", "dof_lower",
                                   "dof_upper", "corr_noise", "noise_count")] + [("dr", DR),
                                                                                 ("termination_height", C.c_double),
-                                                                                ("step_count_dev", C.c_void_p)]
+                                                                                ("step_count_dev", C.c_void_p),
+                                                                                ("goals", C.c_void_p)]
 
 
 def dof_limits(model):
@@ -117,9 +118,9 @@ class EnvBatch:
         self.config = cfg = config.validate()
         E = cfg.num_envs
         self.model = self._model()
-        self.scene = self.sim = Scene([self.model], E, self._sim_params(), device=cfg.device,
+        self.scene = self.sim = Scene(self._models(), E, self._sim_params(), device=cfg.device,
                                       precision=cfg.precision, env_offset=cfg.env_offset,
-                                      total_envs=cfg.total_envs)
+                                      total_envs=cfg.total_envs, **self._scene_kwargs())
         self.buffers = SimBuffers(self.scene)
         s = self.scene
         dev, dt = s.device, s.dtype
@@ -139,6 +140,8 @@ class EnvBatch:
         self._mask = torch.zeros(E, dtype=torch.uint8, device=dev)
         self.corr_noise = torch.zeros((E, self.obs_dim), dtype=dt, device=dev)
         self.noise_count = torch.zeros(E, dtype=torch.int32, device=dev)
+        self.goals = torch.zeros((E, 8), dtype=dt, device=dev) if self.task_kind == TASK_CUBE else None
+        self._setup()
         # domain randomisation (envs.py:94-96): snapshot after scene construction
         self._graph = None
         self.randomizer = (DomainRandomizer(self.scene, DEFAULT_SCHEDULE, seed=cfg.seed)
@@ -152,12 +155,22 @@ class EnvBatch:
                                                    self.dof_lower, self.dof_upper, self.corr_noise,
                                                    self.noise_count)),
                           self.randomizer.struct if self.randomizer is not None else DR(),
-                          float(self.termination_height))
+                          float(self.termination_height), None,
+                          self.goals.data_ptr() if self.goals is not None else None)
         self.reset()
 
     # ------------------------------------------------------------ hooks
     def _model(self):
         raise NotImplementedError
+
+    def _models(self):
+        return [self.model]
+
+    def _scene_kwargs(self):
+        return {}
+
+    def _setup(self):
+        """Task buffers / fixed poses to set before the first reset."""
 
     def _sim_params(self):
         return SimParams(dt=self.config.sim_dt)
@@ -470,8 +483,55 @@ class HumanoidEnv(EnvBatch):
         return M.humanoid()
 
 
+class ShadowHandEnv(EnvBatch):
+    """In-hand cube reorientation (BASELINE.json config 5, "Shadow Hand"):
+    the authored 24-DOF hand (models.shadow_hand_doc: fixed forearm, coupling
+    tendons, fingertip spheres, palm box) with a 6 cm cube on the palm and
+    box pair contacts.  The reference has this task's reward
+    (cube_reorientation_reward, rewards.py:161-176) but no env, so the env
+    layer is ours: targets = 0.4 a for all 24 DOFs; 96-dim obs (layout in
+    include/batchsim_b200.h, BSIM_TASK_CUBE); the cube falling 0.24 m from
+    the goal point ends the episode; a success (rot_dist <= 0.4) draws a new
+    goal orientation and counts in `goals[:, 7]`.  Reset: hand DOFs U(+-0.1)
+    inside their limits, the cube at the spawn point with a random yaw, a
+    uniform random goal orientation -- all drawn per env from PCG64 streams
+    keyed (seed, global env id, reset count), like the locomotion tasks."""
+
+    name = "shadow-hand"
+    obs_dim = 2 * 24 + 24 + 24
+    act_dim = 24
+    action_scale = 0.4
+    task_kind = TASK_CUBE
+
+    def __init__(self, config=None):
+        cfg = config or EnvConfig()
+        super().__init__(replace(cfg, sim_dt=1.0 / 120.0, control_dt=1.0 / 60.0))
+
+    def _model(self):
+        return M.shadow_hand()
+
+    def _models(self):
+        return [self.model, M.cube("cube", M.SHADOW_CUBE_HALF, 0.1)]
+
+    def _scene_kwargs(self):
+        return {"shape_pairs": "all"}
+
+    def _setup(self):
+        s = self.scene
+        E, B = self.config.num_envs, s.bodies_per_env
+        roots = s.body_q.view(E, B, 13)
+        roots[:, 0, 0:3] = torch.tensor(M.SHADOW_HAND_ROOT, dtype=s.dtype)
+        self.goals[:, 0:3] = torch.tensor(M.SHADOW_CUBE_SPAWN, dtype=s.dtype)
+
+    @property
+    def successes(self):
+        """Consecutive goal orientations reached in the current episode."""
+        return self.goals[:, 7]
+
+
 TASKS = {
     "quadruped": QuadrupedEnv,
+    "shadow-hand": ShadowHandEnv,
     "quadruped-anymal-obs": AnymalObsEnv,
     "humanoid": HumanoidEnv,
 }
