@@ -266,39 +266,23 @@ def measure(task, E, args, rank, world, clocks=None, policy=False, kernel=True, 
 
 
 def measure_franka(E, args, rank, world):
-    """Franka cube-stack (BASELINE.json config 4, physics + reward): the
+    """Franka cube-stack (BASELINE.json config 4): FrankaCubeStackEnv -- the
     authored arm + gripper and two cubes with box / capsule pair contacts
-    (shape_pairs="all"), random PD targets around the home pose, 2 substeps,
-    and the reference franka_stack_reward kernel on the new state per step.
-    There is no reference env for this config: no obs /
-    reset layer."""
+    (shape_pairs="all"), 2 substeps, and the fused stacking task tail
+    (franka_stack_reward, stacked / timeout, 54-dim obs, auto-reset) per
+    control step, uniform random actions.  The reference has the reward but
+    no env for this config: the env layer is ours."""
     import torch
     import torch.distributed as dist
 
-    from paper_2108_10470_b200 import models as M
-    from paper_2108_10470_b200 import rewards as RW
-    from paper_2108_10470_b200.params import SimParams
-    from paper_2108_10470_b200.scene import Scene
-    s = Scene([M.franka(), M.cube("cubeA", M.CUBE_A_HALF, 0.3), M.cube("cubeB", M.CUBE_B_HALF, 0.5)], E,
-              SimParams(dt=1 / 120), shape_pairs="all", env_offset=rank * E, total_envs=world * E)
-    B, D = s.bodies_per_env, s.dofs_per_env
-    roots = s.body_q.view(E, B, 13)
-    roots[:, 10, 0:3] = torch.tensor([0.45, 0.0, M.CUBE_A_HALF], dtype=s.dtype)
-    roots[:, 11, 0:3] = torch.tensor([0.45, 0.15, M.CUBE_B_HALF], dtype=s.dtype)
-    home = torch.tensor(M.FRANKA_HOME, dtype=s.dtype, device=s.device).repeat(E)
-    s.dof_state[:, 0] = home
-    s.forward_kinematics()
-    scale = torch.tensor([0.4] * 7 + [0.04, 0.04], dtype=s.dtype, device=s.device).repeat(E)
-    gen = torch.Generator(device=s.device).manual_seed(99 + rank)
-    prm = RW.FrankaStackParams()
-    st = s.body_state.view(E, B, 13)
+    from paper_2108_10470_b200.envs import make_env
+    env = make_env("franka-cube-stack", num_envs=E, seed=0, env_offset=rank * E, total_envs=world * E)
+    gen = torch.Generator(device=env.obs.device).manual_seed(99 + rank)
+    s = env.scene
 
     def step():
-        s.ctrl_dof_pos_target.copy_(home + scale * (torch.rand(E * D, generator=gen, device=s.device,
-                                                               dtype=s.dtype) * 2 - 1))
-        s.step(2)
-        return RW.franka_stack_reward(st[:, 10, 0:3], st[:, 11, 0:3], st[:, 7, 0:3], st[:, 8, 0:3],
-                                      st[:, 9, 0:3], prm)
+        a = torch.rand((E, env.act_dim), generator=gen, device=env.obs.device, dtype=s.dtype) * 2 - 1
+        return env.step(a).reward
 
     for _ in range(args.warmup):
         step()
@@ -315,7 +299,7 @@ def measure_franka(E, args, rank, world):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ok = bool(torch.isfinite(r).all()) and int(s.nonfinite.sum()) == 0
-    s.close()
+    env.close()
     return world * E * args.steps / (float(t.item()) / 1e3), ok
 
 
@@ -386,8 +370,9 @@ def run_gpu(args):
         fv, fok = measure_franka(8192, a2, rank, world)
         others["franka_cube_stack"] = {"value": fv, "unit": UNIT, "envs_per_gpu": 8192, "steps": a2.steps,
                                        "finite": fok,
-                                       "note": "physics (arm + 2 cubes, box pair contacts) + franka_stack_reward; "
-                                               "no reference env exists for this config"}
+                                       "note": "FrankaCubeStackEnv: physics (arm + 2 cubes, box pair contacts) + "
+                                               "fused stacking task tail (reward, stacked / timeout, obs, "
+                                               "auto-reset); the reference has the reward but no env"}
         hv, hok = measure_shadow_hand(16384, a2, rank, world)
         others["shadow_hand"] = {"value": hv, "unit": UNIT, "envs_per_gpu": 16384, "steps": a2.steps,
                                  "finite": hok,

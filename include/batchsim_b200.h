@@ -221,8 +221,17 @@ int bsim_collide(const bsim_layout_t *layout, const bsim_params_t *params,
    0.2 angvel 3, goal pos 3, goal quat 4, cube quat (x) conj(goal quat) 4,
    actions (A)]; reward = cube_reorientation_reward with the reference's
    CubeRewardParams defaults; done = cube farther than fall_dist from the
-   goal | timeout | poisoned; a success draws a new goal orientation. */
-enum bsim_task_kind { BSIM_TASK_QUADRUPED = 1, BSIM_TASK_ANYMAL = 2, BSIM_TASK_HUMANOID = 3, BSIM_TASK_CUBE = 4 };
+   goal | timeout | poisoned; a success draws a new goal orientation.
+   STACK: Franka cube stacking (BASELINE.json config "Franka cube-stack"; the
+   reference has franka_stack_reward, rewards.py:200-219, but no env): the
+   arm (actor 0; its last five bodies are hand, left finger, right finger)
+   then cube A and cube B (single-body actors, the env's last two bodies);
+   obs = [2(q-lo)/(hi-lo)-1 (D), 0.1 qd (D), hand pos 3, hand quat 4, A pos 3,
+   A quat 4, A - hand 3, B pos 3, B quat 4, A - B 3, actions (A)]; reward =
+   franka_stack_reward with the reference's FrankaStackParams defaults;
+   done = stacked | timeout | poisoned. */
+enum bsim_task_kind { BSIM_TASK_QUADRUPED = 1, BSIM_TASK_ANYMAL = 2, BSIM_TASK_HUMANOID = 3, BSIM_TASK_CUBE = 4,
+                      BSIM_TASK_STACK = 5 };
 
 /* Domain randomisation (reference randomize.py:86-189).  Targets in the
    reference's order: 0 dims, 1 masses, 2 friction, 3 damping, 4 gains,
@@ -265,7 +274,9 @@ typedef struct bsim_task_t {
     const int64_t *step_count_dev;  /* optional device copy of step_count (CUDA-graph replay);
                                        NULL: use step_count */
     void *goals;                /* CUBE: [E][8] goal pos xyz (the cube's spawn point, set by the
-                                   caller), goal quat xyzw, consecutive successes; NULL otherwise */
+                                   caller), goal quat xyzw, consecutive successes;
+                                   STACK: [E][8] spawn points of cube A and cube B (set by the
+                                   caller; resets add U(+-0.05) in x and y); NULL otherwise */
 } bsim_task_t;
 
 /* DomainRandomizer.randomize(env_indices, step) on its own (randomize.py:116-134). */

@@ -21,6 +21,9 @@ inline bool task_args_ok(const bsim_layout_t *L, const bsim_task_t *t) {
     if (t->kind == BSIM_TASK_CUBE)
         return t->goals && t->act_dim == L->dofs_per_env && L->actors_per_env == 2 &&
                t->obs_dim == 2 * L->dofs_per_env + 24 + t->act_dim;
+    if (t->kind == BSIM_TASK_STACK)
+        return t->goals && t->act_dim == L->dofs_per_env && L->actors_per_env == 3 && L->bodies_per_env >= 5 &&
+               t->obs_dim == 2 * L->dofs_per_env + 27 + t->act_dim;
     const bool kind_ok = t->kind == BSIM_TASK_QUADRUPED || t->kind == BSIM_TASK_ANYMAL || t->kind == BSIM_TASK_HUMANOID;
     return kind_ok && t->act_dim == L->dofs_per_env && L->actors_per_env == 1 &&
            t->obs_dim == 12 + 2 * t->act_dim + (t->kind == BSIM_TASK_ANYMAL ? 0 : 6 * L->sensors_per_env) + t->act_dim;
@@ -82,23 +85,36 @@ template <class R> BS_HD const R *cube_row(const Ctx<R> &c, int e) {
 
 // hand DOFs U(+-0.1) clamped into their limits, zero rates; the cube at the
 // goal position (its spawn point above the palm) with a random yaw, at rest
-template <class R> __device__ void cube_reset_state(const Ctx<R> &c, const TaskView<R> &tv, int e, NpRng &rng) {
-    const Dims &d = c.d;
-    R *hand = c.s.body_q + (size_t)e * d.B * 13;   // fixed-base root: the pose stays, the twist is zeroed
-    for (int k = 7; k < 13; ++k) hand[k] = R(0);
-    R *dof = c.s.dof_state + 2 * (size_t)e * d.D;
+template <class R> __device__ void arm_reset_dofs(const Ctx<R> &c, const TaskView<R> &tv, int e, NpRng &rng) {
+    R *root = c.s.body_q + (size_t)e * c.d.B * 13;  // fixed-base root: the pose stays, the twist is zeroed
+    for (int k = 7; k < 13; ++k) root[k] = R(0);
+    R *dof = c.s.dof_state + 2 * (size_t)e * c.d.D;
     for (int k = 0; k < tv.t.act_dim; ++k) {
         double q = np_uniform(rng, -0.1, 0.1);
         const double lo = (double)tv.lo(k), hi = (double)tv.hi(k);
         dof[2 * k] = R(q < lo ? lo : (q > hi ? hi : q));
         dof[2 * k + 1] = R(0);
     }
+}
+// a single-body actor at rest at `p` (+ U(+-jitter) in x, y) with a random yaw
+template <class R> __device__ void place_box(R *row, const R *p, double jitter, NpRng &rng) {
+    const double jx = jitter > 0.0 ? np_uniform(rng, -jitter, jitter) : 0.0;
+    const double jy = jitter > 0.0 ? np_uniform(rng, -jitter, jitter) : 0.0;
     const double yaw = np_uniform(rng, -3.141592653589793, 3.141592653589793);
-    const R *g = tv.goal(e);
-    R *cb = hand + (size_t)(d.B - 1) * 13;
-    cb[0] = g[0]; cb[1] = g[1]; cb[2] = g[2];
-    cb[3] = R(0); cb[4] = R(0); cb[5] = R(sin(yaw / 2.0)); cb[6] = R(cos(yaw / 2.0));
-    for (int k = 7; k < 13; ++k) cb[k] = R(0);
+    row[0] = R((double)p[0] + jx); row[1] = R((double)p[1] + jy); row[2] = p[2];
+    row[3] = R(0); row[4] = R(0); row[5] = R(sin(yaw / 2.0)); row[6] = R(cos(yaw / 2.0));
+    for (int k = 7; k < 13; ++k) row[k] = R(0);
+}
+template <class R> __device__ void cube_reset_state(const Ctx<R> &c, const TaskView<R> &tv, int e, NpRng &rng) {
+    arm_reset_dofs(c, tv, e, rng);
+    place_box(c.s.body_q + ((size_t)e * c.d.B + c.d.B - 1) * 13, tv.goal(e), 0.0, rng);
+}
+// Franka stacking: arm DOFs as above, cube A / B near their spawn points
+template <class R> __device__ void stack_reset_state(const Ctx<R> &c, const TaskView<R> &tv, int e, NpRng &rng) {
+    arm_reset_dofs(c, tv, e, rng);
+    R *rows = c.s.body_q + (size_t)e * c.d.B * 13;
+    place_box(rows + (size_t)(c.d.B - 2) * 13, tv.goal(e), 0.05, rng);
+    place_box(rows + (size_t)(c.d.B - 1) * 13, tv.goal(e) + 3, 0.05, rng);
 }
 
 // a new goal orientation, uniform on SO(3) (Shoemake), from the stream keyed
@@ -125,10 +141,12 @@ template <class R> __device__ void task_reset_env(const Ctx<R> &c, const TaskVie
     const uint32_t genv = (uint32_t)(c.L.env_offset + e);
     uint32_t key[4] = {t.seed, genv, (uint32_t)t.reset_count[e], 0xCu};
     NpRng rng = np_rng(key, 3);
-    const bool cube = t.kind == BSIM_TASK_CUBE;
-    const bool loco = t.kind != BSIM_TASK_ANYMAL && !cube;
+    const bool cube = t.kind == BSIM_TASK_CUBE, stack = t.kind == BSIM_TASK_STACK;
+    const bool loco = t.kind != BSIM_TASK_ANYMAL && !cube && !stack;
     if (cube) {
         cube_reset_state(c, tv, e, rng);
+    } else if (stack) {
+        stack_reset_state(c, tv, e, rng);
     } else {
         double qx = 0.0, qy = 0.0, qz = 0.0, qw = 1.0;
         if (loco) {
@@ -165,7 +183,7 @@ template <class R> __device__ void task_reset_env(const Ctx<R> &c, const TaskVie
         R z = R(t.rest_height + 0.02);
         R dist = r_sqrt(R(QUAD_TARGET_X) * R(QUAD_TARGET_X) + z * z);
         tv.potential(e) = -dist / R(t.control_dt);
-    } else {
+    } else if (!stack) {   // anymal velocity commands
         key[2] = (uint32_t)t.reset_count[e];
         NpRng cr = np_rng(key, 4);
         R *cmd = tv.cmd(e);
@@ -343,9 +361,60 @@ template <class R, int G> __device__ void cube_obs_g(const Ctx<R> &c, const Task
     for (int k = sl; k < A; k += G) o[2 * D + 24 + k] = a[k];
 }
 
+// franka_stack_reward (rewards.py:200-219) with the FrankaStackParams
+// defaults (rewards.py:68-75); done = stacked (the r_stack condition)
+template <class R> BS_HD const R *body_row(const Ctx<R> &c, int e, int b) {
+    return c.s.body_q + ((size_t)e * c.d.B + b) * 13;
+}
+template <class R> __device__ R stack_reward(const Ctx<R> &c, int e, bool &done) {
+    const int B = c.d.B;
+    const R *a = body_row(c, e, B - 2), *b = body_row(c, e, B - 1), *g = body_row(c, e, B - 5);
+    const R *lf = body_row(c, e, B - 4), *rf = body_row(c, e, B - 3);
+    auto d3 = [](const R *x, const R *y) {
+        R dx = x[0] - y[0], dy = x[1] - y[1], dz = x[2] - y[2];
+        return r_sqrt(dx * dx + dy * dy + dz * dz);
+    };
+    R xy = r_sqrt((a[0] - b[0]) * (a[0] - b[0]) + (a[1] - b[1]) * (a[1] - b[1]));
+    const bool lifted = a[2] > R(0.04), aligned = xy < R(0.02);
+    R dg = d3(g, a);
+    const bool stacked = a[2] > b[2] && aligned && dg > R(0.04);
+    R rs = stacked ? R(16.0) : R(0);
+    R ral = lifted ? R(2.0) * (R(1) - tanh(R(10) * xy)) : R(0);
+    R rl = lifted ? R(1.5) : R(0);
+    R ds = dg + d3(lf, a) + d3(rf, a);
+    R rr = R(0.1) * (R(1) - tanh((R(10) / R(3)) * ds));
+    R alt = ral + rl + rr;
+    done = stacked;
+    return rs > alt ? rs : alt;
+}
+
+// stacking observation (layout in include/batchsim_b200.h, BSIM_TASK_STACK)
+template <class R, int G> __device__ void stack_obs_g(const Ctx<R> &c, const TaskView<R> &tv, int e, int sl) {
+    const int D = c.d.D, A = tv.t.act_dim, B = c.d.B;
+    R *o = tv.obs(e);
+    const R *dof = c.s.dof_state + 2 * (size_t)e * D;
+    for (int k = sl; k < D; k += G) {
+        R lo = tv.lo(k), hi = tv.hi(k), q = dof[2 * k];
+        o[k] = finite_r(lo) && finite_r(hi) ? R(2) * (q - lo) / (hi - lo) - R(1) : q;
+        o[D + k] = dof[2 * k + 1] * R(0.1);
+    }
+    if (sl == 0) {
+        const R *h = body_row(c, e, B - 5), *a = body_row(c, e, B - 2), *b = body_row(c, e, B - 1);
+        R *p = o + 2 * D;
+        for (int k = 0; k < 7; ++k) p[k] = h[k];
+        for (int k = 0; k < 7; ++k) p[7 + k] = a[k];
+        for (int k = 0; k < 3; ++k) p[14 + k] = a[k] - h[k];
+        for (int k = 0; k < 7; ++k) p[17 + k] = b[k];
+        for (int k = 0; k < 3; ++k) p[24 + k] = a[k] - b[k];
+    }
+    const R *a = tv.act(e);
+    for (int k = sl; k < A; k += G) o[2 * D + 27 + k] = a[k];
+}
+
 template <class R, int G> __device__ void task_obs_g(const Ctx<R> &c, const TaskView<R> &tv, int e, int sl) {
     const bsim_task_t &t = tv.t;
     if (t.kind == BSIM_TASK_CUBE) cube_obs_g<R, G>(c, tv, e, sl);
+    else if (t.kind == BSIM_TASK_STACK) stack_obs_g<R, G>(c, tv, e, sl);
     else if (t.kind != BSIM_TASK_ANYMAL) quad_obs_g<R, G>(c, tv, e, sl);
     else anymal_obs_g<R, G>(c, tv, e, sl);
     if (t.obs_noise) {  // perturb_observations (randomize.py:231-237): one sequential stream per env
@@ -383,6 +452,7 @@ template <class R, int G> __device__ void task_step_env_g(const Ctx<R> &c, const
     bool done, success = false;
     R rew;
     if (t.kind == BSIM_TASK_CUBE) rew = cube_reward_g<R, G>(c, tv, e, sl, done, success);
+    else if (t.kind == BSIM_TASK_STACK) rew = stack_reward(c, e, done);
     else if (t.kind != BSIM_TASK_ANYMAL) rew = quad_reward_g<R, G>(c, tv, e, sl, r, quad_frame(r), done);
     else rew = anymal_reward_g<R, G>(c, tv, e, sl, r, done);
     const bool timeout = steps >= t.episode_length;

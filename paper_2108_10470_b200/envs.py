@@ -34,7 +34,7 @@ from .randomize import DEFAULT_SCHEDULE, DR, DomainRandomizer
 from .scene import Scene
 
 ALL = None
-TASK_QUADRUPED, TASK_ANYMAL, TASK_HUMANOID, TASK_CUBE = 1, 2, 3, 4
+TASK_QUADRUPED, TASK_ANYMAL, TASK_HUMANOID, TASK_CUBE, TASK_STACK = 1, 2, 3, 4, 5
 
 
 @dataclass
@@ -140,7 +140,8 @@ class EnvBatch:
         self._mask = torch.zeros(E, dtype=torch.uint8, device=dev)
         self.corr_noise = torch.zeros((E, self.obs_dim), dtype=dt, device=dev)
         self.noise_count = torch.zeros(E, dtype=torch.int32, device=dev)
-        self.goals = torch.zeros((E, 8), dtype=dt, device=dev) if self.task_kind == TASK_CUBE else None
+        self.goals = (torch.zeros((E, 8), dtype=dt, device=dev) if self.task_kind in (TASK_CUBE, TASK_STACK)
+                      else None)
         self._setup()
         # domain randomisation (envs.py:94-96): snapshot after scene construction
         self._graph = None
@@ -529,8 +530,46 @@ class ShadowHandEnv(EnvBatch):
         return self.goals[:, 7]
 
 
+class FrankaCubeStackEnv(EnvBatch):
+    """Franka cube stacking (BASELINE.json config 4): the authored 7-DOF arm
+    + parallel gripper (models.franka_doc) and two free cubes (box pair
+    contacts).  The reference has this task's reward (franka_stack_reward,
+    rewards.py:200-219) but no env, so the env layer is ours: targets = 0.4 a
+    for the 9 DOFs (the finger targets saturate at the 4 cm limit); 54-dim obs
+    (layout in include/batchsim_b200.h, BSIM_TASK_STACK); a stack (cube A on
+    B, aligned, gripper away) or the timeout ends the episode.  Reset: arm
+    DOFs U(+-0.1) inside their limits, cube A / B at their spawn points
+    + U(+-5 cm) in x and y with a random yaw, from per-env PCG64 streams
+    keyed (seed, global env id, reset count)."""
+
+    name = "franka-cube-stack"
+    obs_dim = 2 * 9 + 27 + 9
+    act_dim = 9
+    action_scale = 0.4
+    task_kind = TASK_STACK
+
+    def __init__(self, config=None):
+        cfg = config or EnvConfig()
+        super().__init__(replace(cfg, sim_dt=1.0 / 120.0, control_dt=1.0 / 60.0))
+
+    def _model(self):
+        return M.franka()
+
+    def _models(self):
+        return [self.model, M.cube("cubeA", M.CUBE_A_HALF, 0.3), M.cube("cubeB", M.CUBE_B_HALF, 0.5)]
+
+    def _scene_kwargs(self):
+        return {"shape_pairs": "all"}
+
+    def _setup(self):
+        s = self.scene
+        self.goals[:, 0:3] = torch.tensor(M.FRANKA_CUBE_A_SPAWN, dtype=s.dtype)
+        self.goals[:, 3:6] = torch.tensor(M.FRANKA_CUBE_B_SPAWN, dtype=s.dtype)
+
+
 TASKS = {
     "quadruped": QuadrupedEnv,
+    "franka-cube-stack": FrankaCubeStackEnv,
     "shadow-hand": ShadowHandEnv,
     "quadruped-anymal-obs": AnymalObsEnv,
     "humanoid": HumanoidEnv,
