@@ -257,8 +257,12 @@ def measure(task, E, args, rank, world, clocks=None, policy=False, kernel=True, 
         d2h = sum(t.numel() * t.element_size() for t in (o.obs, o.reward, o.done, *o.info.values()))
         out["e2e"] = {"value": world * E * args.steps / (maxr(e0.elapsed_time(e1)) / 1e3), "unit": UNIT,
                       "h2d_bytes_per_step": h_act[0].numel() * h_act[0].element_size(),
-                      "d2h_bytes_per_step": d2h, "chunks": env.host_chunk_count(),
-                      "api": "EnvBatch.step_host (wave-sized env chunks, copies overlapped on a copy stream)"}
+                      "d2h_bytes_per_step": d2h,
+                      "api": "EnvBatch.step_host, zero-copy: one fused launch whose CTAs read the pinned host "
+                             "actions and write obs / reward / done / info to pinned host memory over PCIe"
+                      if env.host_zero_copy else
+                      f"EnvBatch.step_host, {env.host_chunk_count()} wave-sized env chunks with the copies "
+                      "overlapped on a copy stream"}
     env.close()
     del flush
     torch.cuda.empty_cache()

@@ -369,7 +369,12 @@ typedef struct bsim_host_io_t {
     uint8_t *done, *timeout, *poisoned;   /* [E] host                             */
     int32_t n_chunks;           /* env chunks; <= 0: one per step-kernel wave     */
     int32_t fused;              /* 1: one bsim_env_step_range launch per chunk;
-                                   0: bsim_step_range + bsim_task_step_range      */
+                                   0: bsim_step_range + bsim_task_step_range;
+                                   2: zero-copy -- ONE bsim_env_step launch that reads
+                                   the actions from and writes obs / reward / done /
+                                   timeout / poisoned straight to the (page-locked,
+                                   device-mapped) host buffers; n_chunks unused, the
+                                   device obs / reward / flag buffers are not written */
 } bsim_host_io_t;
 /* One control step from and to host memory, pipelined in ONE call: the envs
    are split into n_chunks ranges; every chunk's actions go host->device on a

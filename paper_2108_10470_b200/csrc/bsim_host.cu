@@ -98,6 +98,32 @@ int step_host(const bsim_layout_t *l, const typename Api<R>::P *p, const typenam
     }
     const int E = l->num_envs;
     if (E == 0) return BSIM_OK;
+    if (io->fused == 2) {   // zero-copy: one launch reading / writing the mapped host buffers
+        cudaStream_t main = (cudaStream_t)stream;
+        void *dp[6];
+        const void *hp[6] = {io->actions, io->obs, io->reward, io->done, io->timeout, io->poisoned};
+        for (int i = 0; i < 6; ++i) {
+            cudaPointerAttributes at;
+            cudaError_t e = cudaPointerGetAttributes(&at, hp[i]);
+            if (e != cudaSuccess || at.type != cudaMemoryTypeHost || !at.devicePointer) {
+                cudaGetLastError();
+                h_err = "bsim_env_step_host: zero-copy mode needs page-locked (mapped) host buffers";
+                return BSIM_E_INVALID;
+            }
+            dp[i] = at.devicePointer;
+        }
+        bsim_actions_t a2 = *act;
+        a2.actions = dp[0];
+        bsim_task_t t2 = *t;
+        t2.obs = dp[1];
+        t2.reward = dp[2];
+        t2.done = (uint8_t *)dp[3];
+        t2.timeout = (uint8_t *)dp[4];
+        t2.poisoned = (uint8_t *)dp[5];
+        int rc = Api<R>::env_step(l, p, s, n_sub, &a2, &t2, 0, E, main);
+        if (rc != BSIM_OK) h_err = "bsim_env_step_host: zero-copy launch failed (see bsim_last_error)";
+        return rc;
+    }
     int n = io->n_chunks;
     if (n <= 0) {
         int32_t wave = 0;
@@ -181,7 +207,8 @@ template <class R>
 int host_graph_create(const bsim_layout_t *l, const typename Api<R>::P *p, const typename Api<R>::S *s,
                       int32_t n_sub, const bsim_actions_t *act, const bsim_task_t *t, const bsim_host_io_t *io,
                       int64_t *count_host, bsim_host_graph **out) {
-    if (!out || !t || !t->step_count_dev || !count_host || !io || !io->actions || !act || !act->actions) {
+    if (!out || !t || !t->step_count_dev || !count_host || !io || !io->actions || !act || !act->actions ||
+        io->fused == 2) {   // zero-copy is one launch with the host pointers baked in: nothing to capture
         h_err = "bsim_env_step_host_graph: invalid arguments";
         return BSIM_E_INVALID;
     }

@@ -107,8 +107,9 @@ template <int NW> __device__ unsigned claim_sweep_smsp(const int *warp_smsp, uns
     return bit;
 }
 
-template <class R> __device__ __noinline__ void task_step_env_call(const Ctx<R> &c, const bsim_task_t &t, int e, int sl) {
-    task_step_env_g<R, BSIM_TASK_G>(c, TaskView<R>{t}, e, sl);
+template <class R>
+__device__ __noinline__ void task_step_env_call(const Ctx<R> &c, const bsim_task_t &t, R *stage, int e0, int e, int sl) {
+    task_step_env_g<R, BSIM_TASK_G>(c, TaskView<R>{t, stage, e0}, e, sl);
 }
 
 #ifndef BSIM_MINB
@@ -209,8 +210,15 @@ __global__ void __launch_bounds__(Shape<R>::NTH, BSIM_MINB)
     }
     if (tid == 0 && s_sweep_bit) atomicAnd(&g_sweep_smsp[s_sm_slot], ~s_sweep_bit);
     if (with_task) {   // EnvBatch.step tail for this CTA's envs (bsim_env_step)
-        __syncthreads();   // the CTA's state stores above are visible to its threads
-        if (tid < BSIM_TASK_G * ne) task_step_env_call(c, task, e0 + tid / BSIM_TASK_G, tid % BSIM_TASK_G);
+        __syncthreads();   // the CTA's state stores above are visible; the workspace is dead
+        // observation rows are staged in the dead workspace and leave as one
+        // coalesced block (task.obs may be mapped host memory: bsim_env_step_host
+        // zero-copy mode, where a scattered row store would be a PCIe write each)
+        R *stage = ws;
+        if (tid < BSIM_TASK_G * ne) task_step_env_call(c, task, stage, e0, e0 + tid / BSIM_TASK_G, tid % BSIM_TASK_G);
+        __syncthreads();
+        R *dst = reinterpret_cast<R *>(task.obs) + (size_t)e0 * task.obs_dim;
+        for (int i = tid; i < ne * task.obs_dim; i += NTH) dst[i] = stage[i];
     }
 }
 
@@ -507,6 +515,10 @@ int launch_step_t(const Ctx<R> &c, size_t smem, int n_substeps, const bsim_actio
     const int grid = (e_count + epc - 1) / epc;
     bsim_task_t tk;
     if (task) tk = *task; else std::memset(&tk, 0, sizeof tk);
+    if (task && (size_t)epc * task->obs_dim * sizeof(R) > step_ws_bytes<R>(c.d, epc)) {
+        g_err = "bsim_env_step: observation rows do not fit the CTA workspace";
+        return BSIM_E_TOO_LARGE;
+    }
     step_kernel<R, T><<<grid, Shape<R>::NTH, pl.smem, st>>>(c, n_substeps, act, epc, e_begin, e_begin + e_count, tk,
                                                            task != nullptr);
     return check_launch("step_kernel");

@@ -165,6 +165,7 @@ def test_host_buffer_step_equals_device_step(task, fused, chunks, graph):
     kw = dict(num_envs=131, seed=5, episode_length=5, randomize=True)
     a, b = EV.make_env(task, **kw), EV.make_env(task, **kw)
     b.host_fused, b.host_chunks, b.host_graph = fused, chunks, graph
+    b.host_zero_copy = False
     rng = np.random.default_rng(8)
     pinned = torch.empty((131, a.act_dim), pin_memory=True)
     for t in range(12):
@@ -184,6 +185,38 @@ def test_host_buffer_step_equals_device_step(task, fused, chunks, graph):
     assert a.scene.step_count == b.scene.step_count
     assert int(a.reset_count.sum()) > 131     # resets happened
     assert (b._host["graph"] is not None) == graph
+    b.close()
+
+
+@pytest.mark.parametrize("task", ["quadruped", "humanoid", "shadow-hand", "franka-cube-stack"])
+def test_zero_copy_host_step_equals_device_step(task):
+    """step_host in zero-copy mode (bsim_env_step_host mode 2: one fused
+    launch whose CTAs read the pinned host actions and write obs / reward /
+    flags straight to the pinned host outputs) == EnvBatch.step, bitwise,
+    through resets and DR, with the host action buffer alternating."""
+    from paper_2108_10470_b200 import envs as EV
+    kw = dict(num_envs=131, seed=5, episode_length=5, randomize=True)
+    a, b = EV.make_env(task, **kw), EV.make_env(task, **kw)
+    b.host_zero_copy = True
+    rng = np.random.default_rng(9)
+    pins = [torch.empty((131, a.act_dim), pin_memory=True) for _ in range(2)]
+    for t in range(11):
+        act = rng.uniform(-1.2, 1.2, (131, a.act_dim)).astype(np.float32)
+        oa = a.step(torch.as_tensor(act, device="cuda"))
+        if t % 3 == 2:
+            ob = b.step_host(act)                                  # numpy: staged through the pinned buffer
+        else:
+            pins[t % 2].copy_(torch.from_numpy(act))
+            ob = b.step_host(pins[t % 2])
+        for x, y in ((oa.obs, ob.obs), (oa.reward, ob.reward), (oa.done, ob.done),
+                     (oa.info["timeout"], ob.info["timeout"]), (oa.info["poisoned"], ob.info["poisoned"])):
+            assert torch.equal(x.cpu(), y), t
+        assert torch.equal(a.scene.body_q, b.scene.body_q), t
+        assert torch.equal(a.actions, b.actions), t
+    assert int(a.reset_count.sum()) > 131
+    with pytest.raises(Exception):          # pageable host buffers are refused, not silently copied
+        b._step_host_zero_copy(torch.zeros((131, a.act_dim)), b._host, *b.scene._structs(), 0)
+    a.close()
     b.close()
 
 

@@ -59,3 +59,10 @@ print(f"  host time step_host(sync=False)    {host_time(lambda: env.step_host(h_
 print(f"  host time h_act.to(cuda) + step    {host_time(lambda: env.step(h_act.to('cuda', non_blocking=True))):7.1f} us")
 s = torch.cuda.current_stream()
 print(f"  empty sync round trip              {host_time(lambda: s.synchronize()):7.1f} us")
+env.host_zero_copy = True
+print(f"  host time step_host zero-copy (sync=False) {host_time(lambda: env.step_host(h_act, sync=False)):7.1f} us")
+env.host_zero_copy = False
+env.fused = True
+print(f"  device fused step (task tail in the step kernel) {ev_time(lambda: env.step(d_act)):7.1f} us")
+env.fused = False
+print(f"  device two-launch step                           {ev_time(lambda: env.step(d_act)):7.1f} us")

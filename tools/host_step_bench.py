@@ -66,3 +66,7 @@ for graph in (False, True):
             env.host_chunks = n
             print(f"  step_host graph={graph!s:5} fused={fused!s:5} chunks={env.host_chunk_count()} "
                   f"{timed(host):8.1f} us")
+
+env.host_zero_copy = True
+print(f"  step_host zero-copy                  {timed(host):8.1f} us")
+env.host_zero_copy = False
