@@ -192,7 +192,7 @@ def measure(task, E, args, rank, world, clocks=None, policy=False, kernel=True, 
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    out = {"task": task, "envs_per_gpu": E}
+    out = {"task": task, "envs_per_gpu": E, "launches_per_step": 1 if env.fused else 2}
     if clocks is not None:      # nvidia-smi sampler running through warm-up and the timed steps
         clocks.__enter__()
     for i in range(args.warmup):
@@ -412,7 +412,7 @@ def run_gpu(args):
                    "substeps": 2, "position_iterations": 8, "velocity_iterations": 1,
                    "precision": args.precision, "parallelism": f"env-shard x{world}",
                    "l2": "flushed between timed steps (256 MiB write)"},
-        "gpu_launches": 2 * args.steps,
+        "gpu_launches": m["launches_per_step"] * args.steps,
         "clocks": clocks.summary(),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / pk["hbm_gbs"], "traffic": tr[0] if tr else None,

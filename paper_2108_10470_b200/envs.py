@@ -233,10 +233,12 @@ class EnvBatch:
                           {"timeout": self.timeout, "poisoned": self.poisoned})
 
     # True: one launch per control step (bsim_env_step, the task tail runs in
-    # the physics kernel).  Measured on B200 (tools/fused_bench.py): 3 % faster
-    # at 4096 envs, 1.5 % slower at 16384 (the tail's 16 active threads per CTA
-    # extend every CTA's lifetime), so the default is the two-launch path.
-    fused = False
+    # the physics kernel, obs rows staged in the dead workspace and stored
+    # coalesced); its ctypes argument block is built once and re-pointed per
+    # call.  Measured on B200 (16384 Ant envs): device time equal to the
+    # two-launch path (266 vs 265 us) and ~15 us less host time per step, so
+    # it is the default; False = bsim_step then bsim_task_step.
+    fused = True
 
     def _step_launches(self, a, graph=False):
         """The control step's launches: the fused physics + task-tail launch
@@ -247,11 +249,18 @@ class EnvBatch:
             self._step_count_dev.add_(cfg.decimation)
         if self.fused:
             lay, par, st = sc._structs()
-            act = N.Actions(a.data_ptr(), self.actions.data_ptr(), float(self.action_scale), MODE_POSITION, 0)
+            key = (id(lay), id(par), id(st), sc._s, graph)
+            fz = self.__dict__.get("_fused_args")
+            if fz is None or fz[0] != key:
+                act = N.Actions(0, self.actions.data_ptr(), float(self.action_scale), MODE_POSITION, 0)
+                args = (C.byref(lay), C.byref(par), C.byref(st), int(cfg.decimation), C.byref(act),
+                        C.byref(self._task), sc._s)
+                fz = self._fused_args = (key, act, args, sc._sfx("bsim_env_step"))
+            _, act, args, fn = fz
+            act.actions = a.data_ptr()
             self._task.step_count = int(sc.step_count) + cfg.decimation
             self._task.step_count_dev = self._step_count_dev.data_ptr() if graph else None
-            rc = sc._sfx("bsim_env_step")(C.byref(lay), C.byref(par), C.byref(st), int(cfg.decimation),
-                                           C.byref(act), C.byref(self._task), sc._s)
+            rc = fn(*args)
             self._task.step_count_dev = None
             N.check(rc, "bsim_env_step")
             sc.step_count += cfg.decimation

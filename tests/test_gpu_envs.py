@@ -131,14 +131,15 @@ def test_cuda_graph_step_equals_eager(task):
     assert int(a.done.sum()) >= 0 and int(a.reset_count.sum()) > 2 * 64   # resets happened
 
 
-@pytest.mark.parametrize("task", ["quadruped", "quadruped-anymal-obs", "humanoid"])
+@pytest.mark.parametrize("task", ["quadruped", "quadruped-anymal-obs", "humanoid", "shadow-hand",
+                                  "franka-cube-stack"])
 def test_fused_env_step_launch_equals_two_launches(task):
     """bsim_env_step (physics + task tail in one kernel) == bsim_step then
     bsim_task_step, bitwise, through resets, DR and graph capture."""
     from paper_2108_10470_b200 import envs as EV
     kw = dict(num_envs=48, seed=9, episode_length=6, randomize=True)
     a, b = EV.make_env(task, **kw), EV.make_env(task, **kw)
-    b.fused = True
+    a.fused, b.fused = False, True
     rng = np.random.default_rng(4)
     for t in range(14):
         if t == 7:
