@@ -54,3 +54,27 @@ def test_quadruped_learns_forward_progress():
     progress = [_quadruped_progress(seed) for seed in (0, 1, 2)]
     wins = sum(p > 0.0 for p in progress)
     assert wins >= 2, progress
+
+
+def test_throughput_scales_with_envs():
+    """Reference test_accept_throughput_scaling (tests/test_acceptance.py:
+    168-219) on the device: 16384 envs step >= 4x the env-steps/s of 1024
+    envs (the batch fills the 148 SMs instead of a fraction of one wave)."""
+    from paper_2108_10470_b200.envs import make_env
+
+    def fps(E, steps=20):
+        env = make_env("quadruped", num_envs=E, seed=0)
+        a = torch.rand((E, env.act_dim), device=env.obs.device) * 2 - 1
+        for _ in range(3):
+            env.step(a)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            env.step(a)
+        e1.record()
+        torch.cuda.synchronize()
+        env.close()
+        return E * steps / (e0.elapsed_time(e1) / 1e3)
+
+    ratio = fps(16384) / fps(1024)
+    assert ratio >= 4.0, ratio
