@@ -1056,7 +1056,8 @@ template <class R, class T, bool BIASED> BS_HD void sweep_static(const Ctx<R> &c
 // so the result is the reference's Gauss-Seidel order (physics.py:761-775):
 // j_2s+1 and j_2s+2 share no body, and a plane row may run as soon as its
 // body's last joint row is done because no later joint row touches it.
-// 8 joint + 5 plane row times become 5 + 3.  (The same pipeline for 3-joint
+// 8 joint row times become 5; the plane rows and the delta accumulation run
+// after a CTA barrier on every lane (star_body_tail).  (The same pipeline for 3-joint
 // legs -- the ANYmal analog -- measured slower than the register-resident
 // sequential sweep, so codegen only marks 2-joint stars.)
 template <class R, class T>
@@ -1093,17 +1094,47 @@ __device__ void sweep_star(const Ctx<R> &c, const Ws<R> &w, R h, bool biased, in
         if (p == 1) P = hip;
     }
     if (p == 0) store_bv(d, w, 0, P);
-    __syncwarp(mask);
-    // plane rows: slot q on the root (q = 0) or on knee q-1, round-robin over the lanes
-    for (int q = p; q < T::P; q += 2) {
-        const int b = q == 0 ? 0 : 2 * q;
-        BV<R> X = load_bv(d, w, b);
+}
+
+// The rest of the star pass, one item per (env, body) over the whole CTA
+// after a barrier: the body's plane row (slot q with plane_body[q] == b; the
+// star topologies carry at most one slot per body, so rows on distinct
+// bodies commute and the reference's slot order is kept) and, after a
+// biased pass, dpos += v h, dang += w h (physics.py:571-572).  One SIMT
+// path for every lane, so the 5 plane rows of an env cost one row time
+// instead of three on the two sweep lanes.
+template <class T> BS_HD constexpr int star_plane_of(int b) {
+    for (int q = 0; q < T::P; ++q)
+        if (T::plane_body[q] == b) return q;
+    return -1;
+}
+template <class T> BS_HD constexpr bool star_planes_unique() {
+    for (int q = 0; q < T::P; ++q)
+        for (int r = q + 1; r < T::P; ++r)
+            if (T::plane_body[q] == T::plane_body[r]) return false;
+    return true;
+}
+// body -> slot, folded at compile time (the tables are host constexpr arrays:
+// device code must not index them at run time)
+template <class T, int k = 0> __device__ __forceinline__ int star_plane_index(int b) {
+    if constexpr (k < T::B) {
+        constexpr int q = star_plane_of<T>(k);
+        return b == k ? q : star_plane_index<T, k + 1>(b);
+    } else {
+        return -1;
+    }
+}
+template <class R, class T>
+__device__ void star_body_tail(const Ctx<R> &c, const Ws<R> &w, int b, R h, bool biased) {
+    static_assert(star_planes_unique<T>(), "star tail assumes one plane slot per body");
+    const Dims &d = c.d;
+    const int q = star_plane_index<T>(b);
+    BV<R> X = load_bv(d, w, b);
+    if (q >= 0) {
         row_plane(c, w, q, X);
         store_bv(d, w, b, X);
     }
-    __syncwarp(mask);
-    if (biased)   // dpos += v h, dang += w h (physics.py:571-572) from the final velocities
-        for (int b = p; b < T::B; b += 2) accumulate_deltas(d, w, b, load_bv(d, w, b), h);
+    if (biased) accumulate_deltas(d, w, b, X, h);
 }
 #endif
 
@@ -1360,6 +1391,8 @@ template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> 
                     const unsigned mask = 2 * g.ne >= 32 ? 0xffffffffu : ((1u << (2 * g.ne)) - 1u);
                     sweep_star<R, T>(c, g.env(t >> 1), h, biased, t & 1, mask);
                 }
+                BS_SYNC();
+                BS_ITEMS(g, T::B, el, b) { star_body_tail<R, T>(c, g.env(el), b, h, biased); }
             } else
 #endif
             {
