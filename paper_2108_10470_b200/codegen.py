@@ -55,7 +55,7 @@ def _star_chain(L):
     J = L.joints
     if L.pairs_per_env or L.tendons_per_env or L.bodies_per_env != len(J) + 1 or not J:
         return 0
-    for ch in (2,):   # 3-joint legs (ANYmal) measured slower pipelined: DESIGN.md 3.1
+    for ch in (2, 3):   # K lanes per env, one joint stage each (sweep_star)
         if len(J) % ch:
             continue
         ok = all(j.kind == JOINT_KIND["revolute"] and j.has_limits and j.dof == i and j.child == i + 1

@@ -1060,15 +1060,18 @@ template <class R, class T, bool BIASED> BS_HD void sweep_static(const Ctx<R> &c
 // after a CTA barrier on every lane (star_body_tail).  (The same pipeline for 3-joint
 // legs -- the ANYmal analog -- measured slower than the register-resident
 // sequential sweep, so codegen only marks 2-joint stars.)
+template <class T> BS_HD constexpr int star_lanes() { return T::star_chain <= 2 ? 2 : 4; }
 template <class R, class T>
 __device__ void sweep_star(const Ctx<R> &c, const Ws<R> &w, R h, bool biased, int p, unsigned mask) {
     const Dims &d = c.d;
-    constexpr int L = T::J / 2;
-    BV<R> P = load_bv(d, w, 0), C;              // lane 0 keeps the root in P
-    for (int s = 0; s <= L; ++s) {
-        // lane 0: joint 2s (root -> hip s); lane 1: joint 2s - 1 (hip s-1 -> knee s-1)
-        const bool active = p == 0 ? s < L : s >= 1;
-        const int j = p == 0 ? 2 * s : 2 * s - 1;
+    constexpr int K = T::star_chain, G = star_lanes<T>(), L = T::J / K;
+    static_assert(K >= 2 && K <= G && T::J % K == 0, "star chains of 2..4 joints");
+    BV<R> P = load_bv(d, w, 0), C = P;          // lane 0 keeps the root in P
+    for (int s = 0; s < L + K - 1; ++s) {
+        // lane p: joint K (s - p) + p, stage p of leg s - p (link j -> link j + 1; the root for p = 0)
+        const int leg = s - p;
+        const bool active = p < K && leg >= 0 && leg < L;
+        const int j = K * leg + p;
         const int cb = j + 1, pb = p == 0 ? 0 : j;
         if (active) {
             C = load_bv(d, w, cb);
@@ -1077,21 +1080,19 @@ __device__ void sweep_star(const Ctx<R> &c, const Ws<R> &w, R h, bool biased, in
             else
                 joint_rows(c, w, j, BSIM_REVOLUTE, j, true, pb, cb, h, false, C, P);
         }
-        // lane 1 is done with hip s-1 (P) and knee s-1 (C): both final for the joints
-        if (p == 1 && active) {
-            store_bv(d, w, pb, P);
-            store_bv(d, w, cb, C);
-        }
-        // hand hip s (lane 0's C after joint 2s) to lane 1 for joint 2s+1
-        BV<R> hip;
-        hip.v.x = __shfl_xor_sync(mask, C.v.x, 1);
-        hip.v.y = __shfl_xor_sync(mask, C.v.y, 1);
-        hip.v.z = __shfl_xor_sync(mask, C.v.z, 1);
-        hip.w.x = __shfl_xor_sync(mask, C.w.x, 1);
-        hip.w.y = __shfl_xor_sync(mask, C.w.y, 1);
-        hip.w.z = __shfl_xor_sync(mask, C.w.z, 1);
-        hip.m = __shfl_xor_sync(mask, C.m, 1);
-        if (p == 1) P = hip;
+        // link j is final after its outgoing joint; the leg's last link after its own
+        if (active && p >= 1) store_bv(d, w, pb, P);
+        if (active && p == K - 1) store_bv(d, w, cb, C);
+        // hand link j + 1 (C) to the next stage for joint j + 1
+        BV<R> nx;
+        nx.v.x = __shfl_up_sync(mask, C.v.x, 1, G);
+        nx.v.y = __shfl_up_sync(mask, C.v.y, 1, G);
+        nx.v.z = __shfl_up_sync(mask, C.v.z, 1, G);
+        nx.w.x = __shfl_up_sync(mask, C.w.x, 1, G);
+        nx.w.y = __shfl_up_sync(mask, C.w.y, 1, G);
+        nx.w.z = __shfl_up_sync(mask, C.w.z, 1, G);
+        nx.m = __shfl_up_sync(mask, C.m, 1, G);
+        if (p >= 1) P = nx;
     }
     if (p == 0) store_bv(d, w, 0, P);
 }
@@ -1386,11 +1387,13 @@ template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> 
         for (int r = 0; r < reps; ++r) {
 #if defined(__CUDA_ARCH__)
             if constexpr (topo_star<T>()) {   // two lanes per env (sweep_star)
-                const int t = g.tid - g.lane0;
-                if (t >= 0 && t < 2 * g.ne) {
-                    const unsigned mask = 2 * g.ne >= 32 ? 0xffffffffu : ((1u << (2 * g.ne)) - 1u);
-                    sweep_star<R, T>(c, g.env(t >> 1), h, biased, t & 1, mask);
-                }
+                // star_lanes lanes per env from the claimed sweep warp on (wrapping
+                // into the next warp when the CTA's envs need more than 32 lanes)
+                constexpr int G = star_lanes<T>();
+                const int t = (g.tid - g.lane0 + g.nth) % g.nth;
+                const bool on = t < G * g.ne;
+                const unsigned mask = __ballot_sync(0xffffffffu, on);
+                if (on) sweep_star<R, T>(c, g.env(t / G), h, biased, t % G, mask);
                 BS_SYNC();
                 BS_ITEMS(g, T::B, el, b) { star_body_tail<R, T>(c, g.env(el), b, h, biased); }
             } else
