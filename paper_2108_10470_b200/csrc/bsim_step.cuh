@@ -1125,17 +1125,24 @@ template <class T, int k = 0> __device__ __forceinline__ int star_plane_index(in
         return -1;
     }
 }
+template <class R> BS_HD void body_phase_item(const Ctx<R> &c, const Ws<R> &w, int e, int b, int k, int N);
 template <class R, class T>
-__device__ void star_body_tail(const Ctx<R> &c, const Ws<R> &w, int b, R h, bool biased) {
+__device__ void star_body_tail(const Ctx<R> &c, const Ws<R> &w, int e, int b, R h, int k, int N) {
     static_assert(star_planes_unique<T>(), "star tail assumes one plane slot per body");
     const Dims &d = c.d;
+    const bool biased = k < N;
     const int q = star_plane_index<T>(b);
     BV<R> X = load_bv(d, w, b);
     if (q >= 0) {
         row_plane(c, w, q, X);
         store_bv(d, w, b, X);
     }
-    if (biased) accumulate_deltas(d, w, b, X, h);
+    if (biased) {
+        accumulate_deltas(d, w, b, X, h);
+        // pass k + 1's body phase needs only this body's own deltas: its
+        // effective pose and world inverse inertia, in the same item
+        body_phase_item(c, w, e, b, k + 1, N);
+    }
 }
 #endif
 
@@ -1288,6 +1295,19 @@ template <class T> constexpr bool topo_tendons() {
     if constexpr (T::is_static) return T::has_tendons; else return true;
 }
 
+// Per body, before the rows of pass k > 0 (refresh 718-756): [integrate
+// (574-575) at k = N,] effective orientation, world inverse inertia.
+template <class R> BS_HD void body_phase_item(const Ctx<R> &c, const Ws<R> &w, int e, int b, int k, int N) {
+    const Dims &d = c.d;
+    const bool deltas = k > 0 && k < N;
+    if (k == N) {
+        w.s3(ib(d, b, BP), w.l3(ib(d, b, BP)) + w.l3(ib(d, b, BDP)));
+        w.s4(ib(d, b, BQ), qnormalize(qmul(qexp(w.l3(ib(d, b, BDA))), w.l4(ib(d, b, BQ)))));
+    }
+    if (deltas) w.s4(ib(d, b, BQE), qnormalize(qmul(qexp(w.l3(ib(d, b, BDA))), w.l4(ib(d, b, BQ)))));
+    body_inertia(c, w, e, b, deltas ? BQE : BQ);
+}
+
 // ====================================================== the group step
 // Loops over (env, item) pairs distributed over the CTA's threads; on the
 // host (tid 0 of 1) they degenerate to plain sequential loops.
@@ -1335,6 +1355,11 @@ template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> 
         BS_SYNC();
     }
 
+#if defined(__CUDA_ARCH__)
+    constexpr bool tail_body = topo_star<T>();   // body phase fused into the star tail
+#else
+    constexpr bool tail_body = false;
+#endif
     for (int k = 0; k <= N; ++k) {
         const bool biased = k < N, freeze = k == 0, deltas = k > 0 && k < N;
         // phase A: orientations -> inertias -> joint/contact geometry and row
@@ -1342,17 +1367,8 @@ template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> 
 #ifdef BSIM_EXP_SKIP_A   // timing experiment only: reuse the freeze-time constants
         if (!freeze && k < N) goto phase_b;
 #endif
-        if (!freeze) {   // per body: [integrate (574-575) at k = N,] orientation, world inverse inertia
-            BS_ITEMS(g, d.B, el, b) {
-                Ws<R> w = g.env(el);
-                if (k == N) {
-                    w.s3(ib(d, b, BP), w.l3(ib(d, b, BP)) + w.l3(ib(d, b, BDP)));
-                    w.s4(ib(d, b, BQ), qnormalize(qmul(qexp(w.l3(ib(d, b, BDA))), w.l4(ib(d, b, BQ)))));
-                }
-                if (deltas)
-                    w.s4(ib(d, b, BQE), qnormalize(qmul(qexp(w.l3(ib(d, b, BDA))), w.l4(ib(d, b, BQ)))));
-                body_inertia(c, w, g.e0 + el, b, deltas ? BQE : BQ);
-            }
+        if (!freeze && !(tail_body && k > 0)) {   // (tail_body: the previous pass's tail ran it)
+            BS_ITEMS(g, d.B, el, b) { body_phase_item(c, g.env(el), g.e0 + el, b, k, N); }
             BS_SYNC();
         }
         BS_ITEMS(g, d.J, el, j) {
@@ -1395,7 +1411,7 @@ template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> 
                 const unsigned mask = __ballot_sync(0xffffffffu, on);
                 if (on) sweep_star<R, T>(c, g.env(t / G), h, biased, t % G, mask);
                 BS_SYNC();
-                BS_ITEMS(g, T::B, el, b) { star_body_tail<R, T>(c, g.env(el), b, h, biased); }
+                BS_ITEMS(g, T::B, el, b) { star_body_tail<R, T>(c, g.env(el), g.e0 + el, b, h, k, N); }
             } else
 #endif
             {
