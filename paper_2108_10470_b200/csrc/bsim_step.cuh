@@ -1060,6 +1060,9 @@ template <class R, class T, bool BIASED> BS_HD void sweep_static(const Ctx<R> &c
 // after a CTA barrier on every lane (star_body_tail).  (The same pipeline for 3-joint
 // legs -- the ANYmal analog -- measured slower than the register-resident
 // sequential sweep, so codegen only marks 2-joint stars.)
+#ifndef BSIM_PLANE_OVERLAP
+#define BSIM_PLANE_OVERLAP 1   // plane row constants built beside the chain sweep
+#endif
 template <class T> BS_HD constexpr int star_lanes() { return T::star_chain <= 2 ? 2 : 4; }
 template <class R, class T>
 __device__ void sweep_star(const Ctx<R> &c, const Ws<R> &w, R h, bool biased, int p, unsigned mask) {
@@ -1357,8 +1360,10 @@ template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> 
 
 #if defined(__CUDA_ARCH__)
     constexpr bool tail_body = topo_star<T>();   // body phase fused into the star tail
+    // plane constants built beside the chain sweep by the warps without sweep lanes
+    constexpr bool plane_overlap = BSIM_PLANE_OVERLAP && topo_star<T>();
 #else
-    constexpr bool tail_body = false;
+    constexpr bool tail_body = false, plane_overlap = false;
 #endif
     for (int k = 0; k <= N; ++k) {
         const bool biased = k < N, freeze = k == 0, deltas = k > 0 && k < N;
@@ -1375,12 +1380,15 @@ template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> 
             joint_item<R, T, topo_rev<T>(), topo_idf<T>()>(c, g.env(el), g.e0 + el, j, h, biased, freeze, deltas,
                                                            g.jt);
         }
-        BS_ITEMS(g, d.P, el, i) {
+        auto plane_item = [&](int el, int i) {
             Ws<R> w = g.env(el);
             const int pb = plane_body_of<T>(c, i);
             if (freeze) plane_freeze(c, w, g.e0 + el, i, pb);
             plane_constants(c, w, i, pb);
             plane_pass_constants(c, w, i, biased, pb);
+        };
+        if (!plane_overlap) {
+            BS_ITEMS(g, d.P, el, i) { plane_item(el, i); }
         }
         if (topo_pairs<T>()) {
             BS_ITEMS(g, d.Q, el, i) {
@@ -1409,7 +1417,16 @@ template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> 
                 const int t = (g.tid - g.lane0 + g.nth) % g.nth;
                 const bool on = t < G * g.ne;
                 const unsigned mask = __ballot_sync(0xffffffffu, on);
-                if (on) sweep_star<R, T>(c, g.env(t / G), h, biased, t % G, mask);
+                if (on) {
+                    sweep_star<R, T>(c, g.env(t / G), h, biased, t % G, mask);
+                } else if (plane_overlap && r == 0) {
+                    // the plane slots' row constants need only the bodies' pass
+                    // poses: the warps without sweep lanes build them while the
+                    // sweep runs (the plane rows use them in the tail below)
+                    const int w0 = 32 * ((G * g.ne + 31) / 32);
+                    for (int it = t - w0; it >= 0 && it < g.ne * d.P; it += g.nth - w0)
+                        plane_item(it % g.ne, it / g.ne);
+                }
                 BS_SYNC();
                 BS_ITEMS(g, T::B, el, b) { star_body_tail<R, T>(c, g.env(el), g.e0 + el, b, h, k, N); }
             } else
