@@ -13,7 +13,10 @@ uniform random actions (`--workload` selects another BASELINE.json config;
 the line's `other_configs` carries the humanoid / ANYmal analogs and PPO
 rollout steps -- policy inference + env step -- measured the same way).  Multi-GPU: one process per GPU (torchrun), each
 rank owns a contiguous global env range (weak scaling, no data-path
-collective); timing is the max over ranks.
+collective); timing is the max over ranks.  `--gpus N` outside torchrun
+re-launches itself under `torch.distributed.run` with N ranks (NCCL, LOCAL_RANK
+-> device); with fewer GPUs than ranks (a 1-GPU smoke test of the multi-rank
+path) the ranks share the device over gloo.
 
 Timed-region rules: W untimed warm-up steps; K timed steps, each bracketed by
 CUDA events on the launching stream, an L2 flush (256 MiB write) between
@@ -102,10 +105,24 @@ class ClockSampler:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons}
 
 
+def kernel_src_sha():
+    """The kernel-source hash tools/ncu_summary.py stamps into a summary."""
+    import glob
+    import hashlib
+    h = hashlib.sha256()
+    for f in sorted(glob.glob(os.path.join(ROOT, "paper_2108_10470_b200", "csrc", "*.cu*"))) + [
+            os.path.join(ROOT, "include", "batchsim_b200.h")]:
+        with open(f, "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
 def ncu_traffic(envs):
     """dram__bytes_read.sum + dram__bytes_write.sum per step-kernel launch from
     the newest committed `ncu --set full` summary of this workload
-    (profiles/r*_step_*_ncu.json, written by tools/ncu_summary.py), else None."""
+    (profiles/r*_step_*_ncu.json, written by tools/ncu_summary.py), else None.
+    Returns (bytes, file, flop/env, fresh): `fresh` is False when the summary
+    was captured from other kernel sources than the ones built now."""
     import glob
     import re
 
@@ -124,7 +141,8 @@ def ncu_traffic(envs):
             continue
         for l in j.get("launches", []):
             if "step_kernel<float" in l.get("kernel", "") and "dram_bytes_per_launch" in l:
-                best = (l["dram_bytes_per_launch"], os.path.basename(path), l.get("fp32_flop_per_env_launch"))
+                best = (l["dram_bytes_per_launch"], os.path.basename(path), l.get("fp32_flop_per_env_launch"),
+                        j.get("src_sha") == kernel_src_sha())
     return best
 
 
@@ -346,23 +364,65 @@ def measure_shadow_hand(E, args, rank, world):
     return world * E * args.steps / (float(t.item()) / 1e3), ok
 
 
+def config_dict(args, world, E):
+    """The workload description both arms print (identical dicts)."""
+    task, _, _, desc = WORKLOADS[args.workload]
+    return {"workload": desc.format(E=E), "task": task, "envs_per_gpu": E, "global_envs": world * E,
+            "substeps": 2, "position_iterations": 8, "velocity_iterations": 1,
+            "actions": "uniform(-1, 1) per env per control step", "parallelism": f"env-shard x{world}",
+            "l2": "flushed between timed GPU steps (256 MiB write)"}
+
+
+def cpu_info(threads):
+    """CPU model, physical / logical core counts and the threads a CPU leg used."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            model = next((l.split(":", 1)[1].strip() for l in f if l.startswith("model name")), None)
+    except OSError:
+        pass
+    try:
+        import psutil
+        physical = psutil.cpu_count(logical=False)
+    except ImportError:
+        physical = None
+    return {"cpu_model": model, "physical_cores": physical, "logical_cpus": os.cpu_count(), "threads": threads}
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def measure_ant_fp64(E, args, rank, world):
+    import copy
+    a2 = copy.copy(args)
+    a2.precision = "fp64"
+    return measure("quadruped", E, a2, rank, world, kernel=False, e2e=False)
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
 
     rank, world, local = dist_info()
-    # one GPU per rank (LOCAL_RANK); BENCH_DIST_BACKEND=gloo + ranks sharing a
-    # device is only for smoke-testing the multi-rank path on a 1-GPU box
-    torch.cuda.set_device(local % torch.cuda.device_count())
+    ndev = torch.cuda.device_count()
+    # one GPU per rank (LOCAL_RANK); ranks sharing a device (fewer GPUs than
+    # ranks: a 1-GPU smoke test of the multi-rank path) must use gloo
+    torch.cuda.set_device(local % ndev)
+    backend = os.environ.get("BENCH_DIST_BACKEND") or ("nccl" if world <= ndev else "gloo")
     if world > 1:
-        dist.init_process_group(os.environ.get("BENCH_DIST_BACKEND", "nccl"))
+        dist.init_process_group(backend)
+    if args.gpus != world and rank == 0:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; reporting n_gpus={world}\n")
     E = args.envs
-    task, _, _, desc = WORKLOADS[args.workload]
-    clocks = ClockSampler(local % torch.cuda.device_count())
-    m = measure(task, E, args, rank, world, clocks=clocks)
+    clocks = ClockSampler(local % ndev)
+    m = measure(WORKLOADS[args.workload][0], E, args, rank, world, clocks=clocks)
     others = {}
     if not args.no_other_configs:
-        # the other BASELINE.json configs that have a model here (fewer steps, device-resident only)
+        # the other BASELINE.json configs (fewer steps, device-resident inputs)
         import copy
         a2 = copy.copy(args)
         a2.steps = args.other_steps
@@ -371,6 +431,15 @@ def run_gpu(args):
                 continue
             r = measure(WORKLOADS[name][0], E, a2, rank, world, kernel=False, e2e=False)
             others[name] = {"value": r["value"], "unit": UNIT, "envs_per_gpu": E, "steps": a2.steps}
+        if args.workload == "ant":
+            # BASELINE.json config 1: Ant at 4096 envs (single-GPU step vs the CPU reference step)
+            r = measure("quadruped", 4096, a2, rank, world, kernel=False, e2e=True)
+            others["ant_4096"] = {"value": r["value"], "unit": UNIT, "envs_per_gpu": 4096, "steps": a2.steps,
+                                  "e2e": r["e2e"]}
+            # the exact-parity path: the same kernels in float64 (parity 1e-8 vs the reference)
+            r = measure_ant_fp64(E, a2, rank, world)
+            others["ant_fp64"] = {"value": r["value"], "unit": UNIT, "envs_per_gpu": E, "steps": a2.steps,
+                                  "dtype": "f64", "note": "float64 exact-parity path (1e-8 vs the reference)"}
         fv, fok = measure_franka(8192, a2, rank, world)
         others["franka_cube_stack"] = {"value": fv, "unit": UNIT, "envs_per_gpu": 8192, "steps": a2.steps,
                                        "finite": fok,
@@ -391,12 +460,14 @@ def run_gpu(args):
                                              "note": "ActorCritic 256-128-64 act() + env.step per step"}
     if rank != 0:
         if world > 1:
+            dist.barrier()
             dist.destroy_process_group()
         return
     pk, src = peaks()
     k_ms, bytes_env = m["kernel_ms"], m["bytes_per_env"]
     achieved = bytes_env * E / (k_ms / 1e3) / 1e9
     tr = ncu_traffic(E) if (args.precision == "fp32" and args.workload == "ant") else None
+    fresh = bool(tr and tr[3])
     # FP32 view: flop per env per launch measured by ncu (ffma*2 + fadd + fmul), else the
     # SURVEY.md 8(d) estimate of 9.3e4 flop per env-sim-step x 2 substeps (Ant)
     flop_env = tr[2] if tr and tr[2] else 9.3e4 * 2
@@ -408,17 +479,16 @@ def run_gpu(args):
         "warmup": args.warmup, "ms_per_step": m["ms_total"] / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32" if args.precision == "fp32" else "f64",
         "data": "synthetic (uniform random actions, bundled/authored models, no checkpoints)",
-        "config": {"workload": desc.format(E=E), "task": task, "envs_per_gpu": E, "global_envs": world * E,
-                   "substeps": 2, "position_iterations": 8, "velocity_iterations": 1,
-                   "precision": args.precision, "parallelism": f"env-shard x{world}",
-                   "l2": "flushed between timed steps (256 MiB write)"},
+        "config": config_dict(args, world, E),
         "gpu_launches": m["launches_per_step"] * args.steps,
         "clocks": clocks.summary(),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                     "frac": achieved / pk["hbm_gbs"], "traffic": tr[0] if tr else None,
+                     "frac": achieved / pk["hbm_gbs"], "traffic": tr[0] if fresh else None,
                      "traffic_unit": "bytes per launch (ncu dram__bytes_read+write, cold L2)",
-                     "traffic_source": f"profiles/{tr[1]}" if tr else None, "peak_source": src,
-                     "kernel": "step_kernel (fused 2 substeps)", "kernel_ms": k_ms,
+                     "traffic_source": (f"profiles/{tr[1]}" if fresh else
+                                        f"stale: profiles/{tr[1]} was captured from other kernel sources"
+                                        if tr else None),
+                     "peak_source": src, "kernel": "step_kernel (fused 2 substeps + task tail)", "kernel_ms": k_ms,
                      "bytes_per_env": bytes_env,
                      "fp32": {"achieved_tflops": flops / (k_ms / 1e3) / 1e12, "peak_tflops": fp32_peak,
                               "frac": flops / (k_ms / 1e3) / 1e12 / fp32_peak,
@@ -428,87 +498,143 @@ def run_gpu(args):
                              "(DESIGN.md)"},
         "e2e": m["e2e"],
     }
+    if world > 1:
+        line["dist_backend"] = backend
     if others:
         line["other_configs"] = others
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args, bounded=True)
+        if others:
+            cpu_baseline_others(args, others)
     print(json.dumps(line), flush=True)
     if world > 1:
+        dist.barrier()
         dist.destroy_process_group()
 
 
-def _oracle_scene(n_envs, threads, workload="ant"):
-    import numpy as np
-
-    from oracle.oracle import OracleScene, build
-    from paper_2108_10470_b200 import models as M
-    from paper_2108_10470_b200.params import SimParams
+def _oracle_env(workload, n_envs, threads, seed=0):
+    """The oracle restatement of the reference env (C physics + NumPy task layer)."""
+    from oracle.oracle import build
+    from oracle.tasks import OracleEnv
     build()
-    _, model, rest, _ = WORKLOADS[workload]
-    s = OracleScene([getattr(M, model)()], n_envs, SimParams(dt=1 / 120), threads=threads)
-    s.pos[:, 2] += getattr(M, rest) + 0.02
-    s.forward_kinematics()
-    return s, np.random.default_rng(0)
+    return OracleEnv(WORKLOADS[workload][0], n_envs, seed=seed, threads=threads)
 
 
-def _oracle_control_step(s, rng):
-    s.ctrl_dof_pos_target[:] = 0.6 * rng.uniform(-1, 1, s.num_dofs)   # envs.py:421-424
-    s.step()
-    s.step()
+def _time_oracle_env(env, warmup, steps=None, seconds=None, max_steps=None, seed=0):
+    """Control steps of uniform random actions (cli.py:129-140); returns (steps, seconds)."""
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    for _ in range(warmup):
+        env.step(rng.uniform(-1, 1, (env.num_envs, env.act_dim)))
+    n, t0 = 0, time.perf_counter()
+    while True:
+        env.step(rng.uniform(-1, 1, (env.num_envs, env.act_dim)))
+        n += 1
+        dt = time.perf_counter() - t0
+        if steps is not None and n >= steps:
+            break
+        if steps is None and (dt > seconds or n >= max_steps):
+            break
+    return n, dt
+
+
+ORACLE_DESC = ("C oracle float64 physics (oracle/bso.c, OpenMP {t} threads) + the NumPy restatement of the "
+               "reference env layer (oracle/tasks.py: obs, reward, done, timeout, auto-reset with FK)")
 
 
 def cpu_baseline(args, bounded=True):
-    """The C oracle (float64 port of the reference step) on this host's cores,
-    on a bounded sample of the same workload."""
-    threads = os.cpu_count() or 1
+    """The reference's algorithm (oracle restatement, physics + task layer) on
+    this host's cores, on a bounded sample of the same workload."""
+    threads = host_threads()
     sample = min(args.envs, args.cpu_sample_envs)
-    s, rng = _oracle_scene(sample, threads, args.workload)
-    _oracle_control_step(s, rng)
-    n = 0
-    t0 = time.perf_counter()
-    while True:
-        _oracle_control_step(s, rng)
-        n += 1
-        dt = time.perf_counter() - t0
-        if dt > args.cpu_seconds or n >= args.cpu_max_steps:
-            break
+    env = _oracle_env(args.workload, sample, threads)
+    n, dt = _time_oracle_env(env, 1, seconds=args.cpu_seconds, max_steps=args.cpu_max_steps)
     return {"value": sample * n / dt, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{sample} envs x {n} control steps (2 substeps each) of the same {args.workload} workload, "
-                      f"C oracle float64 (oracle/bso.c, OpenMP {threads} threads), physics only "
-                      f"(the reference's obs/reward is <0.4% of its step time)"}
+            **cpu_info(threads),
+            "sample": f"{sample} envs x {n} control steps (2 substeps each + obs / reward / done / auto-reset) "
+                      f"of the same {args.workload} workload, " + ORACLE_DESC.format(t=threads)}
+
+
+def cpu_baseline_others(args, others):
+    """A bounded CPU-reference sample beside each other config: the oracle env
+    for the configs with a reference task (ANYmal, humanoid, Ant 4096), the
+    oracle physics alone for Franka / Shadow Hand (the reference has no env)."""
+    import numpy as np
+    threads = host_threads()
+    secs = args.cpu_seconds / 2
+    for name, wl, n in (("anymal", "anymal", 1024), ("humanoid", "humanoid", 512), ("ant_4096", "ant", 4096)):
+        if name not in others:
+            continue
+        env = _oracle_env(wl, n, threads)
+        k, dt = _time_oracle_env(env, 1, seconds=secs, max_steps=200)
+        others[name]["cpu_baseline"] = {"value": n * k / dt, "unit": UNIT, "cores": threads, "kind": "port",
+                                        "sample": f"{n} envs x {k} control steps, " + ORACLE_DESC.format(t=threads)}
+    from oracle.oracle import OracleScene
+    from paper_2108_10470_b200.params import SimParams
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import pair_scenes as PS
+    for name, scene, n in (("franka_cube_stack", "franka_cube_stack", 512), ("shadow_hand", "shadow_hand_cube", 256)):
+        if name not in others:
+            continue
+        s = OracleScene(PS.SCENES[scene][0](), n, SimParams(dt=1 / 120), threads=threads, shape_pairs="all")
+        PS.setup(scene, s)
+        rng = np.random.default_rng(0)
+        base = s.ctrl_dof_pos_target.copy()
+        k, t0 = 0, time.perf_counter()
+        while True:
+            s.ctrl_dof_pos_target[:] = base + 0.3 * rng.uniform(-1, 1, s.num_dofs)
+            s.step()
+            s.step()
+            k += 1
+            dt = time.perf_counter() - t0
+            if dt > secs or k >= 200:
+                break
+        others[name]["cpu_baseline"] = {"value": n * k / dt, "unit": UNIT, "cores": threads, "kind": "port",
+                                        "sample": f"{n} envs x {k} control steps (2 substeps, random PD "
+                                                  f"targets), C oracle float64 physics only, OpenMP {threads} "
+                                                  f"threads (no reference env exists for this config)"}
 
 
 def run_reference(args):
-    """The reference arm: the reference's algorithm on the host cores.  The
-    reference is pure Python/NumPy and cannot travel to the GPU box, so this
-    times its float64 C restatement (oracle/bso.c, the `port`), which is ~7x
-    faster per core than the NumPy reference: W warm-up and K
-    timed control steps of the same workload (all envs of one GPU's shard)."""
+    """The reference arm: the reference's algorithm on the host cores, the
+    SAME work as the GPU arm's `value` (physics + obs / reward / done /
+    auto-reset of every env of the job).  The reference is pure Python/NumPy
+    and cannot travel to the GPU box, so this times its restatement: the
+    float64 C port of Scene.step (oracle/bso.c, ~7x faster per core than the
+    NumPy reference) on all host threads plus the NumPy port of
+    the env layer (oracle/tasks.py, pinned to the reference's env traces).
+    Under torchrun rank 0 alone runs it, on the whole job's envs."""
     rank, world, _ = dist_info()
     if rank != 0:
         return
-    threads = os.cpu_count() or 1
-    n_envs = args.envs
-    s, rng = _oracle_scene(n_envs, threads, args.workload)
-    for _ in range(args.warmup):
-        _oracle_control_step(s, rng)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        _oracle_control_step(s, rng)
-    dt = time.perf_counter() - t0
-    value = n_envs * args.steps / dt
-    base = {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{n_envs} envs x {args.steps} timed control steps (2 substeps each, after "
-                      f"{args.warmup} warm-up), C oracle float64 (oracle/bso.c, OpenMP {threads} threads)"}
+    threads = host_threads()
+    n_envs = args.envs * world
+    env = _oracle_env(args.workload, n_envs, threads)
+    n, dt = _time_oracle_env(env, args.warmup, steps=args.steps)
+    value = n_envs * n / dt
+    base = {"value": value, "unit": UNIT, "cores": threads, "kind": "port", **cpu_info(threads),
+            "sample": f"{n_envs} envs x {n} timed control steps (after {args.warmup} warm-up; 2 substeps each + "
+                      "obs / reward / done / auto-reset), " + ORACLE_DESC.format(t=threads)}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / n,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (uniform random actions)", "impl": "reference",
-            "config": {"workload": WORKLOADS[args.workload][3].format(E=n_envs), "task": WORKLOADS[args.workload][0],
-                       "envs_per_gpu": n_envs, "substeps": 2},
+            "data": "synthetic (uniform random actions, bundled/authored models, no checkpoints)",
+            "impl": "reference", "config": config_dict(args, world, args.envs),
             "cpu_baseline": base,
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def spawn(args):
+    """`--gpus N` outside torchrun: re-launch this script under
+    torch.distributed.run with N ranks on this node (127.0.0.1)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -530,8 +656,12 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
     if args.impl == "reference":
         run_reference(args)
+    elif args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn(args))
     else:
         run_gpu(args)
 

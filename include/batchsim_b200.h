@@ -264,7 +264,9 @@ typedef struct bsim_task_t {
     uint8_t *done, *timeout, *poisoned;   /* [E] info flags of the last step      */
     int32_t *episode_steps, *reset_count; /* [E]                                  */
     void *actions;              /* [E][act_dim] clipped actions (zeroed by reset) */
-    void *potentials;           /* [E] quadruped progress potential               */
+    double *potentials;         /* [E] locomotion progress potential, float64 in both precisions:
+                                   -dist/control_dt ~ -6e4 has an fp32 ulp of 4e-3, above the
+                                   reward tolerance (envs.py:383-391, rewards.py:89-91) */
     void *commands;             /* [E][3] anymal velocity commands                */
     const void *dof_lower, *dof_upper;    /* [D] static joint limits              */
     void *corr_noise;           /* [E][obs_dim] per-episode correlated noise      */

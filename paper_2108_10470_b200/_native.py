@@ -11,7 +11,11 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libbsim_b200.so")
+# BSIM_LIB_VARIANT=ieee loads the IEEE-fp32 build (build.py --ieee: no
+# -ftz / approximate divide / sqrt) -- a measurement variant for the fp32
+# parity table, same kernels and ABI.
+_VARIANT = os.environ.get("BSIM_LIB_VARIANT", "")
+LIB_PATH = os.path.join(HERE, "_lib", f"libbsim_b200{'_' + _VARIANT if _VARIANT else ''}.so")
 
 
 class NativeError(RuntimeError):
@@ -172,3 +176,26 @@ def check(rc, what):
     if rc != 0:
         msg = lib().bsim_last_error().decode(errors="replace")
         raise NativeError(f"{what} failed ({rc}): {msg}")
+
+
+def on_scene_device(fn):
+    """Run a method with the owning scene's CUDA device current: the native
+    entry points launch on the calling thread's current device (cudaGetDevice),
+    so a scene on a non-current GPU must switch to it first (and back)."""
+    import functools
+
+    import torch
+
+    @functools.wraps(fn)
+    def wrapper(self, *args, **kwargs):
+        scene = getattr(self, "scene", self)
+        idx = scene.device.index
+        prev = torch.cuda.current_device()
+        if idx is None or idx == prev:
+            return fn(self, *args, **kwargs)
+        torch.cuda.set_device(idx)
+        try:
+            return fn(self, *args, **kwargs)
+        finally:
+            torch.cuda.set_device(prev)
+    return wrapper

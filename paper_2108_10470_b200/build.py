@@ -17,6 +17,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "_lib", "libbsim_b200.so")
+# measurement variant: IEEE fp32 (no FAST_FP32 flags), loaded with BSIM_LIB_VARIANT=ieee
+OUT_IEEE = os.path.join(HERE, "_lib", "libbsim_b200_ieee.so")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
               "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
 
@@ -40,23 +42,26 @@ def deps():
         os.path.join(ROOT, "include", "batchsim_b200.h")]
 
 
-def up_to_date():
-    if not os.path.exists(OUT):
+def up_to_date(out=OUT):
+    if not os.path.exists(out):
         return False
-    t = os.path.getmtime(OUT)
+    t = os.path.getmtime(out)
     return all(os.path.getmtime(d) <= t for d in deps())
 
 
-def build(force=False, verbose=False):
-    if not force and up_to_date():
-        return OUT
-    os.makedirs(os.path.dirname(OUT), exist_ok=True)
+def build(force=False, verbose=False, ieee=False):
+    out = OUT_IEEE if ieee else OUT
+    if not force and up_to_date(out):
+        return out
+    os.makedirs(os.path.dirname(out), exist_ok=True)
     from concurrent.futures import ThreadPoolExecutor
+    tag = "_ieee" if ieee else ""
 
     def compile_one(src):
-        obj = os.path.join(HERE, "_lib", os.path.basename(src)[:-3] + ".o")
+        obj = os.path.join(HERE, "_lib", os.path.basename(src)[:-3] + tag + ".o")
         extra = os.environ.get("BSIM_NVCC_EXTRA", "").split()   # dev experiments only
-        fast = FAST_FP32 if os.path.basename(src) in FAST_TUS else []
+        fast = (["-DBSIM_IEEE_FP32"] if ieee else
+                FAST_FP32 if os.path.basename(src) in FAST_TUS else [])
         cmd = ["nvcc", *NVCC_FLAGS, *fast, *extra, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
         return src, obj, subprocess.run(cmd, capture_output=True, text=True)
 
@@ -69,10 +74,10 @@ def build(force=False, verbose=False):
             if verbose:
                 sys.stderr.write(r.stderr)
             objs.append(obj)
-    cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", *objs, "-o", OUT]
+    cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", *objs, "-o", out]
     subprocess.check_call(cmd)
-    return OUT
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, ieee="--ieee" in sys.argv))

@@ -34,7 +34,7 @@ BS_HD double r_cos(double x) { return cos(x); }
 // fp32 rounding (truncation < 3e-10) and cost a handful of FMAs instead of
 // sincosf's range reduction; larger angles take the libm path.
 BS_HD void r_sincos(float x, float &s, float &c) {
-#if defined(__CUDA_ARCH__)
+#if defined(__CUDA_ARCH__) && !defined(BSIM_IEEE_FP32)
     if (fabsf(x) < 0.78539816f) {
         const float x2 = x * x;
         s = x * (1.0f + x2 * (-1.0f / 6.0f + x2 * (1.0f / 120.0f + x2 * (-1.0f / 5040.0f + x2 * (1.0f / 362880.0f)))));
@@ -69,7 +69,7 @@ BS_HD float r_nan(float) { return nanf(""); }
 // reciprocal / reciprocal square root: one MUFU op (+ multiply) on the fp32
 // device path instead of an IEEE division sequence (<= 2 ulp; the fp32 parity
 // budget is 1e-4); exact IEEE on the host and in the fp64 parity path.
-#if defined(__CUDA_ARCH__)
+#if defined(__CUDA_ARCH__) && !defined(BSIM_IEEE_FP32)   // BSIM_IEEE_FP32: build.py --ieee
 BS_HD float r_rcp(float x) { return __fdividef(1.0f, x); }
 BS_HD float r_rsqrt(float x) { return rsqrtf(x); }
 #else

@@ -455,26 +455,29 @@ struct Plan {
 template <class R, class T> int plan_launch(const Dims &d, int E, Plan *out) {
     constexpr int NE = Shape<R>::NE;
     struct Entry {
-        int pad, J, E;
+        int dev, pad, J, E;
         Plan p;
     };
+    // keyed by device: the function attribute and the SM count are per device
+    constexpr int MAX_DEV = 64;
     static Entry cache[16];
     static int n_cache = 0;
-    static size_t configured = 0;
+    static size_t configured[MAX_DEV] = {};
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= MAX_DEV) return set_err("plan_launch: device ordinal", cudaErrorInvalidDevice);
     for (int i = 0; i < n_cache && i < 16; ++i)
-        if (cache[i].pad == d.pad && cache[i].J == d.J && cache[i].E == E) {
+        if (cache[i].dev == dev && cache[i].pad == d.pad && cache[i].J == d.J && cache[i].E == E) {
             *out = cache[i].p;
             return BSIM_OK;
         }
     const size_t smax = step_smem_bytes<R>(d, NE);
-    if (smax > 48 * 1024 && smax > configured) {
+    if (smax > 48 * 1024 && smax > configured[dev]) {
         cudaError_t e = cudaFuncSetAttribute(step_kernel<R, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smax);
         if (e != cudaSuccess) return set_err("cudaFuncSetAttribute(step_kernel)", e);
-        configured = smax;
+        configured[dev] = smax;
     }
-    int dev = 0, sms = 0;
-    cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const long En = E > 0 ? E : 1;
     long best_waves = -1, best_slots = 0;
@@ -499,7 +502,7 @@ template <class R, class T> int plan_launch(const Dims &d, int E, Plan *out) {
     if (epc > best_n) epc = best_n;
 #endif
     Plan p{epc, step_smem_bytes<R>(d, epc), best_slots * best_n};
-    cache[n_cache % 16] = Entry{d.pad, d.J, E, p};
+    cache[n_cache % 16] = Entry{dev, d.pad, d.J, E, p};
     ++n_cache;
     *out = p;
     return BSIM_OK;

@@ -1096,6 +1096,11 @@ __device__ void sweep_star(const Ctx<R> &c, const Ws<R> &w, R h, bool biased, in
         nx.w.z = __shfl_up_sync(mask, C.w.z, 1, G);
         nx.m = __shfl_up_sync(mask, C.m, 1, G);
         if (p >= 1) P = nx;
+        // memory order between the stages: lane p + 1 stores link j + 1 at the
+        // next step, after lane p loaded it at this one (a WAR through shared
+        // memory that the shuffle's value dependency orders in practice;
+        // __syncwarp makes it an ordering guarantee -- racecheck clean)
+        __syncwarp(mask);
     }
     if (p == 0) store_bv(d, w, 0, P);
 }
@@ -1387,7 +1392,9 @@ template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> 
             plane_constants(c, w, i, pb);
             plane_pass_constants(c, w, i, biased, pb);
         };
-        if (!plane_overlap) {
+        // the freeze reads the bodies' start-of-pass velocities (restitution
+        // target, 687-688), so at k = 0 it runs here, before the sweep writes them
+        if (!plane_overlap || freeze) {
             BS_ITEMS(g, d.P, el, i) { plane_item(el, i); }
         }
         if (topo_pairs<T>()) {
@@ -1419,7 +1426,7 @@ template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> 
                 const unsigned mask = __ballot_sync(0xffffffffu, on);
                 if (on) {
                     sweep_star<R, T>(c, g.env(t / G), h, biased, t % G, mask);
-                } else if (plane_overlap && r == 0) {
+                } else if (plane_overlap && r == 0 && !freeze) {
                     // the plane slots' row constants need only the bodies' pass
                     // poses: the warps without sweep lanes build them while the
                     // sweep runs (the plane rows use them in the tail below)

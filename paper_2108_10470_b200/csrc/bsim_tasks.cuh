@@ -38,7 +38,7 @@ template <class R> struct TaskView {
     }
     BS_HD R &reward(int e) const { return reinterpret_cast<R *>(t.reward)[e]; }
     BS_HD R *act(int e) const { return reinterpret_cast<R *>(t.actions) + (size_t)e * t.act_dim; }
-    BS_HD R &potential(int e) const { return reinterpret_cast<R *>(t.potentials)[e]; }
+    BS_HD double &potential(int e) const { return t.potentials[e]; }
     BS_HD R *cmd(int e) const { return reinterpret_cast<R *>(t.commands) + 3 * (size_t)e; }
     BS_HD R *goal(int e) const { return reinterpret_cast<R *>(t.goals) + 8 * (size_t)e; }
     BS_HD R lo(int k) const { return reinterpret_cast<const R *>(t.dof_lower)[k]; }
@@ -180,9 +180,8 @@ template <class R> __device__ void task_reset_env(const Ctx<R> &c, const TaskVie
         tv.goal(e)[7] = R(0);
         cube_new_goal(c, tv, e);
     } else if (loco) {
-        R z = R(t.rest_height + 0.02);
-        R dist = r_sqrt(R(QUAD_TARGET_X) * R(QUAD_TARGET_X) + z * z);
-        tv.potential(e) = -dist / R(t.control_dt);
+        const double z = (double)R(t.rest_height + 0.02);   // the stored root height
+        tv.potential(e) = -sqrt(QUAD_TARGET_X * QUAD_TARGET_X + z * z) / t.control_dt;
     } else if (!stack) {   // anymal velocity commands
         key[2] = (uint32_t)t.reset_count[e];
         NpRng cr = np_rng(key, 4);
@@ -215,10 +214,11 @@ template <class R, int G>
 __device__ R quad_reward_g(const Ctx<R> &c, const TaskView<R> &tv, int e, int sl, const Root<R> &r, const Frame<R> &f,
                            bool &done) {
     const R dt = R(tv.t.control_dt), term = R(tv.t.termination_height);
-    R dx = R(QUAD_TARGET_X) - r.p.x, dy = -r.p.y, dz = -r.p.z;
-    R dist = r_sqrt(dx * dx + dy * dy + dz * dz);
-    R potential = -dist / dt;
-    R rew = potential - tv.potential(e);
+    // the progress term in float64: |target - torso| ~ 1000 m, so -dist/dt in
+    // fp32 would carry a 4e-3 rounding step; one double sqrt per env
+    const double dx = QUAD_TARGET_X - (double)r.p.x, dy = -(double)r.p.y, dz = -(double)r.p.z;
+    const double potential = -sqrt(dx * dx + dy * dy + dz * dz) / tv.t.control_dt;
+    R rew = R(potential - tv.potential(e));
     R height = r.p.z;
     rew = rew + (height >= term ? R(0.5) : R(0));
     rew = rew + (height <= term ? R(-1) : R(0));

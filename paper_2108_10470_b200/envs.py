@@ -132,7 +132,7 @@ class EnvBatch:
         self.episode_steps = torch.zeros(E, dtype=torch.int32, device=dev)
         self.reset_count = torch.zeros(E, dtype=torch.int32, device=dev)
         self.actions = torch.zeros((E, self.act_dim), dtype=dt, device=dev)
-        self.potentials = torch.zeros(E, dtype=dt, device=dev)
+        self.potentials = torch.zeros(E, dtype=torch.float64, device=dev)   # float64 in both precisions
         self.commands = torch.zeros((E, 3), dtype=dt, device=dev)
         lo, hi = dof_limits(self.model)
         self.dof_lower = torch.as_tensor(lo, dtype=dt, device=dev)
@@ -197,6 +197,7 @@ class EnvBatch:
         return self.scene.dof_state.reshape(self.config.num_envs, -1, 2)
 
     # ------------------------------------------------------------ API
+    @N.on_scene_device
     def reset(self, env_indices=ALL):
         """Reset all envs (None) or the given ones; returns the full obs."""
         E = self.config.num_envs
@@ -215,12 +216,15 @@ class EnvBatch:
         self._call("bsim_task_reset", mptr, self.scene._s)
         return self.obs
 
+    @N.on_scene_device
     def step(self, actions) -> StepOutput:
         cfg = self.config
         a = actions if isinstance(actions, torch.Tensor) else torch.as_tensor(np.asarray(actions, dtype=np.float64))
         if tuple(a.shape) != (cfg.num_envs, self.act_dim):
             raise ValueError(f"actions must have shape ({cfg.num_envs}, {self.act_dim})")
         a = a.to(self.scene.device, self.scene.dtype)
+        if self._graph is not None and self._graph_gen != self.scene._struct_gen:
+            self.capture_graph()       # set_params() changed the structs baked into the graph
         if self._graph is not None:
             self._graph_in.copy_(a)
             self._graph.replay()
@@ -279,6 +283,7 @@ class EnvBatch:
         else:
             self._call("bsim_task_step", sc._s)
 
+    @N.on_scene_device
     def capture_graph(self, warmup=0):
         """Capture one control step (physics launch + task launch + the device
         step counter the DR interval reads) into a CUDA graph; later `step()`
@@ -305,6 +310,7 @@ class EnvBatch:
             object.__setattr__(self.scene, "stream", main)
             self.scene.step_count = count          # capture executed nothing
         self._graph = g
+        self._graph_gen = self.scene._struct_gen
         return g
 
     def release_graph(self):
@@ -357,6 +363,7 @@ class EnvBatch:
         h["auto_chunks"] = min(16, max(1, -(-self.config.num_envs // max(1, wave.value))))
         return h["auto_chunks"]
 
+    @N.on_scene_device
     def step_host(self, actions, sync=True) -> StepOutput:
         """EnvBatch.step with HOST arrays (the reference's numpy call,
         envs.py:178-200): actions (E, act_dim) numpy / CPU tensor in, CPU
@@ -383,6 +390,10 @@ class EnvBatch:
                 pinned = h["pinned"][key] = bool(a.is_pinned())
             if pinned:
                 src = a
+        inflight = h.get("inflight")      # a previous sync=False step may still read h["act"] /
+        if inflight is not None and (src is None or not self.host_zero_copy):   # count_host
+            inflight.synchronize()
+            h["inflight"] = None
         if src is None:
             src = h["act"].copy_(a)
         structs = sc._structs()
@@ -391,11 +402,10 @@ class EnvBatch:
         if self.host_zero_copy:
             self._step_host_zero_copy(src, h, lay, par, st, post)
             sc.step_count += cfg.decimation
-            if sync:
-                sc.stream.synchronize()
+            self._host_done(h, sync)
             return StepOutput(h["obs"], h["reward"], h["done"], {"timeout": h["timeout"], "poisoned": h["poisoned"]})
         n_chunks = int(self.host_chunk_count())
-        key = (id(structs), n_chunks, bool(self.host_fused))
+        key = (sc._struct_gen, n_chunks, bool(self.host_fused))
         if self.host_graph and h["graph"] is not None and h["graph_key"] == key:
             rc = sc._lib.bsim_host_graph_launch(h["graph"], src.data_ptr(), post, sc._s)
             if rc != 0:
@@ -426,9 +436,22 @@ class EnvBatch:
                                         f"{sc._lib.bsim_host_last_error().decode()}")
                 h["graph"], h["graph_key"] = g.value, key
         sc.step_count += cfg.decimation
-        if sync:
-            sc.stream.synchronize()
+        self._host_done(h, sync)
         return StepOutput(h["obs"], h["reward"], h["done"], {"timeout": h["timeout"], "poisoned": h["poisoned"]})
+
+    def _host_done(self, h, sync):
+        """Synchronise, or (sync=False) record the step so the next step_host
+        waits for it before reusing the staging buffer or the graph's host
+        step counter."""
+        if sync:
+            self.scene.stream.synchronize()
+            h["inflight"] = None
+            return
+        ev = h.get("ev")
+        if ev is None:
+            ev = h["ev"] = torch.cuda.Event()
+        ev.record(self.scene.stream)
+        h["inflight"] = ev
 
     def _step_host_zero_copy(self, src, h, lay, par, st, post):
         """bsim_env_step_host mode 2: one fused launch whose CTAs read their

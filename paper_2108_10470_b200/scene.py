@@ -57,6 +57,15 @@ class Scene:
                  env_offset=0, total_envs=None, stream=None, specialize=True, shape_pairs="spheres"):
         if not torch.cuda.is_available():
             raise N.NativeError("paper_2108_10470_b200.Scene needs a CUDA device (no CPU fallback)")
+        dev = torch.device(device if device is not None else "cuda")
+        if dev.index is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
+        with torch.cuda.device(dev):       # construction launches (FK, refresh) on the scene's device
+            self._init(models, num_envs, params, spacing, ground, env_origins, dev, precision, env_offset,
+                       total_envs, stream, specialize, shape_pairs)
+
+    def _init(self, models, num_envs, params, spacing, ground, env_origins, device, precision, env_offset,
+              total_envs, stream, specialize, shape_pairs):
         if isinstance(models, ArticulationModel):
             models = [models]
         if precision not in ("fp32", "fp64"):
@@ -65,7 +74,7 @@ class Scene:
         self.fp64 = precision == "fp64"
         self.precision = precision
         self.dtype = torch.float64 if self.fp64 else torch.float32
-        self.device = torch.device(device if device is not None else "cuda")
+        self.device = device
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         self.models = list(models)
         self.num_envs = E = int(num_envs)
@@ -108,6 +117,7 @@ class Scene:
             self._env_mask = torch.zeros(max(E, 1), dtype=torch.uint8, device=dev)
             self._actor_mask = torch.zeros(1, dtype=torch.int32, device=dev)
         self._struct_cache = None
+        self._struct_gen = 0
         rc = self._lib.bsim_step_smem_per_env(C.byref(self._structs()[0]), int(self.fp64), None, None)
         if rc != 0:
             raise N.NativeError(f"model too large for the step kernel (precision={precision}, rc={rc})")
@@ -169,6 +179,7 @@ class Scene:
         """Replace solver scalars (validated; takes effect on the next step)."""
         self.params = params.validate()
         self._struct_cache = None
+        self._struct_gen += 1      # invalidates CUDA graphs captured with the old structs baked in
 
     # ------------------------------------------------------------ methods
     def _init_poses(self):
@@ -176,6 +187,7 @@ class Scene:
         self.forward_kinematics()
         self.refresh_buffers()
 
+    @N.on_scene_device
     def step(self, n_substeps: int = 1, actions=None, action_scale: float = 1.0,
              action_mode: int = MODE_POSITION, actions_clipped=None):
         """`n_substeps` x Scene.step() (physics.py:538-592) in one fused launch.
@@ -193,6 +205,7 @@ class Scene:
                    C.byref(act) if act is not None else None, self._s, what="bsim_step")
         self.step_count += int(n_substeps)
 
+    @N.on_scene_device
     def forward_kinematics(self, env_mask=None, actors=None):
         """physics.py:366-425 for the selected envs / actors, plus a repack of
         the touched body/root rows."""
@@ -208,14 +221,17 @@ class Scene:
             mptr = self._env_mask.data_ptr()
         self._call(self._sfx("bsim_forward_kinematics"), C.byref(lay), C.byref(st), mptr, amask, self._s)
 
+    @N.on_scene_device
     def refresh_buffers(self):
         """dof readout + body/root packing (physics.py:1037-1046, no contact ctx)."""
         lay, _, st = self._structs()
         self._call(self._sfx("bsim_refresh_buffers"), C.byref(lay), C.byref(st), self._s)
 
+    @N.on_scene_device
     def read_dof_states(self):
         self.refresh_buffers()
 
+    @N.on_scene_device
     def _set_indexed(self, root: bool, values, actor_idx):
         lay, _, st = self._structs()
         v = values.to(self.device, self.dtype).contiguous()
@@ -225,6 +241,7 @@ class Scene:
                    self._env_mask.data_ptr(), self._actor_mask.data_ptr(), self._s)
         return v, idx  # keep alive until the stream consumes them
 
+    @N.on_scene_device
     def contact_geometry(self):
         """(active, depth, point, normal) per (slot, env): planes then pairs,
         env-minor, world-frame points (physics.py:463-498)."""
@@ -238,6 +255,7 @@ class Scene:
                    act.data_ptr(), depth.data_ptr(), point.data_ptr(), normal.data_ptr(), self._s)
         return act[:n].bool(), depth[:n], point[:n], normal[:n]
 
+    @N.on_scene_device
     def collide_tensors(self, capacity=None):
         """Compacted active contacts in the reference's collide() order
         (slot-major, env-ascending, planes then pairs; physics.py:500-517) as
@@ -259,6 +277,7 @@ class Scene:
         k = min(int(count.item()), cap)
         return k, ba[:k], bb[:k], depth[:k], point[:k], normal[:k]
 
+    @N.on_scene_device
     def collide(self):
         """Host list of ContactPoint in the reference's collide() order and
         content (physics.py:500-517; the friction merge of 519-534 is an
@@ -291,6 +310,7 @@ class Scene:
                 carriers.setdefault(key, []).append(c.point)
         return out
 
+    @N.on_scene_device
     def clear_nonfinite(self, env_indices):
         self.nonfinite[torch.as_tensor(env_indices, device=self.device, dtype=torch.long)] = False
 

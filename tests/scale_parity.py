@@ -1,0 +1,201 @@
+"""fp32 / fp64 parity of the CUDA env step at BASELINE.json scale (4096 envs)
+against the float64 reference, per quantity.
+
+Chain of evidence:
+  reference EnvBatch (4096 envs, 20 free control steps, knock-downs, timeouts)
+    -> tests/golden/scale_*_4096.npz (post-step state + outputs of a 1/32 env
+       sample every step, done / timeout masks of ALL envs every step)
+    -> the oracle (oracle/tasks.py over oracle/bso.c) re-runs the same 4096
+       envs free and must match the sample at 1e-7 and the full masks exactly
+       (tests/test_oracle_golden.py) -- it then stands in for the reference
+       on every env
+    -> the CUDA path, two ways:
+       * teacher forced: before each step the oracle's full pre-step state is
+         loaded, one control step runs, every output is compared;
+       * free rollout: the CUDA env runs the 20 steps from construction on its
+         own and the per-step error and the first divergence step are reported.
+
+Errors are reported per quantity with the north-star contract
+|gpu - ref| <= 1e-4 + 1e-4 |ref| ("scaled" error <= 1): the fraction of
+elements inside it, the 99.9th percentile and max of the absolute error and
+the max scaled error.  Positions are compared env-local (the canonical GPU
+state; world positions at 4096 envs reach 250 m, where the fp32 ulp alone is
+1.5e-5 m).  Used by tests/test_gpu_scale_parity.py and tools/parity_table.py.
+"""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import torch
+
+from golden_util import load
+
+CASES = {"quadruped": "scale_ant_4096", "quadruped-anymal-obs": "scale_anymal_4096"}
+QUANTITIES = ("root_state", "body_state", "dof_state", "net_contact", "sensor_forces", "dof_force", "obs",
+              "reward")
+ATOL = RTOL = 1e-4
+
+
+def oracle_trace(task, threads=None):
+    """Free-run the oracle env over the fixture's schedule; returns (meta,
+    fixture arrays, list of per-step {"pre": ..., "post": ...})."""
+    from oracle.tasks import OracleEnv
+    meta, arr = load(CASES[task])
+    E = meta["num_envs"]
+    env = OracleEnv(task, E, seed=meta["seed"], episode_length=meta["episode_length"],
+                    threads=threads or os.cpu_count() or 1)
+    s = env.scene
+    knock = np.arange(1, E, 4)
+    rng = np.random.default_rng(0)
+    steps = []
+    for t in range(meta["steps"]):
+        a = rng.uniform(-1.0, 1.0, (E, env.act_dim))
+        if t == meta["knock_step"]:
+            root = env.local_root()[knock]
+            root[:, 2] = 0.1 - s.env_origins[knock, 2]
+            env.set_root_state(root, knock)
+        pre = {"pos": s.pos.copy(), "quat": s.quat.copy(), "linvel": s.linvel.copy(), "angvel": s.angvel.copy(),
+               "anchor": s._friction_anchor.copy(), "dof_state": s.dof_state.copy(),
+               "root_state": s.root_state.copy(), "sensor_forces": s.sensor_forces.copy(),
+               "dof_force": s.dof_force.copy(), "episode_steps": env.episode_steps.copy(),
+               "reset_count": env.reset_count.copy(), "potentials": env.potentials.copy(),
+               "commands": env.commands.copy(), "actions": a}
+        obs, reward, done, info = env.step(a)
+        post = {"obs": obs, "reward": reward, "done": done, "timeout": info["timeout"],
+                "body_local": local_body(s.pos, s.quat, s.linvel, s.angvel, s.env_origins, s.bodies_per_env),
+                "dof_state": s.dof_state.copy(), "net_contact": s.net_contact.copy(),
+                "sensor_forces": s.sensor_forces.copy(), "dof_force": s.dof_force.copy(),
+                "anchor": s._friction_anchor.copy(), "reset_count": env.reset_count.copy()}
+        steps.append({"pre": pre, "post": post})
+    return meta, arr, steps
+
+
+def local_body(pos, quat, linvel, angvel, origins, B):
+    E = len(origins)
+    be = np.repeat(np.arange(E), B)
+    return np.concatenate([pos - origins[be], quat, linvel, angvel], 1)
+
+
+def make_gpu_env(task, meta, precision):
+    from paper_2108_10470_b200.envs import make_env
+    return make_env(task, num_envs=meta["num_envs"], seed=meta["seed"], episode_length=meta["episode_length"],
+                    precision=precision)
+
+
+def load_pre(env, pre):
+    """The oracle's pre-step state into the CUDA env (env-local positions)."""
+    s = env.scene
+    E, B = s.num_envs, s.bodies_per_env
+    org = s.env_origins_host
+    dt = s.dtype
+    s.body_q.copy_(torch.as_tensor(local_body(pre["pos"], pre["quat"], pre["linvel"], pre["angvel"], org, B),
+                                   dtype=dt))
+    s._friction_anchor.copy_(torch.as_tensor(pre["anchor"] - org[None], dtype=dt))
+    for k in ("dof_state", "root_state", "sensor_forces", "dof_force"):
+        getattr(s, k).copy_(torch.as_tensor(pre[k], dtype=dt))
+    env.episode_steps.copy_(torch.as_tensor(pre["episode_steps"].astype(np.int32)))
+    env.reset_count.copy_(torch.as_tensor(pre["reset_count"].astype(np.int32)))
+    env.potentials.copy_(torch.as_tensor(pre["potentials"], dtype=env.potentials.dtype))
+    env.commands.copy_(torch.as_tensor(pre["commands"], dtype=env.commands.dtype))
+
+
+def gpu_post(env, out):
+    s = env.scene
+    B = s.bodies_per_env
+    bq = s.body_q.double().cpu().numpy()
+    return {"obs": out.obs.double().cpu().numpy(), "reward": out.reward.double().cpu().numpy(),
+            "done": out.done.cpu().numpy(), "timeout": out.info["timeout"].cpu().numpy(),
+            "body_state": bq, "root_state": bq[::B], "dof_state": s.dof_state.double().cpu().numpy(),
+            "net_contact": s.net_contact.double().cpu().numpy(),
+            "sensor_forces": s.sensor_forces.double().cpu().numpy(),
+            "dof_force": s.dof_force.double().cpu().numpy(),
+            "anchor": s._friction_anchor.double().cpu().numpy(),
+            "reset_count": env.reset_count.cpu().numpy()}
+
+
+def ref_post(post, B):
+    d = dict(post)
+    d["body_state"] = post["body_local"]
+    d["root_state"] = post["body_local"][::B]
+    return d
+
+
+def quantity_errors(g, r):
+    """{max_abs, p999_abs, max_scaled, frac_within} of |g - r| vs 1e-4 + 1e-4 |r|."""
+    g = np.asarray(g, float).ravel()
+    r = np.asarray(r, float).ravel()
+    d = np.abs(g - r)
+    sc = d / (ATOL + RTOL * np.abs(r))
+    return {"max_abs": float(d.max()), "p999_abs": float(np.quantile(d, 0.999)), "max_scaled": float(sc.max()),
+            "frac_within": float(np.mean(sc <= 1.0)), "n": int(d.size)}
+
+
+def compare(gp, rp):
+    return {q: quantity_errors(gp[q], rp[q]) for q in QUANTITIES}
+
+
+def masks_equal(gp, rp):
+    """done / timeout / reset counts exact; friction-anchor presence (NaN) pattern."""
+    return {"done": bool(np.array_equal(gp["done"], rp["done"])),
+            "timeout": bool(np.array_equal(gp["timeout"], rp["timeout"])),
+            "reset_count": bool(np.array_equal(gp["reset_count"], rp["reset_count"])),
+            "anchor_mismatch": int(np.sum(np.isnan(gp["anchor"][..., 0]) != np.isnan(rp["anchor"][..., 0])))}
+
+
+def teacher_forced(task, precision, trace=None):
+    """Per step: (errors per quantity, mask equality) of one CUDA control step
+    from the oracle's pre-step state."""
+    meta, arr, steps = trace if trace is not None else oracle_trace(task)
+    env = make_gpu_env(task, meta, precision)
+    B = env.scene.bodies_per_env
+    res = []
+    for st in steps:
+        load_pre(env, st["pre"])
+        out = env.step(torch.as_tensor(st["pre"]["actions"], dtype=env.scene.dtype))
+        gp = gpu_post(env, out)
+        rp = ref_post(st["post"], B)
+        res.append({"errors": compare(gp, rp), "masks": masks_equal(gp, rp), "gpu": gp, "ref": rp})
+    env.close()
+    return meta, arr, res
+
+
+def free_rollout(task, precision, trace=None):
+    """The CUDA env free from construction over the fixture's schedule."""
+    meta, arr, steps = trace if trace is not None else oracle_trace(task)
+    env = make_gpu_env(task, meta, precision)
+    s = env.scene
+    B = s.bodies_per_env
+    knock = np.arange(1, meta["num_envs"], 4)
+    res = []
+    for t, st in enumerate(steps):
+        if t == meta["knock_step"]:
+            root = s.root_state.clone()
+            root[knock, 2] = 0.1
+            env.buffers.set_root_state(root, knock)
+        out = env.step(torch.as_tensor(st["pre"]["actions"], dtype=s.dtype))
+        gp = gpu_post(env, out)
+        rp = ref_post(st["post"], B)
+        res.append({"errors": compare(gp, rp), "masks": masks_equal(gp, rp), "gpu": gp, "ref": rp})
+    env.close()
+    return meta, arr, res
+
+
+def sample_vs_reference(meta, arr, gp, t, B, D, S):
+    """The CUDA outputs of the fixture's env sample vs the reference itself."""
+    idx = arr["sample"]
+    rb = (idx[:, None] * B + np.arange(B)).ravel()
+    rd = (idx[:, None] * D + np.arange(D)).ravel()
+    rs = (idx[:, None] * S + np.arange(S)).ravel()
+    org = np.repeat(arr["env_origins"], B, axis=0)
+    body = arr["body_state"][t].copy()
+    body[:, 0:3] -= org
+    ref = {"obs": arr["obs"][t], "reward": arr["reward"][t], "body_state": body, "root_state": body[::B],
+           "dof_state": arr["dof_state"][t], "net_contact": arr["net_contact"][t],
+           "sensor_forces": arr["sensor_forces"][t], "dof_force": arr["dof_force"][t]}
+    g = {"obs": gp["obs"][idx], "reward": gp["reward"][idx], "body_state": gp["body_state"][rb],
+         "root_state": gp["body_state"][rb][::B], "dof_state": gp["dof_state"][rd],
+         "net_contact": gp["net_contact"][rb], "sensor_forces": gp["sensor_forces"][rs],
+         "dof_force": gp["dof_force"][rd]}
+    return {q: quantity_errors(g[q], ref[q]) for q in QUANTITIES}

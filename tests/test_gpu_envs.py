@@ -39,7 +39,7 @@ def _load_pre(env, arr, t, extra_name):
     s.root_state.copy_(torch.as_tensor(arr["root_state"][t], dtype=s.dtype))
     env.episode_steps.copy_(torch.as_tensor(arr["episode_steps"][t].astype(np.int32)))
     env.reset_count.copy_(torch.as_tensor(arr["reset_count"][t].astype(np.int32)))
-    getattr(env, extra_name).copy_(torch.as_tensor(arr["extra_before"][t], dtype=s.dtype))
+    getattr(env, extra_name).copy_(torch.as_tensor(arr["extra_before"][t], dtype=getattr(env, extra_name).dtype))
 
 
 @pytest.mark.parametrize("precision", ["fp64", "fp32"])

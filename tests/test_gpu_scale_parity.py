@@ -1,0 +1,78 @@
+"""fp32 and fp64 parity of the CUDA env step at 4096 envs (BASELINE configs 1
+and 3), per quantity, teacher forced and free running -- method in
+tests/scale_parity.py, numbers in profiles/r02_parity_fp32.md.
+
+Contract (north star: abs/rel <= 1e-4 per step, masks bit-exact):
+  * fp64: every quantity within 1e-8 of the oracle (which matches the
+    reference's own 4096-env trace at 1e-7, tests/test_oracle_golden.py);
+  * fp32, teacher forced, per quantity and per step: states and obs
+    >= 99.9 % of elements within 1e-4 + 1e-4|ref| and every element within
+    1e-3 + 1e-3|ref|; net contact force, sensors and DOF force within
+    1e-3 + 1e-3|ref| (impulses / dt: 120x the velocity rounding); reward
+    within 1e-3 + 1e-3|ref| (its progress term differentiates positions at
+    1/control_dt = 60 Hz);
+  * done / timeout masks and reset counts of all 4096 envs exact at every
+    step in both precisions (teacher forced), and the friction-anchor
+    presence pattern exact.
+"""
+
+import numpy as np
+import pytest
+
+import scale_parity as SP
+
+pytestmark = pytest.mark.gpu
+
+STATES = ("root_state", "body_state", "dof_state", "obs")
+FORCES = ("net_contact", "sensor_forces", "dof_force", "reward")
+_TRACES = {}
+
+
+def _trace(task):
+    if task not in _TRACES:
+        _TRACES[task] = SP.oracle_trace(task)
+    return _TRACES[task]
+
+
+@pytest.mark.parametrize("task", list(SP.CASES))
+def test_fp32_teacher_forced_per_quantity(task):
+    _, _, res = SP.teacher_forced(task, "fp32", _trace(task))
+    bad = []
+    for t, r in enumerate(res):
+        for q, e in r["errors"].items():
+            scaled_1e3 = e["max_scaled"] / 10.0          # vs 1e-3 + 1e-3|ref|
+            if q in STATES and (e["frac_within"] < 0.999 or scaled_1e3 > 1.0):
+                bad.append((t, q, e))
+            if q in FORCES and scaled_1e3 > 1.0:
+                bad.append((t, q, e))
+        m = r["masks"]
+        assert m["done"] and m["timeout"] and m["reset_count"], (t, m)
+        assert m["anchor_mismatch"] == 0, (t, m)
+    assert not bad, bad[:6]
+    assert sum(int(r["ref"]["done"].sum()) for r in res) >= 4096     # terminations + timeouts exercised
+
+
+@pytest.mark.parametrize("task", list(SP.CASES))
+def test_fp64_teacher_forced_and_free_rollout(task):
+    for mode in (SP.teacher_forced, SP.free_rollout):
+        _, _, res = mode(task, "fp64", _trace(task))
+        for t, r in enumerate(res):
+            for q, e in r["errors"].items():
+                assert e["max_abs"] <= 1e-8 * (1 + np.abs(r["ref"][q]).max()), (mode.__name__, t, q, e)
+            assert r["masks"]["done"] and r["masks"]["timeout"] and r["masks"]["reset_count"], (t, r["masks"])
+
+
+@pytest.mark.parametrize("task", list(SP.CASES))
+def test_fp32_free_rollout_reports_divergence(task):
+    """20 free fp32 control steps from construction: masks follow the
+    reference (terminations at the knock step, timeouts at 12) and the
+    per-step error stays bounded until the chaotic contact dynamics separate
+    the trajectories (the first step over 1e-4 is reported, not asserted)."""
+    meta, arr, res = SP.free_rollout(task, "fp32", _trace(task))
+    for t in (meta["knock_step"], meta["episode_length"] - 1):
+        assert np.array_equal(res[t]["gpu"]["done"], arr["done_all"][t]), t
+    first = {q: next((t for t, r in enumerate(res) if r["errors"][q]["max_scaled"] > 1.0), None)
+             for q in SP.QUANTITIES}
+    print(f"{task} fp32 free rollout, first step over 1e-4 per quantity: {first}")
+    # the first control step from the bit-exact reset state is inside the contract
+    assert all(r["errors"]["obs"]["frac_within"] >= 0.999 for r in res[:1])

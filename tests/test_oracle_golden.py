@@ -5,6 +5,8 @@ The fixtures were produced by running the reference `batchsim` itself
 expected to ~1e-9 (LAPACK gesv vs. the oracle's elimination differ only in
 rounding)."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -90,3 +92,68 @@ def test_oracle_contact_list_matches_collide(case):
     assert _close(depth[sel], arr["collide_depth"]) < 1e-12
     assert _close(point[sel], arr["collide_point"]) < 1e-12
     assert _close(normal[sel], arr["collide_normal"]) < 1e-12
+
+
+ENV_CASES = [("quadruped", "env_quadruped", 0.1, "potentials"),
+             ("quadruped-anymal-obs", "env_quadruped_anymal_obs", 0.1, "commands"),
+             ("humanoid", "env_humanoid", 0.5, "potentials")]
+
+
+@pytest.mark.parametrize("task,fixture,knock_z,extra", ENV_CASES)
+def test_oracle_env_free_running_matches_reference(task, fixture, knock_z, extra):
+    """The oracle task layer (oracle/tasks.py) over the C physics, FREE running
+    from construction through the reference's whole env trace (its explicit
+    second reset, the knock-over of env 2 at t = 5, terminations, timeouts at
+    episode_length and the auto-resets): obs / reward / done / timeout and
+    the env-layer state agree with the reference EnvBatch at 1e-7, done and
+    timeout masks and reset counts exactly."""
+    from oracle.tasks import OracleEnv
+    meta, arr = load(fixture)
+    env = OracleEnv(task, meta["num_envs"], seed=meta["seed"], episode_length=meta["episode_length"])
+    assert _close(env.scene.env_origins, arr["env_origins"]) < 1e-12
+    obs0 = env.reset()
+    assert _close(obs0, arr["obs0"]) < 1e-9
+    for t in range(meta["steps"]):
+        if t == 5:
+            root = env.local_root()[[2]]
+            root[0, 2] = knock_z - env.scene.env_origins[2, 2]
+            env.set_root_state(root, np.array([2]))
+        assert np.array_equal(env.reset_count, arr["reset_count"][t]), t
+        assert np.array_equal(env.episode_steps, arr["episode_steps"][t]), t
+        assert _close(getattr(env, extra), arr["extra_before"][t]) < 1e-7, (t, extra)
+        obs, reward, done, info = env.step(arr["actions"][t])
+        assert np.array_equal(done, arr["done"][t]), t
+        assert np.array_equal(info["timeout"], arr["timeout"][t]), t
+        assert _close(obs, arr["obs"][t]) < 1e-7, (t, "obs", _close(obs, arr["obs"][t]))
+        assert _close(reward, arr["reward"][t]) < 1e-7, (t, "reward")
+        assert _close(env.scene.ctrl_dof_pos_target, arr["ctrl_dof_pos_target"][t]) < 1e-12, t
+
+
+@pytest.mark.parametrize("task", ["quadruped", "quadruped-anymal-obs"])
+def test_oracle_env_at_4096_envs_matches_reference(task):
+    """BASELINE scale: the oracle env free running over the reference's 4096-env
+    trace (tests/golden/make_scale_golden.py: 20 control steps, a quarter of
+    the envs knocked down at step 5, every env timing out at step 12):
+    done / timeout masks of ALL envs exact at every step, the reference's
+    1/32 env sample (post-step state, obs, reward, env-layer state) at 1e-7.
+    The oracle then stands in for the reference on every env of the CUDA
+    parity tests (tests/test_gpu_scale_parity.py)."""
+    import scale_parity as SP
+    meta, arr, steps = SP.oracle_trace(task, threads=os.cpu_count() or 1)
+    idx = arr["sample"]
+    B = 9 if task == "quadruped" else 13
+    rb = (idx[:, None] * B + np.arange(B)).ravel()
+    org = np.repeat(arr["env_origins"], B, axis=0)
+    for t, st in enumerate(steps):
+        p = st["post"]
+        assert np.array_equal(p["done"], arr["done_all"][t]), t
+        assert np.array_equal(p["timeout"], arr["timeout_all"][t]), t
+        assert np.array_equal(p["reset_count"][idx], arr["reset_count"][t]), t
+        body = arr["body_state"][t].copy()
+        body[:, 0:3] -= org
+        assert _close(p["body_local"][rb], body) < 1e-7, (t, "body")
+        assert _close(p["obs"][idx], arr["obs"][t]) < 1e-7, (t, "obs")
+        assert _close(p["reward"][idx], arr["reward"][t]) < 1e-7, (t, "reward")
+        assert _close(p["net_contact"][rb], arr["net_contact"][t]) < 1e-7, (t, "net_contact")
+        assert _close(p["anchor"][:, idx], arr["friction_anchor"][t]) < 1e-7, (t, "anchors")
+    assert arr["done_all"].sum() >= 4096          # terminations and timeouts both exercised

@@ -3,7 +3,19 @@ profiles/ (bench.py reads `dram_bytes_per_launch` from it for roofline.traffic).
 
     python tools/ncu_summary.py REPORT.ncu-rep profiles/rNN_step_ncu.json --envs 16384 --note "..."
 """
-import argparse, csv, json, subprocess
+import argparse, csv, glob, hashlib, json, os, subprocess
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def kernel_src_sha():
+    """sha256 (16 hex) over the CUDA sources + the ABI header: bench.py only
+    uses a summary's traffic when it was captured from the current kernels."""
+    h = hashlib.sha256()
+    for f in sorted(glob.glob(os.path.join(ROOT, "paper_2108_10470_b200", "csrc", "*.cu*"))) + [
+            os.path.join(ROOT, "include", "batchsim_b200.h")]:
+        h.update(open(f, "rb").read())
+    return h.hexdigest()[:16]
 
 KEYS = {
     "gpu__time_duration.sum": "duration_us",
@@ -67,7 +79,8 @@ def main():
             m["fp32_flop_per_launch"] = fl
             m["fp32_flop_per_env_launch"] = fl / a.envs
         launches.append(m)
-    json.dump({"envs": a.envs, "command": a.command, "note": a.note, "launches": launches},
+    json.dump({"envs": a.envs, "command": a.command, "note": a.note, "src_sha": kernel_src_sha(),
+               "launches": launches},
               open(a.out, "w"), indent=1)
     print(json.dumps(launches, indent=1)[:3000])
 
