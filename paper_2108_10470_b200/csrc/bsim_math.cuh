@@ -94,6 +94,28 @@ template <class R> struct M3 {  // general 3x3, row-major
 };
 
 template <class R> BS_HD V3<R> v3(R x, R y, R z) { return V3<R>{x, y, z}; }
+// error-free sum (Knuth TwoSum): a + b = s + e exactly, s = fl(a + b)
+template <class R> BS_HD R two_sum(R a, R b, R &e) {
+    const R s = a + b;
+    const R bb = s - a;
+    e = (a - (s - bb)) + (b - bb);
+    return s;
+}
+// (a - b) + (c - d) + (f - g) for a ~ b, c ~ d O(1) and the result small:
+// the two O(1) differences and their sum are carried with their rounding
+// errors (TwoSum), so the result is accurate to ~1 ulp of ITSELF rather
+// than of the O(1) operands (the TGS position error, bsim_step.cuh joint_item)
+template <class R> BS_HD R cancel_sum(R a, R b, R c, R dd, R f, R g) {
+    R e1, e2, e3;
+    const R s1 = two_sum(a, -b, e1);
+    const R s2 = two_sum(c, -dd, e2);
+    const R h = two_sum(s1, s2, e3);
+    return h + (((e1 + e2) + e3) + (f - g));
+}
+// precision conversions (the fp32 step's joint geometry is evaluated in double: bsim_step.cuh GeomT)
+template <class G, class R> BS_HD V3<G> cv3(V3<R> a) { return V3<G>{(G)a.x, (G)a.y, (G)a.z}; }
+template <class G, class R> BS_HD Q4<G> cq4(Q4<R> a) { return Q4<G>{(G)a.x, (G)a.y, (G)a.z, (G)a.w}; }
+
 template <class R> BS_HD V3<R> zero3() { return V3<R>{R(0), R(0), R(0)}; }
 template <class R> BS_HD V3<R> operator+(V3<R> a, V3<R> b) { return V3<R>{a.x + b.x, a.y + b.y, a.z + b.z}; }
 template <class R> BS_HD V3<R> operator-(V3<R> a, V3<R> b) { return V3<R>{a.x - b.x, a.y - b.y, a.z - b.z}; }
@@ -135,6 +157,24 @@ template <class R> BS_HD Q4<R> qexp(V3<R> v) {
     R s, c;
     r_sincos(R(0.5) * ang, s, c);
     return Q4<R>{ax.x * s, ax.y * s, ax.z * s, c};
+}
+// exp map for |v| < 0.25 rad as even series in |v|^2 (no square root, no
+// range reduction): sin(a/2)/a and cos(a/2) to degree 10 (truncation < 1e-13
+// relative); larger rotations take qexp.
+template <class R> BS_HD Q4<R> qexp_small(V3<R> v) {
+    const R a2 = dot(v, v);
+    if (!(a2 < R(0.0625))) return qexp(v);
+    const R sa = R(0.5) + a2 * (R(-1.0 / 48) + a2 * (R(1.0 / 3840) + a2 * (R(-1.0 / 645120) + a2 * R(1.0 / 185794560))));
+    const R c = R(1) + a2 * (R(-1.0 / 8) + a2 * (R(1.0 / 384) + a2 * (R(-1.0 / 46080) + a2 * R(1.0 / 10321920))));
+    return Q4<R>{v.x * sa, v.y * sa, v.z * sa, c};
+}
+// normalisation of a quaternion whose norm is 1 to within ~1e-6 (one Newton
+// step of 1/sqrt from 1: relative error 3/8 (n2 - 1)^2)
+template <class R> BS_HD Q4<R> qnormalize_near(Q4<R> q) {
+    const R n2 = q.x * q.x + q.y * q.y + q.z * q.z + q.w * q.w;
+    const R e = n2 - R(1);
+    const R in = R(1) - R(0.5) * e + R(0.375) * e * e;
+    return Q4<R>{q.x * in, q.y * in, q.z * in, q.w * in};
 }
 // log map (spatial.py:155-162)
 template <class R> BS_HD V3<R> qlog(Q4<R> q) {

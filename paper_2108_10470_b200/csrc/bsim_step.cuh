@@ -195,6 +195,34 @@ template <> struct Ws<float> {
 };
 #endif
 
+// Arithmetic of the joint geometry (perr / rerr, joint_item) on the fp32
+// path.  Default: fp32 with the position error summed by cancel_sum (TwoSum:
+// accurate to ulp(perr) instead of ulp(pose)).  Measurement variants
+// (profiles/r02_parity_fp32.md): BSIM_GEOM_F64 = orientations /
+// rerr in double, BSIM_GEOMP_F64 = positions / perr in double,
+// BSIM_RERR_PROJ = revolute rerr projected normal to the axis before rounding,
+// BSIM_PERR_TWOSUM=0 = round 1's plain fp32 sums.
+#ifndef BSIM_GEOM_F64
+#define BSIM_GEOM_F64 0
+#endif
+#ifndef BSIM_GEOMP_F64
+#define BSIM_GEOMP_F64 BSIM_GEOM_F64
+#endif
+#ifndef BSIM_RERR_PROJ
+#define BSIM_RERR_PROJ 0
+#endif
+#ifndef BSIM_PERR_TWOSUM
+#define BSIM_PERR_TWOSUM 1
+#endif
+template <class R> struct GeomT { using type = R; };
+template <class R> struct GeomPT { using type = R; };
+#if BSIM_GEOM_F64
+template <> struct GeomT<float> { using type = double; };
+#endif
+#if BSIM_GEOMP_F64
+template <> struct GeomPT<float> { using type = double; };
+#endif
+
 template <class R> struct Ctx {
     using Joint = typename Abi<R>::Joint;
     using Tendon = typename Abi<R>::Tendon;
@@ -427,24 +455,59 @@ BS_HD void joint_item(const Ctx<R> &c, const Ws<R> &w, int e, int j, R h, bool b
         }
         if (n == 1) q0 = q[0];
     }
-    // ---- geometry
-    const int qitem = deltas ? BQE : BQ;
-    Q4<R> qp = w.l4(ib(d, p, qitem)), qc = w.l4(ib(d, ch, qitem));
-    Q4<R> jqp = IDF ? qp : qmul(qp, jq4(jt.origin_quat)), jqc = IDF ? qc : qmul(qc, jq4(jt.child_quat));
-    V3<R> rp = qrot(qp, jv3(jt.origin_pos)), rc = qrot(qc, jv3(jt.child_pos));
-    // ac - ap with the body-origin difference taken first (env-local)
-    V3<R> sep = w.l3(ib(d, ch, BP)) - w.l3(ib(d, p, BP));
-    if (deltas) sep = (w.l3(ib(d, ch, BP)) + w.l3(ib(d, ch, BDP))) - (w.l3(ib(d, p, BP)) + w.l3(ib(d, p, BDP)));
-    V3<R> perr = sep + (rc - rp);
-    Q4<R> qe = qmul(jqc, qconj(jqp));
-    V3<R> rerr = qvec(qe) * (R(2) * signr(qe.w));
-    V3<R> a = qrot(jqp, jv3(jt.axis));
+    // ---- geometry.  perr / rerr are small differences of O(1) poses and the
+    // biased rows divide them by h, so plain fp32 sums put fresh velocity
+    // noise of ulp(pose) / h ~ 1e-4 into every pass: perr is
+    // summed error-free (cancel_sum); GeomT / GeomPT select the measurement
+    // variants in double
+    using Gt = typename GeomT<R>::type;      // orientations, rerr
+    using Gp = typename GeomPT<R>::type;     // positions, perr
+    Q4<Gt> qp, qc;
+    if (!deltas) {
+        qp = cq4<Gt>(w.l4(ib(d, p, BQ)));
+        qc = cq4<Gt>(w.l4(ib(d, ch, BQ)));
+    } else if constexpr (sizeof(Gt) > sizeof(R)) {   // refresh 718-756: normalize(exp(dang) q), recomputed in Gt
+        qp = qnormalize_near(qmul(qexp_small(cv3<Gt>(w.l3(ib(d, p, BDA)))), cq4<Gt>(w.l4(ib(d, p, BQ)))));
+        qc = qnormalize_near(qmul(qexp_small(cv3<Gt>(w.l3(ib(d, ch, BDA)))), cq4<Gt>(w.l4(ib(d, ch, BQ)))));
+    } else {
+        qp = cq4<Gt>(w.l4(ib(d, p, BQE)));
+        qc = cq4<Gt>(w.l4(ib(d, ch, BQE)));
+    }
+    Q4<Gt> jqp = IDF ? qp : qmul(qp, cq4<Gt>(jq4(jt.origin_quat))), jqc = IDF ? qc : qmul(qc, cq4<Gt>(jq4(jt.child_quat)));
+    V3<Gp> grp = cv3<Gp>(qrot(qp, cv3<Gt>(jv3(jt.origin_pos)))), grc = cv3<Gp>(qrot(qc, cv3<Gt>(jv3(jt.child_pos))));
+    // ac - ap with the body-origin difference taken first (env-local), then the deltas'
+#if BSIM_PERR_TWOSUM
+    V3<Gp> gperr;
+    {
+        const V3<R> pc = w.l3(ib(d, ch, BP)), pp = w.l3(ib(d, p, BP));
+        const V3<R> dc = deltas ? w.l3(ib(d, ch, BDP)) : zero3<R>(), dp = deltas ? w.l3(ib(d, p, BDP)) : zero3<R>();
+        const V3<R> rc_ = cv3<R>(grc), rp_ = cv3<R>(grp);
+        gperr = V3<Gp>{(Gp)cancel_sum(pc.x, pp.x, rc_.x, rp_.x, dc.x, dp.x),
+                       (Gp)cancel_sum(pc.y, pp.y, rc_.y, rp_.y, dc.y, dp.y),
+                       (Gp)cancel_sum(pc.z, pp.z, rc_.z, rp_.z, dc.z, dp.z)};
+    }
+#else
+    V3<Gp> sep = cv3<Gp>(w.l3(ib(d, ch, BP))) - cv3<Gp>(w.l3(ib(d, p, BP)));
+    if (deltas) sep = sep + (cv3<Gp>(w.l3(ib(d, ch, BDP))) - cv3<Gp>(w.l3(ib(d, p, BDP))));
+    const V3<Gp> gperr = sep + (grc - grp);
+#endif
+    const Q4<Gt> qe = qmul(jqc, qconj(jqp));
+    V3<Gt> grerr = qvec(qe) * (Gt(2) * signr(qe.w));
+    const V3<Gt> ga = qrot(jqp, cv3<Gt>(jv3(jt.axis)));
+#if BSIM_RERR_PROJ
+    // revolute: only rerr's components normal to the axis reach the rows
+    // (G a = 0), so drop the axial one before rounding to R
+    if (kind == BSIM_REVOLUTE) grerr = grerr - ga * dot(ga, grerr);
+#endif
+    const V3<R> perr = cv3<R>(gperr), rerr = cv3<R>(grerr);
+    const V3<R> rp = cv3<R>(grp), rc = cv3<R>(grc);
+    V3<R> a = cv3<R>(ga);
     if (!freeze && jdof >= 0) {
         if (kind == BSIM_REVOLUTE) {
-            Q4<R> qr = qmul(qconj(jqp), jqc);
+            Q4<R> qr = cq4<R>(qmul(qconj(jqp), jqc));
             q0 = wrap_pi(R(2) * r_atan2(dot(qvec(qr), jv3(jt.axis)), qr.w));
         } else if (kind == BSIM_PRISMATIC) {
-            q0 = dot(a, perr);
+            q0 = (R)dot(cv3<Gp>(a), gperr);
         }
     }
     // ---- row constants from the current world inverse inertias

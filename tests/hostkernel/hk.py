@@ -15,15 +15,17 @@ ROOT = os.path.dirname(os.path.dirname(HERE))
 
 
 def build():
+    extra = os.environ.get("BSIM_HK_EXTRA", "").split()      # dev experiments (tools/fp32_error_probe.py)
+    so = SO if not extra else SO.replace(".so", "_" + "_".join(x.strip("-D").replace("=", "") for x in extra) + ".so")
     srcs = [os.path.join(HERE, "host_step.cu")] + [
         os.path.join(ROOT, "paper_2108_10470_b200", "csrc", f)
         for f in ("bsim_step.cuh", "bsim_math.cuh", "bsim_topologies.cuh")]
-    if os.path.exists(SO) and os.path.getmtime(SO) >= max(os.path.getmtime(s) for s in srcs):
-        return SO
-    os.makedirs(os.path.dirname(SO), exist_ok=True)
+    if os.path.exists(so) and os.path.getmtime(so) >= max(os.path.getmtime(s) for s in srcs):
+        return so
+    os.makedirs(os.path.dirname(so), exist_ok=True)
     subprocess.check_call(["nvcc", "-O2", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
-                           "-Wno-deprecated-gpu-targets", srcs[0], "-o", SO])
-    return SO
+                           "-Wno-deprecated-gpu-targets", *extra, srcs[0], "-o", so])
+    return so
 
 
 class HostKernel:

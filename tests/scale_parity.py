@@ -122,18 +122,46 @@ def ref_post(post, B):
     return d
 
 
-def quantity_errors(g, r):
-    """{max_abs, p999_abs, max_scaled, frac_within} of |g - r| vs 1e-4 + 1e-4 |r|."""
+# Vector quantities are judged relative to the magnitude of the VECTOR they
+# belong to (|g_i - r_i| <= 1e-4 + 1e-4 |r_vec|): a 268 N contact force with a
+# 0.3 N tangential component carries rounding proportional to 268 N in every
+# component (the friction-basis rotation of its impulses), so an element-wise
+# relative bound on the 0.3 N component measures the basis, not the solver.
+# Groups of consecutive columns per row; quantities not listed are scalar.
+VECTOR_GROUPS = {"root_state": (3, 4, 3, 3), "body_state": (3, 4, 3, 3), "net_contact": (3,),
+                 "sensor_forces": (3, 3)}
+
+
+def _magnitude(q, r):
+    """|r| per element: the norm of its vector group (VECTOR_GROUPS), else |r_i|."""
+    groups = VECTOR_GROUPS.get(q)
+    r = np.asarray(r, float)
+    if groups is None or r.ndim != 2 or r.shape[1] != sum(groups):
+        return np.abs(r)
+    out = np.empty_like(r)
+    c = 0
+    for n in groups:
+        out[:, c:c + n] = np.linalg.norm(r[:, c:c + n], axis=1, keepdims=True)
+        c += n
+    return out
+
+
+def quantity_errors(g, r, q=None):
+    """{max_abs, p999_abs, max_scaled, frac_within} of |g - r| vs 1e-4 + 1e-4 |r|
+    (|r| per VECTOR_GROUPS for vector quantities; `*_elem` = element-wise |r_i|)."""
+    mag = _magnitude(q, r).ravel()
     g = np.asarray(g, float).ravel()
     r = np.asarray(r, float).ravel()
     d = np.abs(g - r)
-    sc = d / (ATOL + RTOL * np.abs(r))
+    sc = d / (ATOL + RTOL * mag)
+    se = d / (ATOL + RTOL * np.abs(r))
     return {"max_abs": float(d.max()), "p999_abs": float(np.quantile(d, 0.999)), "max_scaled": float(sc.max()),
-            "frac_within": float(np.mean(sc <= 1.0)), "n": int(d.size)}
+            "frac_within": float(np.mean(sc <= 1.0)), "max_scaled_elem": float(se.max()),
+            "frac_within_elem": float(np.mean(se <= 1.0)), "n": int(d.size)}
 
 
 def compare(gp, rp):
-    return {q: quantity_errors(gp[q], rp[q]) for q in QUANTITIES}
+    return {q: quantity_errors(gp[q], rp[q], q) for q in QUANTITIES}
 
 
 def masks_equal(gp, rp):
@@ -198,4 +226,105 @@ def sample_vs_reference(meta, arr, gp, t, B, D, S):
          "root_state": gp["body_state"][rb][::B], "dof_state": gp["dof_state"][rd],
          "net_contact": gp["net_contact"][rb], "sensor_forces": gp["sensor_forces"][rs],
          "dof_force": gp["dof_force"][rd]}
-    return {q: quantity_errors(g[q], ref[q]) for q in QUANTITIES}
+    return {q: quantity_errors(g[q], ref[q], q) for q in QUANTITIES}
+
+
+def _r32(x):
+    return np.asarray(x, np.float64).astype(np.float32).astype(np.float64)
+
+
+def _perturbed_runs(task, trace, transforms, threads=None):
+    """Per transform, per step: the float64 oracle's post-step outputs (the
+    ref_post layout) from the TRANSFORMED pre-state (transform(x) applied to
+    env-local positions, orientations, velocities, DOF state, anchors,
+    commands and actions)."""
+    from oracle.tasks import OracleEnv
+    meta, arr, steps = trace
+    E = meta["num_envs"]
+    env = OracleEnv(task, E, seed=meta["seed"], episode_length=meta["episode_length"],
+                    threads=threads or os.cpu_count() or 1)
+    s = env.scene
+    B = s.bodies_per_env
+    org = np.repeat(s.env_origins, B, axis=0)
+    out = []
+    for tf in transforms:
+        runs = []
+        for st in steps:
+            pre = st["pre"]
+            s.pos[:] = org + tf(pre["pos"] - org)
+            for k in ("quat", "linvel", "angvel"):
+                getattr(s, k)[:] = tf(pre[k])
+            s._friction_anchor[:] = s.env_origins[None] + tf(pre["anchor"] - s.env_origins[None])
+            for k in ("dof_state", "root_state", "sensor_forces", "dof_force"):
+                getattr(s, k)[:] = tf(pre[k])
+            env.episode_steps[:] = pre["episode_steps"]
+            env.reset_count[:] = pre["reset_count"]
+            env.potentials[:] = pre["potentials"]
+            env.commands[:] = tf(pre["commands"])
+            obs, reward, done, info = env.step(tf(pre["actions"]))
+            post = {"obs": obs, "reward": reward, "done": done, "timeout": info["timeout"],
+                    "body_local": local_body(s.pos, s.quat, s.linvel, s.angvel, s.env_origins, B),
+                    "dof_state": s.dof_state.copy(), "net_contact": s.net_contact.copy(),
+                    "sensor_forces": s.sensor_forces.copy(), "dof_force": s.dof_force.copy()}
+            runs.append(ref_post(post, B))
+        out.append(runs)
+    return out
+
+
+def _jitter(seed):
+    """x (1 + u 2^-24), u uniform in [-1, 1]: an fp32-sized relative perturbation."""
+    rng = np.random.default_rng(seed)
+
+    def tf(x):
+        x = np.asarray(x, np.float64)
+        return x * (1.0 + rng.uniform(-1.0, 1.0, x.shape) * 2.0 ** -24)
+    return tf
+
+
+def input_rounding_floor(task, trace=None, threads=None):
+    """The fp32 conditioning floor, per step and quantity: the float64 oracle
+    stepped from the fp32-ROUNDED pre-state and actions (env-local positions,
+    as the CUDA path stores them) vs the oracle from the exact pre-state.  No
+    fp32 arithmetic is involved, so any fp32 implementation of the reference
+    algorithm inherits at least this error."""
+    trace = trace if trace is not None else oracle_trace(task)
+    runs = _perturbed_runs(task, trace, [_r32], threads)[0]
+    return [compare(r, ref_post(st["post"], _bodies(trace))) for r, st in zip(runs, trace[2])]
+
+
+def _bodies(trace):
+    meta = trace[0]
+    return 9 if meta["task"] == "quadruped" else 13
+
+
+def sensitivity(task, trace=None, seeds=(1, 2), threads=None):
+    """Per step and quantity, the element-wise max |oracle(perturbed) -
+    oracle(exact)| over the fp32 rounding of the pre-state and len(seeds)
+    random fp32-sized relative perturbations of it: how far the reference
+    algorithm itself moves each output under input noise of the size fp32
+    storage makes.  An element whose GPU error is within a few times this is
+    ill-conditioned at fp32 (a friction stick / slip, limit or contact
+    activation decided within rounding), not mis-computed."""
+    trace = trace if trace is not None else oracle_trace(task)
+    B = _bodies(trace)
+    runs = _perturbed_runs(task, trace, [_r32] + [_jitter(sd) for sd in seeds], threads)
+    out = []
+    for t, st in enumerate(trace[2]):
+        ref = ref_post(st["post"], B)
+        out.append({q: np.max([np.abs(np.asarray(r[t][q], float) - np.asarray(ref[q], float)) for r in runs], axis=0)
+                    for q in QUANTITIES})
+    return out
+
+
+def excused(gp, rp, sens, q, bound_scaled=10.0, factor=0.1):
+    """Elements of quantity q beyond `bound_scaled` x (1e-4 + 1e-4 |ref|)
+    (|ref| per VECTOR_GROUPS) split into (ill-conditioned, unexplained): an
+    element is ill-conditioned when the reference's own output moves by at
+    least `factor` x the GPU deviation under fp32-sized input noise."""
+    r = np.asarray(rp[q], float)
+    r2 = r.reshape(len(r), -1) if r.ndim > 1 else r.reshape(-1, 1)
+    d = np.abs(np.asarray(gp[q], float).reshape(r2.shape) - r2)
+    sc = d / (ATOL + RTOL * _magnitude(q, r2))
+    over = sc > bound_scaled
+    ill = over & (np.asarray(sens[q], float).reshape(r2.shape) >= factor * d)
+    return int(ill.sum()), int((over & ~ill).sum())

@@ -61,9 +61,10 @@ def test_env_step_teacher_forced(task, fixture, precision):
     meta, arr = load(fixture)
     env = _make(task, meta, precision)
     extra = "commands" if task == "quadruped-anymal-obs" else "potentials"
-    # fp32: the physics step carries the documented fp32 tolerance, and the
-    # progress reward differentiates positions at 1/control_dt = 60 Hz
-    otol, rtol_ = (1e-7, 1e-7) if precision == "fp64" else (2e-3, 2e-2)
+    # fp32 contract (tests/test_gpu_scale_parity.py): obs and reward >= 99.9 %
+    # within 1e-4 + 1e-4 |ref| and every element within 1e-3 + 1e-3 |ref|
+    otol = rtol_ = 1e-7 if precision == "fp64" else 1e-3
+    pooled = []
     n_resets = 0
     for t in range(meta["steps"]):
         _load_pre(env, arr, t, extra)
@@ -73,6 +74,8 @@ def test_env_step_teacher_forced(task, fixture, precision):
         assert np.array_equal(out.info["timeout"].cpu().numpy(), arr["timeout"][t])
         assert rel_err(out.obs.double().cpu().numpy(), arr["obs"][t], otol, otol) <= 1, (t, "obs")
         assert rel_err(out.reward.double().cpu().numpy(), arr["reward"][t], rtol_, rtol_) <= 1, (t, "reward")
+        for g, w in ((out.obs, arr["obs"][t]), (out.reward, arr["reward"][t])):
+            pooled.append((np.abs(g.double().cpu().numpy() - w) / (1e-4 + 1e-4 * np.abs(w))).ravel())
         n_resets += int(done.sum())
         if t + 1 < meta["steps"] and done.any():
             # the reset rows equal the reference's next pre-step state
@@ -86,6 +89,9 @@ def test_env_step_teacher_forced(task, fixture, precision):
             assert rel_err(getattr(env, extra).double().cpu().numpy(), arr["extra_before"][t + 1],
                            1e-6, 1e-6) <= 1
     assert n_resets > 0, "trace should exercise the auto-reset path"
+    if precision == "fp32":
+        frac = float(np.mean(np.concatenate(pooled) <= 1.0))
+        assert frac >= 0.999, (task, frac)
 
 
 def test_step_validates_actions():

@@ -7,9 +7,13 @@ reference produced.  Larger sizes are compared against the float64 C oracle.
 
 Tolerance contract:
   fp64 path: |gpu - ref| <= 1e-8 + 1e-8 |ref| for every element.
-  fp32 path: every element within 2e-3 + 2e-3 |ref| (fp32 conditioning of the
-             1/h-scaled TGS bias), >= 99% of elements within the north-star
-             1e-4 + 1e-4 |ref|; contact-active masks bit-exact.
+  fp32 path, PER QUANTITY (|ref| = the norm of the element's vector for the
+  vector quantities, tests/scale_parity.py VECTOR_GROUPS):
+    states (root / body / DOF state): >= 99.9 % of the elements within the
+      north-star 1e-4 + 1e-4 |ref| and every element within 1e-3 + 1e-3 |ref|;
+    contact force, sensors, DOF force (impulses / dt: 120x the velocity
+      rounding): every element within 1e-3 + 1e-3 |ref|;
+  contact-active masks, poison flags and friction-anchor presence bit-exact.
 """
 
 import numpy as np
@@ -19,9 +23,12 @@ import torch
 from golden_util import (build_models, gpu_outputs, gpu_scene_from_fixture, load, load_gpu_state,
                          physics_cases, rel_err, sim_params)
 
+import scale_parity as SP
+
 pytestmark = pytest.mark.gpu
 
 OUTS = ("root_state", "body_state", "dof_state", "net_contact", "dof_force", "sensor_forces")
+STATES = ("root_state", "body_state", "dof_state")
 
 
 def _poisoned_rows(meta, arr, t, key, B, D, S, A):
@@ -40,8 +47,7 @@ def _poisoned_rows(meta, arr, t, key, B, D, S, A):
 def test_step_matches_reference_teacher_forced(case, precision):
     meta, arr = load(case)
     s = gpu_scene_from_fixture(meta, arr, precision)
-    tol = 1e-8 if precision == "fp64" else 2e-3
-    within, total = 0, 0
+    pooled = {k: [] for k in OUTS}
     for t in range(meta["steps"]):
         load_gpu_state(s, arr, t)
         s.step()
@@ -52,16 +58,26 @@ def test_step_matches_reference_teacher_forced(case, precision):
             keep = ~_poisoned_rows(meta, arr, t, k, s.bodies_per_env, s.dofs_per_env,
                                    s.sensors_per_env, s.actors_per_env)
             g, w = got[k][keep], want[keep]
-            e = rel_err(g, w, tol, tol)
-            assert e <= 1.0, (case, precision, t, k, e)
-            if precision == "fp32":
-                d = np.abs(g - w) / (1e-4 + 1e-4 * np.abs(w))
-                within += int((d <= 1.0).sum())
-                total += d.size
+            if precision == "fp64":
+                e = rel_err(g, w, 1e-8, 1e-8)
+                assert e <= 1.0, (case, precision, t, k, e)
+            elif g.size:
+                d = np.where(np.isnan(g) & np.isnan(w), 0.0, np.abs(g - w)).reshape(len(w), -1)
+                pooled[k].append(d / (1e-4 + 1e-4 * SP._magnitude(k, w.reshape(len(w), -1))))
         a = got["_friction_anchor"]
         assert np.array_equal(np.isnan(a), np.isnan(arr["out__friction_anchor"][t])), (case, t)
     if precision == "fp32":
-        assert within >= 0.99 * total, (case, within / total)
+        stats = {}
+        for k, ds in pooled.items():
+            if ds:
+                sc = np.concatenate([x.ravel() for x in ds])
+                stats[k] = (float(np.mean(sc <= 1.0)), float(sc.max() / 10.0))
+        print(case, {k: (round(f, 5), round(m, 3)) for k, (f, m) in stats.items()})
+        for k, (frac, max_1e3) in stats.items():
+            if k in STATES:
+                assert frac >= 0.999 and max_1e3 <= 1.0, (case, k, frac, max_1e3)
+            else:
+                assert max_1e3 <= 1.0, (case, k, max_1e3)
 
 
 @pytest.mark.parametrize("precision", ["fp64", "fp32"])
@@ -112,7 +128,7 @@ def test_step_matches_oracle_4096_envs(precision):
     ref, gpu, rng = _oracle_pair(4096, precision)
     E, B = 4096, gpu.bodies_per_env
     be = np.repeat(np.arange(E), B)
-    tol = 1e-8 if precision == "fp64" else 2e-3
+    pooled = {k: [] for k in OUTS}
     for t in range(4):
         tgt = rng.uniform(-0.6, 0.6, ref.num_dofs)
         ref.ctrl_dof_pos_target[:] = tgt
@@ -125,8 +141,21 @@ def test_step_matches_oracle_4096_envs(precision):
         gpu.step()
         got = gpu_outputs(gpu)
         for k in OUTS:
-            e = rel_err(got[k], getattr(ref, k), tol, tol)
-            assert e <= 1.0, (precision, t, k, e)
+            want = getattr(ref, k)
+            if precision == "fp64":
+                e = rel_err(got[k], want, 1e-8, 1e-8)
+                assert e <= 1.0, (precision, t, k, e)
+            else:
+                w = want.reshape(len(want), -1)
+                pooled[k].append(np.abs(got[k].reshape(len(w), -1) - w) / (1e-4 + 1e-4 * SP._magnitude(k, w)))
+    for k, ds in pooled.items():     # fp32: the per-quantity contract of the module docstring
+        if ds:
+            sc = np.concatenate([x.ravel() for x in ds])
+            frac, max_1e3 = float(np.mean(sc <= 1.0)), float(sc.max() / 10.0)
+            if k in STATES:
+                assert frac >= 0.999 and max_1e3 <= 1.0, (k, frac, max_1e3)
+            else:
+                assert max_1e3 <= 1.0, (k, max_1e3)
 
 
 def test_determinism_bitwise():
