@@ -54,20 +54,33 @@ template <class R> BS_HD void fk_env(const Ctx<R> &c, int e, uint32_t amask) {
 }
 
 // repack body_state/root_state rows of the masked actors (buffers.py:109-123)
+// The four arrays are distinct allocations (__restrict__): without it every
+// load of the element-wise copy had to wait behind the previous element's
+// store (may-alias), i.e. one L2 round trip per element of the env's rows --
+// the auto-reset's dominant latency.
 template <class R> BS_HD void repack_env(const Ctx<R> &c, int e, uint32_t amask) {
     const Dims &d = c.d;
-    const R *o = c.s.env_origins + 3 * (size_t)e;
+    const R *__restrict__ o = c.s.env_origins + 3 * (size_t)e;
+    const R ox = o[0], oy = o[1], oz = o[2];
     for (int a = 0; a < d.A; ++a) {
         if (!((amask >> a) & 1u)) continue;
         int b0 = c.L.actor_body_offset[a], b1 = c.L.actor_body_offset[a + 1];
-        for (int b = b0; b < b1; ++b) {
-            const R *src = c.s.body_q + 13 * ((size_t)e * d.B + b);
-            R *dst = c.s.body_state + 13 * ((size_t)e * d.B + b);
-            for (int k = 0; k < 13; ++k) dst[k] = k < 3 ? src[k] + o[k] : src[k];
+        const R *__restrict__ src = c.s.body_q + 13 * ((size_t)e * d.B + b0);
+        R *__restrict__ dst = c.s.body_state + 13 * ((size_t)e * d.B + b0);
+        R *__restrict__ rr = c.s.root_state + 13 * ((size_t)e * d.A + a);
+#pragma unroll 3
+        for (int b = 0; b < b1 - b0; ++b) {   // a whole 13-word row per batch of independent loads
+            R v[13];
+#pragma unroll
+            for (int k = 0; k < 13; ++k) v[k] = src[13 * b + k];
+            v[0] += ox; v[1] += oy; v[2] += oz;
+#pragma unroll
+            for (int k = 0; k < 13; ++k) dst[13 * b + k] = v[k];
+            if (b == 0) {
+#pragma unroll
+                for (int k = 0; k < 13; ++k) rr[k] = v[k];
+            }
         }
-        const R *rb = c.s.body_state + 13 * ((size_t)e * d.B + b0);
-        R *rr = c.s.root_state + 13 * ((size_t)e * d.A + a);
-        for (int k = 0; k < 13; ++k) rr[k] = rb[k];
     }
 }
 

@@ -839,3 +839,12 @@ int bsim_collide_f64(const bsim_layout_t *l, const bsim_params64_t *p, const bsi
 
 }  // extern "C"
 #endif  // BSIM_LARGE_TU
+
+#if defined(BSIM_EXP_RESET_CLOCKS) && !defined(BSIM_LARGE_TU)
+// timing experiment only (tools/reset_clocks.py): read and clear the reset phase counters
+extern "C" int bsim_exp_reset_clocks(unsigned long long *out8) {
+    if (cudaMemcpyFromSymbol(out8, bsim::bsim_reset_clk, sizeof(unsigned long long) * 8) != cudaSuccess) return -1;
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    return cudaMemcpyToSymbol(bsim::bsim_reset_clk, z, sizeof(z)) == cudaSuccess ? 0 : -1;
+}
+#endif

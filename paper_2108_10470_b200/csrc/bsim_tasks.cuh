@@ -132,12 +132,32 @@ template <class R> __device__ void cube_new_goal(const Ctx<R> &c, const TaskView
 // ------------------------------------------------------------ reset
 // EnvBatch.reset for one env (envs.py:145-166) with the task's _reset_envs
 // (404-419 / 517-531) and _post_reset (385-397 / 506-515).
+#if defined(BSIM_EXP_RESET_CLOCKS) && defined(__CUDACC__)
+// timing experiment only: cycles per reset phase summed over all resets ([7] = count)
+__device__ unsigned long long bsim_reset_clk[8];
+#define BSIM_RCLK(i)                                              \
+    do {                                                          \
+        unsigned long long t_ = clock64();                        \
+        atomicAdd(&bsim_reset_clk[i], t_ - t_prev_);              \
+        t_prev_ = t_;                                             \
+    } while (0)
+#else
+#define BSIM_RCLK(i) \
+    do {             \
+    } while (0)
+#endif
+
 template <class R> __device__ void task_reset_env(const Ctx<R> &c, const TaskView<R> &tv, int e) {
+#if defined(BSIM_EXP_RESET_CLOCKS) && defined(__CUDACC__)
+    unsigned long long t_prev_ = clock64();
+    atomicAdd(&bsim_reset_clk[7], 1ull);
+#endif
     const bsim_task_t &t = tv.t;
     const Dims &d = c.d;
     if (c.s.nonfinite[e]) c.s.nonfinite[e] = 0;   // clear_nonfinite (physics.py:1090)
     const int64_t step_count = t.step_count_dev ? *t.step_count_dev : t.step_count;
     dr_randomize_env(c, t.dr, e, step_count);     // randomizer.randomize (envs.py:154-155)
+    BSIM_RCLK(0);
     const uint32_t genv = (uint32_t)(c.L.env_offset + e);
     uint32_t key[4] = {t.seed, genv, (uint32_t)t.reset_count[e], 0xCu};
     NpRng rng = np_rng(key, 3);
@@ -165,13 +185,17 @@ template <class R> __device__ void task_reset_env(const Ctx<R> &c, const TaskVie
             dof[2 * k + 1] = R(0);
         }
     }
+    BSIM_RCLK(1);
     if (t.obs_noise) {  // per-episode correlated noise continues the reset stream (envs.py:161-164)
         R *cn = reinterpret_cast<R *>(t.corr_noise) + (size_t)e * t.obs_dim;
         for (int k = 0; k < t.obs_dim; ++k)
             cn[k] = t.obs_noise_corr > 0.0 ? R(0.0 + t.obs_noise_corr * np_std_normal(rng)) : R(0);
     }
+    BSIM_RCLK(2);
     fk_env(c, e, 0xffffffffu);
+    BSIM_RCLK(3);
     repack_env(c, e, 0xffffffffu);
+    BSIM_RCLK(4);
     t.episode_steps[e] = 0;
     t.reset_count[e] += 1;
     R *a = tv.act(e);
@@ -188,6 +212,7 @@ template <class R> __device__ void task_reset_env(const Ctx<R> &c, const TaskVie
         R *cmd = tv.cmd(e);
         for (int k = 0; k < 3; ++k) cmd[k] = R(np_uniform(cr, -1.0, 1.0));
     }
+    BSIM_RCLK(5);
 }
 
 // ------------------------------------------------------------ group form
