@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define BSIM_ABI_VERSION 1
+#define BSIM_ABI_VERSION 2
 
 enum bsim_status {
     BSIM_OK = 0,
@@ -84,6 +84,8 @@ typedef struct bsim_layout_t {
             planes_per_env, pairs_per_env, sensors_per_env, tendons_per_env, env_offset;
     int32_t topology_id;   /* 0 = generic; k > 0 = the AOT-specialised topology k
                               (paper_2108_10470_b200/csrc/bsim_topologies.cuh) */
+    int32_t sched_stages, sched_width;     /* the Gauss-Seidel row schedule below (0 = none:
+                                              one lane per env in reference order) */
     const void *joints;                    /* [J]    */
     const int32_t *plane_body;             /* [P]    */
     const int32_t *pair_body;              /* [Q][2] */
@@ -96,6 +98,14 @@ typedef struct bsim_layout_t {
     const int32_t *pair_kind;              /* [Q] BSIM_PAIR_* */
     const void *pair_ext;                  /* [Q][4] real: PB box half extents of b; PC (0, hh_b);
                                               CC (hh_a, hh_b); SS unused */
+    const int32_t *sweep_sched;            /* [sched_stages][sched_width] rows of one solver pass
+                                              (physics.py:760-775): r < J joint r, r < J + P plane
+                                              slot r - J, else pair slot r - J - P; -1 = idle lane.
+                                              Rows of one stage touch disjoint bodies, and every
+                                              row comes after each earlier row (reference order)
+                                              that shares a body with it, so running a stage's rows
+                                              side by side gives the reference's sequential result
+                                              (paper_2108_10470_b200/layout.py sweep_schedule). */
 } bsim_layout_t;
 
 /* Pair-slot narrow phase kinds.  SS is the reference's only pair type

@@ -83,9 +83,10 @@ class Params64(C.Structure):
 
 LAYOUT_INTS = ("num_envs", "actors_per_env", "bodies_per_env", "dofs_per_env", "joints_per_env",
                "planes_per_env", "pairs_per_env", "sensors_per_env", "tendons_per_env", "env_offset",
-               "topology_id")
+               "topology_id", "sched_stages", "sched_width")
 LAYOUT_PTRS = ("joints", "plane_body", "pair_body", "sensor_body", "actor_body_offset",
-               "actor_dof_offset", "tendons", "tendon_elems", "spatial_paths", "pair_kind", "pair_ext")
+               "actor_dof_offset", "tendons", "tendon_elems", "spatial_paths", "pair_kind", "pair_ext",
+               "sweep_sched")
 
 
 class Layout(C.Structure):
@@ -167,7 +168,7 @@ def lib():
         _declare(_lib)
         from . import _tasks_native  # noqa: F401  (declares the task / reward entry points)
         _tasks_native.declare(_lib)
-        if _lib.bsim_abi_version() != 1:
+        if _lib.bsim_abi_version() != 2:
             raise NativeError("ABI version mismatch")
     return _lib
 

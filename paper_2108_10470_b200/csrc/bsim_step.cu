@@ -119,6 +119,17 @@ __device__ __noinline__ void task_step_env_call(const Ctx<R> &c, const bsim_task
 // number of waves of resident CTAs (148 SMs x CTAs/SM).  The grid covers envs
 // [e_begin, e_end) -- all of them, or one wave-sized chunk of the pipelined
 // host-buffer step (bsim_env_step_range).
+#ifdef BSIM_EXP_PHASE_CLOCKS
+// timing experiment only: thread-0 cycles per step_kernel phase summed over CTAs ([7] = CTAs),
+// and per CTA of the last launch: SM id, %globaltimer at entry, before the task tail, at exit
+__device__ unsigned long long g_phase_clk[8];
+__device__ unsigned long long g_cta_times[4096][4];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
 template <class R, class T>
 __global__ void __launch_bounds__(Shape<R>::NTH, BSIM_MINB)
     step_kernel(const __grid_constant__ Ctx<R> c, int n_substeps, bsim_actions_t act, int epc, int e_begin,
@@ -129,6 +140,26 @@ __global__ void __launch_bounds__(Shape<R>::NTH, BSIM_MINB)
     R *ws = reinterpret_cast<R *>(smem_raw);
     const int tid = threadIdx.x;
     const int e0 = e_begin + blockIdx.x * epc;   // envs [e_begin, e_end) of the scene's E
+#ifdef BSIM_EXP_PHASE_CLOCKS
+    unsigned long long pc_prev = clock64();
+    if (tid == 0) atomicAdd(&g_phase_clk[7], 1ull);
+    if (tid == 0 && blockIdx.x < 4096) {
+        g_cta_times[blockIdx.x][0] = hw_sm_id();
+        g_cta_times[blockIdx.x][1] = gtimer();
+    }
+#define BSIM_PCLK(i)                                                             \
+    do {                                                                         \
+        if (tid == 0) {                                                          \
+            unsigned long long t_ = clock64();                                   \
+            atomicAdd(&g_phase_clk[i], t_ - pc_prev);                            \
+            pc_prev = t_;                                                        \
+        }                                                                        \
+    } while (0)
+#else
+#define BSIM_PCLK(i) \
+    do {             \
+    } while (0)
+#endif
     const int ne = min(epc, e_end - e0);
     const int per_env = 13 * d.B;
     constexpr int NW = NTH / 32;
@@ -159,6 +190,7 @@ __global__ void __launch_bounds__(Shape<R>::NTH, BSIM_MINB)
     __syncthreads();
     const Grp<R> g{ws, e0, ne, tid, NTH, 32 * s_sweep_warp, d.pad,
                    JTab<R>{smem_raw + step_ws_bytes<R>(d, epc), jtab_stride_smem<R>()}};
+    BSIM_PCLK(0);
     stage_group(c, g);
     if (act.actions) {  // fused action mapping (envs.py:180, 421-424)
         BS_ITEMS(g, d.D, el, k) {
@@ -173,6 +205,7 @@ __global__ void __launch_bounds__(Shape<R>::NTH, BSIM_MINB)
         }
     }
     __syncthreads();
+    BSIM_PCLK(1);
     for (int s = 0; s < n_substeps; ++s) {
         group_step<R, T>(c, g, s == n_substeps - 1, s);
         if (d.T && s != n_substeps - 1) {  // fixed tendons read dof_state next substep
@@ -180,6 +213,7 @@ __global__ void __launch_bounds__(Shape<R>::NTH, BSIM_MINB)
             __syncthreads();
         }
     }
+    BSIM_PCLK(2);
     readout_group(c, g);
     BS_ITEMS(g, d.P, el, i) {
         for (int k = 0; k < 3; ++k)
@@ -211,15 +245,30 @@ __global__ void __launch_bounds__(Shape<R>::NTH, BSIM_MINB)
     if (tid == 0 && s_sweep_bit) atomicAnd(&g_sweep_smsp[s_sm_slot], ~s_sweep_bit);
     if (with_task) {   // EnvBatch.step tail for this CTA's envs (bsim_env_step)
         __syncthreads();   // the CTA's state stores above are visible; the workspace is dead
+        BSIM_PCLK(3);
+#ifdef BSIM_EXP_PHASE_CLOCKS
+        if (tid == 0 && blockIdx.x < 4096) g_cta_times[blockIdx.x][2] = gtimer();
+#endif
         // observation rows are staged in the dead workspace and leave as one
         // coalesced block (task.obs may be mapped host memory: bsim_env_step_host
         // zero-copy mode, where a scattered row store would be a PCIe write each)
         R *stage = ws;
+#ifndef BSIM_EXP_SKIP_TAIL   // timing experiment only: the launch without the tail's work
         if (tid < BSIM_TASK_G * ne) task_step_env_call(c, task, stage, e0, e0 + tid / BSIM_TASK_G, tid % BSIM_TASK_G);
+#endif
         __syncthreads();
+        BSIM_PCLK(4);
         R *dst = reinterpret_cast<R *>(task.obs) + (size_t)e0 * task.obs_dim;
         for (int i = tid; i < ne * task.obs_dim; i += NTH) dst[i] = stage[i];
+        BSIM_PCLK(5);
     }
+#ifdef BSIM_EXP_PHASE_CLOCKS
+    if (tid == 0 && blockIdx.x < 4096) {
+        if (!with_task) g_cta_times[blockIdx.x][2] = gtimer();
+        g_cta_times[blockIdx.x][3] = gtimer();
+    }
+#endif
+#undef BSIM_PCLK
 }
 
 template <class R>
@@ -846,5 +895,17 @@ extern "C" int bsim_exp_reset_clocks(unsigned long long *out8) {
     if (cudaMemcpyFromSymbol(out8, bsim::bsim_reset_clk, sizeof(unsigned long long) * 8) != cudaSuccess) return -1;
     unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     return cudaMemcpyToSymbol(bsim::bsim_reset_clk, z, sizeof(z)) == cudaSuccess ? 0 : -1;
+}
+#endif
+
+#if defined(BSIM_EXP_PHASE_CLOCKS) && !defined(BSIM_LARGE_TU)
+// timing experiment only (tools/phase_clocks.py): read and clear the step_kernel phase counters
+extern "C" int bsim_exp_phase_clocks(unsigned long long *out8) {
+    if (cudaMemcpyFromSymbol(out8, g_phase_clk, sizeof(unsigned long long) * 8) != cudaSuccess) return -1;
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    return cudaMemcpyToSymbol(g_phase_clk, z, sizeof(z)) == cudaSuccess ? 0 : -1;
+}
+extern "C" int bsim_exp_cta_times(unsigned long long *out) {   // [4096][4]
+    return cudaMemcpyFromSymbol(out, g_cta_times, sizeof(unsigned long long) * 4096 * 4) == cudaSuccess ? 0 : -1;
 }
 #endif

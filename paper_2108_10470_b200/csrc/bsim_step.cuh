@@ -1061,6 +1061,66 @@ template <class R> BS_HD void sweep(const Ctx<R> &c, const Ws<R> &w, R h, bool b
         for (int b = 0; b < d.B; ++b) accumulate_deltas(d, w, b, load_bv(d, w, b), h);
 }
 
+// One pass on the layout's row schedule (SceneLayout.sweep_schedule): stage
+// by stage, lane l of the env runs row sched[s][l] on the body velocities in
+// shared memory.  Rows of a stage touch disjoint bodies and every row follows
+// each earlier row it shares a body with, so the result is the sequential
+// sweep's (rows on disjoint bodies commute: same arithmetic, same values).
+// `lane` in [0, lanes) indexes the env's threads; the stage loop runs on
+// every thread of the CTA (uniform trip count) and __syncwarp(mask) orders a
+// stage's shared-memory writes before the next stage's reads.
+template <class R>
+BS_HD void sched_row(const Ctx<R> &c, const Ws<R> &w, int r, R h, bool biased) {
+    const Dims &d = c.d;
+    if (r < d.J) {
+        const auto &jt = c.joints[r];
+        BV<R> C = load_bv(d, w, jt.child), P = load_bv(d, w, jt.parent);
+        joint_rows(c, w, r, jt.kind, jt.dof, jt.has_limits != 0, jt.parent, jt.child, h, biased, C, P);
+        store_bv(d, w, jt.child, C);
+        store_bv(d, w, jt.parent, P);
+    } else if (r < d.J + d.P) {
+        const int i = r - d.J, b = c.L.plane_body[i];
+        BV<R> X = load_bv(d, w, b);
+        row_plane(c, w, i, X);
+        store_bv(d, w, b, X);
+    } else {
+        const int i = r - d.J - d.P, pa = c.L.pair_body[2 * i], pb = c.L.pair_body[2 * i + 1];
+        BV<R> A = load_bv(d, w, pa), X = load_bv(d, w, pb);
+        row_pair(c, w, i, A, X);
+        store_bv(d, w, pa, A);
+        store_bv(d, w, pb, X);
+    }
+}
+#if defined(__CUDA_ARCH__)
+template <class R>
+__device__ void sweep_sched(const Ctx<R> &c, const Ws<R> *w, R h, bool biased, int lane, int lanes, unsigned mask) {
+    const Dims &d = c.d;
+    const int S = c.L.sched_stages, W = c.L.sched_width;
+    for (int s = 0; s < S; ++s) {
+        if (w)
+            for (int i = lane; i < W; i += lanes) {   // a stage's rows are independent: any lane may take any
+                const int r = __ldg(c.L.sweep_sched + s * W + i);
+                if (r >= 0) sched_row(c, *w, r, h, biased);
+            }
+        __syncwarp(mask);
+    }
+    if (biased && w)
+        for (int b = lane; b < d.B; b += lanes) accumulate_deltas(d, *w, b, load_bv(d, *w, b), h);
+}
+#else
+template <class R> void sweep_sched_host(const Ctx<R> &c, const Ws<R> &w, R h, bool biased) {
+    const Dims &d = c.d;
+    const int S = c.L.sched_stages, W = c.L.sched_width;
+    for (int s = 0; s < S; ++s)
+        for (int l = 0; l < W; ++l) {
+            const int r = c.L.sweep_sched[s * W + l];
+            if (r >= 0) sched_row(c, w, r, h, biased);
+        }
+    if (biased)
+        for (int b = 0; b < d.B; ++b) accumulate_deltas(d, w, b, load_bv(d, w, b), h);
+}
+#endif
+
 // The same pass with the topology known at compile time (T = a generated
 // bsim_topologies.cuh entry): every body velocity of the env stays in
 // registers for the whole pass and rows on disjoint bodies can overlap.
@@ -1502,7 +1562,27 @@ template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> 
             } else
 #endif
             {
-                BS_ENVS(g, el) { sweep_any<R, T>(c, g.env(el), h, biased); }
+#if defined(__CUDA_ARCH__)
+                if (!topo_register_sweep<T>() && c.L.sched_stages > 0) {
+                    // the row schedule on the claimed sweep warp: 32 / NE lanes per env (the
+                    // CTA's envs share one warp, as the one-lane sweep did, so the issue
+                    // cost stays one warp's while a stage's rows run side by side)
+                    constexpr int NE = Shape<R>::NE, LPE = NE >= 32 ? 1 : 32 / NE;
+                    const int t = (g.tid - g.lane0 + g.nth) % g.nth;
+                    if (t < 32) {
+                        const int el = t / LPE, lane = t % LPE;
+                        const Ws<R> w = g.env(el);
+                        sweep_sched<R>(c, el < g.ne ? &w : nullptr, h, biased, lane, LPE, 0xffffffffu);
+                    }
+                } else
+#else
+                if (!topo_register_sweep<T>() && c.L.sched_stages > 0) {
+                    BS_ENVS(g, el) { sweep_sched_host<R>(c, g.env(el), h, biased); }
+                } else
+#endif
+                {
+                    BS_ENVS(g, el) { sweep_any<R, T>(c, g.env(el), h, biased); }
+                }
             }
             BS_SYNC();
         }

@@ -252,6 +252,7 @@ __device__ R quad_reward_g(const Ctx<R> &c, const TaskView<R> &tv, int e, int sl
     const R *a = tv.act(e);
     const R *dof = c.s.dof_state + 2 * (size_t)e * c.d.D;
     R sa = R(0), se = R(0), near_ = R(0);
+    #pragma unroll 4
     for (int k = sl; k < tv.t.act_dim; k += G) {
         sa = sa + a[k] * a[k];
         se = se + a[k] * R(1) * dof[2 * k + 1];
@@ -276,7 +277,7 @@ __device__ R quad_reward_g(const Ctx<R> &c, const TaskView<R> &tv, int e, int sl
 // 60-dim observation (envs.py:441-461)
 template <class R, int G> __device__ void quad_obs_g(const Ctx<R> &c, const TaskView<R> &tv, int e, int sl) {
     Root<R> r = root_of(c, e);
-    R *o = tv.obs(e);
+    R *__restrict__ o = tv.obs(e);   // the obs row aliases no input: loads may run ahead of the stores
     if (sl == 0) {
         Frame<R> f = quad_frame(r);
         R x = r.q.x, y = r.q.y, z = r.q.z, w = r.q.w;
@@ -291,13 +292,16 @@ template <class R, int G> __device__ void quad_obs_g(const Ctx<R> &c, const Task
     }
     const int A = tv.t.act_dim, S = c.d.S;
     const R *dof = c.s.dof_state + 2 * (size_t)e * c.d.D;
+    #pragma unroll 4
     for (int k = sl; k < A; k += G) {
         o[12 + k] = R(2) * (dof[2 * k] - tv.lo(k)) / (tv.hi(k) - tv.lo(k)) - R(1);
         o[12 + A + k] = dof[2 * k + 1] * R(0.05);
     }
     const R *sf = c.s.sensor_forces + 6 * (size_t)e * S;
+    #pragma unroll 4
     for (int k = sl; k < 6 * S; k += G) o[12 + 2 * A + k] = sf[k] * R(0.01);
     const R *a = tv.act(e);
+    #pragma unroll 4
     for (int k = sl; k < A; k += G) o[12 + 2 * A + 6 * S + k] = a[k];
 }
 
@@ -311,6 +315,7 @@ __device__ R anymal_reward_g(const Ctx<R> &c, const TaskView<R> &tv, int e, int 
     R err_xy = ex * ex + ey * ey, err_yaw = ez * ez;
     R tq = R(0);
     const R *df = c.s.dof_force + (size_t)e * c.d.D;
+    #pragma unroll 4
     for (int k = sl; k < tv.t.act_dim; k += G) tq = tq + df[k] * df[k];
     tq = group_sum<G>(tq);
     R rew = R(1) * dt * exp_r(-err_xy / R(0.25)) + R(0.5) * dt * exp_r(-err_yaw / R(0.25)) - R(0.00002) * dt * tq;
@@ -322,7 +327,7 @@ __device__ R anymal_reward_g(const Ctx<R> &c, const TaskView<R> &tv, int e, int 
 // 48-dim observation (envs.py:538-550)
 template <class R, int G> __device__ void anymal_obs_g(const Ctx<R> &c, const TaskView<R> &tv, int e, int sl) {
     Root<R> r = root_of(c, e);
-    R *o = tv.obs(e);
+    R *__restrict__ o = tv.obs(e);   // the obs row aliases no input: loads may run ahead of the stores
     if (sl == 0) {
         V3<R> lin_b = rot_inv(r.q, r.v), ang_b = rot_inv(r.q, r.w), gb = rot_inv(r.q, v3(R(0), R(0), R(-1)));
         o[0] = lin_b.x; o[1] = lin_b.y; o[2] = lin_b.z;
@@ -333,11 +338,13 @@ template <class R, int G> __device__ void anymal_obs_g(const Ctx<R> &c, const Ta
     }
     const int A = tv.t.act_dim;
     const R *dof = c.s.dof_state + 2 * (size_t)e * c.d.D;
+    #pragma unroll 4
     for (int k = sl; k < A; k += G) {
         o[12 + k] = dof[2 * k];
         o[12 + A + k] = dof[2 * k + 1] * R(0.05);
     }
     const R *a = tv.act(e);
+    #pragma unroll 4
     for (int k = sl; k < A; k += G) o[12 + 2 * A + k] = a[k];
 }
 
@@ -354,6 +361,7 @@ __device__ R cube_reward_g(const Ctx<R> &c, const TaskView<R> &tv, int e, int sl
     R rd = R(2) * asin(nn);                   // rot_dist (spatial.py:125-132)
     const R *a = tv.act(e);
     R sa = R(0);
+    #pragma unroll 4
     for (int k = sl; k < tv.t.act_dim; k += G) sa = sa + a[k] * a[k];
     sa = group_sum<G>(sa);
     R rew = gd * R(-10.0) + (R(1) / (fabs(rd) + R(0.1))) * R(1.0) + sa * R(-0.0002);
@@ -366,8 +374,9 @@ __device__ R cube_reward_g(const Ctx<R> &c, const TaskView<R> &tv, int e, int sl
 // cube task observation (layout in include/batchsim_b200.h, BSIM_TASK_CUBE)
 template <class R, int G> __device__ void cube_obs_g(const Ctx<R> &c, const TaskView<R> &tv, int e, int sl) {
     const int D = c.d.D, A = tv.t.act_dim;
-    R *o = tv.obs(e);
+    R *__restrict__ o = tv.obs(e);   // the obs row aliases no input: loads may run ahead of the stores
     const R *dof = c.s.dof_state + 2 * (size_t)e * D;
+    #pragma unroll 4
     for (int k = sl; k < D; k += G) {
         R lo = tv.lo(k), hi = tv.hi(k), q = dof[2 * k];
         o[k] = finite_r(lo) && finite_r(hi) ? R(2) * (q - lo) / (hi - lo) - R(1) : q;
@@ -375,7 +384,7 @@ template <class R, int G> __device__ void cube_obs_g(const Ctx<R> &c, const Task
     }
     if (sl == 0) {
         const R *cb = cube_row(c, e), *g = tv.goal(e);
-        R *p = o + 2 * D;
+        R *__restrict__ p = o + 2 * D;
         for (int k = 0; k < 10; ++k) p[k] = cb[k];
         for (int k = 10; k < 13; ++k) p[k] = cb[k] * R(0.2);
         for (int k = 0; k < 7; ++k) p[13 + k] = g[k];
@@ -383,6 +392,7 @@ template <class R, int G> __device__ void cube_obs_g(const Ctx<R> &c, const Task
         p[20] = dq.x; p[21] = dq.y; p[22] = dq.z; p[23] = dq.w;
     }
     const R *a = tv.act(e);
+    #pragma unroll 4
     for (int k = sl; k < A; k += G) o[2 * D + 24 + k] = a[k];
 }
 
@@ -416,8 +426,9 @@ template <class R> __device__ R stack_reward(const Ctx<R> &c, int e, bool &done)
 // stacking observation (layout in include/batchsim_b200.h, BSIM_TASK_STACK)
 template <class R, int G> __device__ void stack_obs_g(const Ctx<R> &c, const TaskView<R> &tv, int e, int sl) {
     const int D = c.d.D, A = tv.t.act_dim, B = c.d.B;
-    R *o = tv.obs(e);
+    R *__restrict__ o = tv.obs(e);   // the obs row aliases no input: loads may run ahead of the stores
     const R *dof = c.s.dof_state + 2 * (size_t)e * D;
+    #pragma unroll 4
     for (int k = sl; k < D; k += G) {
         R lo = tv.lo(k), hi = tv.hi(k), q = dof[2 * k];
         o[k] = finite_r(lo) && finite_r(hi) ? R(2) * (q - lo) / (hi - lo) - R(1) : q;
@@ -425,7 +436,7 @@ template <class R, int G> __device__ void stack_obs_g(const Ctx<R> &c, const Tas
     }
     if (sl == 0) {
         const R *h = body_row(c, e, B - 5), *a = body_row(c, e, B - 2), *b = body_row(c, e, B - 1);
-        R *p = o + 2 * D;
+        R *__restrict__ p = o + 2 * D;
         for (int k = 0; k < 7; ++k) p[k] = h[k];
         for (int k = 0; k < 7; ++k) p[7 + k] = a[k];
         for (int k = 0; k < 3; ++k) p[14 + k] = a[k] - h[k];
@@ -433,6 +444,7 @@ template <class R, int G> __device__ void stack_obs_g(const Ctx<R> &c, const Tas
         for (int k = 0; k < 3; ++k) p[24 + k] = a[k] - b[k];
     }
     const R *a = tv.act(e);
+    #pragma unroll 4
     for (int k = sl; k < A; k += G) o[2 * D + 27 + k] = a[k];
 }
 
@@ -445,7 +457,7 @@ template <class R, int G> __device__ void task_obs_g(const Ctx<R> &c, const Task
     if (t.obs_noise) {  // perturb_observations (randomize.py:231-237): one sequential stream per env
         __syncwarp(group_mask<G>());
         if (sl == 0) {
-            R *o = tv.obs(e);
+            R *__restrict__ o = tv.obs(e);   // the obs row aliases no input: loads may run ahead of the stores
             const R *cn = reinterpret_cast<const R *>(t.corr_noise) + (size_t)e * t.obs_dim;
             if (t.obs_noise_uncorr > 0.0) {
                 uint32_t key[4] = {t.seed, 0xE7u, (uint32_t)(c.L.env_offset + e), (uint32_t)t.noise_count[e]};

@@ -8,6 +8,8 @@ from __future__ import annotations
 
 import ctypes as C
 
+import os
+
 import numpy as np
 
 from . import _native as N
@@ -68,7 +70,17 @@ def pack_tables(L: SceneLayout, fp64: bool = False):
         "pair_kind": np.ascontiguousarray(L.pair_kind, np.int32) if L.pairs_per_env else np.zeros(1, np.int32),
         "pair_ext": (np.ascontiguousarray(L.pair_ext, np.float64 if fp64 else np.float32).reshape(-1)
                      if L.pairs_per_env else np.zeros(4, np.float64 if fp64 else np.float32)),
+        "sweep_sched": sched_table(L),
     }
+
+
+def sched_table(L: SceneLayout):
+    """[stages][width] int32 row ids of SceneLayout.sweep_schedule, -1 padded."""
+    stages, width = L.sweep_schedule()
+    t = np.full((max(len(stages), 1), max(width, 1)), -1, np.int32)
+    for k, st in enumerate(stages):
+        t[k, :len(st)] = st
+    return t.reshape(-1)
 
 
 def init_state_arrays(L: SceneLayout, E: int, params: SimParams, env_origins: np.ndarray,
@@ -127,6 +139,10 @@ def layout_struct(L: SceneLayout, E: int, ptrs: dict, env_offset: int = 0,
      s.planes_per_env, s.pairs_per_env, s.sensors_per_env, s.tendons_per_env, s.env_offset) = (
         E, L.actors_per_env, L.bodies_per_env, L.dofs_per_env, L.joints_per_env,
         L.planes_per_env, L.pairs_per_env, L.sensors_per_env, L.tendons_per_env, env_offset)
+    stages, width = L.sweep_schedule()
+    s.sched_stages, s.sched_width = len(stages), width
+    if not L.use_sweep_schedule() or os.environ.get("BSIM_NO_SCHED"):   # env knob: timing experiment
+        s.sched_stages = 0                       # the one-lane sequential sweep
     for name in N.LAYOUT_PTRS:
         setattr(s, name, C.c_void_p(ptrs[name]))
     return s

@@ -34,7 +34,7 @@ def test_library_exports_every_declared_function(lib_path):
     missing = [n for n in names if not hasattr(lib, n)]
     assert not missing, missing
     lib.bsim_abi_version.restype = C.c_int
-    assert lib.bsim_abi_version() == 1
+    assert lib.bsim_abi_version() == 2
 
 
 def test_loader_declares_every_function(lib_path):
