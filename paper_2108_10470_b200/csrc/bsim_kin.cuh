@@ -9,6 +9,45 @@ namespace bsim {
 // --------------------------------------------------------- kinematics
 // Scene.forward_kinematics (physics.py:366-425) for one env directly on
 // global memory (reset path; not the hot loop).  Positions env-local.
+template <class R, class J>
+BS_HD void fk_joint(const J &jt_ref, R *__restrict__ bq, const R *__restrict__ dof) {
+    const J jt = jt_ref;   // the whole record at once (vector loads), not field by field behind the stores
+    R *P = bq + 13 * jt.parent, *Cc = bq + 13 * jt.child;
+    Q4<R> qp = Q4<R>{P[3], P[4], P[5], P[6]};
+    V3<R> pp = V3<R>{P[0], P[1], P[2]};
+    Q4<R> jq = qmul(qp, jq4(jt.origin_quat));
+    V3<R> jrel = qrot(qp, jv3(jt.origin_pos));   // joint origin relative to the parent body
+    Q4<R> mq = Q4<R>{0, 0, 0, 1};
+    V3<R> mp = zero3<R>(), qda = zero3<R>(), qdl = zero3<R>();
+    if (jt.kind == BSIM_REVOLUTE) {
+        R q = dof[2 * jt.dof], qd = dof[2 * jt.dof + 1];
+        R sh = r_sin(R(0.5) * q), ch = r_cos(R(0.5) * q);
+        mq = Q4<R>{jt.axis[0] * sh, jt.axis[1] * sh, jt.axis[2] * sh, ch};
+        qda = qrot(jq, jv3(jt.axis)) * qd;
+    } else if (jt.kind == BSIM_PRISMATIC) {
+        R q = dof[2 * jt.dof], qd = dof[2 * jt.dof + 1];
+        mp = jv3(jt.axis) * q;
+        qdl = qrot(jq, jv3(jt.axis)) * qd;
+    } else if (jt.kind == BSIM_SPHERICAL) {
+        V3<R> q3 = v3(dof[2 * jt.dof], dof[2 * jt.dof + 2], dof[2 * jt.dof + 4]);
+        V3<R> qd3 = v3(dof[2 * jt.dof + 1], dof[2 * jt.dof + 3], dof[2 * jt.dof + 5]);
+        mq = qexp(q3);
+        qda = qrot(jq, qd3);
+    }
+    Q4<R> qcf = qmul(jq, mq);
+    V3<R> arel = jrel + qrot(jq, mp);                   // anchor relative to the parent body
+    Q4<R> qc = qnormalize(qmul(qcf, qconj(jq4(jt.child_quat))));
+    V3<R> crel = arel - qrot(qc, jv3(jt.child_pos));    // child body relative to the parent body
+    V3<R> pc = pp + crel;
+    V3<R> wp = V3<R>{P[10], P[11], P[12]}, vp = V3<R>{P[7], P[8], P[9]};
+    V3<R> wc = wp + qda;
+    V3<R> vc = vp + cross(wp, arel) + qdl + cross(wc, crel - arel);
+    Cc[0] = pc.x; Cc[1] = pc.y; Cc[2] = pc.z;
+    Cc[3] = qc.x; Cc[4] = qc.y; Cc[5] = qc.z; Cc[6] = qc.w;
+    Cc[7] = vc.x; Cc[8] = vc.y; Cc[9] = vc.z;
+    Cc[10] = wc.x; Cc[11] = wc.y; Cc[12] = wc.z;
+}
+
 template <class R> BS_HD void fk_env(const Ctx<R> &c, int e, uint32_t amask) {
     const Dims &d = c.d;
     R *bq = c.s.body_q + (size_t)e * d.B * 13;
@@ -16,42 +55,43 @@ template <class R> BS_HD void fk_env(const Ctx<R> &c, int e, uint32_t amask) {
     for (int j = 0; j < d.J; ++j) {
         const auto &jt = c.joints[j];
         if (!((amask >> jt.actor) & 1u)) continue;
-        R *P = bq + 13 * jt.parent, *Cc = bq + 13 * jt.child;
-        Q4<R> qp = Q4<R>{P[3], P[4], P[5], P[6]};
-        V3<R> pp = V3<R>{P[0], P[1], P[2]};
-        Q4<R> jq = qmul(qp, jq4(jt.origin_quat));
-        V3<R> jrel = qrot(qp, jv3(jt.origin_pos));   // joint origin relative to the parent body
-        Q4<R> mq = Q4<R>{0, 0, 0, 1};
-        V3<R> mp = zero3<R>(), qda = zero3<R>(), qdl = zero3<R>();
-        if (jt.kind == BSIM_REVOLUTE) {
-            R q = dof[2 * jt.dof], qd = dof[2 * jt.dof + 1];
-            R sh = r_sin(R(0.5) * q), ch = r_cos(R(0.5) * q);
-            mq = Q4<R>{jt.axis[0] * sh, jt.axis[1] * sh, jt.axis[2] * sh, ch};
-            qda = qrot(jq, jv3(jt.axis)) * qd;
-        } else if (jt.kind == BSIM_PRISMATIC) {
-            R q = dof[2 * jt.dof], qd = dof[2 * jt.dof + 1];
-            mp = jv3(jt.axis) * q;
-            qdl = qrot(jq, jv3(jt.axis)) * qd;
-        } else if (jt.kind == BSIM_SPHERICAL) {
-            V3<R> q3 = v3(dof[2 * jt.dof], dof[2 * jt.dof + 2], dof[2 * jt.dof + 4]);
-            V3<R> qd3 = v3(dof[2 * jt.dof + 1], dof[2 * jt.dof + 3], dof[2 * jt.dof + 5]);
-            mq = qexp(q3);
-            qda = qrot(jq, qd3);
-        }
-        Q4<R> qcf = qmul(jq, mq);
-        V3<R> arel = jrel + qrot(jq, mp);                   // anchor relative to the parent body
-        Q4<R> qc = qnormalize(qmul(qcf, qconj(jq4(jt.child_quat))));
-        V3<R> crel = arel - qrot(qc, jv3(jt.child_pos));    // child body relative to the parent body
-        V3<R> pc = pp + crel;
-        V3<R> wp = V3<R>{P[10], P[11], P[12]}, vp = V3<R>{P[7], P[8], P[9]};
-        V3<R> wc = wp + qda;
-        V3<R> vc = vp + cross(wp, arel) + qdl + cross(wc, crel - arel);
-        Cc[0] = pc.x; Cc[1] = pc.y; Cc[2] = pc.z;
-        Cc[3] = qc.x; Cc[4] = qc.y; Cc[5] = qc.z; Cc[6] = qc.w;
-        Cc[7] = vc.x; Cc[8] = vc.y; Cc[9] = vc.z;
-        Cc[10] = wc.x; Cc[11] = wc.y; Cc[12] = wc.z;
+        fk_joint(jt, bq, dof);
     }
 }
+
+#if defined(__CUDACC__)
+// Forward kinematics of all actors of one env by the G lanes of its group,
+// on a shared-memory copy of the env's rows (`bq`, 13 B words) and DOF
+// state (`dof`): in each round every lane takes the not-yet-placed joints
+// (j = lane, lane + G, ...) whose parent body is placed, so the tree is
+// walked level by level (the Ant analog's 8 joints in 2 rounds, not 8 in
+// sequence).  A child's pose depends only on its parent's final pose, so the
+// result equals fk_env's joint-index order.  B <= 64 (the placed-body mask).
+template <int G, class R>
+__device__ void fk_group(const Ctx<R> &c, R *bq, const R *dof, int sl, unsigned gmask) {
+    const Dims &d = c.d;
+    uint64_t placed = d.B >= 64 ? ~0ull : ((1ull << d.B) - 1);
+    for (int j = 0; j < d.J; ++j) placed &= ~(1ull << c.joints[j].child);   // actor roots
+    uint32_t mine_done = 0;                       // this lane's joints placed (j = sl + G i -> bit i)
+    for (int round = 0; round < d.J; ++round) {
+        uint64_t grown = 0;
+        int i = 0;
+        for (int j = sl; j < d.J; j += G, ++i) {
+            const auto &jt = c.joints[j];
+            if (!((mine_done >> i) & 1u) && ((placed >> jt.parent) & 1ull)) {
+                fk_joint(jt, bq, dof);
+                mine_done |= 1u << i;
+                grown |= 1ull << jt.child;
+            }
+        }
+        __syncwarp(gmask);                        // the new rows are visible to the group
+        const uint32_t lo = __reduce_or_sync(gmask, (uint32_t)grown), hi = __reduce_or_sync(gmask, (uint32_t)(grown >> 32));
+        const uint64_t all = ((uint64_t)hi << 32) | lo;
+        if (!all) break;                          // every joint placed (uniform over the group)
+        placed |= all;
+    }
+}
+#endif
 
 // repack body_state/root_state rows of the masked actors (buffers.py:109-123)
 // The four arrays are distinct allocations (__restrict__): without it every

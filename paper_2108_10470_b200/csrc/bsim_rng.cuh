@@ -84,6 +84,23 @@ BS_HD uint64_t np_next64(NpRng &r) {  // XSL-RR output of the advanced state
     return (x >> rot) | (x << ((64u - rot) & 63u));
 }
 
+// Jump the stream `delta` draws ahead (pcg_advance_lcg_128: the LCG's
+// affine map squared log2(delta) times), so lane k of an env's reset group
+// can take draw k of the env's stream without the k - 1 draws before it.
+BS_HD void np_advance(NpRng &r, uint64_t delta) {
+    unsigned __int128 acc_mult = 1, acc_plus = 0, cur_mult = pcg_mult(), cur_plus = r.inc;
+    while (delta > 0) {
+        if (delta & 1) {
+            acc_mult *= cur_mult;
+            acc_plus = acc_plus * cur_mult + cur_plus;
+        }
+        cur_plus = (cur_mult + 1) * cur_plus;
+        cur_mult *= cur_mult;
+        delta >>= 1;
+    }
+    r.state = acc_mult * r.state + acc_plus;
+}
+
 // Generator.uniform(lo, hi) = lo + (hi - lo) * next_double
 BS_HD double np_uniform(NpRng &r, double lo, double hi) {
     double u = (double)(np_next64(r) >> 11) * (1.0 / 9007199254740992.0);

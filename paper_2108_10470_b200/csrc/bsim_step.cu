@@ -108,10 +108,17 @@ template <int NW> __device__ unsigned claim_sweep_smsp(const int *warp_smsp, uns
 }
 
 template <class R>
-__device__ __noinline__ void task_step_env_call(const Ctx<R> &c, const bsim_task_t &t, R *stage, int e0, int e, int sl) {
-    task_step_env_g<R, BSIM_TASK_G>(c, TaskView<R>{t, stage, e0}, e, sl);
+__device__ __noinline__ void task_step_env_call(const Ctx<R> &c, const bsim_task_t &t, R *stage, int e0, int e, int sl,
+                                                R *scratch) {
+    TaskView<R> tv{t, stage, e0};
+    tv.scratch = scratch;
+    tv.scratch_stride = (13 * c.d.B + 2 * c.d.D + 3) & ~3;
+    task_step_env_g<R, BSIM_TASK_G>(c, tv, e, sl);
 }
 
+#ifndef BSIM_HALVES
+#define BSIM_HALVES 0
+#endif
 #ifndef BSIM_MINB
 #define BSIM_MINB 4   // 4 x 128 threads at <= 128 registers: matches the shared-memory limit
 #endif
@@ -124,6 +131,8 @@ __device__ __noinline__ void task_step_env_call(const Ctx<R> &c, const bsim_task
 // and per CTA of the last launch: SM id, %globaltimer at entry, before the task tail, at exit
 __device__ unsigned long long g_phase_clk[8];
 __device__ unsigned long long g_cta_times[4096][4];
+__device__ unsigned long long g_last_end;        // latest CTA exit %globaltimer (previous launches)
+__device__ unsigned long long g_gap_sum, g_gap_n;   // first-CTA start - previous launch's last exit
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -146,6 +155,13 @@ __global__ void __launch_bounds__(Shape<R>::NTH, BSIM_MINB)
     if (tid == 0 && blockIdx.x < 4096) {
         g_cta_times[blockIdx.x][0] = hw_sm_id();
         g_cta_times[blockIdx.x][1] = gtimer();
+    }
+    if (tid == 0 && blockIdx.x == 0) {   // block 0 starts first: the gap since the previous launch's last CTA
+        const unsigned long long prev = *(volatile unsigned long long *)&g_last_end, now = gtimer();
+        if (prev && now > prev && now - prev < 1000000ull) {
+            atomicAdd(&g_gap_sum, now - prev);
+            atomicAdd(&g_gap_n, 1ull);
+        }
     }
 #define BSIM_PCLK(i)                                                             \
     do {                                                                         \
@@ -206,13 +222,35 @@ __global__ void __launch_bounds__(Shape<R>::NTH, BSIM_MINB)
     }
     __syncthreads();
     BSIM_PCLK(1);
+    // BSIM_HALVES (experiment): the substeps run on two independent 64-thread
+    // halves of the CTA (envs [0, n0) and [n0, ne), each with its own named
+    // barrier and sweep warp), so one half's phase A can overlap the other's
+    // sweep instead of the whole CTA waiting at every barrier
+#if BSIM_HALVES
+    constexpr bool halves = NTH == 128 && Shape<R>::NE == 16 && sizeof(R) == 4;
+#else
+    constexpr bool halves = false;
+#endif
+    Grp<R> gs = g;
+    if (halves) {
+        const int h = tid >> 6, n0 = (ne + 1) >> 1, first = h ? n0 : 0;
+        gs.ws = ws + (size_t)first * d.pad;
+        gs.e0 = e0 + first;
+        gs.ne = h ? ne - n0 : n0;
+        gs.tid = tid & 63;
+        gs.nth = 64;
+        gs.lane0 = 0;
+        gs.bar = 1 + h;
+    }
     for (int s = 0; s < n_substeps; ++s) {
-        group_step<R, T>(c, g, s == n_substeps - 1, s);
+        group_step<R, T>(c, gs, s == n_substeps - 1, s);
         if (d.T && s != n_substeps - 1) {  // fixed tendons read dof_state next substep
+            if (halves) __syncthreads();
             readout_group(c, g);
             __syncthreads();
         }
     }
+    if (halves) __syncthreads();
     BSIM_PCLK(2);
     readout_group(c, g);
     BS_ITEMS(g, d.P, el, i) {
@@ -253,8 +291,13 @@ __global__ void __launch_bounds__(Shape<R>::NTH, BSIM_MINB)
         // coalesced block (task.obs may be mapped host memory: bsim_env_step_host
         // zero-copy mode, where a scattered row store would be a PCIe write each)
         R *stage = ws;
+        // the resets' FK scratch rows follow the obs rows in the dead workspace
+        const size_t obs_words = ((size_t)ne * task.obs_dim + 3) & ~(size_t)3;
+        const size_t scr_words = (size_t)ne * ((13 * d.B + 2 * d.D + 3) & ~3);
+        R *scratch = obs_words + scr_words <= (size_t)epc * d.pad ? ws + obs_words : nullptr;
 #ifndef BSIM_EXP_SKIP_TAIL   // timing experiment only: the launch without the tail's work
-        if (tid < BSIM_TASK_G * ne) task_step_env_call(c, task, stage, e0, e0 + tid / BSIM_TASK_G, tid % BSIM_TASK_G);
+        if (tid < BSIM_TASK_G * ne)
+            task_step_env_call(c, task, stage, e0, e0 + tid / BSIM_TASK_G, tid % BSIM_TASK_G, scratch);
 #endif
         __syncthreads();
         BSIM_PCLK(4);
@@ -266,6 +309,10 @@ __global__ void __launch_bounds__(Shape<R>::NTH, BSIM_MINB)
     if (tid == 0 && blockIdx.x < 4096) {
         if (!with_task) g_cta_times[blockIdx.x][2] = gtimer();
         g_cta_times[blockIdx.x][3] = gtimer();
+    }
+    if (tid == 0) {
+        __threadfence();
+        atomicMax(&g_last_end, gtimer());
     }
 #endif
 #undef BSIM_PCLK
@@ -907,5 +954,13 @@ extern "C" int bsim_exp_phase_clocks(unsigned long long *out8) {
 }
 extern "C" int bsim_exp_cta_times(unsigned long long *out) {   // [4096][4]
     return cudaMemcpyFromSymbol(out, g_cta_times, sizeof(unsigned long long) * 4096 * 4) == cudaSuccess ? 0 : -1;
+}
+extern "C" int bsim_exp_launch_gap(unsigned long long *out2) {   // (sum ns, count); read and clear
+    if (cudaMemcpyFromSymbol(out2, g_gap_sum, 8) != cudaSuccess) return -1;
+    if (cudaMemcpyFromSymbol(out2 + 1, g_gap_n, 8) != cudaSuccess) return -1;
+    unsigned long long z = 0;
+    cudaMemcpyToSymbol(g_gap_sum, &z, 8);
+    cudaMemcpyToSymbol(g_gap_n, &z, 8);
+    return cudaMemcpyToSymbol(g_last_end, &z, 8) == cudaSuccess ? 0 : -1;
 }
 #endif

@@ -25,7 +25,9 @@
 #include "../../include/batchsim_b200.h"
 
 #if defined(__CUDA_ARCH__)
-#define BS_SYNC() __syncthreads()
+// the step's barrier: the group's named barrier (g.bar > 0: a sub-CTA env
+// group of g.nth threads, bsim_step.cu BSIM_HALVES) or the CTA's
+#define BS_SYNC() bsim::bs_bar(g.bar, g.nth)
 #else
 #define BS_SYNC() ((void)0)
 #endif
@@ -214,6 +216,11 @@ template <> struct Ws<float> {
 #ifndef BSIM_PERR_TWOSUM
 #define BSIM_PERR_TWOSUM 1
 #endif
+// contact slots that are inactive this substep (depth <= -slop at the freeze)
+// skip their row constants and rows (measurement variant: BSIM_SKIP_INACTIVE=0)
+#ifndef BSIM_SKIP_INACTIVE
+#define BSIM_SKIP_INACTIVE 1
+#endif
 template <class R> struct GeomT { using type = R; };
 template <class R> struct GeomPT { using type = R; };
 #if BSIM_GEOM_F64
@@ -264,8 +271,17 @@ template <class R> struct Grp {
     R *ws;
     int e0, ne, tid, nth, lane0, pad;
     JTab<R> jt;   // the joint table: a shared-memory copy on the device
+    int bar = 0;  // 0: the CTA barrier; k > 0: named barrier k over the group's nth threads
     BS_HD Ws<R> env(int el) const { return Ws<R>{ws + (size_t)el * pad}; }
 };
+#if defined(__CUDA_ARCH__)
+__device__ __forceinline__ void bs_bar(int id, int n) {
+    if (id == 0)
+        __syncthreads();
+    else
+        asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+#endif
 
 // ====================================================== phase A pieces
 template <class R> BS_HD void stage_env(const Ctx<R> &c, const Ws<R> &w, int e) {
@@ -953,8 +969,11 @@ template <class R> BS_HD void row_plane(const Ctx<R> &c, const Ws<R> &w, int i, 
     // whole record groups: [r | act], [I xn | m_n], [I x1 | m_1], [I x2 | m_2],
     // [lam_n lt0 lt1 | tgt], [st1 st2 | d0 rest]
     const Q4<R> ra = w.l4(ipl(d, i, CR)), gn = w.l4(ipl(d, i, CIXN));
-    const Q4<R> acc = w.l4(ipl(d, i, CLN)), stc = w.l4(ipl(d, i, CST1));
     const bool act = ra.w != R(0);
+#if BSIM_SKIP_INACTIVE
+    if (!act) return;   // an inactive slot applies no impulse (bitwise the branch-free result)
+#endif
+    const Q4<R> acc = w.l4(ipl(d, i, CLN)), stc = w.l4(ipl(d, i, CST1));
     V3<R> r = qvec(ra);
     R vn = X.v.z + dot(plane_xn(r), X.w);
     R lam_n = acc.x;
@@ -1045,12 +1064,18 @@ template <class R> BS_HD void sweep(const Ctx<R> &c, const Ws<R> &w, R h, bool b
         store_bv(d, w, jt.parent, P);
     }
     for (int i = 0; i < d.P; ++i) {
+#if BSIM_SKIP_INACTIVE
+        if (w.at(ipl(d, i, CACT)) == R(0)) continue;
+#endif
         int b = c.L.plane_body[i];
         BV<R> X = load_bv(d, w, b);
         row_plane(c, w, i, X);
         store_bv(d, w, b, X);
     }
     for (int i = 0; i < d.Q; ++i) {
+#if BSIM_SKIP_INACTIVE
+        if (w.at(ipr(d, i, QACT)) == R(0)) continue;
+#endif
         int pa = c.L.pair_body[2 * i], pb = c.L.pair_body[2 * i + 1];
         BV<R> A = load_bv(d, w, pa), X = load_bv(d, w, pb);
         row_pair(c, w, i, A, X);
@@ -1080,11 +1105,17 @@ BS_HD void sched_row(const Ctx<R> &c, const Ws<R> &w, int r, R h, bool biased) {
         store_bv(d, w, jt.parent, P);
     } else if (r < d.J + d.P) {
         const int i = r - d.J, b = c.L.plane_body[i];
+#if BSIM_SKIP_INACTIVE
+        if (w.at(ipl(d, i, CACT)) == R(0)) return;
+#endif
         BV<R> X = load_bv(d, w, b);
         row_plane(c, w, i, X);
         store_bv(d, w, b, X);
     } else {
         const int i = r - d.J - d.P, pa = c.L.pair_body[2 * i], pb = c.L.pair_body[2 * i + 1];
+#if BSIM_SKIP_INACTIVE
+        if (w.at(ipr(d, i, QACT)) == R(0)) return;
+#endif
         BV<R> A = load_bv(d, w, pa), X = load_bv(d, w, pb);
         row_pair(c, w, i, A, X);
         store_bv(d, w, pa, A);
@@ -1512,6 +1543,11 @@ template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> 
             Ws<R> w = g.env(el);
             const int pb = plane_body_of<T>(c, i);
             if (freeze) plane_freeze(c, w, g.e0 + el, i, pb);
+#if BSIM_SKIP_INACTIVE
+            // an inactive slot's rows apply nothing (row_plane returns before
+            // reading them), so its row constants are not built
+            if (w.at(ipl(d, i, CACT)) == R(0)) return;
+#endif
             plane_constants(c, w, i, pb);
             plane_pass_constants(c, w, i, biased, pb);
         };
@@ -1524,6 +1560,9 @@ template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> 
             BS_ITEMS(g, d.Q, el, i) {
                 Ws<R> w = g.env(el);
                 if (freeze) pair_freeze(c, w, g.e0 + el, i);
+#if BSIM_SKIP_INACTIVE
+                if (w.at(ipr(d, i, QACT)) == R(0)) continue;   // row_pair returns before using them
+#endif
                 pair_constants(c, w, i);
                 pair_pass_constants(c, w, i, biased);
             }

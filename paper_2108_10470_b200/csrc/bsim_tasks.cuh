@@ -33,6 +33,8 @@ template <class R> struct TaskView {
     const bsim_task_t &t;
     R *stage = nullptr;   // optional shared-memory obs rows of envs [stage_e0, ...) (coalesced copy-out)
     int stage_e0 = 0;
+    R *scratch = nullptr; // optional per-env shared-memory scratch of envs [stage_e0, ...): 13 B body-row
+    int scratch_stride = 0;   // words + 2 D DOF words each (the group reset, task_reset_env_g)
     BS_HD R *obs(int e) const {
         return stage ? stage + (size_t)(e - stage_e0) * t.obs_dim : reinterpret_cast<R *>(t.obs) + (size_t)e * t.obs_dim;
     }
@@ -232,6 +234,128 @@ template <int G, class R> __device__ __forceinline__ R group_sum(R v) {
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(m, v, o);
     return v;
+}
+
+// task_reset_env for the locomotion / ANYmal tasks by the G lanes of the env's
+// group, on the env's shared-memory scratch (TaskView::scratch): draw k of the
+// env's reset stream is taken by lane k % G after np_advance(k) -- the same
+// doubles in the same roles as the sequential draws -- the DOF rows and the
+// root row are set in the scratch copy, forward kinematics walks the tree
+// level by level (fk_group), and the rows go back to HBM in parallel.  The
+// arithmetic per value is task_reset_env's, so results are bitwise equal; the
+// latency of one reset (on the critical path of the CTA that holds it) drops
+// from ~20 us of dependent single-lane global round trips.
+template <class R, int G>
+__device__ void task_reset_env_g(const Ctx<R> &c, const TaskView<R> &tv, int e, int sl) {
+#if defined(BSIM_EXP_RESET_CLOCKS)
+    unsigned long long t_prev_ = clock64();
+    if (sl == 0) atomicAdd(&bsim_reset_clk[7], 1ull);
+#define BSIM_GRCLK(i)                                                \
+    do {                                                             \
+        if (sl == 0) {                                               \
+            unsigned long long t_ = clock64();                       \
+            atomicAdd(&bsim_reset_clk[i], t_ - t_prev_);             \
+            t_prev_ = t_;                                            \
+        }                                                            \
+    } while (0)
+#else
+#define BSIM_GRCLK(i) \
+    do {              \
+    } while (0)
+#endif
+    const bsim_task_t &t = tv.t;
+    const Dims &d = c.d;
+    const unsigned gm = group_mask<G>();
+    const bool loco = t.kind != BSIM_TASK_ANYMAL;
+    const uint32_t genv = (uint32_t)(c.L.env_offset + e);
+    const uint32_t rc = (uint32_t)t.reset_count[e];
+    R *__restrict__ bq = tv.scratch + (size_t)(e - tv.stage_e0) * tv.scratch_stride;
+    R *__restrict__ dq = bq + 13 * d.B;
+    // the env's rows into the scratch (actor roots keep theirs unless reset below)
+    const R *__restrict__ gq = c.s.body_q + (size_t)e * d.B * 13;
+#pragma unroll 8
+    for (int i = sl; i < 13 * d.B; i += G) bq[i] = gq[i];   // unrolled: the loads issue back to back
+    if (sl == 0) {
+        if (c.s.nonfinite[e]) c.s.nonfinite[e] = 0;   // clear_nonfinite (physics.py:1090)
+        const int64_t step_count = t.step_count_dev ? *t.step_count_dev : t.step_count;
+        dr_randomize_env(c, t.dr, e, step_count);     // randomizer.randomize (envs.py:154-155)
+    }
+    BSIM_GRCLK(0);
+    uint32_t key[4] = {t.seed, genv, rc, 0xCu};
+    const NpRng rng = np_rng(key, 3);                 // every lane: the stream's start
+    const int first = loco ? 1 : 0;                   // draw 0 = the locomotion yaw
+    for (int k = sl; k < t.act_dim; k += G) {         // draw first + k -> DOF k (envs.py:404-419 / 536-549)
+        NpRng r = rng;
+        np_advance(r, (uint64_t)(first + k));
+        dq[2 * k] = R(np_uniform(r, -0.1, 0.1));
+        dq[2 * k + 1] = R(0);
+    }
+    for (int k = t.act_dim + sl; k < d.D; k += G) {   // (no other DOFs in these tasks; keep the state)
+        dq[2 * k] = c.s.dof_state[2 * ((size_t)e * d.D + k)];
+        dq[2 * k + 1] = c.s.dof_state[2 * ((size_t)e * d.D + k) + 1];
+    }
+    if (sl == 0) {
+        double qx = 0.0, qy = 0.0, qz = 0.0, qw = 1.0;
+        if (loco) {
+            NpRng r = rng;
+            double yaw = np_uniform(r, -0.1, 0.1);
+            qz = sin(yaw / 2.0);
+            qw = cos(yaw / 2.0);
+        }
+        double n = sqrt(qx * qx + qy * qy + qz * qz + qw * qw);  // set_root_state renormalises (buffers.py:145)
+        bq[0] = R(0); bq[1] = R(0); bq[2] = R(t.rest_height + 0.02);
+        bq[3] = R(qx / n); bq[4] = R(qy / n); bq[5] = R(qz / n); bq[6] = R(qw / n);
+        for (int k = 7; k < 13; ++k) bq[k] = R(0);
+        if (t.obs_noise) {  // per-episode correlated noise continues the reset stream (envs.py:161-164)
+            NpRng r = rng;
+            np_advance(r, (uint64_t)(first + t.act_dim));
+            R *cn = reinterpret_cast<R *>(t.corr_noise) + (size_t)e * t.obs_dim;
+            for (int k = 0; k < t.obs_dim; ++k)
+                cn[k] = t.obs_noise_corr > 0.0 ? R(0.0 + t.obs_noise_corr * np_std_normal(r)) : R(0);
+        }
+    }
+    __syncwarp(gm);
+    BSIM_GRCLK(1);
+    fk_group<G>(c, bq, dq, sl, gm);
+    BSIM_GRCLK(3);
+    // rows back to HBM: body_q (env-local), body_state (world), root_state, dof_state
+    const R *__restrict__ o = c.s.env_origins + 3 * (size_t)e;
+    R *__restrict__ dst_q = c.s.body_q + (size_t)e * d.B * 13;
+    R *__restrict__ dst_s = c.s.body_state + (size_t)e * d.B * 13;
+    const R ox = o[0], oy = o[1], oz = o[2];
+#pragma unroll 8
+    for (int i = sl; i < 13 * d.B; i += G) {
+        const int k = i % 13;
+        const R v = bq[i];
+        dst_q[i] = v;
+        dst_s[i] = v + (k == 0 ? ox : k == 1 ? oy : k == 2 ? oz : R(0));
+    }
+    for (int i = sl; i < 13 * d.A; i += G) {
+        const int a = i / 13, k = i - 13 * a;
+        const R v = bq[13 * c.L.actor_body_offset[a] + k];
+        c.s.root_state[13 * ((size_t)e * d.A + a) + k] = v + (k == 0 ? ox : k == 1 ? oy : k == 2 ? oz : R(0));
+    }
+#pragma unroll 4
+    for (int i = sl; i < 2 * d.D; i += G) c.s.dof_state[2 * (size_t)e * d.D + i] = dq[i];
+    R *a = tv.act(e);
+    for (int k = sl; k < t.act_dim; k += G) a[k] = R(0);
+    BSIM_GRCLK(4);
+    __syncwarp(gm);                                   // every lane read reset_count before it moves
+    if (sl == 0) {
+        t.episode_steps[e] = 0;
+        t.reset_count[e] = (int32_t)(rc + 1u);
+        if (loco) {
+            const double z = (double)R(t.rest_height + 0.02);   // the stored root height
+            tv.potential(e) = -sqrt(QUAD_TARGET_X * QUAD_TARGET_X + z * z) / t.control_dt;
+        } else {                                      // anymal velocity commands
+            key[2] = rc + 1u;
+            NpRng cr = np_rng(key, 4);
+            R *cmd = tv.cmd(e);
+            for (int k = 0; k < 3; ++k) cmd[k] = R(np_uniform(cr, -1.0, 1.0));
+        }
+    }
+    BSIM_GRCLK(5);
+#undef BSIM_GRCLK
 }
 
 // locomotion_reward (rewards.py:78-112); returns the reward, lane 0 writes the new potential
@@ -475,6 +599,10 @@ template <class R, int G> __device__ void task_obs_g(const Ctx<R> &c, const Task
 template <class R> __device__ __noinline__ void task_reset_env_call(const Ctx<R> &c, const TaskView<R> &tv, int e) {
     task_reset_env(c, tv, e);
 }
+template <class R, int G>
+__device__ __noinline__ void task_reset_env_g_call(const Ctx<R> &c, const TaskView<R> &tv, int e, int sl) {
+    task_reset_env_g<R, G>(c, tv, e, sl);
+}
 // goal reset after a success (cube task): successes + 1, a new goal orientation
 template <class R> __device__ __noinline__ void cube_goal_call(const Ctx<R> &c, const TaskView<R> &tv, int e) {
     tv.goal(e)[7] = tv.goal(e)[7] + R(1);
@@ -496,15 +624,19 @@ template <class R, int G> __device__ void task_step_env_g(const Ctx<R> &c, const
     const bool pois = c.s.nonfinite[e] != 0;
     done = done || timeout || pois;
     __syncwarp(group_mask<G>());           // every lane read the pre-step state
+    // locomotion / ANYmal resets run on the whole group (task_reset_env_g)
+    const bool group_reset = tv.scratch && c.d.B <= 64 &&
+                             (t.kind == BSIM_TASK_QUADRUPED || t.kind == BSIM_TASK_ANYMAL || t.kind == BSIM_TASK_HUMANOID);
     if (sl == 0) {
         t.episode_steps[e] = steps;
         tv.reward(e) = pois ? R(0) : rew;
         t.done[e] = done;
         t.timeout[e] = timeout;
         t.poisoned[e] = pois;
-        if (done) task_reset_env_call(c, tv, e);
-        else if (success) cube_goal_call(c, tv, e);
+        if (done && !group_reset) task_reset_env_call(c, tv, e);
+        else if (!done && success) cube_goal_call(c, tv, e);
     }
+    if (done && group_reset) task_reset_env_g_call<R, G>(c, tv, e, sl);   // done is uniform over the group
     __syncwarp(group_mask<G>());           // the reset state is visible to the group
     task_obs_g<R, G>(c, tv, e, sl);        // reset rows get the post-reset observation (envs.py:195-198)
 }

@@ -28,7 +28,11 @@ def main(task="quadruped", E=16384, steps=30):
         env.step(torch.rand((E, env.act_dim), generator=gen, device="cuda") * 2 - 1)
     torch.cuda.synchronize()
     fn(buf)
+    knock = torch.arange(0, E, 50, device="cuda")      # 2 % of the envs fall every step: resets at the next
     for _ in range(steps):
+        root = env.scene.root_state.clone()
+        root[:, 2] = 0.05
+        env.buffers.set_root_state(root, knock)
         env.step(torch.rand((E, env.act_dim), generator=gen, device="cuda") * 2 - 1)
     torch.cuda.synchronize()
     fn(buf)
