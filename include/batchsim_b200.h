@@ -86,6 +86,8 @@ typedef struct bsim_layout_t {
                               (paper_2108_10470_b200/csrc/bsim_topologies.cuh) */
     int32_t sched_stages, sched_width;     /* the Gauss-Seidel row schedule below (0 = none:
                                               one lane per env in reference order) */
+    int32_t sched_flags;                   /* bit 0: the schedule holds the joint rows only; the
+                                              contact rows follow in reference order on one lane */
     const void *joints;                    /* [J]    */
     const int32_t *plane_body;             /* [P]    */
     const int32_t *pair_body;              /* [Q][2] */

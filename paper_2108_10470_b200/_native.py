@@ -83,7 +83,7 @@ class Params64(C.Structure):
 
 LAYOUT_INTS = ("num_envs", "actors_per_env", "bodies_per_env", "dofs_per_env", "joints_per_env",
                "planes_per_env", "pairs_per_env", "sensors_per_env", "tendons_per_env", "env_offset",
-               "topology_id", "sched_stages", "sched_width")
+               "topology_id", "sched_stages", "sched_width", "sched_flags")
 LAYOUT_PTRS = ("joints", "plane_body", "pair_body", "sensor_body", "actor_body_offset",
                "actor_dof_offset", "tendons", "tendon_elems", "spatial_paths", "pair_kind", "pair_ext",
                "sweep_sched")

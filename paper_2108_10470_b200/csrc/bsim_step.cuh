@@ -1135,6 +1135,9 @@ __device__ void sweep_sched(const Ctx<R> &c, const Ws<R> *w, R h, bool biased, i
             }
         __syncwarp(mask);
     }
+    if ((c.L.sched_flags & 1) && w && lane == 0)      // joint-only schedule: the contact rows in order
+        for (int r = d.J; r < d.J + d.P + d.Q; ++r) sched_row(c, *w, r, h, biased);
+    if (c.L.sched_flags & 1) __syncwarp(mask);
     if (biased && w)
         for (int b = lane; b < d.B; b += lanes) accumulate_deltas(d, *w, b, load_bv(d, *w, b), h);
 }
@@ -1147,6 +1150,8 @@ template <class R> void sweep_sched_host(const Ctx<R> &c, const Ws<R> &w, R h, b
             const int r = c.L.sweep_sched[s * W + l];
             if (r >= 0) sched_row(c, w, r, h, biased);
         }
+    if (c.L.sched_flags & 1)
+        for (int r = d.J; r < d.J + d.P + d.Q; ++r) sched_row(c, w, r, h, biased);
     if (biased)
         for (int b = 0; b < d.B; ++b) accumulate_deltas(d, w, b, load_bv(d, w, b), h);
 }

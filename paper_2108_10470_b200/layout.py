@@ -304,72 +304,112 @@ class SceneLayout:
         return n + joint_index
 
     # ------------------------------------------------------------ packing
-    def sweep_schedule(self, width=32):
-        """Stages of one Gauss-Seidel pass (physics.py:760-775: joints, then
-        plane slots, then pair slots, each in index order).  Row r goes to
-        stage 1 + max(stage of the last earlier row touching any of its
-        bodies), so rows of a stage touch disjoint bodies and every row runs
-        after each earlier row it shares a body with: executing a stage's rows
-        side by side (one lane each) reproduces the sequential sweep exactly
-        (rows on disjoint bodies commute).  Stages wider than `width` are
-        split (the kernel also lets a lane take several rows of a stage).  Row ids: joint j -> j, plane slot i -> J + i, pair slot q ->
-        J + P + q.  Returns (stages, width) with stages a list of row-id
-        lists."""
+    def _sched_rows(self):
         J, P = self.joints_per_env, self.planes_per_env
         rows = [(j, {jt.parent, jt.child}) for j, jt in enumerate(self.joints)]
         rows += [(J + i, {int(b)}) for i, b in enumerate(self.plane_body)]
         rows += [(J + P + q, {int(a), int(b)}) for q, (a, b) in enumerate(self.pair_body)]
+        return rows
 
-        def levels(phased):
-            # ASAP levels; `phased`: no contact row before the last joint row's
-            # stage (every contact row follows every joint row in the reference
-            # order, so this is also valid) -- stages then hold one row type,
-            # which a warp runs without divergence
-            last, stage_of, floor = {}, [], 0
-            for r, bodies in rows:
-                if phased and r == J:
-                    floor = max(stage_of, default=-1) + 1
-                st = max(floor, 1 + max(last.get(b, -1) for b in bodies))
-                stage_of.append(st)
-                for b in bodies:
-                    last[b] = st
-            n = max(stage_of) + 1 if stage_of else 0
-            out = []
-            for k in range(n):
-                st = [r for (r, _), s in zip(rows, stage_of) if s == k]
-                out += [st[i:i + width] for i in range(0, len(st), width)]
-            return out
+    def _levels(self, rows, phased, width):
+        """ASAP stages of `rows` (reference order): row r goes to 1 + the
+        stage of the last earlier row sharing a body with it; `phased`: no
+        contact row before the last joint stage."""
+        J = self.joints_per_env
+        last, stage_of, floor = {}, [], 0
+        for r, bodies in rows:
+            if phased and r == J:
+                floor = max(stage_of, default=-1) + 1
+            st = max(floor, 1 + max(last.get(b, -1) for b in bodies))
+            stage_of.append(st)
+            for b in bodies:
+                last[b] = st
+        out = []
+        for k in range(max(stage_of) + 1 if stage_of else 0):
+            st = [r for (r, _), s in zip(rows, stage_of) if s == k]
+            out += [st[i:i + width] for i in range(0, len(st), width)]
+        return out
 
-        # the cheaper by the cost model on 2 lanes (measured: the humanoid's
-        # ASAP schedule, 11 mixed stages, 1886 us per 16384-env step vs 1987 us
-        # for the phased one the 8-lane model prefers)
-        stages = min((levels(False), levels(True)), key=self._sched_cost)
-        return stages, max((len(s) for s in stages), default=0)
+    def sweep_schedules(self, width=32):
+        """The candidate row schedules of one Gauss-Seidel pass
+        (physics.py:760-775: joints, then plane slots, then pair slots, each in
+        index order).  Rows of a stage touch disjoint bodies and every row runs
+        after each earlier row it shares a body with, so running a stage's
+        rows side by side (one lane each) reproduces the sequential sweep
+        exactly (rows on disjoint bodies commute).  Row ids: joint j -> j,
+        plane slot i -> J + i, pair slot q -> J + P + q.
+          "asap":   all rows, ASAP stages;
+          "phased": all rows, contact rows only after the last joint stage
+                    (stages of one row type: no divergence in a warp);
+          "joints": the joint rows only (sched_flags bit 0: the contact rows
+                    follow in reference order on one lane -- every contact
+                    row comes after every joint row in the reference order).
+        Stages wider than `width` are split."""
+        rows = self._sched_rows()
+        J = self.joints_per_env
+        return {"asap": self._levels(rows, False, width), "phased": self._levels(rows, True, width),
+                "joints": self._levels(rows[:J], False, width)}
 
-    def _sched_cost(self, stages, lanes=2, per_stage=0.3):
-        """Row times of a schedule on `lanes` lanes per env: per stage, each
-        row type present (joint / plane / pair: divergent code paths in a
-        warp) costs ceil(rows of that type / lanes), plus a per-stage overhead
-        (schedule load, __syncwarp)."""
-        J, P = self.joints_per_env, self.planes_per_env
+    def _sched_cost(self, mode, stages, lanes=2, per_stage=0.3, contact=0.5, mixed=0.5):
+        """Modelled row times of a pass: per stage, the costliest row type
+        present (joint / plane / pair) costs ceil(rows of the type / lanes),
+        each further type `mixed` x its own (divergent paths of a warp partly
+        overlap), plus `per_stage` (schedule load, __syncwarp); a contact row
+        counts `contact` (inactive slots skip, BSIM_SKIP_INACTIVE); mode
+        "joints" adds its sequential contact rows.  The weights are fitted to
+        the measured mode rankings quoted in sweep_schedule."""
+        J, P, Q = self.joints_per_env, self.planes_per_env, self.pairs_per_env
         cost = 0.0
         for st in stages:
             n = [0, 0, 0]
             for r in st:
                 n[0 if r < J else (1 if r < J + P else 2)] += 1
-            cost += per_stage + sum(-(-k // lanes) for k in n if k)
+            ts = sorted((-(-k // lanes) * (1.0 if t == 0 else contact) for t, k in enumerate(n) if k), reverse=True)
+            cost += per_stage + (ts[0] + mixed * sum(ts[1:]) if ts else 0.0)
+        if mode == "joints":
+            cost += contact * (P + Q)
         return cost
 
-    def use_sweep_schedule(self):
-        """The kernel runs the schedule only where it pays: its modelled cost
-        (_sched_cost, 2 lanes per env -- the default CTA's share of the sweep
-        warp) below 0.8 of the sequential row count.  Measured on B200: the
-        humanoid (43 rows, 11 stages) 2418 -> 1886 us per 16384-env control
-        step; the Franka cube-stack scene (47 rows, 28 mixed-type stages)
-        7.1 -> 5.8 M env-steps/s slower, hence the threshold."""
-        stages, _ = self.sweep_schedule()
-        n_rows = self.joints_per_env + self.planes_per_env + self.pairs_per_env
-        return bool(stages) and self._sched_cost(stages) < 0.8 * n_rows
+    def _sweep_lanes(self):
+        """Lanes per env the kernel gives the schedule: 8 on the large-
+        articulation CTA (4 envs share the sweep warp), 2 on the default one
+        (16 envs).  Mirrors csrc: make_dims' record size (BODY 36, JOINT 44,
+        PLANE 28, PAIR 76, ANCHOR 4, DOF 2 items, ENV 8, pad = 4 mod 8) and
+        use_large_variant (a 16-env fp32 workspace over 113 KB)."""
+        items = (36 * self.bodies_per_env + 44 * self.joints_per_env + 28 * self.planes_per_env +
+                 76 * self.pairs_per_env + 4 * self.planes_per_env + 2 * self.dofs_per_env)
+        items = ((items + 3) & ~3) + 8
+        while items % 8 != 4:
+            items += 1
+        return 8 if 16 * items * 4 > 113 * 1024 else 2
+
+    def sweep_schedule(self, width=32):
+        """(mode, stages, width) of the schedule the kernel runs, or mode
+        None: the sequential one-lane sweep.  The cheapest candidate by the
+        cost model (on the kernel's lanes per env, _sweep_lanes), used when it
+        is below 0.8 of the sequential cost.  Measured on B200, fp32, with
+        every mode forced (tools/gpu_r02_p.sh): humanoid 16384 envs none /
+        asap / phased / joints 2297 / 1800 / 1946 / 1886 us per control step
+        -> asap; Shadow Hand 3.38 / 3.28 / 3.19 / 3.93 M env-steps/s -> joints;
+        Franka cube-stack 7.47 / 6.15 / 5.80 / 6.21 M -> none.  The model
+        picks the same three.
+        BSIM_SCHED_MODE=asap|phased|joints|none forces a mode (experiments)."""
+        import os
+        cands = self.sweep_schedules(width)
+        J = self.joints_per_env
+        seq = J + 0.5 * (self.planes_per_env + self.pairs_per_env)
+        forced = os.environ.get("BSIM_SCHED_MODE")
+        if forced:
+            mode = None if forced == "none" else forced
+        else:
+            lanes = self._sweep_lanes()
+            mode = min(cands, key=lambda m: self._sched_cost(m, cands[m], lanes))
+            if not cands[mode] or self._sched_cost(mode, cands[mode], lanes) >= 0.8 * seq:
+                mode = None
+        if mode is None:
+            return None, [], 0
+        st = cands[mode]
+        return mode, st, max((len(s) for s in st), default=0)
 
     def joint_table(self):
         """(J, 8) int32 and (J, 24) float32 views of bsim_joint_t rows."""

@@ -76,7 +76,7 @@ def pack_tables(L: SceneLayout, fp64: bool = False):
 
 def sched_table(L: SceneLayout):
     """[stages][width] int32 row ids of SceneLayout.sweep_schedule, -1 padded."""
-    stages, width = L.sweep_schedule()
+    _, stages, width = L.sweep_schedule()
     t = np.full((max(len(stages), 1), max(width, 1)), -1, np.int32)
     for k, st in enumerate(stages):
         t[k, :len(st)] = st
@@ -139,10 +139,11 @@ def layout_struct(L: SceneLayout, E: int, ptrs: dict, env_offset: int = 0,
      s.planes_per_env, s.pairs_per_env, s.sensors_per_env, s.tendons_per_env, s.env_offset) = (
         E, L.actors_per_env, L.bodies_per_env, L.dofs_per_env, L.joints_per_env,
         L.planes_per_env, L.pairs_per_env, L.sensors_per_env, L.tendons_per_env, env_offset)
-    stages, width = L.sweep_schedule()
-    s.sched_stages, s.sched_width = len(stages), width
-    if not L.use_sweep_schedule() or os.environ.get("BSIM_NO_SCHED"):   # env knob: timing experiment
-        s.sched_stages = 0                       # the one-lane sequential sweep
+    mode, stages, width = L.sweep_schedule()
+    s.sched_stages, s.sched_width = len(stages), width        # 0 stages: the one-lane sequential sweep
+    s.sched_flags = 1 if mode == "joints" else 0
+    if os.environ.get("BSIM_NO_SCHED"):          # timing experiment
+        s.sched_stages = 0
     for name in N.LAYOUT_PTRS:
         setattr(s, name, C.c_void_p(ptrs[name]))
     return s
