@@ -116,9 +116,10 @@ __device__ __noinline__ void task_step_env_call(const Ctx<R> &c, const bsim_task
     task_step_env_g<R, BSIM_TASK_G>(c, tv, e, sl);
 }
 
-#ifndef BSIM_HALVES
-#define BSIM_HALVES 0
+#ifndef BSIM_SUBGROUPS
+#define BSIM_SUBGROUPS 1
 #endif
+static_assert(BSIM_SUBGROUPS >= 1 && BSIM_SUBGROUPS <= 8, "1..8 sub-CTA env groups");
 #ifndef BSIM_MINB
 #define BSIM_MINB 4   // 4 x 128 threads at <= 128 registers: matches the shared-memory limit
 #endif
@@ -222,23 +223,23 @@ __global__ void __launch_bounds__(Shape<R>::NTH, BSIM_MINB)
     }
     __syncthreads();
     BSIM_PCLK(1);
-    // BSIM_HALVES (experiment): the substeps run on two independent 64-thread
-    // halves of the CTA (envs [0, n0) and [n0, ne), each with its own named
-    // barrier and sweep warp), so one half's phase A can overlap the other's
-    // sweep instead of the whole CTA waiting at every barrier
-#if BSIM_HALVES
-    constexpr bool halves = NTH == 128 && Shape<R>::NE == 16 && sizeof(R) == 4;
-#else
-    constexpr bool halves = false;
-#endif
+    // BSIM_SUBGROUPS = K > 1: the substeps run on K independent groups of
+    // NTH / K threads (envs split evenly, each group with its own named
+    // barrier and sweep warp), so one group's phase A overlaps another's
+    // sweep instead of the whole CTA waiting at every barrier.  Measured
+    // slower on both CTAs, so K = 1: the default CTA with K = 2
+    // (Ant 234 -> 252 us), the large CTA with K = 4 (humanoid 1804 -> 2417 us)
+    constexpr int K = NTH / 32 < BSIM_SUBGROUPS ? NTH / 32 : BSIM_SUBGROUPS;   // named barriers: >= 1 warp each
+    constexpr bool halves = K > 1;
     Grp<R> gs = g;
     if (halves) {
-        const int h = tid >> 6, n0 = (ne + 1) >> 1, first = h ? n0 : 0;
+        constexpr int TG = NTH / K;
+        const int h = tid / TG, per = (ne + K - 1) / K, first = min(ne, h * per);
         gs.ws = ws + (size_t)first * d.pad;
         gs.e0 = e0 + first;
-        gs.ne = h ? ne - n0 : n0;
-        gs.tid = tid & 63;
-        gs.nth = 64;
+        gs.ne = min(ne, first + per) - first;
+        gs.tid = tid % TG;
+        gs.nth = TG;
         gs.lane0 = 0;
         gs.bar = 1 + h;
     }

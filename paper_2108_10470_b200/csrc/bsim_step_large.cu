@@ -13,5 +13,9 @@
 #define BSIM_NE64 2
 #define BSIM_NTH64 64
 #define BSIM_MINB 5   // 5 x 128 threads: the 20-env-per-SM occupancy the record size allows
+#ifndef BSIM_LARGE_SUBGROUPS
+#define BSIM_LARGE_SUBGROUPS 1   // 4 = one warp per env with its own named barrier: measured 1804 -> 2417 us
+#endif                           // per 16384-env humanoid step, so the CTA stays whole
+#define BSIM_SUBGROUPS BSIM_LARGE_SUBGROUPS
 #define bsim bsim_large
 #include "bsim_step.cu"
