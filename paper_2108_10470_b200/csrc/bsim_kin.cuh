@@ -68,16 +68,18 @@ template <class R> BS_HD void fk_env(const Ctx<R> &c, int e, uint32_t amask) {
 // sequence).  A child's pose depends only on its parent's final pose, so the
 // result equals fk_env's joint-index order.  B <= 64 (the placed-body mask).
 template <int G, class R>
-__device__ void fk_group(const Ctx<R> &c, R *bq, const R *dof, int sl, unsigned gmask) {
+__device__ void fk_group(const Ctx<R> &c, R *bq, const R *dof, int sl, unsigned gmask, uint32_t amask = ~0u) {
     const Dims &d = c.d;
     uint64_t placed = d.B >= 64 ? ~0ull : ((1ull << d.B) - 1);
-    for (int j = 0; j < d.J; ++j) placed &= ~(1ull << c.joints[j].child);   // actor roots
+    for (int j = 0; j < d.J; ++j)                 // actor roots, and every link of an actor not in amask
+        if ((amask >> c.joints[j].actor) & 1u) placed &= ~(1ull << c.joints[j].child);
     uint32_t mine_done = 0;                       // this lane's joints placed (j = sl + G i -> bit i)
     for (int round = 0; round < d.J; ++round) {
         uint64_t grown = 0;
         int i = 0;
         for (int j = sl; j < d.J; j += G, ++i) {
             const auto &jt = c.joints[j];
+            if (!((amask >> jt.actor) & 1u)) continue;
             if (!((mine_done >> i) & 1u) && ((placed >> jt.parent) & 1ull)) {
                 fk_joint(jt, bq, dof);
                 mine_done |= 1u << i;
@@ -125,17 +127,15 @@ template <class R> BS_HD void repack_env(const Ctx<R> &c, int e, uint32_t amask)
 }
 
 // dof readout for one env straight from global memory (physics.py:427-459)
-template <class R> BS_HD void readout_env(const Ctx<R> &c, int e) {
-    const Dims &d = c.d;
-    const R *bq = c.s.body_q + (size_t)e * d.B * 13;
-    for (int j = 0; j < d.J; ++j) {
-        const auto &jt = c.joints[j];
-        if (jt.dof < 0) continue;
+template <class R, class J> BS_HD void readout_joint(const Ctx<R> &c, const J &jt, const R *bq, R *dof_env) {
+    (void)c;
+    if (jt.dof < 0) return;
+    {
         const R *P = bq + 13 * jt.parent, *Cc = bq + 13 * jt.child;
         Q4<R> qp = Q4<R>{P[3], P[4], P[5], P[6]}, qc = Q4<R>{Cc[3], Cc[4], Cc[5], Cc[6]};
         Q4<R> jqp = qmul(qp, jq4(jt.origin_quat)), jqc = qmul(qc, jq4(jt.child_quat));
         V3<R> wp = V3<R>{P[10], P[11], P[12]}, wc = V3<R>{Cc[10], Cc[11], Cc[12]};
-        R *o = c.s.dof_state + 2 * ((size_t)e * d.D + jt.dof);
+        R *o = dof_env + 2 * jt.dof;
         if (jt.kind == BSIM_REVOLUTE) {
             Q4<R> qr = qmul(qconj(jqp), jqc);
             V3<R> ax = jv3(jt.axis);
@@ -154,6 +154,11 @@ template <class R> BS_HD void readout_env(const Ctx<R> &c, int e) {
             o[0] = rv.x; o[1] = wr.x; o[2] = rv.y; o[3] = wr.y; o[4] = rv.z; o[5] = wr.z;
         }
     }
+}
+template <class R> BS_HD void readout_env(const Ctx<R> &c, int e) {
+    const Dims &d = c.d;
+    const R *bq = c.s.body_q + (size_t)e * d.B * 13;
+    for (int j = 0; j < d.J; ++j) readout_joint(c, c.joints[j], bq, c.s.dof_state + 2 * (size_t)e * d.D);
 }
 
 }  // namespace bsim

@@ -319,21 +319,91 @@ __global__ void __launch_bounds__(Shape<R>::NTH, BSIM_MINB)
 #undef BSIM_PCLK
 }
 
+// Scene.forward_kinematics(env_mask, actors) + the buffers' repack
+// (physics.py:366-425, buffers.py:109-123): a group of FK_G lanes per env on
+// a shared-memory copy of the env's rows and DOF state (fk_group walks the
+// tree level by level), FK_EPC envs per CTA; bodies >= 64 (fk_group's mask)
+// fall back to one lane per env on global memory.
+constexpr int FK_G = 8, FK_EPC = 16;
+template <class R> __host__ __device__ int fk_stride(const Dims &d) { return (13 * d.B + 2 * d.D + 3) & ~3; }
 template <class R>
-__global__ void fk_kernel(Ctx<R> c, const uint8_t *env_mask, const uint32_t *amask_dev, uint32_t amask) {
-    int e = blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= c.d.E) return;
-    if (env_mask && !env_mask[e]) return;
-    uint32_t m = amask_dev ? *amask_dev : amask;
-    fk_env(c, e, m);
-    repack_env(c, e, m);
+__global__ void __launch_bounds__(FK_G * FK_EPC)
+    fk_kernel(Ctx<R> c, const uint8_t *env_mask, const uint32_t *amask_dev, uint32_t amask) {
+    extern __shared__ __align__(16) unsigned char fk_smem[];
+    const Dims &d = c.d;
+    const int el = threadIdx.x / FK_G, sl = threadIdx.x % FK_G;
+    const int e = blockIdx.x * FK_EPC + el;
+    if (e >= d.E || (env_mask && !env_mask[e])) return;   // whole groups leave together
+    const uint32_t m = amask_dev ? *amask_dev : amask;
+    if (d.B > 64) {
+        if (sl == 0) {
+            fk_env(c, e, m);
+            repack_env(c, e, m);
+        }
+        return;
+    }
+    constexpr unsigned gm_base = (1u << FK_G) - 1u;
+    const unsigned gm = gm_base << ((threadIdx.x & 31u) & ~(unsigned)(FK_G - 1));
+    R *__restrict__ bq = reinterpret_cast<R *>(fk_smem) + (size_t)el * fk_stride<R>(d);
+    R *__restrict__ dq = bq + 13 * d.B;
+    const R *__restrict__ gq = c.s.body_q + (size_t)e * d.B * 13;
+    const R *__restrict__ gd = c.s.dof_state + 2 * (size_t)e * d.D;
+#pragma unroll 4
+    for (int i = sl; i < 13 * d.B; i += FK_G) bq[i] = gq[i];
+#pragma unroll 4
+    for (int i = sl; i < 2 * d.D; i += FK_G) dq[i] = gd[i];
+    __syncwarp(gm);
+    fk_group<FK_G>(c, bq, dq, sl, gm, m);
+    const R *__restrict__ o = c.s.env_origins + 3 * (size_t)e;
+    const R ox = o[0], oy = o[1], oz = o[2];
+    for (int a = 0; a < d.A; ++a) {               // rows of the masked actors (fk_env + repack_env)
+        if (!((m >> a) & 1u)) continue;
+        const int b0 = c.L.actor_body_offset[a], n = 13 * (c.L.actor_body_offset[a + 1] - b0);
+        R *__restrict__ dst_q = c.s.body_q + 13 * ((size_t)e * d.B + b0);
+        R *__restrict__ dst_s = c.s.body_state + 13 * ((size_t)e * d.B + b0);
+        const R *src = bq + 13 * b0;
+        for (int i = sl; i < n; i += FK_G) {
+            const int k = i % 13;
+            const R v = src[i];
+            dst_q[i] = v;
+            dst_s[i] = v + (k == 0 ? ox : k == 1 ? oy : k == 2 ? oz : R(0));
+        }
+        R *__restrict__ rr = c.s.root_state + 13 * ((size_t)e * d.A + a);
+        for (int k = sl; k < 13; k += FK_G) rr[k] = src[k] + (k == 0 ? ox : k == 1 ? oy : k == 2 ? oz : R(0));
+    }
 }
 
-template <class R> __global__ void refresh_kernel(Ctx<R> c) {
-    int e = blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= c.d.E) return;
-    readout_env(c, e);
-    repack_env(c, e, 0xffffffffu);
+// refresh_buffers without a contact context (physics.py:1037-1046): DOF
+// readout and body / root packing for REF_EPC envs per CTA.  The CTA's
+// contiguous [envs x B x 13] slab of body_q is staged in shared memory with
+// one coalesced pass, body_state / root_state leave coalesced from it, and
+// the DOF readout runs one thread per (env, joint) on the staged rows.
+constexpr int REF_EPC = 16, REF_NTH = 256;
+template <class R> __global__ void __launch_bounds__(REF_NTH) refresh_kernel(Ctx<R> c) {
+    extern __shared__ __align__(16) unsigned char ref_smem[];
+    const Dims &d = c.d;
+    const int e0 = blockIdx.x * REF_EPC, ne = min(REF_EPC, d.E - e0), per = 13 * d.B;
+    R *__restrict__ sq = reinterpret_cast<R *>(ref_smem);
+    const R *__restrict__ gq = c.s.body_q + (size_t)e0 * per;
+    R *__restrict__ gs = c.s.body_state + (size_t)e0 * per;
+    const R *__restrict__ org = c.s.env_origins + 3 * (size_t)e0;
+    for (int i = threadIdx.x; i < ne * per; i += REF_NTH) {
+        const R v = gq[i];
+        const int el = i / per, k = (i - el * per) % 13;
+        sq[i] = v;
+        gs[i] = k < 3 ? v + org[3 * el + k] : v;
+    }
+    __syncthreads();
+    R *__restrict__ gr = c.s.root_state + (size_t)e0 * d.A * 13;
+    for (int i = threadIdx.x; i < ne * d.A * 13; i += REF_NTH) {
+        const int el = i / (13 * d.A), rem = i - el * 13 * d.A, a = rem / 13, k = rem - a * 13;
+        const R v = sq[el * per + 13 * c.L.actor_body_offset[a] + k];
+        gr[i] = k < 3 ? v + org[3 * el + k] : v;
+    }
+    for (int i = threadIdx.x; i < ne * d.J; i += REF_NTH) {
+        const int el = i / d.J, j = i - el * d.J;
+        readout_joint(c, c.joints[j], sq + (size_t)el * per, c.s.dof_state + 2 * (size_t)(e0 + el) * d.D);
+    }
 }
 
 // set_root_state: write the root bodies of the listed actors (env-local), renormalise quats
@@ -703,13 +773,23 @@ int launch_step(const bsim_layout_t *layout, const typename Abi<R>::Params *para
 #endif
 }
 
+// dynamic shared memory above the default 48 KB needs the kernel's opt-in (once per size and device)
+template <class K> int allow_smem(K *kernel, size_t bytes) {
+    if (bytes <= 48 * 1024) return BSIM_OK;
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    return e == cudaSuccess ? BSIM_OK : set_err("cudaFuncSetAttribute(aux kernel)", e);
+}
+
 template <class R>
 int launch_fk(const bsim_layout_t *layout, const typename Abi<R>::State *state, const uint8_t *env_mask,
               uint32_t actor_mask, void *stream) {
     if (bad_layout(layout) || !state) return BSIM_E_INVALID;
     Ctx<R> c = make_ctx<R>(layout, nullptr, state);
     if (c.d.E == 0) return BSIM_OK;
-    fk_kernel<R><<<(c.d.E + 127) / 128, 128, 0, (cudaStream_t)stream>>>(c, env_mask, nullptr, actor_mask);
+    const size_t smem = FK_EPC * fk_stride<R>(c.d) * sizeof(R);
+    if (int rc = allow_smem(fk_kernel<R>, smem)) return rc;
+    fk_kernel<R><<<(c.d.E + FK_EPC - 1) / FK_EPC, FK_G * FK_EPC, smem, (cudaStream_t)stream>>>(c, env_mask, nullptr,
+                                                                                             actor_mask);
     return check_launch("fk_kernel");
 }
 
@@ -717,7 +797,9 @@ template <class R> int launch_refresh(const bsim_layout_t *layout, const typenam
     if (bad_layout(layout) || !state) return BSIM_E_INVALID;
     Ctx<R> c = make_ctx<R>(layout, nullptr, state);
     if (c.d.E == 0) return BSIM_OK;
-    refresh_kernel<R><<<(c.d.E + 127) / 128, 128, 0, (cudaStream_t)stream>>>(c);
+    const size_t smem = REF_EPC * 13 * c.d.B * sizeof(R);
+    if (int rc = allow_smem(refresh_kernel<R>, smem)) return rc;
+    refresh_kernel<R><<<(c.d.E + REF_EPC - 1) / REF_EPC, REF_NTH, smem, (cudaStream_t)stream>>>(c);
     return check_launch("refresh_kernel");
 }
 
@@ -739,7 +821,9 @@ int launch_set(bool root, const bsim_layout_t *layout, const typename Abi<R>::St
     int r = check_launch(root ? "set_root_kernel" : "set_dof_kernel");
     if (r) return r;
     // FK over (touched envs) x (touched actors), then repack (buffers.py:151-152, 177-178)
-    fk_kernel<R><<<(c.d.E + 127) / 128, 128, 0, st>>>(c, env_mask, amask, 0u);
+    const size_t smem = FK_EPC * fk_stride<R>(c.d) * sizeof(R);
+    if (int rc = allow_smem(fk_kernel<R>, smem)) return rc;
+    fk_kernel<R><<<(c.d.E + FK_EPC - 1) / FK_EPC, FK_G * FK_EPC, smem, st>>>(c, env_mask, amask, 0u);
     return check_launch("fk_kernel");
 }
 

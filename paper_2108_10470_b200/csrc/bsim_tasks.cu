@@ -44,18 +44,34 @@ __global__ void task_step_kernel(const __grid_constant__ Ctx<R> c, const __grid_
     obs_copy_out(t, stage, cta_e0, min(e_end, cta_e0 + epc));
 }
 
+// EnvBatch.reset(env_indices) (envs.py:141-166) + the post-reset observation:
+// TASK_G lanes per env, 128 / TASK_G envs per CTA.  Locomotion / ANYmal envs
+// reset on the whole group (task_reset_env_g: parallel draws by PCG64
+// jump-ahead, level-parallel FK on the env's shared-memory scratch after the
+// CTA's obs rows); the other tasks, or models over 64 bodies, on lane 0.
 template <class R>
 __global__ void task_reset_kernel(const __grid_constant__ Ctx<R> c, const __grid_constant__ bsim_task_t t,
                                   const uint8_t *mask) {
     extern __shared__ __align__(16) unsigned char task_smem[];
+    constexpr int G = TASK_G, EPC = 128 / TASK_G;
     R *stage = reinterpret_cast<R *>(task_smem);
-    const int cta_e0 = blockIdx.x * blockDim.x, e = cta_e0 + threadIdx.x;
+    const int cta_e0 = blockIdx.x * EPC, e = cta_e0 + threadIdx.x / G, sl = threadIdx.x % G;
     if (e < c.d.E) {
         TaskView<R> tv{t, stage, cta_e0};
-        if (!mask || mask[e]) task_reset_env(c, tv, e);
-        task_obs_g<R, 1>(c, tv, e, 0);
+        tv.scratch = stage + (((size_t)EPC * t.obs_dim + 3) & ~(size_t)3);
+        tv.scratch_stride = (13 * c.d.B + 2 * c.d.D + 3) & ~3;
+        const bool group = c.d.B <= 64 && (t.kind == BSIM_TASK_QUADRUPED || t.kind == BSIM_TASK_ANYMAL ||
+                                          t.kind == BSIM_TASK_HUMANOID);
+        if (!mask || mask[e]) {
+            if (group)
+                task_reset_env_g<R, G>(c, tv, e, sl);
+            else if (sl == 0)
+                task_reset_env(c, tv, e);
+        }
+        __syncwarp(group_mask<G>());
+        task_obs_g<R, G>(c, tv, e, sl);
     }
-    obs_copy_out(t, stage, cta_e0, min(c.d.E, cta_e0 + (int)blockDim.x));
+    obs_copy_out(t, stage, cta_e0, min(c.d.E, cta_e0 + EPC));
 }
 
 template <class R>
@@ -103,8 +119,26 @@ int launch_task(const bsim_layout_t *L, const typename Abi<R>::State *s, const b
         return BSIM_E_TOO_LARGE;
     }
     cudaStream_t st = (cudaStream_t)stream;
-    if (reset) {
-        task_reset_kernel<R><<<(env_count + tpb - 1) / tpb, tpb, tpb * row, st>>>(c, *t, mask);
+    if (reset) {   // TASK_G lanes per env; the obs rows, then each env's reset scratch
+        const int epc = 128 / TASK_G;
+        const size_t smem = ((((size_t)epc * t->obs_dim + 3) & ~(size_t)3) +
+                             (size_t)epc * ((13 * c.d.B + 2 * c.d.D + 3) & ~3)) * sizeof(R);
+        if (smem > 48 * 1024) {
+            cudaError_t ea = cudaFuncSetAttribute(task_reset_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  (int)smem);
+            if (ea != cudaSuccess) return t_set_err("cudaFuncSetAttribute(task_reset_kernel)", ea);
+        }
+        bsim_task_t tr = *t;
+        if (tr.dr.enabled && !tr.step_count_dev) {
+            // domain randomisation of the reset envs first, one thread per env (full warps; inside the
+            // group reset it would run on one lane of eight), then the resets without it -- the DR
+            // draws are keyed apart from the reset draws, so the order does not change a value
+            randomize_kernel<R><<<(c.d.E + 127) / 128, 128, 0, st>>>(c, tr.dr, mask, tr.step_count);
+            cudaError_t ed = cudaGetLastError();
+            if (ed != cudaSuccess) return t_set_err("randomize_kernel", ed);
+            tr.dr.enabled = 0;
+        }
+        task_reset_kernel<R><<<(c.d.E + epc - 1) / epc, 128, smem, st>>>(c, tr, mask);
     } else {   // TASK_G lanes per env: 128 / TASK_G envs per CTA
         const int epc = 128 / TASK_G;
         task_step_kernel<R><<<(env_count + epc - 1) / epc, 128, epc * row, st>>>(c, *t, env_begin,

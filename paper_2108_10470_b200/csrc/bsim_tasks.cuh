@@ -275,6 +275,7 @@ __device__ void task_reset_env_g(const Ctx<R> &c, const TaskView<R> &tv, int e, 
     const R *__restrict__ gq = c.s.body_q + (size_t)e * d.B * 13;
 #pragma unroll 8
     for (int i = sl; i < 13 * d.B; i += G) bq[i] = gq[i];   // unrolled: the loads issue back to back
+    __syncwarp(gm);                                   // the copy lands before lane 0 rewrites the root row
     if (sl == 0) {
         if (c.s.nonfinite[e]) c.s.nonfinite[e] = 0;   // clear_nonfinite (physics.py:1090)
         const int64_t step_count = t.step_count_dev ? *t.step_count_dev : t.step_count;
