@@ -94,6 +94,9 @@ template <class R> struct M3 {  // general 3x3, row-major
 };
 
 template <class R> BS_HD V3<R> v3(R x, R y, R z) { return V3<R>{x, y, z}; }
+template <class G, class R> BS_HD S3<G> cs3(const S3<R> &m) {
+    return S3<G>{(G)m.xx, (G)m.xy, (G)m.xz, (G)m.yy, (G)m.yz, (G)m.zz};
+}
 // error-free sum (Knuth TwoSum): a + b = s + e exactly, s = fl(a + b)
 template <class R> BS_HD R two_sum(R a, R b, R &e) {
     const R s = a + b;

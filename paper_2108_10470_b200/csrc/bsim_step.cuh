@@ -216,6 +216,10 @@ template <> struct Ws<float> {
 #ifndef BSIM_PERR_TWOSUM
 #define BSIM_PERR_TWOSUM 1
 #endif
+// BSIM_EXP_I64 / BSIM_EXP_G64 / BSIM_EXP_K64 (off): world inverse inertias /
+// revolute angular blocks / point blocks in double on the fp32 path --
+// measurement variants for the Shadow Hand's fp32 error (tools/
+// hand_fp32_probe.py: no change), kept so the finding can be re-measured
 // contact slots that are inactive this substep (depth <= -slop at the freeze)
 // skip their row constants and rows (measurement variant: BSIM_SKIP_INACTIVE=0)
 #ifndef BSIM_SKIP_INACTIVE
@@ -304,7 +308,11 @@ template <class R> BS_HD void body_inertia(const Ctx<R> &c, const Ws<R> &w, int 
     (void)e;
     const int bi = ib(c.d, b, BI);
     V3<R> d{w.at(bi + 6), w.at(bi + 7), w.at(ib(c.d, b, BW) + 3)};
+#if BSIM_EXP_I64   // experiment: the world inverse inertia in double
+    w.sS(bi, cs3<R>(world_inertia(cq4<double>(w.l4(ib(c.d, b, qitem))), cv3<double>(d))));
+#else
     w.sS(bi, world_inertia(w.l4(ib(c.d, b, qitem)), d));
+#endif
 }
 
 // external forces on body b (physics.py:545-552)
@@ -533,11 +541,19 @@ BS_HD void joint_item(const Ctx<R> &c, const Ws<R> &w, int e, int j, R h, bool b
     if (kind != BSIM_REVOLUTE) tangents(a, t1, t2);
     S3<R> KI, G{R(0), R(0), R(0), R(0), R(0), R(0)};
     if (kind != BSIM_PRISMATIC) {   // point-3 K^-1 (872-890)
+#if BSIM_EXP_K64   // experiment: the point block in double
+        double m = (double)mp + (double)mc;
+        S3<double> K{m, 0.0, 0.0, m, 0.0, m};
+        add_rIr(K, cv3<double>(rp), cs3<double>(Ip));
+        add_rIr(K, cv3<double>(rc), cs3<double>(Ic));
+        KI = cs3<R>(sinv(K));
+#else
         R m = mp + mc;
         S3<R> K{m, R(0), R(0), m, R(0), m};
         add_rIr(K, rp, Ip);
         add_rIr(K, rc, Ic);
         KI = sinv(K);
+#endif
     } else {                        // prismatic perpendicular pair (908-928)
         R m = mp + mc;
         V3<R> p1 = cross(rp, t1), p2 = cross(rp, t2), c1 = cross(rc, t1), c2 = cross(rc, t2);
@@ -553,11 +569,16 @@ BS_HD void joint_item(const Ctx<R> &c, const Ws<R> &w, int e, int j, R h, bool b
             // T^T (T M T^T)^-1 T for the two directions normal to the axis a,
             // M = Isum: the same matrix as M^-1 - (M^-1 a)(M^-1 a)^T / (a . M^-1 a)
             // (the projected inverse), which needs no tangent basis
-            S3<R> Mi = sinv(Isum);
-            V3<R> u = smul(Mi, a);
-            R is = r_rcp(dot(a, u));
-            G = S3<R>{Mi.xx - u.x * u.x * is, Mi.xy - u.x * u.y * is, Mi.xz - u.x * u.z * is,
-                      Mi.yy - u.y * u.y * is, Mi.yz - u.y * u.z * is, Mi.zz - u.z * u.z * is};
+#if BSIM_EXP_G64   // experiment: the angular block in double
+            using Gd = double;
+#else
+            using Gd = R;
+#endif
+            S3<Gd> Mi = sinv(cs3<Gd>(Isum));
+            V3<Gd> ad = cv3<Gd>(a), u = smul(Mi, ad);
+            Gd is = r_rcp(dot(ad, u));
+            G = cs3<R>(S3<Gd>{Mi.xx - u.x * u.x * is, Mi.xy - u.x * u.y * is, Mi.xz - u.x * u.z * is,
+                              Mi.yy - u.y * u.y * is, Mi.yz - u.y * u.z * is, Mi.zz - u.z * u.z * is});
         } else {
             G = proj3(t1, t2, a, Isum);
         }

@@ -121,3 +121,46 @@ def oracle_trace(name, E=4, steps=12, warm=30, dt=1 / 120, jitter=0.3):
     arr.update({k: np.stack(v) for k, v in rec.items()})
     meta = {"kind": "physics", "num_envs": E, "steps": steps, "params": {"dt": dt}, "spacing": 4.0, "ground": True}
     return models, p, meta, arr
+
+
+def oracle_sensitivity(models, p, meta, arr, seeds=(1, 2)):
+    """Per step and output, the element-wise max |oracle(perturbed pre-state) -
+    oracle(exact pre-state)| over the fp32 rounding of the pre-state (env-local
+    positions, as the CUDA path stores them) and len(seeds) random 2^-24
+    relative jitters of it: how far the float64 reference algorithm itself
+    moves each output under fp32-sized input noise (tests/scale_parity.py
+    `sensitivity`, for these small authored scenes)."""
+    from oracle.oracle import OracleScene
+    E = meta["num_envs"]
+    s = OracleScene(models, E, p, shape_pairs="all", env_origins=arr["param_env_origins"])
+    for k in ("inv_mass", "inertia_local", "inv_inertia_local", "gravity", "mu_static", "mu_dynamic",
+              "joint_stiffness", "joint_damping", "joint_armature", "joint_friction", "joint_limit_lo",
+              "joint_limit_hi", "plane_off", "plane_rad", "pair_off", "pair_rad"):
+        getattr(s, k)[...] = arr[f"param_{k}"]
+    org = np.repeat(arr["param_env_origins"], s.bodies_per_env, axis=0)
+
+    def r32(x):
+        return np.asarray(x, np.float64).astype(np.float32).astype(np.float64)
+
+    def jitter(seed):
+        rng = np.random.default_rng(seed)
+        return lambda x: np.asarray(x, np.float64) * (1.0 + rng.uniform(-1, 1, np.shape(x)) * 2.0 ** -24)
+
+    outs = ("root_state", "body_state", "net_contact", "dof_state")
+    sens = []
+    for t in range(meta["steps"]):
+        dev = {k: 0.0 for k in outs}
+        for tf in [r32] + [jitter(sd) for sd in seeds]:
+            s.pos[...] = org + tf(arr["in_pos"][t] - org)
+            for k in ("quat", "linvel", "angvel", "dof_state"):
+                getattr(s, k)[...] = tf(arr[f"in_{k}"][t])
+            a = arr["in__friction_anchor"][t]
+            s._friction_anchor[...] = arr["param_env_origins"][None] + tf(a - arr["param_env_origins"][None])
+            for k in ("ctrl_dof_force", "ctrl_dof_pos_target", "ctrl_dof_vel_target", "ctrl_body_force",
+                      "ctrl_body_torque", "dof_mode", "nonfinite"):
+                getattr(s, k)[...] = arr[f"in_{k}"][t]
+            s.step()
+            for k in outs:
+                dev[k] = np.maximum(dev[k], np.abs(np.asarray(getattr(s, k), float) - arr[f"out_{k}"][t]))
+        sens.append(dev)
+    return sens

@@ -24,38 +24,57 @@ def _gpu(models, p, E, precision, arr=None):
 @pytest.mark.parametrize("precision", ["fp64", "fp32"])
 @pytest.mark.parametrize("name", sorted(SCENES))
 def test_step_matches_oracle_teacher_forced(name, precision):
+    """fp64: every element within 1e-8.  fp32: every element of the root /
+    body state and the contact force within 1e-3 + 1e-3 |ref| (|ref| the norm
+    of the element's vector, tests/scale_parity.py) -- except elements the
+    float64 reference itself cannot resolve at fp32: its output moves by at
+    least 10 % of the GPU deviation when its pre-state is rounded to fp32 or
+    jittered by 2^-24 relative (pair_scenes.oracle_sensitivity).  The Franka
+    arm (light roll links in a kp-2000 drive chain, pad-cube contact events)
+    and the Shadow Hand (gram-scale phalanges, I ~ 1e-6 kg m^2: rounding only
+    the inputs of one step moves finger angular velocities by 50-260x the
+    1e-3 bound) are where this matters.  The hand in fp32 is worse than its
+    input conditioning: fp32 ARITHMETIC on the phalanges' 1e-6 kg m^2 inertias
+    under kp-drives and explicit tendon springs departs from the float64
+    trajectory by up to ~2 rad/s in one step on a few fingers (the float64
+    path matches at 1e-8), so for it the count of such elements is reported
+    and bounded (<= 10 %) rather than required to be 0.  Evaluating the
+    world inverse inertias, the angular blocks, the point blocks and the joint
+    geometry of phase A in double changes the count by < 3 %
+    (BSIM_EXP_I64 / G64 / K64, BSIM_GEOM_F64): the loss is in the fp32 sweep
+    itself, where gram-scale links meet the palm in one row."""
+    import scale_parity as SP
+    from pair_scenes import oracle_sensitivity
     models, p, meta, arr = oracle_trace(name)
     s = _gpu(models, p, meta["num_envs"], precision, arr)
-    tol = 1e-8 if precision == "fp64" else 2e-3
-    # the Franka arm's light roll links between heavier segments amplify fp32
-    # rounding in a stiff (kp 2000) drive chain through pad-cube contact
-    # events: in fp32 at most one env per step may leave the contract (all
-    # finite); fp64 stays at 1e-8 everywhere
-    loose = precision == "fp32" and name == "franka_cube_stack"
-    # the hand's gram-scale phalanges (I ~ 1e-6 kg m^2) are ill-conditioned
-    # beyond fp32: rounding only the INPUTS of one step to fp32 (computing in
-    # float64) already moves finger angular velocities by 50-260x the 2e-3
-    # contract, and the cube and palm inherit it through the fingertip
-    # contacts: per-step fp32 parity is not defined for this model.  fp32 is
-    # checked for finiteness here and for the resting property in
-    # test_shadow_hand_holds_cube_on_palm; fp64 stays at 1e-8 on everything.
-    hand32 = precision == "fp32" and name == "shadow_hand_cube"
-    E = meta["num_envs"]
+    sens = oracle_sensitivity(models, p, meta, arr) if precision == "fp32" else None
+    n_ill = n_bad = n_all = 0
+    hand = name == "shadow_hand_cube"
     for t in range(meta["steps"]):
         load_gpu_state(s, arr, t)
         s.step()
         got = gpu_outputs(s)
-        if hand32:
-            assert np.isfinite(got["body_state"]).all() and not got["nonfinite"].any(), (name, t)
-            continue
+        assert np.isfinite(got["body_state"]).all() and not got["nonfinite"].any(), (name, t)
         for k in ("root_state", "body_state", "net_contact"):
-            if loose:
-                w = arr[f"out_{k}"][t]
-                ok = (np.abs(got[k] - w) <= tol + tol * np.abs(w)).reshape(E, -1).all(1)
-                assert np.isfinite(got[k]).all() and ok.sum() >= E - 1, (name, t, k, ok)
+            if precision == "fp64":
+                e = rel_err(got[k], arr[f"out_{k}"][t], 1e-8, 1e-8)
+                assert e <= 1.0, (name, precision, t, k, e)
                 continue
-            e = rel_err(got[k], arr[f"out_{k}"][t], tol, tol)
-            assert e <= 1.0, (name, precision, t, k, e)
+            ill, unexplained = SP.excused({k: got[k]}, {k: arr[f"out_{k}"][t]}, sens[t], k)
+            assert hand or unexplained == 0, (name, t, k, unexplained)
+            n_ill += ill
+            n_bad += unexplained
+            n_all += got[k].size
+    if precision == "fp32":
+        print(f"{name}: {n_ill} of {n_all} elements beyond 1e-3 and ill-conditioned in the reference itself, "
+              f"{n_bad} beyond 1e-3 otherwise")
+        if hand:
+            # the hand in fp32: see the docstring -- a reported bound, not the per-step contract
+            # (measured: 1222 + 535 of 21216 elements; the host build of the same kernel 1637 of
+            # 19968, and float64 arithmetic on fp32-rounded inputs alone 242 -- tools/hand_fp32_probe.py)
+            assert n_bad + n_ill <= 0.10 * n_all, (n_bad, n_ill, n_all)
+        else:
+            assert n_ill == 0, (name, n_ill)
 
 
 @pytest.mark.parametrize("name", sorted(SCENES))
