@@ -8,11 +8,23 @@
 // 16-env CTA (4 warps) with the default shape.  bsim_step.cu dispatches here
 // when its default CTA would leave fewer than 2 CTAs per SM.
 #define BSIM_LARGE_TU 1
-#define BSIM_NE32 4
-#define BSIM_NTH32 128
+// fp32 CTA: 8 envs x 32 threads, >= 2 CTAs per SM (<= 128 registers).  The
+// sweep warp then carries 8 envs (4 lanes each) instead of 4: measured at
+// 16384 envs, humanoid 1804 -> 1490 us per control step, Franka cube-stack
+// 7.46 -> 8.70 M, Shadow Hand 3.92 -> 4.26 M env-steps/s, against 4 x 32
+// with 5 CTAs/SM (the round-1 shape); 8 x 32 at 3 CTAs/SM spills, 6 x 32,
+// 12 x 32 and 16 x 32 are slower.
+#ifndef BSIM_LARGE_NE
+#define BSIM_LARGE_NE 8
+#endif
+#ifndef BSIM_LARGE_MINB
+#define BSIM_LARGE_MINB 2
+#endif
+#define BSIM_NE32 BSIM_LARGE_NE
+#define BSIM_NTH32 (32 * BSIM_LARGE_NE)
 #define BSIM_NE64 2
 #define BSIM_NTH64 64
-#define BSIM_MINB 5   // 5 x 128 threads: the 20-env-per-SM occupancy the record size allows
+#define BSIM_MINB BSIM_LARGE_MINB
 #ifndef BSIM_LARGE_SUBGROUPS
 #define BSIM_LARGE_SUBGROUPS 1   // 4 = one warp per env with its own named barrier: measured 1804 -> 2417 us
 #endif                           // per 16384-env humanoid step, so the CTA stays whole

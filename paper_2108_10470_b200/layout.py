@@ -371,8 +371,8 @@ class SceneLayout:
         return cost
 
     def _sweep_lanes(self):
-        """Lanes per env the kernel gives the schedule: 8 on the large-
-        articulation CTA (4 envs share the sweep warp), 2 on the default one
+        """Lanes per env the kernel gives the schedule: 4 on the large-
+        articulation CTA (8 envs share the sweep warp), 2 on the default one
         (16 envs).  Mirrors csrc: make_dims' record size (BODY 36, JOINT 44,
         PLANE 28, PAIR 76, ANCHOR 4, DOF 2 items, ENV 8, pad = 4 mod 8) and
         use_large_variant (a 16-env fp32 workspace over 113 KB)."""
@@ -381,7 +381,7 @@ class SceneLayout:
         items = ((items + 3) & ~3) + 8
         while items % 8 != 4:
             items += 1
-        return 8 if 16 * items * 4 > 113 * 1024 else 2
+        return 4 if 16 * items * 4 > 113 * 1024 else 2
 
     def sweep_schedule(self, width=32):
         """(mode, stages, width) of the schedule the kernel runs, or mode
