@@ -198,7 +198,28 @@ __global__ void __launch_bounds__(Shape<R>::NTH, BSIM_MINB)
         float4 *jd = reinterpret_cast<float4 *>(smem_raw + step_ws_bytes<R>(d, epc));
         for (int i = tid; i < d.J * rec16; i += NTH) jd[(i / rec16) * str16 + i % rec16] = js[i];
     }
+    // the per-env inputs and the fused action mapping (envs.py:180, 421-424)
+    // in the same phase as the slab load: their global loads overlap instead
+    // of waiting behind a barrier (they write workspace items the slab does
+    // not, and the targets are read after the barriers below)
+    {
+        const Grp<R> g0{ws, e0, ne, tid, NTH, 0, d.pad, JTab<R>{nullptr, 0}};
+        stage_group(c, g0);
+        if (act.actions) {
+            BS_ITEMS(g0, d.D, el, k) {
+                size_t o = (size_t)(e0 + el) * d.D + k;
+                R a = clampr(reinterpret_cast<const R *>(act.actions)[o], R(-1), R(1));
+                if (act.actions_clipped) reinterpret_cast<R *>(act.actions_clipped)[o] = a;
+                R v = R(act.scale) * a;
+                if (act.mode == BSIM_MODE_POSITION)
+                    c.s.ctrl_dof_pos_target[o] = v;
+                else
+                    c.s.ctrl_dof_force[o] = v;
+            }
+        }
+    }
     __syncthreads();
+    BSIM_PCLK(0);
     if (tid == 0) {
         int w;
         s_sweep_bit = claim_sweep_smsp<NW>(s_warp_smsp, &s_sm_slot, w);
@@ -207,21 +228,6 @@ __global__ void __launch_bounds__(Shape<R>::NTH, BSIM_MINB)
     __syncthreads();
     const Grp<R> g{ws, e0, ne, tid, NTH, 32 * s_sweep_warp, d.pad,
                    JTab<R>{smem_raw + step_ws_bytes<R>(d, epc), jtab_stride_smem<R>()}};
-    BSIM_PCLK(0);
-    stage_group(c, g);
-    if (act.actions) {  // fused action mapping (envs.py:180, 421-424)
-        BS_ITEMS(g, d.D, el, k) {
-            size_t o = (size_t)(e0 + el) * d.D + k;
-            R a = clampr(reinterpret_cast<const R *>(act.actions)[o], R(-1), R(1));
-            if (act.actions_clipped) reinterpret_cast<R *>(act.actions_clipped)[o] = a;
-            R v = R(act.scale) * a;
-            if (act.mode == BSIM_MODE_POSITION)
-                c.s.ctrl_dof_pos_target[o] = v;
-            else
-                c.s.ctrl_dof_force[o] = v;
-        }
-    }
-    __syncthreads();
     BSIM_PCLK(1);
     // BSIM_SUBGROUPS = K > 1: the substeps run on K independent groups of
     // NTH / K threads (envs split evenly, each group with its own named
@@ -259,7 +265,8 @@ __global__ void __launch_bounds__(Shape<R>::NTH, BSIM_MINB)
             c.s.friction_anchor[3 * ((size_t)i * d.E + e0 + el) + k] =
                 g.env(el).at(d.o_anchor + ANCHOR_ITEMS * i + k);
     }
-    __syncthreads();
+    // (no barrier: the readout above and the stores below only read the
+    // workspace, final since group_step's last barrier)
     // coalesced stores: canonical env-local state, world-frame body_state / root_state
     {
         R *dq = c.s.body_q + (size_t)e0 * per_env;
