@@ -1056,3 +1056,12 @@ extern "C" int bsim_exp_launch_gap(unsigned long long *out2) {   // (sum ns, cou
     return cudaMemcpyToSymbol(g_last_end, &z, 8) == cudaSuccess ? 0 : -1;
 }
 #endif
+
+#if defined(BSIM_EXP_PASS_CLOCKS) && !defined(BSIM_LARGE_TU)
+// timing experiment only (tools/pass_clocks.py): read and clear the solver-pass phase counters
+extern "C" int bsim_exp_pass_clocks(unsigned long long *out8) {
+    if (cudaMemcpyFromSymbol(out8, bsim::bsim_pass_clk, sizeof(unsigned long long) * 8) != cudaSuccess) return -1;
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    return cudaMemcpyToSymbol(bsim::bsim_pass_clk, z, sizeof(z)) == cudaSuccess ? 0 : -1;
+}
+#endif

@@ -234,6 +234,26 @@ template <> struct GeomT<float> { using type = double; };
 template <> struct GeomPT<float> { using type = double; };
 #endif
 
+#if defined(BSIM_EXP_PASS_CLOCKS) && defined(__CUDACC__)
+// timing experiment only: thread-0 cycles of each solver pass's phases summed
+// over CTAs and passes -- [0] phase A, [1] sweep, [2] tail items, [7] passes
+__device__ unsigned long long bsim_pass_clk[8];
+#endif
+#if defined(BSIM_EXP_PASS_CLOCKS) && defined(__CUDA_ARCH__)
+#define BSIM_PASSCLK(i)                                                       \
+    do {                                                                      \
+        if (g.tid == 0) {                                                     \
+            unsigned long long t_ = clock64();                                \
+            atomicAdd(&bsim_pass_clk[i], t_ - pass_t0_);                      \
+            pass_t0_ = t_;                                                    \
+        }                                                                     \
+    } while (0)
+#else
+#define BSIM_PASSCLK(i) \
+    do {                \
+    } while (0)
+#endif
+
 template <class R> struct Ctx {
     using Joint = typename Abi<R>::Joint;
     using Tendon = typename Abi<R>::Tendon;
@@ -1552,6 +1572,10 @@ template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> 
 #endif
     for (int k = 0; k <= N; ++k) {
         const bool biased = k < N, freeze = k == 0, deltas = k > 0 && k < N;
+#if defined(BSIM_EXP_PASS_CLOCKS) && defined(__CUDA_ARCH__)
+        unsigned long long pass_t0_ = clock64();
+        if (g.tid == 0) atomicAdd(&bsim_pass_clk[7], 1ull);
+#endif
         // phase A: orientations -> inertias -> joint/contact geometry and row
         // constants (freeze 657-716, refresh 718-756)
 #ifdef BSIM_EXP_SKIP_A   // timing experiment only: reuse the freeze-time constants
@@ -1594,6 +1618,7 @@ template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> 
             }
         }
         BS_SYNC();
+        BSIM_PASSCLK(0);
 #ifdef BSIM_EXP_SKIP_A
     phase_b:
 #endif
@@ -1623,6 +1648,7 @@ template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> 
                         plane_item(it % g.ne, it / g.ne);
                 }
                 BS_SYNC();
+                BSIM_PASSCLK(1);
                 BS_ITEMS(g, T::B, el, b) { star_body_tail<R, T>(c, g.env(el), g.e0 + el, b, h, k, N); }
             } else
 #endif
@@ -1650,6 +1676,7 @@ template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> 
                 }
             }
             BS_SYNC();
+            BSIM_PASSCLK(2);
         }
     }
     // velocity clamps (584-587)
