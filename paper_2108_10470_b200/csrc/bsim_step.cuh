@@ -225,6 +225,9 @@ template <> struct Ws<float> {
 #ifndef BSIM_SKIP_INACTIVE
 #define BSIM_SKIP_INACTIVE 1
 #endif
+#ifndef BSIM_LIMIT_VOTE   // warp-vote skip of inactive limit rows: measured 0.4-2 % slower, off
+#define BSIM_LIMIT_VOTE 0
+#endif
 template <class R> struct GeomT { using type = R; };
 template <class R> struct GeomPT { using type = R; };
 #if BSIM_GEOM_F64
@@ -998,7 +1001,14 @@ BS_HD void joint_rows(const Ctx<R> &c, const Ws<R> &w, int j, int kind, int dof,
     if (kind != BSIM_PRISMATIC) row_linear(d, w, j, o, C, P);
     if (kind != BSIM_SPHERICAL) row_angular(d, w, j, o, C, P);
     if (kind == BSIM_PRISMATIC) row_linear(d, w, j, o, C, P);
+#if defined(__CUDA_ARCH__) && BSIM_LIMIT_VOTE
+    // an inactive limit row applies exactly zero: skip it when no lane of the
+    // warp has its limit active (each lane's own outcome is unchanged either
+    // way; this only shortens the dependent chain of the common case)
+    if (axis && limits && __any_sync(__activemask(), o.lv != R(0))) row_limit(w, d, j, lin, o, C, P);
+#else
     if (axis && limits) row_limit(w, d, j, lin, o, C, P);
+#endif
     if (axis && (biased || limits)) w.at(idf(d, dof, DIMP)) = o.imp;
 }
 
