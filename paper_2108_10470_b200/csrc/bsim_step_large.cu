@@ -20,6 +20,11 @@
 #ifndef BSIM_LARGE_MINB
 #define BSIM_LARGE_MINB 2
 #endif
+#undef BSIM_NE32
+#undef BSIM_NTH32
+#undef BSIM_NE64
+#undef BSIM_NTH64
+#undef BSIM_MINB
 #define BSIM_NE32 BSIM_LARGE_NE
 #define BSIM_NTH32 (32 * BSIM_LARGE_NE)
 #define BSIM_NE64 2
