@@ -934,15 +934,35 @@ int bsim_step(const bsim_layout_t *l, const bsim_params_t *p, const bsim_state_t
               const bsim_actions_t *a, void *st) {
     return launch_step<float>(l, p, s, n, a, st);
 }
+}  // extern "C"
+// Domain randomisation at the auto-resets is deferred to one env-parallel
+// launch right after the step (its mask: the step's done flags, which are
+// exactly the reset envs; its step count: the one the reset would have used).
+// Inside the fused tail it ran on one lane of the env's group and a late CTA
+// with a randomised reset held the whole launch (Shadow Hand, 67 resets per
+// step: 4652 -> ~3800 us).  Nothing the step returns depends on the
+// randomised parameters (the post-reset observation reads state, not
+// masses / gains / friction), and the next step sees them, so the results are
+// the in-tail ones.  The CUDA-graph path (step count on the device) keeps the
+// in-tail form.
+template <class R, class P, class S, class F>
+int env_step_dr_deferred(const bsim_layout_t *l, const P *p, const S *s, int32_t n, const bsim_actions_t *a,
+                         const bsim_task_t *t, void *st, F randomize) {
+    if (!t) return BSIM_E_INVALID;
+    if (!t->dr.enabled || t->step_count_dev || !t->done) return launch_step<R>(l, p, s, n, a, st, t);
+    bsim_task_t t2 = *t;
+    t2.dr.enabled = 0;
+    if (int rc = launch_step<R>(l, p, s, n, a, st, &t2)) return rc;
+    return randomize(l, s, &t->dr, t->done, t->step_count, st);
+}
+extern "C" {
 int bsim_env_step(const bsim_layout_t *l, const bsim_params_t *p, const bsim_state_t *s, int32_t n,
                   const bsim_actions_t *a, const bsim_task_t *t, void *st) {
-    if (!t) return BSIM_E_INVALID;
-    return launch_step<float>(l, p, s, n, a, st, t);
+    return env_step_dr_deferred<float>(l, p, s, n, a, t, st, bsim_randomize);
 }
 int bsim_env_step_f64(const bsim_layout_t *l, const bsim_params64_t *p, const bsim_state64_t *s, int32_t n,
                       const bsim_actions_t *a, const bsim_task_t *t, void *st) {
-    if (!t) return BSIM_E_INVALID;
-    return launch_step<double>(l, p, s, n, a, st, t);
+    return env_step_dr_deferred<double>(l, p, s, n, a, t, st, bsim_randomize_f64);
 }
 int bsim_step_f64(const bsim_layout_t *l, const bsim_params64_t *p, const bsim_state64_t *s, int32_t n,
                   const bsim_actions_t *a, void *st) {
