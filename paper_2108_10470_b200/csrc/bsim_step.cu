@@ -1085,3 +1085,12 @@ extern "C" int bsim_exp_pass_clocks(unsigned long long *out8) {
     return cudaMemcpyToSymbol(bsim::bsim_pass_clk, z, sizeof(z)) == cudaSuccess ? 0 : -1;
 }
 #endif
+
+#if defined(BSIM_EXP_PASS_CLOCKS) && defined(BSIM_LARGE_TU)
+// the large-articulation TU's own counters (timing experiment only)
+extern "C" int bsim_exp_pass_clocks_large(unsigned long long *out8) {
+    if (cudaMemcpyFromSymbol(out8, bsim::bsim_pass_clk, sizeof(unsigned long long) * 8) != cudaSuccess) return -1;
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    return cudaMemcpyToSymbol(bsim::bsim_pass_clk, z, sizeof(z)) == cudaSuccess ? 0 : -1;
+}
+#endif
