@@ -225,6 +225,9 @@ template <> struct Ws<float> {
 #ifndef BSIM_SKIP_INACTIVE
 #define BSIM_SKIP_INACTIVE 1
 #endif
+#ifndef BSIM_DRIVE_POINT_OVERLAP   // revolute: the point row's impulse beside the drive row -- measured
+#define BSIM_DRIVE_POINT_OVERLAP 0    // 3 % slower (Ant 235 -> 242 us) and looser in fp32: off
+#endif
 #ifndef BSIM_LIMIT_VOTE   // warp-vote skip of inactive limit rows: measured 0.4-2 % slower, off
 #define BSIM_LIMIT_VOTE 0
 #endif
@@ -929,13 +932,14 @@ template <class R> BS_HD void axis_apply(bool lin, const JointOps<R> &o, R lam, 
 
 // PD drive / direct actuation / joint friction (physics.py:812-848)
 template <class R>
-BS_HD void row_drive(const Ctx<R> &c, const Ws<R> &w, int j, bool lin, R h, JointOps<R> &o, BV<R> &C, BV<R> &P) {
+BS_HD R row_drive(const Ctx<R> &c, const Ws<R> &w, int j, bool lin, R h, JointOps<R> &o, BV<R> &C, BV<R> &P) {
     R qd = axis_rate(c.d, w, j, lin, o, C, P);
     const R mfh = c.p.max_force * h;
     R lam = o.lf + clampr(o.da - o.db * qd, -mfh, mfh);
     if (o.frh > R(0)) lam = lam + clampr(-qd * o.meff, -o.frh, o.frh);
     axis_apply(lin, o, lam, C, P);
     o.imp += lam;
+    return lam;
 }
 
 // one-sided limit (physics.py:850-870)
@@ -997,8 +1001,33 @@ BS_HD void joint_rows(const Ctx<R> &c, const Ws<R> &w, int j, int kind, int dof,
         o.lb = w.l4(ij(d, j, JG) + 4).z;
         o.imp = w.at(idf(d, dof, DIMP));
     }
-    if (biased && axis) row_drive(c, w, j, lin, h, o, C, P);
-    if (kind != BSIM_PRISMATIC) row_linear(d, w, j, o, C, P);
+#if BSIM_DRIVE_POINT_OVERLAP
+    if (biased && axis && kind == BSIM_REVOLUTE) {
+        // the drive row moves only the angular velocities (w_c += y1 lam,
+        // w_p -= y2 lam), so the point row's input after it is
+        // rel0 + lam (y1 x rc + y2 x rp) and its impulse
+        // K^-1 (pe - rel0) - lam K^-1 (y1 x rc + y2 x rp): both parts are
+        // computed from the pre-drive velocities beside the drive row and
+        // joined by one FMA, instead of the point row waiting for the drive
+        // row's velocity update (the same values in exact arithmetic;
+        // DESIGN.md 8)
+        const V3<R> rc = w.l3(ij(d, j, JRC)), rp = w.l3(ij(d, j, JRP));
+        const S3<R> KI = w.lS(ij(d, j, JKI));
+        const V3<R> rel0 = (C.v + cross(C.w, rc)) - (P.v + cross(P.w, rp));
+        const V3<R> imp0 = smul(KI, w.l3(ij(d, j, JPE)) - rel0);
+        const V3<R> q = smul(KI, cross(o.y1, rc) + cross(o.y2, rp));
+        const R lam = row_drive(c, w, j, false, h, o, C, P);
+        const V3<R> imp = imp0 - q * lam;
+        C.v = C.v + imp * C.m;
+        C.w = C.w + smul(o.Ic, cross(rc, imp));
+        P.v = P.v - imp * P.m;
+        P.w = P.w - smul(o.Ip, cross(rp, imp));
+    } else
+#endif
+    {
+        if (biased && axis) row_drive(c, w, j, lin, h, o, C, P);
+        if (kind != BSIM_PRISMATIC) row_linear(d, w, j, o, C, P);
+    }
     if (kind != BSIM_SPHERICAL) row_angular(d, w, j, o, C, P);
     if (kind == BSIM_PRISMATIC) row_linear(d, w, j, o, C, P);
 #if defined(__CUDA_ARCH__) && BSIM_LIMIT_VOTE
