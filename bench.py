@@ -198,9 +198,14 @@ def measure(task, E, args, rank, world, clocks=None, policy=False, kernel=True, 
         from paper_2108_10470_b200.ppo import PPO
         agent = PPO(env.obs_dim, env.act_dim, device=dev)
 
+    policy_graph = None
+    if agent is not None:     # the policy as one CUDA graph (ppo.PolicyGraph): ~25 small kernels -> 1 launch
+        from paper_2108_10470_b200.ppo import PolicyGraph
+        policy_graph = PolicyGraph(agent.net, agent.gen, env.obs)
+
     def control_step(i):
         if agent is not None:
-            a, _, _ = agent.net.act(env.obs, agent.gen)
+            a, _, _ = policy_graph(env.obs)
             return env.step(a)
         return env.step(acts[i % len(acts)])
 
@@ -457,7 +462,7 @@ def run_gpu(args):
             r = measure(WORKLOADS[name][0], E, a2, rank, world, policy=True, kernel=False, e2e=False)
             others[f"{name}_ppo_rollout"] = {"value": r["value"], "unit": UNIT, "envs_per_gpu": E,
                                              "steps": a2.steps,
-                                             "note": "ActorCritic 256-128-64 act() + env.step per step"}
+                                             "note": "ActorCritic 256-128-64 act() (one CUDA graph) + env.step per step"}
     if rank != 0:
         if world > 1:
             dist.barrier()

@@ -48,3 +48,25 @@ def test_collect_rollout_shapes():
     adv, ret = gae_advantages(roll["rewards"], roll["values"], roll["dones"], roll["last_value"], 0.99, 0.95)
     assert adv.shape == (6, 128) and torch.isfinite(ret).all()
     env.close()
+
+
+def test_policy_graph_matches_eager_act():
+    """ppo.PolicyGraph (act() as one CUDA graph) returns what act() returns:
+    the value and log-probability of its own sample exactly as the eager
+    functions compute them, the sample's noise with the policy's std, and a
+    generator stream that continues across replays (no repeated noise)."""
+    import torch
+    from paper_2108_10470_b200.ppo import PPO, PolicyGraph
+    agent = PPO(60, 8, device="cuda")
+    obs = torch.randn(4096, 60, device="cuda")
+    pg = PolicyGraph(agent.net, agent.gen, obs)
+    a1, lp1, v1 = (x.clone() for x in pg(obs))
+    a2, _, _ = (x.clone() for x in pg(obs))
+    net = agent.net
+    with torch.no_grad():
+        mu = net.actor(obs)
+        assert torch.allclose(v1, net.value(obs), atol=1e-6)
+        assert torch.allclose(lp1, net._log_prob(mu, a1, net._log_std_c()), atol=1e-4)
+        z = (a1 - mu) / torch.exp(net._log_std_c())
+    assert abs(float(z.mean())) < 0.02 and abs(float(z.std()) - 1.0) < 0.02
+    assert not torch.equal(a1, a2)                     # the stream moved on between replays
