@@ -921,13 +921,15 @@ int bsim_step_smem_per_env(const bsim_layout_t *layout, int32_t fp64, int32_t *b
     if (bad_layout(layout)) return BSIM_E_INVALID;
     Dims d = make_dims(*layout, fp64 != 0);
     const bool large = fp64 ? use_large_variant<double>(d) : use_large_variant<float>(d);
-    // the large-articulation TU's CTA: 4 envs (fp32) / 2 envs (fp64)
-    const int ne = large ? (fp64 ? 2 : 4) : (fp64 ? Shape<double>::NE : Shape<float>::NE);
-    size_t total = (size_t)d.pad * ne * (fp64 ? 8 : 4) + 16 +
-                   (size_t)d.J * (fp64 ? sizeof(bsim_joint64_t) + 16 : sizeof(bsim_joint_t) + 16);
+    // the large-articulation TU's CTA (bsim_step_large.cu): 8 envs (fp32) / 2 envs (fp64)
+    const int ne = large ? (fp64 ? 2 : 8) : (fp64 ? Shape<double>::NE : Shape<float>::NE);
+    // too large only when ONE env's workspace and the joint table exceed the
+    // shared memory: the launch plan lowers the envs per CTA to what fits
+    size_t one_env = (size_t)d.pad * (fp64 ? 8 : 4) + 16 +
+                     (size_t)d.J * (fp64 ? sizeof(bsim_joint64_t) + 16 : sizeof(bsim_joint_t) + 16);
     if (bytes_per_env) *bytes_per_env = (int32_t)(d.pad * (fp64 ? 8 : 4));
     if (envs_per_cta) *envs_per_cta = ne;
-    return total > 227 * 1024 ? BSIM_E_TOO_LARGE : BSIM_OK;
+    return one_env > 227 * 1024 ? BSIM_E_TOO_LARGE : BSIM_OK;
 }
 
 int bsim_step(const bsim_layout_t *l, const bsim_params_t *p, const bsim_state_t *s, int32_t n,

@@ -1,12 +1,11 @@
 // bsim_step_large.cu -- the fused step kernel for large articulations.
 //
-// Same source as bsim_step.cu, compiled with a CTA of 4 envs x 32 threads
+// Same source as bsim_step.cu, compiled with a CTA of 8 envs x 32 threads
 // (fp32; fp64: 2 envs x 32) and its own namespace so the two instantiations
-// never collide.  The per-env workspace is item-major / env-minor with stride
-// NE + 1 = 5, so a 22-body / 21-joint / 22-slot humanoid (2,207 items, 8.8 KB
-// per env in fp32) fits 5 CTAs (20 envs, 20 warps) per SM instead of one
-// 16-env CTA (4 warps) with the default shape.  bsim_step.cu dispatches here
-// when its default CTA would leave fewer than 2 CTAs per SM.
+// never collide.  A 22-body / 21-joint / 22-slot humanoid (8.8 KB of
+// workspace per env in fp32) then runs 2 CTAs (16 envs, 16 warps) per SM
+// instead of one 16-env CTA (4 warps) with the default shape.  bsim_step.cu
+// dispatches here when its default CTA's workspace exceeds 113 KB.
 #define BSIM_LARGE_TU 1
 // fp32 CTA: 8 envs x 32 threads, >= 2 CTAs per SM (<= 128 registers).  The
 // sweep warp then carries 8 envs (4 lanes each) instead of 4: measured at
