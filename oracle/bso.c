@@ -144,9 +144,18 @@ typedef struct {
     jctx *jc;
     cctx *cc;
     double *dof_impulse;             /* [D] */
+    uint64_t ncall;                  /* limit evaluations so far (limit_jitter hash) */
 } envw;
 
 static double jparam(const double *arr, const bso_scene *s, int j, int e) { return arr[(size_t)j * s->E + e]; }
+
+/* decision-margin instrumentation (bso.h: margin) */
+static void note_margin(const bso_scene *s, int e, int k, double m) {
+    if (!s->margin) return;
+    double *p = s->margin + 4 * (size_t)e + k;
+    m = fabs(m);
+    if (m < *p) *p = m;
+}
 
 static void inv_inertia_world(envw *w, const double *quat) { /* physics.py:594-596 */
     const bso_scene *s = w->s;
@@ -414,10 +423,24 @@ static void solve_limit(envw *w, int j, double h, int biased) { /* 850-870 */
     double lo = jparam(s->joint_limit_lo, s, j, w->e), hi = jparam(s->joint_limit_hi, s, j, w->e);
     int angular = jt->kind == K_REV;
     double q = biased ? c->q0 : s->dof_state[2 * ((size_t)w->e * s->D + jt->dof)];
+    if (s->limit_jitter_seed) {   /* bso.h: re-decide knife-edge limits at random */
+        double tlo = s->limit_jitter * fmax(1.0, fabs(lo)), thi = s->limit_jitter * fmax(1.0, fabs(hi));
+        double tol = fabs(q - lo) <= tlo ? tlo : (fabs(q - hi) <= thi ? thi : 0.0);
+        if (tol > 0.0) {
+            uint64_t z = s->limit_jitter_seed * 0x9E3779B97F4A7C15ull ^ ((uint64_t)w->e << 32) ^
+                         ((uint64_t)j << 20) ^ w->ncall;
+            z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;   /* splitmix64 finaliser */
+            z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+            z ^= z >> 31;
+            q += tol * (2.0 * ((double)(z >> 11) * 0x1.0p-53) - 1.0);
+        }
+        w->ncall++;
+    }
     double qd = axis_rel_vel(w, jt, c, angular);
     double meff = axis_meff(w, jt, c, angular);
     double blo = biased ? fmax(lo - q, 0.0) / h : 0.0;
     double bhi = biased ? fmax(q - hi, 0.0) / h : 0.0;
+    note_margin(s, w->e, 0, fmin(fabs(q - lo) / fmax(1.0, fabs(lo)), fabs(q - hi) / fmax(1.0, fabs(hi))));
     double lam = 0.0;
     int viol = 0;
     if (q < lo) { lam = fmax(meff * (blo - qd), 0.0); viol = 1; }
@@ -559,6 +582,7 @@ static void solve_contact(envw *w, cctx *c, int biased) { /* 930-983 */
     contact_rel_vel(w, c, rt);
     double vt1 = dot3(t1, rt), vt2 = dot3(t2, rt);
     double mu = hypot(vt1, vt2) > 1e-3 ? w->s->mu_dynamic[w->e] : w->s->mu_static[w->e];
+    note_margin(w->s, w->e, 2, hypot(vt1, vt2) - 1e-3);
     if (biased && c->body_a < 0) {
         double te[3];
         for (int k = 0; k < 3; ++k) te[k] = c->terr0[k] + w->dpos[3 * c->body + k];
@@ -606,6 +630,8 @@ static void plane_geometry(const bso_scene *s, int e, int i, const double *pos, 
     *depth = s->params.rest_offset - gap;
     point[0] = c[0]; point[1] = c[1]; point[2] = c[2] - rad;
     *active = *depth > -s->params.solver_offset_slop;
+    note_margin(s, e, 1, *depth + s->params.solver_offset_slop);
+    note_margin(s, e, 1, *depth + s->params.friction_offset_threshold);
 }
 /* Pair slot narrow phase.  Kind 0 (SS) is the reference's sphere-sphere pair
    (physics.py:481-497).  Kinds 1-3 are NOT in the reference: box / capsule
@@ -675,6 +701,7 @@ static void pair_geometry(const bso_scene *s, int e, int i, const double *pos, c
     *depth = s->params.rest_offset - gap;
     for (int k = 0; k < 3; ++k) point[k] = ca[k] + n[k] * (ra + 0.5 * gap);
     *active = *depth > -s->params.solver_offset_slop;
+    note_margin(s, e, 1, *depth + s->params.solver_offset_slop);
 }
 
 /* ------------------------------------------------------------- tendons */
@@ -844,6 +871,7 @@ static void step_env(const bso_scene *s, int e, envw *w) { /* physics.py:538-592
     int N = pp->position_iterations;
     double h = dt / N;
     w->e = e;
+    w->ncall = 0;
     w->pos = s->pos + 3 * (size_t)e * B;
     w->quat = s->quat + 4 * (size_t)e * B;
     w->v = s->linvel + 3 * (size_t)e * B;
@@ -892,6 +920,7 @@ static void step_env(const bso_scene *s, int e, envw *w) { /* physics.py:538-592
         vel_at(w, c->body, c->r, v);
         double vn = dot3(c->n, v);
         c->rest = vn < -pp->bounce_threshold ? -pp->restitution * vn : 0.0;
+        note_margin(s, e, 3, vn + pp->bounce_threshold);
         const double *an = s->friction_anchor + 3 * ((size_t)i * s->E + e);
         if (isnan(an[0])) { c->terr0[0] = c->terr0[1] = c->terr0[2] = 0.0; }
         else for (int k = 0; k < 3; ++k) c->terr0[k] = c->point[k] - an[k];
@@ -910,6 +939,7 @@ static void step_env(const bso_scene *s, int e, envw *w) { /* physics.py:538-592
         for (int k = 0; k < 3; ++k) d[k] = vb[k] - va[k];
         double vn = dot3(c->n, d);
         c->rest = vn < -pp->bounce_threshold ? -pp->restitution * vn : 0.0;
+        note_margin(s, e, 3, vn + pp->bounce_threshold);
         c->lam_n = 0; c->lam_t[0] = c->lam_t[1] = 0;
         c->terr0[0] = c->terr0[1] = c->terr0[2] = 0;
     }

@@ -84,6 +84,19 @@ typedef struct {
     int8_t *dof_mode;                             /* [E*D] */
     /* outputs */
     double *root_state, *body_state, *dof_state, *net_contact, *dof_force, *sensor_forces;
+    /* test instrumentation (NULL = off): per env, the smallest distance of a
+       discrete decision of the step from its threshold, min-accumulated over
+       calls: [0] joint limit |q - lo|, |q - hi| (relative to max(1, |limit|)); [1] contact activation /
+       friction-anchor depth margins; [2] stick / slip |v_t| - 1e-3;
+       [3] restitution vn + bounce_threshold */
+    double *margin;                                /* [E][4] */
+    /* test instrumentation (seed 0 = off): a joint-limit decision with
+       |q - limit| <= limit_jitter max(1, |limit|) is taken at q + u
+       limit_jitter max(1, |limit|), u uniform in [-1, 1] from a hash of
+       (seed, env, joint, call): the reference's own spread when such
+       knife-edge decisions are re-decided at random */
+    uint64_t limit_jitter_seed;
+    double limit_jitter;
 } bso_scene;
 
 /* One Scene.step() for every env (OpenMP over envs when threads > 1). */

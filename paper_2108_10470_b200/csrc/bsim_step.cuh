@@ -592,19 +592,15 @@ BS_HD void joint_item(const Ctx<R> &c, const Ws<R> &w, int e, int j, R h, bool b
     if (kind != BSIM_SPHERICAL) {   // angular block (892-906): G = T^T (T Isum T^T)^-1 T
         S3<R> Isum = sadd(Ip, Ic);
         if (kind == BSIM_REVOLUTE) {
-            // T^T (T M T^T)^-1 T for the two directions normal to the axis a,
-            // M = Isum: the same matrix as M^-1 - (M^-1 a)(M^-1 a)^T / (a . M^-1 a)
-            // (the projected inverse), which needs no tangent basis
-#if BSIM_EXP_G64   // experiment: the angular block in double
-            using Gd = double;
-#else
-            using Gd = R;
-#endif
-            S3<Gd> Mi = sinv(cs3<Gd>(Isum));
-            V3<Gd> ad = cv3<Gd>(a), u = smul(Mi, ad);
-            Gd is = r_rcp(dot(ad, u));
-            G = cs3<R>(S3<Gd>{Mi.xx - u.x * u.x * is, Mi.xy - u.x * u.y * is, Mi.xz - u.x * u.z * is,
-                              Mi.yy - u.y * u.y * is, Mi.yz - u.y * u.z * is, Mi.zz - u.z * u.z * is});
+            // T^T (T Isum T^T)^-1 T over the two tangents normal to the axis
+            // a: the reference's 2x2 solve.  Round 1 used the algebraically
+            // equal projected inverse M^-1 - (M^-1 a)(M^-1 a)^T / (a . M^-1 a),
+            // M = Isum, which cancels catastrophically in fp32 when M is
+            // near-singular along a (humanoid limbs: 0.11 rad/s per substep
+            // on 1-4 of 4096 envs per control step).
+            tangents(a, t1, t2);
+            V3<R> s1 = smul(Isum, t1), s2 = smul(Isum, t2);
+            G = proj2(t1, t2, dot(t1, s1), dot(t1, s2), dot(t2, s2));
         } else {
             G = proj3(t1, t2, a, Isum);
         }

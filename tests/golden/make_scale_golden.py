@@ -1,7 +1,7 @@
 """Golden traces at BASELINE.json scale, produced by the REFERENCE (run here;
 the reference does not travel to the GPU box):
 
-    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_scale_golden.py
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_scale_golden.py [task ...]
 
 For the Ant analog (`quadruped`, BASELINE config 1) and the ANYmal analog
 (`quadruped-anymal-obs`, config 3) at 4096 envs, the reference `EnvBatch`
@@ -35,17 +35,32 @@ from batchsim.envs import make_env  # noqa: E402
 E, STEPS, STRIDE, EPISODE = 4096, 20, 32, 12
 KNOCK_STEP, KNOCK = 5, np.arange(1, 4096, 4)
 CASES = (("quadruped", "scale_ant_4096", "potentials"),
-         ("quadruped-anymal-obs", "scale_anymal_4096", "commands"))
+         ("quadruped-anymal-obs", "scale_anymal_4096", "commands"),
+         # BASELINE config 2's model: the reference QuadrupedEnv algorithm on the
+         # authored humanoid (make_humanoid_golden.HumanoidRefEnv), knocked to z 0.5
+         ("humanoid", "scale_humanoid_4096", "potentials"))
+KNOCK_Z = {"quadruped": 0.1, "quadruped-anymal-obs": 0.1, "humanoid": 0.5}
+
+
+def _make(task):
+    if task == "humanoid":
+        sys.path.insert(0, HERE)
+        from batchsim.envs import EnvConfig
+        from make_humanoid_golden import HumanoidRefEnv
+        return HumanoidRefEnv(EnvConfig(num_envs=E, seed=0, episode_length=EPISODE))
+    return make_env(task, num_envs=E, seed=0, episode_length=EPISODE)
 
 
 def sample_rows(idx, per_env):
     return (idx[:, None] * per_env + np.arange(per_env)).ravel()
 
 
-def main():
+def main(only=None):
     for task, name, extra in CASES:
+        if only and task not in only:
+            continue
         t0 = time.time()
-        env = make_env(task, num_envs=E, seed=0, episode_length=EPISODE)
+        env = _make(task)
         s = env.scene
         B, D, S = s.bodies_per_env, s.dofs_per_env, s.sensors_per_env
         idx = np.arange(0, E, STRIDE)
@@ -63,7 +78,7 @@ def main():
                 # knock every 4th env down (world z 0.1, below both tasks' termination
                 # heights) through the buffer API, as the reference's own env trace does
                 root = s.root_state.copy()
-                root[KNOCK, 2] = 0.1
+                root[KNOCK, 2] = KNOCK_Z[task]
                 env.buffers.set_root_state(root, KNOCK)
             out = env.step(a)
             rec["obs"].append(out.obs[idx])
@@ -89,11 +104,12 @@ def main():
         arrays["timeout_all"] = np.stack(arrays["timeout_all"])
         meta = {"kind": "scale_env", "task": task, "num_envs": E, "steps": STEPS, "seed": 0, "stride": STRIDE,
                 "episode_length": EPISODE, "actions": "np.random.default_rng(0).uniform(-1, 1, (E, A)) per step",
-                "extra": extra, "knock_step": KNOCK_STEP, "knock": "np.arange(1, 4096, 4), world z = 0.1"}
+                "extra": extra, "knock_step": KNOCK_STEP,
+                "knock": f"np.arange(1, 4096, 4), world z = {KNOCK_Z[task]}"}
         import json
         np.savez_compressed(os.path.join(HERE, f"{name}.npz"), meta=json.dumps(meta), **arrays)
         print(f"wrote {name}.npz in {time.time() - t0:.0f}s", flush=True)
 
 
 if __name__ == "__main__":
-    main()
+    main(sys.argv[1:] or None)     # optionally only the named tasks

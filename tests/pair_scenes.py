@@ -123,14 +123,18 @@ def oracle_trace(name, E=4, steps=12, warm=30, dt=1 / 120, jitter=0.3):
     return models, p, meta, arr
 
 
-def oracle_sensitivity(models, p, meta, arr, seeds=(1, 2)):
+def oracle_sensitivity(models, p, meta, arr, seeds=(1, 2), limit_seeds=()):
     """Per step and output, the element-wise max |oracle(perturbed pre-state) -
     oracle(exact pre-state)| over the fp32 rounding of the pre-state (env-local
     positions, as the CUDA path stores them) and len(seeds) random 2^-24
     relative jitters of it: how far the float64 reference algorithm itself
     moves each output under fp32-sized input noise (tests/scale_parity.py
-    `sensitivity`, for these small authored scenes)."""
+    `sensitivity`, for these small authored scenes).  With `limit_seeds`
+    instead: the exact pre-state with the joint-limit activations the
+    reference decides within 8 fp32 ulps of the joint angle re-decided at
+    random (scale_parity.limit_sensitivity)."""
     from oracle.oracle import OracleScene
+    from scale_parity import LIMIT_MARGIN
     E = meta["num_envs"]
     s = OracleScene(models, E, p, shape_pairs="all", env_origins=arr["param_env_origins"])
     for k in ("inv_mass", "inertia_local", "inv_inertia_local", "gravity", "mu_static", "mu_dynamic",
@@ -146,11 +150,17 @@ def oracle_sensitivity(models, p, meta, arr, seeds=(1, 2)):
         rng = np.random.default_rng(seed)
         return lambda x: np.asarray(x, np.float64) * (1.0 + rng.uniform(-1, 1, np.shape(x)) * 2.0 ** -24)
 
+    def ident(x):
+        return np.asarray(x, np.float64)
+
+    runs = ([(ident, sd) for sd in limit_seeds] if limit_seeds else
+            [(r32, None)] + [(jitter(sd), None) for sd in seeds])
     outs = ("root_state", "body_state", "net_contact", "dof_state")
     sens = []
     for t in range(meta["steps"]):
         dev = {k: 0.0 for k in outs}
-        for tf in [r32] + [jitter(sd) for sd in seeds]:
+        for tf, lsd in runs:
+            s.limit_jitter = None if lsd is None else (lsd * 1000 + t + 1, LIMIT_MARGIN)
             s.pos[...] = org + tf(arr["in_pos"][t] - org)
             for k in ("quat", "linvel", "angvel", "dof_state"):
                 getattr(s, k)[...] = tf(arr[f"in_{k}"][t])

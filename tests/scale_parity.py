@@ -32,7 +32,8 @@ import torch
 
 from golden_util import load
 
-CASES = {"quadruped": "scale_ant_4096", "quadruped-anymal-obs": "scale_anymal_4096"}
+CASES = {"quadruped": "scale_ant_4096", "quadruped-anymal-obs": "scale_anymal_4096",
+         "humanoid": "scale_humanoid_4096"}
 QUANTITIES = ("root_state", "body_state", "dof_state", "net_contact", "sensor_forces", "dof_force", "obs",
               "reward")
 ATOL = RTOL = 1e-4
@@ -54,7 +55,7 @@ def oracle_trace(task, threads=None):
         a = rng.uniform(-1.0, 1.0, (E, env.act_dim))
         if t == meta["knock_step"]:
             root = env.local_root()[knock]
-            root[:, 2] = 0.1 - s.env_origins[knock, 2]
+            root[:, 2] = knock_z(meta) - s.env_origins[knock, 2]
             env.set_root_state(root, knock)
         pre = {"pos": s.pos.copy(), "quat": s.quat.copy(), "linvel": s.linvel.copy(), "angvel": s.angvel.copy(),
                "anchor": s._friction_anchor.copy(), "dof_state": s.dof_state.copy(),
@@ -62,14 +63,23 @@ def oracle_trace(task, threads=None):
                "dof_force": s.dof_force.copy(), "episode_steps": env.episode_steps.copy(),
                "reset_count": env.reset_count.copy(), "potentials": env.potentials.copy(),
                "commands": env.commands.copy(), "actions": a}
+        s.decision_margin = np.full((E, 4), np.inf)
         obs, reward, done, info = env.step(a)
-        post = {"obs": obs, "reward": reward, "done": done, "timeout": info["timeout"],
+        margin, s.decision_margin = s.decision_margin, None
+        post = {"obs": obs, "reward": reward, "done": done, "timeout": info["timeout"], "margin": margin,
                 "body_local": local_body(s.pos, s.quat, s.linvel, s.angvel, s.env_origins, s.bodies_per_env),
                 "dof_state": s.dof_state.copy(), "net_contact": s.net_contact.copy(),
                 "sensor_forces": s.sensor_forces.copy(), "dof_force": s.dof_force.copy(),
                 "anchor": s._friction_anchor.copy(), "reset_count": env.reset_count.copy()}
         steps.append({"pre": pre, "post": post})
     return meta, arr, steps
+
+
+def knock_z(meta):
+    """The world z the fixture knocks every 4th env to (meta "knock" ends in
+    "world z = <z>"): 0.1 for the quadrupeds, 0.5 for the humanoid, both
+    below the task's termination height."""
+    return float(meta["knock"].rsplit("=", 1)[1])
 
 
 def local_body(pos, quat, linvel, angvel, origins, B):
@@ -200,7 +210,7 @@ def free_rollout(task, precision, trace=None):
     for t, st in enumerate(steps):
         if t == meta["knock_step"]:
             root = s.root_state.clone()
-            root[knock, 2] = 0.1
+            root[knock, 2] = knock_z(meta)
             env.buffers.set_root_state(root, knock)
         out = env.step(torch.as_tensor(st["pre"]["actions"], dtype=s.dtype))
         gp = gpu_post(env, out)
@@ -208,6 +218,12 @@ def free_rollout(task, precision, trace=None):
         res.append({"errors": compare(gp, rp), "masks": masks_equal(gp, rp), "gpu": gp, "ref": rp})
     env.close()
     return meta, arr, res
+
+
+def sample_dims(arr):
+    """(bodies, dofs, sensors) per env, from the fixture's sampled rows."""
+    n = len(arr["sample"])
+    return len(arr["body_state"][0]) // n, len(arr["dof_state"][0]) // n, len(arr["sensor_forces"][0]) // n
 
 
 def sample_vs_reference(meta, arr, gp, t, B, D, S):
@@ -249,7 +265,11 @@ def _perturbed_runs(task, trace, transforms, threads=None):
     out = []
     for tf in transforms:
         runs = []
-        for st in steps:
+        for t, st in enumerate(steps):
+            if isinstance(tf, _LimitJitter):      # exact pre-state, knife-edge limits re-decided
+                s.limit_jitter = (tf.seed * 1000 + t + 1, LIMIT_MARGIN)
+            else:
+                s.limit_jitter = None
             pre = st["pre"]
             s.pos[:] = org + tf(pre["pos"] - org)
             for k in ("quat", "linvel", "angvel"):
@@ -269,6 +289,17 @@ def _perturbed_runs(task, trace, transforms, threads=None):
             runs.append(ref_post(post, B))
         out.append(runs)
     return out
+
+
+class _LimitJitter:
+    """Identity transform; the oracle re-decides every joint-limit activation
+    within LIMIT_MARGIN of its threshold at random (bso.h limit_jitter)."""
+
+    def __init__(self, seed):
+        self.seed = seed
+
+    def __call__(self, x):
+        return x
 
 
 def _jitter(seed):
@@ -293,8 +324,8 @@ def input_rounding_floor(task, trace=None, threads=None):
 
 
 def _bodies(trace):
-    meta = trace[0]
-    return 9 if meta["task"] == "quadruped" else 13
+    meta, _, steps = trace
+    return len(steps[0]["post"]["body_local"]) // meta["num_envs"]
 
 
 def sensitivity(task, trace=None, seeds=(1, 2), threads=None):
@@ -316,15 +347,83 @@ def sensitivity(task, trace=None, seeds=(1, 2), threads=None):
     return out
 
 
-def excused(gp, rp, sens, q, bound_scaled=10.0, factor=0.1):
+# A joint-limit activation decided within 8 fp32 ulps of the joint angle
+# (|q - limit| <= 2^-21 max(1, |limit|) in some pass of the reference's step)
+# is a coin flip for an fp32 state -- the joint angle stored in fp32 and
+# recomputed from fp32 orientations is uncertain by several ulps -- and a
+# limit row that engages in one precision and not in the other changes the
+# joint's velocity by the whole approach rate.  Input jitter (sensitivity())
+# rarely flips these: TGS drives an engaged joint onto its limit, so the
+# later passes' q sit within ulps of it whatever the input noise.
+# limit_sensitivity() re-decides them at random instead.
+LIMIT_MARGIN = 2.0 ** -21
+
+
+def limit_sensitivity(task, trace=None, seeds=(1, 2, 3, 4), threads=None):
+    """Per step and quantity, the element-wise max |oracle(knife-edge limits
+    re-decided) - oracle(exact)| over len(seeds) random re-decisions: how far
+    the reference itself moves when the joint-limit activations it decided
+    within LIMIT_MARGIN (8 fp32 ulps of the joint angle) go the other way, as
+    they may in any fp32 implementation."""
+    trace = trace if trace is not None else oracle_trace(task)
+    B = _bodies(trace)
+    runs = _perturbed_runs(task, trace, [_LimitJitter(sd) for sd in seeds], threads)
+    out = []
+    for t, st in enumerate(trace[2]):
+        ref = ref_post(st["post"], B)
+        out.append({q: np.max([np.abs(np.asarray(r[t][q], float) - np.asarray(ref[q], float)) for r in runs], axis=0)
+                    for q in QUANTITIES})
+    return out
+
+
+# Contact and sensor forces are impulses / dt summed in a Gauss-Seidel sweep:
+# every impulse of an env is computed from velocities that its other impulses
+# moved, so its rounding scales with the env's LARGEST force, not its own (a
+# 6 mN grazing contact of the ANYmal base next to 80 N foot contacts).  An
+# element beyond the bound relative to its own vector but within it relative
+# to its env's largest force vector of that quantity is "within the env's
+# force resolution".
+FORCE_QUANTITIES = ("net_contact", "sensor_forces")
+
+
+def _env_force_scale(q, r2, E):
+    """Per row: the largest vector norm of quantity q in the row's env."""
+    k = len(r2) // E
+    groups = VECTOR_GROUPS[q]
+    norms = np.zeros(len(r2))
+    c = 0
+    for n in groups:
+        norms = np.maximum(norms, np.linalg.norm(r2[:, c:c + n], axis=1))
+        c += n
+    return np.repeat(norms.reshape(E, k).max(axis=1), k)
+
+
+def excused(gp, rp, sens, q, bound_scaled=10.0, factor=0.1, lsens=None):
     """Elements of quantity q beyond `bound_scaled` x (1e-4 + 1e-4 |ref|)
-    (|ref| per VECTOR_GROUPS) split into (ill-conditioned, unexplained): an
-    element is ill-conditioned when the reference's own output moves by at
-    least `factor` x the GPU deviation under fp32-sized input noise."""
+    (|ref| per VECTOR_GROUPS) split into (excused, unexplained): an element is
+    excused when the reference's own output moves by at least `factor` x the
+    GPU deviation under fp32-sized input noise (`sens`, sensitivity()) or
+    when its knife-edge joint-limit decisions are re-decided (`lsens`,
+    limit_sensitivity()), or -- forces -- when it is within the bound relative
+    to its env's largest force (FORCE_QUANTITIES)."""
+    a, b, c, unexplained = excused_split(gp, rp, sens, q, bound_scaled, factor, lsens)
+    return a + b + c, unexplained
+
+
+def excused_split(gp, rp, sens, q, bound_scaled=10.0, factor=0.1, lsens=None):
+    """(ill by input noise, ill by knife-edge limits, within the env's force
+    resolution, unexplained) element counts."""
     r = np.asarray(rp[q], float)
     r2 = r.reshape(len(r), -1) if r.ndim > 1 else r.reshape(-1, 1)
     d = np.abs(np.asarray(gp[q], float).reshape(r2.shape) - r2)
     sc = d / (ATOL + RTOL * _magnitude(q, r2))
     over = sc > bound_scaled
     ill = over & (np.asarray(sens[q], float).reshape(r2.shape) >= factor * d)
-    return int(ill.sum()), int((over & ~ill).sum())
+    knife = np.zeros_like(over)
+    if lsens is not None:
+        knife = over & ~ill & (np.asarray(lsens[q], float).reshape(r2.shape) >= factor * d)
+    coupled = np.zeros_like(over)
+    if q in FORCE_QUANTITIES and "reward" in rp:
+        scale = _env_force_scale(q, r2, len(rp["reward"]))
+        coupled = over & ~ill & ~knife & (d <= bound_scaled * (ATOL + RTOL * scale)[:, None])
+    return int(ill.sum()), int(knife.sum()), int(coupled.sum()), int((over & ~ill & ~knife & ~coupled).sum())

@@ -29,25 +29,26 @@ def test_step_matches_oracle_teacher_forced(name, precision):
     of the element's vector, tests/scale_parity.py) -- except elements the
     float64 reference itself cannot resolve at fp32: its output moves by at
     least 10 % of the GPU deviation when its pre-state is rounded to fp32 or
-    jittered by 2^-24 relative (pair_scenes.oracle_sensitivity).  The Franka
-    arm (light roll links in a kp-2000 drive chain, pad-cube contact events)
-    and the Shadow Hand (gram-scale phalanges, I ~ 1e-6 kg m^2: rounding only
-    the inputs of one step moves finger angular velocities by 50-260x the
-    1e-3 bound) are where this matters.  The hand in fp32 is worse than its
-    input conditioning: fp32 ARITHMETIC on the phalanges' 1e-6 kg m^2 inertias
-    under kp-drives and explicit tendon springs departs from the float64
-    trajectory by up to ~2 rad/s in one step on a few fingers (the float64
-    path matches at 1e-8), so for it the count of such elements is reported
-    and bounded (<= 10 %) rather than required to be 0.  Evaluating the
-    world inverse inertias, the angular blocks, the point blocks and the joint
-    geometry of phase A in double changes the count by < 3 %
-    (BSIM_EXP_I64 / G64 / K64, BSIM_GEOM_F64): the loss is in the fp32 sweep
-    itself, where gram-scale links meet the palm in one row."""
+    jittered by 2^-24 relative, or when the joint-limit activations it
+    decides within 8 fp32 ulps of the joint angle are re-decided at random
+    (pair_scenes.oracle_sensitivity, with and without `limit_seeds`).  The
+    Franka arm (light roll links in a kp-2000 drive chain, pad-cube contact
+    events) and the Shadow Hand are where this matters.  The hand's fingers
+    rest on their joint limits: TGS drives an engaged joint onto the limit,
+    so the next passes decide the limit row at |q - limit| ~ 1e-13..1e-8
+    (oracle decision margins) -- a coin flip at fp32 resolution, and a flip
+    changes the finger's velocity by its whole approach rate (up to ~2 rad/s
+    on gram-scale phalanges).  The reference itself, with those decisions
+    re-decided, reproduces the GPU values (tools/hand_fp32_probe.py: the host
+    build of the kernel, 381 + 1312 of 21216 elements excused, 0
+    unexplained).  So for every scene: 0 unexplained elements; the excused
+    count is 0 except on the hand, where it is reported and bounded (<= 10 %)."""
     import scale_parity as SP
     from pair_scenes import oracle_sensitivity
     models, p, meta, arr = oracle_trace(name)
     s = _gpu(models, p, meta["num_envs"], precision, arr)
     sens = oracle_sensitivity(models, p, meta, arr) if precision == "fp32" else None
+    lsens = oracle_sensitivity(models, p, meta, arr, limit_seeds=tuple(range(1, 17))) if precision == "fp32" else None
     n_ill = n_bad = n_all = 0
     hand = name == "shadow_hand_cube"
     for t in range(meta["steps"]):
@@ -60,8 +61,8 @@ def test_step_matches_oracle_teacher_forced(name, precision):
                 e = rel_err(got[k], arr[f"out_{k}"][t], 1e-8, 1e-8)
                 assert e <= 1.0, (name, precision, t, k, e)
                 continue
-            ill, unexplained = SP.excused({k: got[k]}, {k: arr[f"out_{k}"][t]}, sens[t], k)
-            assert hand or unexplained == 0, (name, t, k, unexplained)
+            ill, unexplained = SP.excused({k: got[k]}, {k: arr[f"out_{k}"][t]}, sens[t], k, lsens=lsens[t])
+            assert unexplained == 0, (name, t, k, unexplained)
             n_ill += ill
             n_bad += unexplained
             n_all += got[k].size
@@ -69,10 +70,8 @@ def test_step_matches_oracle_teacher_forced(name, precision):
         print(f"{name}: {n_ill} of {n_all} elements beyond 1e-3 and ill-conditioned in the reference itself, "
               f"{n_bad} beyond 1e-3 otherwise")
         if hand:
-            # the hand in fp32: see the docstring -- a reported bound, not the per-step contract
-            # (measured: 1222 + 535 of 21216 elements; the host build of the same kernel 1637 of
-            # 19968, and float64 arithmetic on fp32-rounded inputs alone 242 -- tools/hand_fp32_probe.py)
-            assert n_bad + n_ill <= 0.10 * n_all, (n_bad, n_ill, n_all)
+            # fingers on their limits (docstring): excused elements reported and bounded
+            assert n_ill <= 0.10 * n_all, (n_ill, n_all)
         else:
             assert n_ill == 0, (name, n_ill)
 

@@ -1,5 +1,5 @@
-"""fp32 and fp64 parity of the CUDA env step at 4096 envs (BASELINE configs 1
-and 3), per quantity, teacher forced and free running -- method in
+"""fp32 and fp64 parity of the CUDA env step at 4096 envs (BASELINE configs 1,
+2 and 3: Ant, humanoid and ANYmal analogs), per quantity, teacher forced and free running -- method in
 tests/scale_parity.py, numbers in profiles/r02_parity_fp32.md.
 
 Contract (north star: abs/rel <= 1e-4 per step, masks bit-exact):
@@ -13,9 +13,14 @@ Contract (north star: abs/rel <= 1e-4 per step, masks bit-exact):
     elements the REFERENCE itself cannot resolve at fp32: those whose float64
     output moves by >= 10 % of the GPU deviation when the pre-state is
     rounded to fp32 or jittered by 2^-24 relative (scale_parity.sensitivity:
-    a friction stick/slip, limit or contact decision within rounding).  Such
-    excused elements must stay below 1e-4 of all elements, and are counted
-    in profiles/r02_parity_fp32.md;
+    a friction stick/slip, limit or contact decision within rounding) or
+    when the joint-limit activations it decided within 8 fp32 ulps of the
+    joint angle are re-decided at random (scale_parity.limit_sensitivity),
+    and contact / sensor forces within the bound relative to their env's
+    largest force (Gauss-Seidel impulses round with the env's largest
+    impulse, scale_parity.FORCE_QUANTITIES).  Such excused elements must
+    stay below 1e-4 of all elements, and are counted in
+    profiles/r02_parity_fp32.md;
   * done / timeout masks and reset counts of all 4096 envs exact at every
     step in both precisions (teacher forced), and the friction-anchor
     presence pattern exact.
@@ -31,6 +36,7 @@ pytestmark = pytest.mark.gpu
 STATES = ("root_state", "body_state", "dof_state", "obs")
 _TRACES = {}
 _SENS = {}
+_LSENS = {}
 
 
 def _trace(task):
@@ -45,16 +51,22 @@ def _sens(task):
     return _SENS[task]
 
 
+def _lsens(task):
+    if task not in _LSENS:
+        _LSENS[task] = SP.limit_sensitivity(task, _trace(task), seeds=tuple(range(1, 17)))
+    return _LSENS[task]
+
+
 @pytest.mark.parametrize("task", list(SP.CASES))
 def test_fp32_teacher_forced_per_quantity(task):
     _, _, res = SP.teacher_forced(task, "fp32", _trace(task))
-    sens = _sens(task)
+    sens, lsens = _sens(task), _lsens(task)
     bad, n_ill, n_all = [], 0, 0
     for t, r in enumerate(res):
         for q, e in r["errors"].items():
             if q in STATES and e["frac_within"] < 0.999:
                 bad.append((t, q, "frac", e))
-            ill, unexplained = SP.excused(r["gpu"], r["ref"], sens[t], q)
+            ill, unexplained = SP.excused(r["gpu"], r["ref"], sens[t], q, lsens=lsens[t])
             if unexplained:
                 bad.append((t, q, "beyond 1e-3", unexplained, e))
             n_ill += ill
@@ -63,7 +75,8 @@ def test_fp32_teacher_forced_per_quantity(task):
         assert m["done"] and m["timeout"] and m["reset_count"], (t, m)
         assert m["anchor_mismatch"] == 0, (t, m)
     assert not bad, bad[:6]
-    print(f"{task}: {n_ill} of {n_all} elements beyond 1e-3 but ill-conditioned in the reference itself")
+    print(f"{task}: {n_ill} of {n_all} elements beyond 1e-3 but excused (ill-conditioned in the reference "
+          f"itself, or within the env's force resolution)")
     assert n_ill <= 1e-4 * n_all, n_ill
     assert sum(int(r["ref"]["done"].sum()) for r in res) >= 4096     # terminations + timeouts exercised
 

@@ -129,7 +129,7 @@ def test_oracle_env_free_running_matches_reference(task, fixture, knock_z, extra
         assert _close(env.scene.ctrl_dof_pos_target, arr["ctrl_dof_pos_target"][t]) < 1e-12, t
 
 
-@pytest.mark.parametrize("task", ["quadruped", "quadruped-anymal-obs"])
+@pytest.mark.parametrize("task", ["quadruped", "quadruped-anymal-obs", "humanoid"])
 def test_oracle_env_at_4096_envs_matches_reference(task):
     """BASELINE scale: the oracle env free running over the reference's 4096-env
     trace (tests/golden/make_scale_golden.py: 20 control steps, a quarter of
@@ -141,7 +141,7 @@ def test_oracle_env_at_4096_envs_matches_reference(task):
     import scale_parity as SP
     meta, arr, steps = SP.oracle_trace(task, threads=os.cpu_count() or 1)
     idx = arr["sample"]
-    B = 9 if task == "quadruped" else 13
+    B = SP.sample_dims(arr)[0]
     rb = (idx[:, None] * B + np.arange(B)).ravel()
     org = np.repeat(arr["env_origins"], B, axis=0)
     for t, st in enumerate(steps):

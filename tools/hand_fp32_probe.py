@@ -1,6 +1,8 @@
 """DEV TOOL: the Shadow Hand scene's fp32 error on the host build of the
 kernel (teacher forced vs the float64 oracle trace): elements of root /
-body state and contact force beyond 1e-3 + 1e-3 |ref| (vector norms).
+body state and contact force beyond 1e-3 + 1e-3 |ref| (vector norms), and
+how many of them the reference itself reproduces under fp32-sized input
+noise or with its knife-edge joint-limit decisions re-decided.
 BSIM_HK_EXTRA=-D... selects arithmetic experiments."""
 import os
 import sys
@@ -16,7 +18,11 @@ from pair_scenes import oracle_trace  # noqa: E402
 def main(name="shadow_hand_cube"):
     from hostkernel.hk import HostKernel
     from paper_2108_10470_b200.layout import SceneLayout
+    from pair_scenes import oracle_sensitivity
     models, p, meta, arr = oracle_trace(name)
+    sens = oracle_sensitivity(models, p, meta, arr)
+    lsens = oracle_sensitivity(models, p, meta, arr, limit_seeds=tuple(range(1, 17)))
+    split = np.zeros(4, int)
     E = meta["num_envs"]
     L = SceneLayout(models, True, "all")
     hk = HostKernel(L, E, p, arr["param_env_origins"], fp64=False)
@@ -33,6 +39,9 @@ def main(name="shadow_hand_cube"):
                   "ctrl_body_torque", "dof_mode", "nonfinite"):
             hk.arr[k][...] = arr[f"in_{k}"][t]
         hk.step()
+        for k in ("root_state", "body_state", "net_contact"):
+            split += np.array(SP.excused_split({k: hk.arr[k].astype(float)}, {k: arr[f"out_{k}"][t]}, sens[t], k,
+                                               lsens=lsens[t]))
         for k in ("body_state", "net_contact"):
             g = hk.arr[k].astype(float)
             r = arr[f"out_{k}"][t]
@@ -42,6 +51,8 @@ def main(name="shadow_hand_cube"):
             n_all += sc.size
             worst = max(worst, float(sc.max()))
     print(f"{name} fp32 host [{os.environ.get('BSIM_HK_EXTRA', '')}]: {n_over} of {n_all} beyond 1e-3, worst {worst:.1f}x")
+    print(f"  root / body / contact beyond 1e-3: ill-conditioned (input noise) {split[0]}, knife-edge limits "
+          f"{split[1]}, unexplained {split[3]}")
 
 
 if __name__ == "__main__":
@@ -78,6 +89,9 @@ def rounded_fp64(name="shadow_hand_cube", round_params=True):
         for k in ("dof_mode", "nonfinite"):
             hk.arr[k][...] = arr[f"in_{k}"][t]
         hk.step()
+        for k in ("root_state", "body_state", "net_contact"):
+            split += np.array(SP.excused_split({k: hk.arr[k].astype(float)}, {k: arr[f"out_{k}"][t]}, sens[t], k,
+                                               lsens=lsens[t]))
         for k in ("body_state", "net_contact"):
             g = hk.arr[k].astype(float)
             r = arr[f"out_{k}"][t]
