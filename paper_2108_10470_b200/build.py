@@ -49,13 +49,17 @@ def up_to_date(out=OUT):
     return all(os.path.getmtime(d) <= t for d in deps())
 
 
-def build(force=False, verbose=False, ieee=False):
+def build(force=False, verbose=False, ieee=False, variant=None):
+    """variant: a dev experiment build, _lib/libbsim_b200_<variant>.so with
+    BSIM_NVCC_EXTRA's flags (loaded with BSIM_LIB_VARIANT=<variant>)."""
     out = OUT_IEEE if ieee else OUT
+    if variant:
+        out = os.path.join(HERE, "_lib", f"libbsim_b200_{variant}.so")
     if not force and up_to_date(out):
         return out
     os.makedirs(os.path.dirname(out), exist_ok=True)
     from concurrent.futures import ThreadPoolExecutor
-    tag = "_ieee" if ieee else ""
+    tag = "_ieee" if ieee else (f"_{variant}" if variant else "")
 
     def compile_one(src):
         obj = os.path.join(HERE, "_lib", os.path.basename(src)[:-3] + tag + ".o")
