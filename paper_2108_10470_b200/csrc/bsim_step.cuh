@@ -222,6 +222,9 @@ template <> struct Ws<float> {
 // hand_fp32_probe.py: no change), kept so the finding can be re-measured
 // contact slots that are inactive this substep (depth <= -slop at the freeze)
 // skip their row constants and rows (measurement variant: BSIM_SKIP_INACTIVE=0)
+#ifndef BSIM_SCHED_WARPS
+#define BSIM_SCHED_WARPS 1   // warps running the row-schedule sweep (bsim_step_large.cu sets its own)
+#endif
 #ifndef BSIM_SKIP_INACTIVE
 #define BSIM_SKIP_INACTIVE 1
 #endif
@@ -1690,12 +1693,15 @@ template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> 
             {
 #if defined(__CUDA_ARCH__)
                 if (!topo_register_sweep<T>() && c.L.sched_stages > 0) {
-                    // the row schedule on the claimed sweep warp: 32 / NE lanes per env (the
-                    // CTA's envs share one warp, as the one-lane sweep did, so the issue
-                    // cost stays one warp's while a stage's rows run side by side)
-                    constexpr int NE = Shape<R>::NE, LPE = NE >= 32 ? 1 : 32 / NE;
+                    // the row schedule on BSIM_SCHED_WARPS warps from the claimed sweep
+                    // warp on: 32 SW / NE lanes per env, each env's lanes inside one warp
+                    // (a stage's rows run side by side; a stage ends at a __syncwarp)
+                    constexpr int NE = Shape<R>::NE, NW = Shape<R>::NTH / 32;
+                    constexpr int SW = BSIM_SCHED_WARPS < NW ? BSIM_SCHED_WARPS : NW;
+                    constexpr int LPE = NE >= 32 * SW ? 1 : (32 * SW / NE > 32 ? 32 : 32 * SW / NE);
+                    static_assert(32 % LPE == 0, "an env's sweep lanes must share a warp");
                     const int t = (g.tid - g.lane0 + g.nth) % g.nth;
-                    if (t < 32) {
+                    if (t < 32 * SW) {
                         const int el = t / LPE, lane = t % LPE;
                         const Ws<R> w = g.env(el);
                         sweep_sched<R>(c, el < g.ne ? &w : nullptr, h, biased, lane, LPE, 0xffffffffu);

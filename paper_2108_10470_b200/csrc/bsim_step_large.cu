@@ -33,5 +33,10 @@
 #define BSIM_LARGE_SUBGROUPS 1   // 4 = one warp per env with its own named barrier: measured 1804 -> 2417 us
 #endif                           // per 16384-env humanoid step, so the CTA stays whole
 #define BSIM_SUBGROUPS BSIM_LARGE_SUBGROUPS
+#ifndef BSIM_LARGE_SCHED_WARPS   // the row-schedule sweep on 4 warps (16 lanes per env): measured
+#define BSIM_LARGE_SCHED_WARPS 4    // humanoid 16384 envs 1610 -> 1541 us per control step (phased
+#endif                              // schedule; 2 warps 1586), Shadow Hand / Franka unchanged
+#undef BSIM_SCHED_WARPS
+#define BSIM_SCHED_WARPS BSIM_LARGE_SCHED_WARPS
 #define bsim bsim_large
 #include "bsim_step.cu"

@@ -371,9 +371,9 @@ class SceneLayout:
         return cost
 
     def _sweep_lanes(self):
-        """Lanes per env the kernel gives the schedule: 4 on the large-
-        articulation CTA (8 envs share the sweep warp), 2 on the default one
-        (16 envs).  Mirrors csrc: make_dims' record size (BODY 36, JOINT 44,
+        """Lanes per env the kernel gives the schedule: 16 on the large-
+        articulation CTA (8 envs on 4 sweep warps, BSIM_LARGE_SCHED_WARPS), 2
+        on the default one (16 envs share one warp).  Mirrors csrc: make_dims' record size (BODY 36, JOINT 44,
         PLANE 28, PAIR 76, ANCHOR 4, DOF 2 items, ENV 8, pad = 4 mod 8) and
         use_large_variant (a 16-env fp32 workspace over 113 KB)."""
         items = (36 * self.bodies_per_env + 44 * self.joints_per_env + 28 * self.planes_per_env +
@@ -381,18 +381,20 @@ class SceneLayout:
         items = ((items + 3) & ~3) + 8
         while items % 8 != 4:
             items += 1
-        return 4 if 16 * items * 4 > 113 * 1024 else 2
+        return 16 if 16 * items * 4 > 113 * 1024 else 2
 
     def sweep_schedule(self, width=32):
         """(mode, stages, width) of the schedule the kernel runs, or mode
         None: the sequential one-lane sweep.  The cheapest candidate by the
         cost model (on the kernel's lanes per env, _sweep_lanes), used when it
         is below 0.8 of the sequential cost.  Measured on B200, fp32, with
-        every mode forced (tools/gpu_r02_p.sh): humanoid 16384 envs none /
-        asap / phased / joints 2297 / 1800 / 1946 / 1886 us per control step
-        -> asap; Shadow Hand 3.38 / 3.28 / 3.19 / 3.93 M env-steps/s -> joints;
-        Franka cube-stack 7.47 / 6.15 / 5.80 / 6.21 M -> none.  The model
-        picks the same three.
+        every mode forced, 16 lanes per env on the large CTA
+        (tools/gpu_r02_t.sh): humanoid 16384 envs none / asap / phased /
+        joints 1917 / 1610 / 1541 / 1761 us per control step -> phased;
+        Shadow Hand 3.87 / 3.59 / 3.49 / 4.29 M env-steps/s -> joints;
+        Franka cube-stack 8.70 / 6.53 / 6.15 / 6.74 M -> none.  The model
+        picks the same three (with 4 lanes, round 2's first shape, it picked
+        asap for the humanoid, as measured then: tools/gpu_r02_p.sh).
         BSIM_SCHED_MODE=asap|phased|joints|none forces a mode (experiments)."""
         import os
         cands = self.sweep_schedules(width)
