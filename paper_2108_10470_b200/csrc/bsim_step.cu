@@ -140,7 +140,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 #endif
-template <class R, class T>
+template <class R, class T, bool SCHED>
 __global__ void __launch_bounds__(Shape<R>::NTH, BSIM_MINB)
     step_kernel(const __grid_constant__ Ctx<R> c, int n_substeps, bsim_actions_t act, int epc, int e_begin,
                 int e_end, const __grid_constant__ bsim_task_t task, int with_task) {
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(Shape<R>::NTH, BSIM_MINB)
         gs.bar = 1 + h;
     }
     for (int s = 0; s < n_substeps; ++s) {
-        group_step<R, T>(c, gs, s == n_substeps - 1, s);
+        group_step<R, T, SCHED>(c, gs, s == n_substeps - 1, s);
         if (d.T && s != n_substeps - 1) {  // fixed tendons read dof_state next substep
             if (halves) __syncthreads();
             readout_group(c, g);
@@ -626,7 +626,7 @@ struct Plan {
     size_t smem;
     long capacity;   // resident envs of one wave (SMs x CTAs/SM x envs/CTA)
 };
-template <class R, class T> int plan_launch(const Dims &d, int E, Plan *out) {
+template <class R, class T, bool SCHED> int plan_launch(const Dims &d, int E, Plan *out) {
     constexpr int NE = Shape<R>::NE;
     struct Entry {
         int dev, pad, J, E;
@@ -647,7 +647,7 @@ template <class R, class T> int plan_launch(const Dims &d, int E, Plan *out) {
         }
     const size_t smax = step_smem_bytes<R>(d, NE);
     if (smax > 48 * 1024 && smax > configured[dev]) {
-        cudaError_t e = cudaFuncSetAttribute(step_kernel<R, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(step_kernel<R, T, SCHED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smax);
         if (e != cudaSuccess) return set_err("cudaFuncSetAttribute(step_kernel)", e);
         configured[dev] = smax;
@@ -658,7 +658,7 @@ template <class R, class T> int plan_launch(const Dims &d, int E, Plan *out) {
     int best_n = 0;
     for (int n = NE; n >= 1; --n) {
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<R, T>, Shape<R>::NTH,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<R, T, SCHED>, Shape<R>::NTH,
                                                       step_smem_bytes<R>(d, n));
         if (per_sm < 1) continue;
         const long slots = (long)sms * per_sm, waves = (En + slots * n - 1) / (slots * n);
@@ -682,12 +682,15 @@ template <class R, class T> int plan_launch(const Dims &d, int E, Plan *out) {
     return BSIM_OK;
 }
 
-template <class R, class T>
-int launch_step_t(const Ctx<R> &c, size_t smem, int n_substeps, const bsim_actions_t &act, const bsim_task_t *task,
-                  int e_begin, int e_count, cudaStream_t st) {
-    (void)smem;
+// the sweep a layout runs on topology T: the row schedule when it has one
+// (and T is neither a star nor a register-sweep topology)
+template <class T> constexpr bool sched_capable() { return !topo_register_sweep<T>() && !topo_star<T>(); }
+
+template <class R, class T, bool SCHED>
+int launch_step_tt(const Ctx<R> &c, int n_substeps, const bsim_actions_t &act, const bsim_task_t *task,
+                   int e_begin, int e_count, cudaStream_t st) {
     Plan pl;
-    if (int rc = plan_launch<R, T>(c.d, c.d.E, &pl)) return rc;
+    if (int rc = plan_launch<R, T, SCHED>(c.d, c.d.E, &pl)) return rc;
     const int epc = pl.epc;
     const int grid = (e_count + epc - 1) / epc;
     bsim_task_t tk;
@@ -696,9 +699,22 @@ int launch_step_t(const Ctx<R> &c, size_t smem, int n_substeps, const bsim_actio
         g_err = "bsim_env_step: observation rows do not fit the CTA workspace";
         return BSIM_E_TOO_LARGE;
     }
-    step_kernel<R, T><<<grid, Shape<R>::NTH, pl.smem, st>>>(c, n_substeps, act, epc, e_begin, e_begin + e_count, tk,
-                                                           task != nullptr);
+    step_kernel<R, T, SCHED><<<grid, Shape<R>::NTH, pl.smem, st>>>(c, n_substeps, act, epc, e_begin,
+                                                                  e_begin + e_count, tk, task != nullptr);
     return check_launch("step_kernel");
+}
+template <class R, class T>
+int launch_step_t(const Ctx<R> &c, size_t smem, int n_substeps, const bsim_actions_t &act, const bsim_task_t *task,
+                  int e_begin, int e_count, cudaStream_t st) {
+    (void)smem;
+    if constexpr (sched_capable<T>())
+        if (c.L.sched_stages > 0) return launch_step_tt<R, T, true>(c, n_substeps, act, task, e_begin, e_count, st);
+    return launch_step_tt<R, T, false>(c, n_substeps, act, task, e_begin, e_count, st);
+}
+template <class R, class T> int plan_launch_for(const bsim_layout_t *l, const Dims &d, Plan *out) {
+    if constexpr (sched_capable<T>())
+        if (l->sched_stages > 0) return plan_launch<R, T, true>(d, d.E, out);
+    return plan_launch<R, T, false>(d, d.E, out);
 }
 
 // the task-layer argument rules of bsim_task_step (bsim_tasks.cu)
@@ -879,7 +895,7 @@ template <class R> int envs_per_wave(const bsim_layout_t *l, int32_t *envs) {
     switch (l->topology_id) {
 #define BSIM_WAVE_TOPO(ID, TYPE) \
     case ID:                     \
-        rc = plan_launch<R, TYPE>(d, d.E, &pl); break;
+        rc = plan_launch_for<R, TYPE>(l, d, &pl); break;
 #ifdef BSIM_LARGE_TU
         BSIM_TOPOLOGIES_LARGE(BSIM_WAVE_TOPO)
 #else
@@ -887,7 +903,7 @@ template <class R> int envs_per_wave(const bsim_layout_t *l, int32_t *envs) {
 #endif
 #undef BSIM_WAVE_TOPO
     default:
-        rc = plan_launch<R, TopoGeneric>(d, d.E, &pl);
+        rc = plan_launch_for<R, TopoGeneric>(l, d, &pl);
     }
     *envs = (int32_t)pl.capacity;
     return rc;

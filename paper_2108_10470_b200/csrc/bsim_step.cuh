@@ -1569,7 +1569,14 @@ template <class R> BS_HD void body_phase_item(const Ctx<R> &c, const Ws<R> &w, i
 // The N biased passes and the final velocity stage share one phase-A body
 // (freeze at k = 0, refresh-with-deltas at 0 < k < N, integrate + refresh at
 // k = N), so every piece of the step appears once in the binary.
-template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> &g, bool write_outputs, int sub) {
+// SCHED: the instantiation's sweep for non-star / non-register topologies --
+// the row schedule (true) or the one-lane sequential sweep (false).  Each
+// kernel carries one of the two: with both compiled in, either ran 6-9 %
+// slower (register allocation / code size), so the launcher
+// picks the instantiation from the layout's schedule.  The host build keeps
+// the run-time choice.
+template <class R, class T, bool SCHED = false>
+BS_HD void group_step(const Ctx<R> &c, const Grp<R> &g, bool write_outputs, int sub) {
     const Dims &d = c.d;
     const int ebad = d.o_env + EBAD + (sub & 1);
     const auto &p = c.p;
@@ -1692,7 +1699,7 @@ template <class R, class T> BS_HD void group_step(const Ctx<R> &c, const Grp<R> 
 #endif
             {
 #if defined(__CUDA_ARCH__)
-                if (!topo_register_sweep<T>() && c.L.sched_stages > 0) {
+                if constexpr (SCHED && !topo_register_sweep<T>()) {   // launcher: sched_stages > 0
                     // the row schedule on BSIM_SCHED_WARPS warps from the claimed sweep
                     // warp on: 32 SW / NE lanes per env, each env's lanes inside one warp
                     // (a stage's rows run side by side; a stage ends at a __syncwarp)
