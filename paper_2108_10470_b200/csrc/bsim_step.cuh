@@ -1173,13 +1173,19 @@ template <class R> BS_HD void sweep(const Ctx<R> &c, const Ws<R> &w, R h, bool b
 // `lane` in [0, lanes) indexes the env's threads; the stage loop runs on
 // every thread of the CTA (uniform trip count) and __syncwarp(mask) orders a
 // stage's shared-memory writes before the next stage's reads.
-template <class R>
+struct TopoGeneric;
+template <class T> constexpr bool topo_rev();
+template <class T> constexpr bool topo_pairs();
+template <class R, class T = TopoGeneric>
 BS_HD void sched_row(const Ctx<R> &c, const Ws<R> &w, int r, R h, bool biased) {
     const Dims &d = c.d;
     if (r < d.J) {
         const auto &jt = c.joints[r];
         BV<R> C = load_bv(d, w, jt.child), P = load_bv(d, w, jt.parent);
-        joint_rows(c, w, r, jt.kind, jt.dof, jt.has_limits != 0, jt.parent, jt.child, h, biased, C, P);
+        // an all-revolute compile-time topology (the humanoid) compiles the
+        // revolute rows only: one copy of the rows, no other kinds' code
+        const int kind = topo_rev<T>() ? (int)BSIM_REVOLUTE : (int)jt.kind;
+        joint_rows(c, w, r, kind, jt.dof, jt.has_limits != 0, jt.parent, jt.child, h, biased, C, P);
         store_bv(d, w, jt.child, C);
         store_bv(d, w, jt.parent, P);
     } else if (r < d.J + d.P) {
@@ -1190,7 +1196,7 @@ BS_HD void sched_row(const Ctx<R> &c, const Ws<R> &w, int r, R h, bool biased) {
         BV<R> X = load_bv(d, w, b);
         row_plane(c, w, i, X);
         store_bv(d, w, b, X);
-    } else {
+    } else if (!T::is_static || topo_pairs<T>()) {
         const int i = r - d.J - d.P, pa = c.L.pair_body[2 * i], pb = c.L.pair_body[2 * i + 1];
 #if BSIM_SKIP_INACTIVE
         if (w.at(ipr(d, i, QACT)) == R(0)) return;
@@ -1202,7 +1208,7 @@ BS_HD void sched_row(const Ctx<R> &c, const Ws<R> &w, int r, R h, bool biased) {
     }
 }
 #if defined(__CUDA_ARCH__)
-template <class R>
+template <class R, class T>
 __device__ void sweep_sched(const Ctx<R> &c, const Ws<R> *w, R h, bool biased, int lane, int lanes, unsigned mask) {
     const Dims &d = c.d;
     const int S = c.L.sched_stages, W = c.L.sched_width;
@@ -1210,12 +1216,12 @@ __device__ void sweep_sched(const Ctx<R> &c, const Ws<R> *w, R h, bool biased, i
         if (w)
             for (int i = lane; i < W; i += lanes) {   // a stage's rows are independent: any lane may take any
                 const int r = __ldg(c.L.sweep_sched + s * W + i);
-                if (r >= 0) sched_row(c, *w, r, h, biased);
+                if (r >= 0) sched_row<R, T>(c, *w, r, h, biased);
             }
         __syncwarp(mask);
     }
     if ((c.L.sched_flags & 1) && w && lane == 0)      // joint-only schedule: the contact rows in order
-        for (int r = d.J; r < d.J + d.P + d.Q; ++r) sched_row(c, *w, r, h, biased);
+        for (int r = d.J; r < d.J + d.P + d.Q; ++r) sched_row<R, T>(c, *w, r, h, biased);
     if (c.L.sched_flags & 1) __syncwarp(mask);
     if (biased && w)
         for (int b = lane; b < d.B; b += lanes) accumulate_deltas(d, *w, b, load_bv(d, *w, b), h);
@@ -1711,7 +1717,7 @@ BS_HD void group_step(const Ctx<R> &c, const Grp<R> &g, bool write_outputs, int 
                     if (t < 32 * SW) {
                         const int el = t / LPE, lane = t % LPE;
                         const Ws<R> w = g.env(el);
-                        sweep_sched<R>(c, el < g.ne ? &w : nullptr, h, biased, lane, LPE, 0xffffffffu);
+                        sweep_sched<R, T>(c, el < g.ne ? &w : nullptr, h, biased, lane, LPE, 0xffffffffu);
                     }
                 } else
 #else
