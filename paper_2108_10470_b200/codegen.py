@@ -31,6 +31,12 @@ SPECIALISED = {
 # bodies do not fit the register-resident sweep)
 SPECIALISED_LARGE = {
     "humanoid": [M.humanoid],
+    # the Shadow Hand and Franka cube-stack scenes of envs.py (box / capsule
+    # pair slots, shape_pairs="all"): compile-time joint kinds (the hand's
+    # rows compile revolute-only), frames, tendon / pair presence, slot bodies
+    "shadow_hand_cube": ([M.shadow_hand, lambda: M.cube("cube", M.SHADOW_CUBE_HALF, 0.1)], "all"),
+    "franka_cube_stack": ([M.franka, lambda: M.cube("cubeA", M.CUBE_A_HALF, 0.3),
+                           lambda: M.cube("cubeB", M.CUBE_B_HALF, 0.5)], "all"),
 }
 
 
@@ -89,8 +95,9 @@ def _packed(vals):
 def generate():
     structs, entries, entries_large, sigs = [], [], [], []
     items = [(n, b, False) for n, b in SPECIALISED.items()] + [(n, b, True) for n, b in SPECIALISED_LARGE.items()]
-    for tid, (name, builders, large) in enumerate(items, start=1):
-        L = SceneLayout([b() for b in builders], ground=True)
+    for tid, (name, spec, large) in enumerate(items, start=1):
+        builders, pairs = spec if isinstance(spec, tuple) else (spec, "spheres")
+        L = SceneLayout([b() for b in builders], ground=True, shape_pairs=pairs)
         J = L.joints
         cname = f"Topo_{name}"
         structs.append(f"""struct {cname} {{

@@ -1133,12 +1133,18 @@ template <class R> BS_HD void accumulate_deltas(const Dims &d, const Ws<R> &w, i
 }
 
 // one Gauss-Seidel pass for one env, any topology (physics.py:760-775)
-template <class R> BS_HD void sweep(const Ctx<R> &c, const Ws<R> &w, R h, bool biased) {
+struct TopoGeneric;
+template <class T> constexpr bool topo_rev();
+template <class T> constexpr bool topo_pairs();
+// (T: the compile-time topology, as in sched_row -- an all-revolute one
+// compiles the revolute rows only, one without pair slots no pair rows)
+template <class R, class T = TopoGeneric> BS_HD void sweep(const Ctx<R> &c, const Ws<R> &w, R h, bool biased) {
     const Dims &d = c.d;
     for (int j = 0; j < d.J; ++j) {
         const auto &jt = c.joints[j];
         BV<R> C = load_bv(d, w, jt.child), P = load_bv(d, w, jt.parent);
-        joint_rows(c, w, j, jt.kind, jt.dof, jt.has_limits != 0, jt.parent, jt.child, h, biased, C, P);
+        const int kind = topo_rev<T>() ? (int)BSIM_REVOLUTE : (int)jt.kind;
+        joint_rows(c, w, j, kind, jt.dof, jt.has_limits != 0, jt.parent, jt.child, h, biased, C, P);
         store_bv(d, w, jt.child, C);
         store_bv(d, w, jt.parent, P);
     }
@@ -1151,7 +1157,7 @@ template <class R> BS_HD void sweep(const Ctx<R> &c, const Ws<R> &w, R h, bool b
         row_plane(c, w, i, X);
         store_bv(d, w, b, X);
     }
-    for (int i = 0; i < d.Q; ++i) {
+    for (int i = 0; i < ((!T::is_static || topo_pairs<T>()) ? d.Q : 0); ++i) {
 #if BSIM_SKIP_INACTIVE
         if (w.at(ipr(d, i, QACT)) == R(0)) continue;
 #endif
@@ -1173,9 +1179,6 @@ template <class R> BS_HD void sweep(const Ctx<R> &c, const Ws<R> &w, R h, bool b
 // `lane` in [0, lanes) indexes the env's threads; the stage loop runs on
 // every thread of the CTA (uniform trip count) and __syncwarp(mask) orders a
 // stage's shared-memory writes before the next stage's reads.
-struct TopoGeneric;
-template <class T> constexpr bool topo_rev();
-template <class T> constexpr bool topo_pairs();
 template <class R, class T = TopoGeneric>
 BS_HD void sched_row(const Ctx<R> &c, const Ws<R> &w, int r, R h, bool biased) {
     const Dims &d = c.d;
@@ -1415,7 +1418,7 @@ template <class R, class T> BS_HD void sweep_any(const Ctx<R> &c, const Ws<R> &w
         else
             sweep_static<R, T, false>(c, w, h);
     } else
-        sweep(c, w, h, biased);
+        sweep<R, T>(c, w, h, biased);
 }
 
 // ------------------------------------------------------------ tendons

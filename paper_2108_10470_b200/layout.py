@@ -387,19 +387,18 @@ class SceneLayout:
         """(mode, stages, width) of the schedule the kernel runs, or mode
         None: the sequential one-lane sweep.  The cheapest candidate by the
         cost model (on the kernel's lanes per env, _sweep_lanes), used when it
-        is below 0.75 of the sequential cost.  Measured on B200, fp32, with
-        every mode forced, 16 lanes per env on the large CTA
-        (tools/gpu_r02_t.sh): humanoid 16384 envs none / asap / phased /
-        joints 1917 / 1610 / 1541 / 1761 us per control step -> phased;
-        Shadow Hand 3.87 / 3.59 / 3.49 / 4.29 M env-steps/s; Franka
-        cube-stack 8.70 / 6.53 / 6.15 / 6.74 M -> none.  Since each kernel
-        instantiation carries one sweep (v27, group_step SCHED), the
-        sequential sweep runs 6-9 % faster: Shadow Hand none 4.26 M vs
-        joints 4.20 M, Franka none 9.21 M, humanoid none 1764 us vs phased
-        1528 us (tools/gpu_r02_x.sh) -- hence 0.75 (the hand's joints form
-        models at 0.78 of its sequential cost).  With 4 lanes, round 2's
-        first shape, the model picked asap for the humanoid, as measured
-        then (tools/gpu_r02_p.sh).
+        is below 0.8 of the sequential cost.  Measured on B200, fp32, every
+        mode forced, on the v29 kernels (16 lanes per env on the large CTA,
+        one sweep per kernel instantiation, rows specialised on the
+        compile-time topology; tools/gpu_r02_ae.sh): humanoid 16384 envs
+        none / asap / phased / joints 1482 / 1397 / 1340 / 1537 us per
+        control step -> phased; Shadow Hand 4.78 / 4.13 / 3.97 / 5.03 M
+        env-steps/s -> joints; Franka cube-stack 9.35 / 6.90 / 6.50 / 7.07 M
+        -> none.  The model picks the same three (the hand's joints form
+        models at 0.78 of its sequential cost; with round 2's earlier kernels
+        it measured slower than the sequential sweep and 0.75 was used:
+        tools/gpu_r02_x.sh; with 4 lanes per env the humanoid picked asap:
+        tools/gpu_r02_p.sh).
         BSIM_SCHED_MODE=asap|phased|joints|none forces a mode (experiments,
         tests/test_gpu_sched_modes.py); read once per layout: the result is
         memoised, so the packed table and the layout struct always agree."""
@@ -418,7 +417,7 @@ class SceneLayout:
         else:
             lanes = self._sweep_lanes()
             mode = min(cands, key=lambda m: self._sched_cost(m, cands[m], lanes))
-            if not cands[mode] or self._sched_cost(mode, cands[mode], lanes) >= 0.75 * seq:
+            if not cands[mode] or self._sched_cost(mode, cands[mode], lanes) >= 0.8 * seq:
                 mode = None
         if mode is None:
             return None, [], 0

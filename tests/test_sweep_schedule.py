@@ -65,7 +65,7 @@ def test_schedule_choice(name):
     measured rankings quoted in SceneLayout.sweep_schedule."""
     L = SCENES[name]
     mode, stages, width = L.sweep_schedule()
-    want = {"humanoid": "phased", "shadow_hand_cube": None, "franka_cube_stack": None}
+    want = {"humanoid": "phased", "shadow_hand_cube": "joints", "franka_cube_stack": None}
     if name in want:
         assert mode == want[name], (name, mode)
     if mode is not None:
