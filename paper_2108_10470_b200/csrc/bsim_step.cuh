@@ -1179,19 +1179,10 @@ template <class R, class T = TopoGeneric> BS_HD void sweep(const Ctx<R> &c, cons
 // `lane` in [0, lanes) indexes the env's threads; the stage loop runs on
 // every thread of the CTA (uniform trip count) and __syncwarp(mask) orders a
 // stage's shared-memory writes before the next stage's reads.
-template <class R, class T = TopoGeneric>
-BS_HD void sched_row(const Ctx<R> &c, const Ws<R> &w, int r, R h, bool biased) {
+// contact row r >= J of the schedule: plane slot r - J or pair slot r - J - P
+template <class R, class T = TopoGeneric> BS_HD void sched_contact_row(const Ctx<R> &c, const Ws<R> &w, int r) {
     const Dims &d = c.d;
-    if (r < d.J) {
-        const auto &jt = c.joints[r];
-        BV<R> C = load_bv(d, w, jt.child), P = load_bv(d, w, jt.parent);
-        // an all-revolute compile-time topology (the humanoid) compiles the
-        // revolute rows only: one copy of the rows, no other kinds' code
-        const int kind = topo_rev<T>() ? (int)BSIM_REVOLUTE : (int)jt.kind;
-        joint_rows(c, w, r, kind, jt.dof, jt.has_limits != 0, jt.parent, jt.child, h, biased, C, P);
-        store_bv(d, w, jt.child, C);
-        store_bv(d, w, jt.parent, P);
-    } else if (r < d.J + d.P) {
+    if (r < d.J + d.P) {
         const int i = r - d.J, b = c.L.plane_body[i];
 #if BSIM_SKIP_INACTIVE
         if (w.at(ipl(d, i, CACT)) == R(0)) return;
@@ -1210,6 +1201,22 @@ BS_HD void sched_row(const Ctx<R> &c, const Ws<R> &w, int r, R h, bool biased) {
         store_bv(d, w, pb, X);
     }
 }
+template <class R, class T = TopoGeneric>
+BS_HD void sched_row(const Ctx<R> &c, const Ws<R> &w, int r, R h, bool biased) {
+    const Dims &d = c.d;
+    if (r < d.J) {
+        const auto &jt = c.joints[r];
+        BV<R> C = load_bv(d, w, jt.child), P = load_bv(d, w, jt.parent);
+        // an all-revolute compile-time topology (the humanoid) compiles the
+        // revolute rows only: one copy of the rows, no other kinds' code
+        const int kind = topo_rev<T>() ? (int)BSIM_REVOLUTE : (int)jt.kind;
+        joint_rows(c, w, r, kind, jt.dof, jt.has_limits != 0, jt.parent, jt.child, h, biased, C, P);
+        store_bv(d, w, jt.child, C);
+        store_bv(d, w, jt.parent, P);
+    } else {
+        sched_contact_row<R, T>(c, w, r);
+    }
+}
 #if defined(__CUDA_ARCH__)
 template <class R, class T>
 __device__ void sweep_sched(const Ctx<R> &c, const Ws<R> *w, R h, bool biased, int lane, int lanes, unsigned mask) {
@@ -1224,7 +1231,7 @@ __device__ void sweep_sched(const Ctx<R> &c, const Ws<R> *w, R h, bool biased, i
         __syncwarp(mask);
     }
     if ((c.L.sched_flags & 1) && w && lane == 0)      // joint-only schedule: the contact rows in order
-        for (int r = d.J; r < d.J + d.P + d.Q; ++r) sched_row<R, T>(c, *w, r, h, biased);
+        for (int r = d.J; r < d.J + d.P + d.Q; ++r) sched_contact_row<R, T>(c, *w, r);   // (no 2nd copy of the joint rows)
     if (c.L.sched_flags & 1) __syncwarp(mask);
     if (biased && w)
         for (int b = lane; b < d.B; b += lanes) accumulate_deltas(d, *w, b, load_bv(d, *w, b), h);
