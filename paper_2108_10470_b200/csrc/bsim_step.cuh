@@ -465,13 +465,33 @@ template <class T, class R> BS_HD int plane_body_of(const Ctx<R> &c, int i) {
 // (read_dof_states, physics.py:557) seed q0, the unbiased limit rows' q and
 // the DOF impulse accumulators.  Per-env gains / limits / controls are read
 // from HBM (L1/L2 resident).
+// The joint kinds a compile-time topology contains (bit k = kind k; every
+// kind for a run-time layout), and a joint's kind folded onto them: code for
+// kinds the scene does not have is then dead (the Franka scene: revolute and
+// prismatic only), without a second copy of the rows.
+template <class T> constexpr unsigned topo_kinds() {
+    if constexpr (T::is_static) {
+        unsigned m = 0;
+        for (int j = 0; j < T::J; ++j) m |= 1u << T::kind[j];
+        return m;
+    } else {
+        return 0xfu;
+    }
+}
+template <class T> BS_HD int fold_kind(int k) {
+    constexpr unsigned m = topo_kinds<T>();
+    if constexpr (m == (1u << BSIM_REVOLUTE)) return BSIM_REVOLUTE;
+    else if constexpr (m == ((1u << BSIM_REVOLUTE) | (1u << BSIM_PRISMATIC)))
+        return k == BSIM_PRISMATIC ? BSIM_PRISMATIC : BSIM_REVOLUTE;
+    else return k;
+}
 template <class R, class T, bool REV = false, bool IDF = false>
 BS_HD void joint_item(const Ctx<R> &c, const Ws<R> &w, int e, int j, R h, bool biased, bool freeze, bool deltas,
                       const JTab<R> &jtab) {
     const Dims &d = c.d;
     const auto &jt = jtab[j];
     const JMeta jm = joint_meta<T>(c, j);
-    const int kind = REV ? (int)BSIM_REVOLUTE : jm.kind;
+    const int kind = REV ? (int)BSIM_REVOLUTE : fold_kind<T>(jm.kind);
     const int p = jm.parent, ch = jm.child, jdof = jm.dof;
     R q0 = R(0);
     // per-env gains / limits / controls: issued first so their L1/L2 latency
@@ -1143,7 +1163,7 @@ template <class R, class T = TopoGeneric> BS_HD void sweep(const Ctx<R> &c, cons
     for (int j = 0; j < d.J; ++j) {
         const auto &jt = c.joints[j];
         BV<R> C = load_bv(d, w, jt.child), P = load_bv(d, w, jt.parent);
-        const int kind = topo_rev<T>() ? (int)BSIM_REVOLUTE : (int)jt.kind;
+        const int kind = fold_kind<T>(jt.kind);
         joint_rows(c, w, j, kind, jt.dof, jt.has_limits != 0, jt.parent, jt.child, h, biased, C, P);
         store_bv(d, w, jt.child, C);
         store_bv(d, w, jt.parent, P);
@@ -1209,7 +1229,7 @@ BS_HD void sched_row(const Ctx<R> &c, const Ws<R> &w, int r, R h, bool biased) {
         BV<R> C = load_bv(d, w, jt.child), P = load_bv(d, w, jt.parent);
         // an all-revolute compile-time topology (the humanoid) compiles the
         // revolute rows only: one copy of the rows, no other kinds' code
-        const int kind = topo_rev<T>() ? (int)BSIM_REVOLUTE : (int)jt.kind;
+        const int kind = fold_kind<T>(jt.kind);
         joint_rows(c, w, r, kind, jt.dof, jt.has_limits != 0, jt.parent, jt.child, h, biased, C, P);
         store_bv(d, w, jt.child, C);
         store_bv(d, w, jt.parent, P);
