@@ -1250,9 +1250,27 @@ __device__ void sweep_sched(const Ctx<R> &c, const Ws<R> *w, R h, bool biased, i
             }
         __syncwarp(mask);
     }
-    if ((c.L.sched_flags & 1) && w && lane == 0)      // joint-only schedule: the contact rows in order
-        for (int r = d.J; r < d.J + d.P + d.Q; ++r) sched_contact_row<R, T>(c, *w, r);   // (no 2nd copy of the joint rows)
-    if (c.L.sched_flags & 1) __syncwarp(mask);
+    if (c.L.sched_flags & 1) {   // joint-only schedule: the contact rows in order
+        // the env's lanes read the slots' activity side by side (one ballot per
+        // `lanes` rows) and lane 0 runs the active rows in reference order,
+        // instead of testing every slot one dependent load after another
+        // (Shadow Hand 3026 -> 2671 us per 16384-env control step; v33)
+        const int nc = d.P + d.Q, wl = (int)(threadIdx.x & 31) - lane;
+        const unsigned sel = lanes >= 32 ? 0xffffffffu : ((1u << lanes) - 1u);
+        for (int base = 0; base < nc; base += lanes) {
+            const int i = base + lane;
+            bool act = false;
+            if (w && i < nc) act = (i < d.P ? w->at(ipl(d, i, CACT)) : w->at(ipr(d, i - d.P, QACT))) != R(0);
+            unsigned bits = (__ballot_sync(mask, act) >> wl) & sel;
+            if (w && lane == 0)
+                while (bits) {
+                    const int b = __ffs(bits) - 1;
+                    bits &= bits - 1;
+                    sched_contact_row<R, T>(c, *w, d.J + base + b);
+                }
+        }
+        __syncwarp(mask);
+    }
     if (biased && w)
         for (int b = lane; b < d.B; b += lanes) accumulate_deltas(d, *w, b, load_bv(d, *w, b), h);
 }
