@@ -19,5 +19,5 @@ print("reference arm:", r.get("value"), "same config:", r.get("config") == d.get
 PY
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/final/launches.csv python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-other-configs > gpurun_out/final/ncu_launch.log 2>&1; echo "launch list rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"step_kernel" -s 6 -c 1 -o gpurun_out/final/step_full -f python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-other-configs > gpurun_out/final/ncu_full.log 2>&1; echo "step ncu rc=$?"
-python tools/ncu_summary.py gpurun_out/final/step_full.ncu-rep gpurun_out/final/r02_step_${VER:-v33}_ncu.json --envs 16384 --command "ncu --set full -k regex:step_kernel -s 6 -c 1 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-other-configs" > /dev/null 2>&1
+python tools/ncu_summary.py gpurun_out/final/step_full.ncu-rep gpurun_out/final/r02_step_${VER:-v34}_ncu.json --envs 16384 --command "ncu --set full -k regex:step_kernel -s 6 -c 1 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-other-configs" > /dev/null 2>&1
 SAN_TIMEOUT=600 bash tools/gpu_sanitize.sh 2>&1 | grep -E "rc=|SUMMARY" | tail -20
