@@ -31,6 +31,12 @@ SCENES = {
     # box B (rotated) resting on box A resting on the ground: 16 PB corner slots
     "box_stack": (lambda: [M.free_box((0.2, 0.2, 0.1), 2.0), M.free_box((0.1, 0.1, 0.1), 1.0)],
                   [((0, 0, 0.1), (0, 0, 1), 0.0), ((0.05, 0.02, 0.3), (0, 0, 1), 0.3)]),
+    # three boxes stacked: 24 plane + 48 PB slots (72 > 64: the sequential
+    # sweep's activity mask runs in two 64-slot chunks)
+    "box_tower": (lambda: [M.free_box((0.2, 0.2, 0.1), 2.0), M.free_box((0.15, 0.15, 0.1), 1.5),
+                           M.free_box((0.1, 0.1, 0.1), 1.0)],
+                  [((0, 0, 0.1), (0, 0, 1), 0.0), ((0.02, 0.01, 0.3), (0, 0, 1), 0.1),
+                   ((-0.01, 0.02, 0.5), (0, 0, 1), 0.2)]),
     # sphere on a box: 1 PB slot
     "sphere_on_box": (lambda: [M.free_box((0.2, 0.2, 0.1), 2.0), M.free_sphere(0.1, 1.0)],
                       [((0, 0, 0.1), (0, 0, 1), 0.0), ((0.05, 0.0, 0.3), (0, 0, 1), 0.0)]),
