@@ -35,6 +35,13 @@ def _scene(name, mode, monkeypatch):
         s.pos[:, 2] += 1.0
         s.forward_kinematics()
         return s
+    if name == "kitchen_sink":      # the default-CTA kernel: every joint kind, tendons, sphere pairs
+        from golden_util import build_models, load, sim_params
+        meta, arr = load("kitchen_sink")
+        s = Scene(build_models(meta), meta["num_envs"], sim_params(meta), precision="fp64",
+                  env_origins=arr["param_env_origins"])
+        load_gpu_state(s, arr, 0)
+        return s
     models, p, meta, arr = _trace(name)
     s = Scene(models, meta["num_envs"], p, precision="fp64", shape_pairs="all", env_origins=arr["param_env_origins"])
     load_gpu_state(s, arr, 0)
@@ -42,7 +49,7 @@ def _scene(name, mode, monkeypatch):
 
 
 @pytest.mark.parametrize("mode", ["asap", "phased", "joints"])
-@pytest.mark.parametrize("name", ["humanoid", "shadow_hand_cube", "franka_cube_stack"])
+@pytest.mark.parametrize("name", ["humanoid", "shadow_hand_cube", "franka_cube_stack", "kitchen_sink"])
 def test_forced_schedule_equals_sequential_sweep(name, mode, monkeypatch):
     a = _scene(name, mode, monkeypatch)
     b = _scene(name, "none", monkeypatch)
